@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native matrix-free operator apply.
+
+Headline (BASELINE.json metric, config 2 = configs[1]): constant-coefficient
+P1 15-point stencil apply with the full ghost-layer (interface replica) update
+on the unit cube split into 6 Kuhn macro-tets at level 8 (17,173,254 slots,
+16,974,593 owned DoFs), fp64, x = random_fill(seed 0). One step = one
+apply (per-cell rows kernel + interface pass). Inputs (x + y = 275 MB) exceed
+the 126 MB L2, so no explicit flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank runs the same per-GPU workload (weak
+scaling, replicas of config 2: its 6 macro-cells do not shard over 8 GPUs);
+times are max over ranks. `--impl reference` times the reference CPU
+implementation (oracle/_ref, the unmodified blocktet headers) on the host
+cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LEVEL = 8
+WORKLOAD = "cube-kuhn (6 macro-tets) L8, P1 const-coeff 15-point stencil apply + interface sync"
+METRIC = "GDoF/s of matrix-free operator apply (fp64)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0, period_ms=100):
+        self.cmd = ["nvidia-smi", f"--id={index}",
+                    "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                    "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                    "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                    "--format=csv,noheader,nounits", f"-lms={period_ms}"]
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(self.cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline_sample(threads=None):
+    """Reference CPU apply (oracle/_ref = blocktet headers, -O3, no -march),
+    config 2 at full size, threads = min(#cells, nproc). Bounded sample:
+    median of 5 applies (~2-10 s)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    nproc = os.cpu_count() or 1
+    threads = threads or min(6, nproc)
+    kind = "reference"
+    try:
+        r = pyoracle.Reference(pyoracle.cube_kuhn_text(), LEVEL, LEVEL)
+        x = r.random_fill(LEVEL, 0)
+        sec = r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=5, threads=threads)
+        owned = r.owned_count(LEVEL)
+    except (FileNotFoundError, OSError):
+        kind = "port"
+        threads = 1
+        o = pyoracle.Oracle(pyoracle.cube_kuhn_text(), LEVEL, LEVEL, with_edges=False)
+        x = o.random_fill(LEVEL, 0)
+        t0 = time.perf_counter()
+        o.apply_stencil(LEVEL, x, 0)
+        sec = time.perf_counter() - t0
+        owned = o.owned_count(LEVEL)
+    return {"value": owned / sec / 1e9, "unit": "GDoF/s", "cores": threads, "kind": kind,
+            "sample": f"median of 5 full config-2 applies (cube-kuhn L8, {owned} owned DoFs), "
+                      f"{threads} threads of {nproc} host cores, {sec * 1e3:.1f} ms/apply"}
+
+
+def run_reference(args):
+    """The reference CPU apply (oracle/_ref, unmodified blocktet headers) on
+    the host cores, same workload/metric; rank 0 only. Each step is one full
+    config-2 apply; K is capped so the run stays within about a minute."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    nproc = os.cpu_count() or 1
+    threads = min(6, nproc)  # the reference parallelises over macro-cells only (threading.hpp:14)
+    try:
+        r = pyoracle.Reference(pyoracle.cube_kuhn_text(), LEVEL, LEVEL)
+        kind = "reference"
+    except (FileNotFoundError, OSError) as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
+        return
+    x = r.random_fill(LEVEL, 0)
+    owned = r.owned_count(LEVEL)
+    for _ in range(min(args.warmup, 1)):
+        r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=1, threads=threads)
+    t0 = time.perf_counter()
+    first = r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=1, threads=threads)
+    K = max(1, min(args.steps, int(60.0 / max(first, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(K):
+        r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=1, threads=threads)
+    sec = (time.perf_counter() - t0) / K
+    value = owned / sec / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": args.gpus,
+            "steps": K, "warmup": min(args.warmup, 1), "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_fill seed 0)",
+            "config": {"workload": WORKLOAD, "level": LEVEL, "cells": 6, "threads": threads},
+            "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": kind,
+                             "sample": f"{K} full config-2 applies, {threads} threads of {nproc} host cores"},
+            "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2308_01792_b200 as bt
+    from paper_2308_01792_b200 import _lib
+
+    dev = torch.cuda.current_device()
+    grid = bt.Grid(bt.cube_kuhn_text(), LEVEL, LEVEL, device=dev)
+    table = bt.compute_stencil(bt.FormId.diffusion(), grid, LEVEL)
+    x = bt.allocate(bt.p1_space(), grid)
+    y = bt.allocate(bt.p1_space(), grid)
+    bt.random_fill(x, LEVEL, 0)
+    owned = bt.owned_dof_count(x, LEVEL)
+    slots = grid.space_size(0, LEVEL)
+    L = _lib.lib
+    stream = torch.cuda.current_stream()
+    sp = bt.api._stream()
+    xp, yp = bt.api._ptr(x.values[LEVEL]), bt.api._ptr(y.values[LEVEL])
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        bt.api._check(L.bt_apply_stencil_cells(table.handle, xp, yp, sp))
+        if ev is not None:
+            ev[1].record(stream)
+        bt.api._check(L.bt_apply_stencil_interface(table.handle, xp, yp, 0, sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = L.bt_launch_count()
+    t_start.record(stream)
+    for q in range(K):
+        step(evs[q])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = L.bt_launch_count() - launches0
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in evs]
+    if ws > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / K
+    value = ws * owned * K / (total_ms * 1e-3) / 1e9
+    kmean = float(np.mean(kern_ms))
+    peak, peak_kind = measured_peaks()
+    alg_bytes = 16.0 * slots  # read x once, write y once
+    achieved = alg_bytes / (kmean * 1e-3) / 1e9
+
+    # e2e through the public API: pinned host x -> device, apply, device y -> pinned host
+    hx = torch.empty(slots, dtype=torch.float64, pin_memory=True)
+    hx.copy_(x.values[LEVEL].cpu())
+    hy = torch.empty(slots, dtype=torch.float64, pin_memory=True)
+    xin = bt.allocate(bt.p1_space(), grid)
+    yout = bt.allocate(bt.p1_space(), grid)
+    e2e_steps = max(3, min(20, K))
+    for _ in range(2):
+        xin.values[LEVEL].copy_(hx, non_blocking=True)
+        bt.apply_stencil(table, xin, yout, LEVEL)
+        hy.copy_(yout.values[LEVEL], non_blocking=True)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        xin.values[LEVEL].copy_(hx, non_blocking=True)
+        bt.apply_stencil(table, xin, yout, LEVEL)
+        hy.copy_(yout.values[LEVEL], non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    assert np.array_equal(hy.numpy(), y.values[LEVEL].cpu().numpy()), "e2e result differs from resident run"
+    e2e_value = ws * owned * e2e_steps / (e2e_ms * 1e-3) / 1e9
+
+    if rank == 0:
+        cpu = cpu_baseline_sample() if ws == 1 and not args.no_cpu else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (random_fill seed 0, reference mt19937_64 stream)",
+            "config": {"workload": WORKLOAD, "level": LEVEL, "cells": 6, "slots": slots, "owned_dofs": owned,
+                       "bc": "none", "l2": "inputs larger than L2 (x+y = %.0f MB)" % (alg_bytes / 1e6),
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "k_stencil",
+                         "kernel_ms": kmean, "kernel_share": kmean / ms_step,
+                         "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs (copy)",
+                         "algorithmic_bytes_per_launch": alg_bytes},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * slots,
+                    "d2h_bytes_per_step": 8 * slots, "steps": e2e_steps},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

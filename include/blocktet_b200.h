@@ -1,0 +1,213 @@
+/* blocktet_b200 — C ABI of the B200-native matrix-free operator path.
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2308.01792's
+ * reference library `blocktet` (header-only C++20, /root/reference/proj).
+ * Every entry point below names the reference interface it replaces
+ * (file:line relative to proj/include/blocktet/). The C++ facade
+ * (include/blocktet_b200.hpp) and the Python mirror
+ * (paper_2308_01792_b200/api.py) both sit on top of exactly these symbols.
+ *
+ * Conventions
+ *  - No C++ or torch types cross the boundary: opaque handles, plain
+ *    pointers, sizes, and a cudaStream_t passed as `void*` (NULL = default
+ *    stream of the handle's device).
+ *  - Vectors are caller-owned DEVICE arrays of double, one array per
+ *    (function, level): cells outer, entries next, lattice slots inner —
+ *    byte-for-byte the layout of FEFunction::values[level][cell][entry]
+ *    (fe_function.hpp:237-261). A P1 vector at level l has
+ *    bt_num_cells(grid) * n_tet(2^l + 1) doubles.
+ *  - Calls are stream-ordered and asynchronous unless they return a host
+ *    scalar (dot, norm2, solver reports), which synchronise the stream.
+ *  - Nothing throws. Failures return a bt_status; bt_last_error() holds the
+ *    message (thread-local). The facades map statuses back to the
+ *    reference's exception types (std::invalid_argument, std::out_of_range,
+ *    std::domain_error, std::logic_error, std::runtime_error).
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point returns BT_CUDA_ERROR.
+ */
+#ifndef BLOCKTET_B200_H
+#define BLOCKTET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BT_OK = 0,
+  BT_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  BT_OUT_OF_RANGE = 2,     /* std::out_of_range */
+  BT_DOMAIN_ERROR = 3,     /* std::domain_error */
+  BT_LOGIC_ERROR = 4,      /* std::logic_error */
+  BT_RUNTIME_ERROR = 5,    /* std::runtime_error (e.g. CG breakdown) */
+  BT_CUDA_ERROR = 6,
+  BT_NCCL_ERROR = 7
+} bt_status;
+
+typedef struct bt_grid bt_grid;           /* Grid (fe_function.hpp:92) */
+typedef struct bt_stencil bt_stencil;     /* StencilTable (operators.hpp:174) */
+typedef struct bt_hierarchy bt_hierarchy; /* GridHierarchy (solvers.hpp:308) */
+typedef struct bt_n1e1 bt_n1e1;           /* N1E1 curl-curl + mass operator (no ref) */
+
+/* Bilinear form descriptor — FormId (forms.hpp:29-41). The reference's
+ * std::function coefficient cannot cross to the device; div_k_grad takes an
+ * analytic coefficient instead (documented API deviation):
+ *   coeff_kind 0: k = c[0]
+ *   coeff_kind 1: k = c[0] + c[1] sin(c[2] x) sin(c[2] y) sin(c[2] z)
+ *   coeff_kind 2: k = c[0] + c[1] x + c[2] y + c[3] z                      */
+typedef enum { BT_FORM_DIFFUSION = 0, BT_FORM_MASS = 1, BT_FORM_DIV_K_GRAD = 2 } bt_form_kind;
+typedef struct {
+  int kind;       /* bt_form_kind */
+  int coeff_kind; /* see above; ignored unless kind == BT_FORM_DIV_K_GRAD */
+  double c[4];
+} bt_form;
+
+typedef enum { BT_BC_NONE = 0, BT_BC_DIRICHLET_IDENTITY = 1 } bt_bc;  /* operators.hpp:17 */
+typedef enum { BT_MODE_REPLACE = 0, BT_MODE_ADD = 1 } bt_apply_mode;  /* operators.hpp:16 */
+typedef enum { BT_SPACE_P1 = 0, BT_SPACE_P2 = 1, BT_SPACE_EDGES = 2 } bt_space;
+
+/* ---- errors / library --------------------------------------------------- */
+const char* bt_last_error(void);
+const char* bt_version(void);
+/* Number of kernel launches issued by this process so far (instrumentation
+ * for bench.py's gpu_launches claim). */
+uint64_t bt_launch_count(void);
+
+/* ---- index algebra (micro_index.hpp:85-165, host side) ------------------ */
+int64_t bt_n_tri(int64_t w);                                /* :85 */
+int64_t bt_n_tet(int64_t w);                                /* :89 */
+int bt_width_formula(int subgroup, int level);              /* :97 */
+bt_status bt_width(int subgroup, int level, int* out);      /* :125 (domain_error if absent) */
+int64_t bt_linearize(int w, int i, int j, int k);           /* :145 */
+bt_status bt_delinearize(int w, int64_t t, int* ijk3);      /* :157 */
+int bt_subgroup_offsets(int subgroup, int* out_xyz);        /* :257, returns arity */
+
+/* ---- grid (Grid ctor fe_function.hpp:106-115 over parse_mesh
+ *      coarse_mesh.hpp:225) ------------------------------------------------ */
+/* Parses the reference mesh text format, builds the implicit interface
+ * tables for levels [min_level, max_level] on CUDA device `device`.
+ * Levels 2..10 (the reference caps at 6, fe_function.hpp:108). */
+bt_status bt_grid_create(const char* mesh_text, int min_level, int max_level, int device,
+                         bt_grid** out);
+void bt_grid_destroy(bt_grid* g);
+int bt_num_cells(const bt_grid* g);
+int bt_grid_min_level(const bt_grid* g);
+int bt_grid_max_level(const bt_grid* g);
+/* doubles in one level of a function of `space` (all cells) */
+int64_t bt_space_size(const bt_grid* g, int space, int level);
+/* owned_dof_count (fe_function.hpp:550) */
+int64_t bt_owned_dof_count(const bt_grid* g, int space, int level);
+/* Grid::masks (fe_function.hpp:128): host copies, n_tet(width) bytes each */
+bt_status bt_grid_masks(const bt_grid* g, int level, int cell, int subgroup, uint8_t* owned,
+                        uint8_t* dirichlet);
+/* Grid::groups (fe_function.hpp:123) expanded from the implicit tables, for
+ * tests: pass NULL arrays to query sizes. Members are sorted (cell, g, t). */
+bt_status bt_grid_groups(const bt_grid* g, int level, int space, int64_t* n_groups,
+                         int64_t* n_members, int64_t* offsets, int32_t* cell, int32_t* subgroup,
+                         int64_t* t);
+/* builder mesh generator for configs 2-5: n^3 unit cubes x 6 Kuhn tets,
+ * interior vertices perturbed by U(-perturb h, perturb h) per component from
+ * mt19937_64(seed). Writes at most buflen bytes; returns bytes needed. */
+int64_t bt_cubes_mesh_text(int n, double perturb, uint64_t seed, char* buf, int64_t buflen);
+
+/* ---- vectors (fe_function.hpp:324-497, solvers.hpp:53-72) ---------------- */
+/* random_fill (fe_function.hpp:479): mt19937_64 on the host in canonical
+ * owned order, uploaded, replicas broadcast on the device. */
+bt_status bt_random_fill(const bt_grid* g, int space, int level, uint64_t seed, double* x,
+                         void* stream);
+bt_status bt_assign(const bt_grid* g, int space, int level, double* x, double value, void* stream);
+bt_status bt_scale(const bt_grid* g, int space, int level, double* x, double s, void* stream);
+bt_status bt_copy(const bt_grid* g, int space, int level, const double* src, double* dst,
+                  void* stream);
+bt_status bt_axpy(const bt_grid* g, int space, int level, double* y, double a, const double* x,
+                  void* stream);
+/* owned-DoF dot (fe_function.hpp:376): fixed-order, GPU-count invariant */
+bt_status bt_dot(const bt_grid* g, int space, int level, const double* x, const double* y,
+                 double* out, void* stream);
+bt_status bt_hadamard(const bt_grid* g, int level, double* x, const double* d, int divide,
+                      void* stream);
+bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, void* stream);  /* :400 */
+bt_status bt_sync_broadcast(const bt_grid* g, int space, int level, double* x, void* stream); /* :425 */
+bt_status bt_impose_dirichlet(const bt_grid* g, int level, const double* src, double* dst,
+                              void* stream);                          /* operators.hpp:98 */
+bt_status bt_zero_dirichlet(const bt_grid* g, int level, double* x, void* stream); /* solvers.hpp:66 */
+
+/* ---- P1 operators (operators.hpp) -------------------------------------- */
+/* compute_stencil (operators.hpp:183): merged 15-point row, class matrices,
+ * typed lattice-boundary rows and the assembled diagonal (device). */
+bt_status bt_stencil_create(const bt_grid* g, const bt_form* form, int level, bt_stencil** out);
+void bt_stencil_destroy(bt_stencil* s);
+/* StencilTable::rows / diagonal (host copies) */
+bt_status bt_stencil_rows(const bt_stencil* s, double* rows15xcells);
+bt_status bt_stencil_diagonal(const bt_stencil* s, double* diag, void* stream);
+/* apply_stencil (operators.hpp:247): y = A x, interface sync, Dirichlet rows */
+bt_status bt_apply_stencil(const bt_stencil* s, const double* x, double* y, int bc, void* stream);
+/* The two phases of bt_apply_stencil, exposed for overlap and measurement:
+ * (1) per-cell rows — merged 15-point rows on interior vertices, per-cell
+ *     partial rows on lattice-boundary vertices (operators.hpp:255-268);
+ * (2) the interface pass — replica sums over macro faces/edges/vertices
+ *     (sync_additive fe_function.hpp:400) and Dirichlet identity rows. */
+bt_status bt_apply_stencil_cells(const bt_stencil* s, const double* x, double* y, void* stream);
+bt_status bt_apply_stencil_interface(const bt_stencil* s, const double* x, double* y, int bc,
+                                     void* stream);
+/* apply_elementwise (operators.hpp:115): on-the-fly element integration
+ * (4-point rule for k, forms.hpp:107-118), sync, Dirichlet rows.
+ * ADD mode needs a scratch level array (NULL: allocated internally). */
+bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level, const double* x,
+                               double* y, int mode, int bc, double* scratch, void* stream);
+/* extract_diagonal (operators.hpp:277) */
+bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, double* diag,
+                              void* stream);
+
+/* ---- transfers (solvers.hpp:227-293) ------------------------------------ */
+/* prolongate_p1; add != 0 fuses v_cycle's axpy(x, 1, ef) (solvers.hpp:536-538) */
+bt_status bt_prolongate(const bt_grid* g, int fine_level, const double* coarse, double* fine,
+                        int add, void* stream);
+/* restrict_p1 (includes the coarse sync_additive) */
+bt_status bt_restrict(const bt_grid* g, int fine_level, const double* fine, double* coarse,
+                      void* stream);
+
+/* ---- hierarchy / smoothers / multigrid (solvers.hpp:308-541) ------------ */
+typedef struct {     /* SmootherConfig (solvers.hpp:379) */
+  int kind;          /* 0 jacobi, 1 gauss-seidel, 2 chebyshev */
+  double omega;
+  int order;
+  double lo, hi;
+  int nu1, nu2;
+} bt_smoother_config;
+typedef struct {     /* MultigridConfig (solvers.hpp:498) */
+  int coarse_level;
+  int cycles;
+  double coarse_tol;
+  int coarse_maxit;
+} bt_multigrid_config;
+/* make_hierarchy (solvers.hpp:323); kernel: 0 elementwise, 1 stencil */
+bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
+                              bt_hierarchy** out);
+void bt_hierarchy_destroy(bt_hierarchy* h);
+bt_status bt_hierarchy_apply(bt_hierarchy* h, int level, const double* x, double* y, int bc,
+                             void* stream);                            /* :352 */
+bt_status bt_hierarchy_diagonal(bt_hierarchy* h, int level, const double** diag);
+bt_status bt_estimate_lambda_max(bt_hierarchy* h, int level, double* out, void* stream); /* :362 */
+bt_status bt_smooth(bt_hierarchy* h, const bt_smoother_config* cfg, const double* rhs, double* x,
+                    int level, int sweeps, int backward, void* stream);  /* :460 */
+/* cg (solvers.hpp:84) through hierarchy_apply with Dirichlet rows;
+ * hist[0..maxit-1] receives relative residuals (may be NULL). */
+bt_status bt_cg(bt_hierarchy* h, int level, double tol, int maxit, const double* rhs, double* x,
+                double* hist, int* iterations, void* stream);
+bt_status bt_v_cycle(bt_hierarchy* h, int level, const double* rhs, double* x,
+                     const bt_smoother_config* sm, const bt_multigrid_config* mg,
+                     void* stream);                                     /* :509 */
+
+/* ---- N1E1 curl-curl + mass (no reference implementation) ----- */
+bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta, bt_n1e1** out);
+void bt_n1e1_destroy(bt_n1e1* op);
+bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, void* stream);
+bt_status bt_n1e1_sync(const bt_grid* g, int level, double* x, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,690 @@
+"""Python mirror of the reference `blocktet` API for the hot path.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/blocktet/*.hpp) so parity tests read like the
+reference's own tests. Storage is device-resident: ``FEFunction.values[l]``
+is a CUDA float64 tensor holding FEFunction::values[l][cell][entry]
+flattened (cells outer, slots inner). Everything goes through the C ABI in
+include/blocktet_b200.h; torch provides device memory and the stream.
+
+Reference exception types map to:
+  std::invalid_argument -> InvalidArgument (ValueError)
+  std::out_of_range     -> OutOfRange (IndexError)
+  std::domain_error     -> DomainError (ArithmeticError)
+  std::logic_error      -> LogicError (RuntimeError)
+  std::runtime_error    -> SolverError (RuntimeError)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import bt_form, bt_multigrid_config, bt_smoother_config
+
+_L = _lib.lib
+
+
+class InvalidArgument(ValueError):
+    pass
+
+
+class OutOfRange(IndexError):
+    pass
+
+
+class DomainError(ArithmeticError):
+    pass
+
+
+class LogicError(RuntimeError):
+    pass
+
+
+class SolverError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERR = {1: InvalidArgument, 2: OutOfRange, 3: DomainError, 4: LogicError, 5: SolverError, 6: CudaError,
+        7: CudaError}
+
+
+def _check(status: int):
+    if status:
+        raise _ERR.get(status, RuntimeError)(_L.bt_last_error().decode())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+        raise InvalidArgument("expected a contiguous CUDA float64 tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------------------
+# micro_index.hpp
+# ---------------------------------------------------------------------------
+class Subgroup(enum.IntEnum):
+    V = 0
+    EdgeX = 1
+    EdgeY = 2
+    EdgeZ = 3
+    EdgeXY = 4
+    EdgeXZ = 5
+    EdgeYZ = 6
+    EdgeXYZ = 7
+    CellIUp = 20
+    CellIDown = 21
+    CellIIUp = 22
+    CellIIDown = 23
+    CellIIIUp = 24
+    CellIIIDown = 25
+
+
+def n_tri(w):
+    return _L.bt_n_tri(w)
+
+
+def n_tet(w):
+    return _L.bt_n_tet(w)
+
+
+def width_formula(g, level):
+    return _L.bt_width_formula(int(g), level)
+
+
+def width(g, level):
+    out = C.c_int()
+    _check(_L.bt_width(int(g), level, C.byref(out)))
+    return out.value
+
+
+def linearize(w, p):
+    return _L.bt_linearize(w, p[0], p[1], p[2])
+
+
+def linearize_checked(w, p):
+    i, j, k = p
+    if not (i >= 0 and j >= 0 and k >= 0 and i + j + k < w):
+        raise OutOfRange("linearize: index outside I_tet(w)")
+    return linearize(w, p)
+
+
+def delinearize(w, t):
+    out = (C.c_int * 3)()
+    _check(_L.bt_delinearize(w, t, out))
+    return (out[0], out[1], out[2])
+
+
+def subgroup_offsets(g):
+    out = (C.c_int * 12)()
+    n = _L.bt_subgroup_offsets(int(g), out)
+    return [tuple(out[3 * i: 3 * i + 3]) for i in range(n)]
+
+
+def index_set(w):
+    return [(i, j, k) for k in range(w) for j in range(w - k) for i in range(w - k - j)]
+
+
+# ---------------------------------------------------------------------------
+# spaces / grid / functions (fe_function.hpp)
+# ---------------------------------------------------------------------------
+class LayoutKind(enum.IntEnum):
+    AoS = 0
+    SoA = 1
+
+
+@dataclass(frozen=True)
+class SpaceDescriptor:
+    name: str
+    space: int  # bt_space
+    layout: LayoutKind = LayoutKind.AoS
+
+
+def p1_space(layout=LayoutKind.AoS):
+    return SpaceDescriptor("p1", 0, layout)
+
+
+def edge_space(layout=LayoutKind.AoS):
+    """The seven edge subgroups (N1E1 storage)."""
+    return SpaceDescriptor("edges", 2, layout)
+
+
+class Grid:
+    """Grid (fe_function.hpp:92): mesh + per-level interface identification,
+    held as implicit macro face/edge/vertex tables on the device."""
+
+    def __init__(self, mesh_text: str, min_level: int, max_level: int, device: Optional[int] = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        torch.cuda.init()
+        h = C.c_void_p()
+        _check(_L.bt_grid_create(mesh_text.encode(), min_level, max_level, device, C.byref(h)))
+        self._h = h
+        self.mesh_text = mesh_text
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _L.bt_grid_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def n_cells(self):
+        return _L.bt_num_cells(self._h)
+
+    def min_level(self):
+        return _L.bt_grid_min_level(self._h)
+
+    def max_level(self):
+        return _L.bt_grid_max_level(self._h)
+
+    def has_level(self, l):
+        return self.min_level() <= l <= self.max_level()
+
+    def space_size(self, space: int, level: int) -> int:
+        return _L.bt_space_size(self._h, space, level)
+
+    def masks(self, level, cell, g):
+        n = n_tet(width_formula(g, level))
+        o = np.zeros(n, np.uint8)
+        d = np.zeros(n, np.uint8)
+        _check(_L.bt_grid_masks(self._h, level, cell, int(g), o.ctypes.data_as(_lib.PU8),
+                                d.ctypes.data_as(_lib.PU8)))
+        return o, d
+
+    def groups(self, level, space=0):
+        ng, nm = C.c_int64(), C.c_int64()
+        _check(_L.bt_grid_groups(self._h, level, space, C.byref(ng), C.byref(nm), None, None, None, None))
+        off = np.zeros(ng.value + 1, np.int64)
+        cell = np.zeros(nm.value, np.int32)
+        g = np.zeros(nm.value, np.int32)
+        t = np.zeros(nm.value, np.int64)
+        _check(_L.bt_grid_groups(self._h, level, space, C.byref(ng), C.byref(nm),
+                                 off.ctypes.data_as(_lib.PI64), cell.ctypes.data_as(_lib.PI32),
+                                 g.ctypes.data_as(_lib.PI32), t.ctypes.data_as(_lib.PI64)))
+        return off, cell, g, t
+
+
+def cubes_mesh_text(n: int, perturb: float = 0.1, seed: int = 0) -> str:
+    need = _L.bt_cubes_mesh_text(n, perturb, seed, None, 0)
+    buf = C.create_string_buffer(need + 1)
+    _L.bt_cubes_mesh_text(n, perturb, seed, buf, need + 1)
+    return buf.value.decode()
+
+
+def ref_tet_text():
+    return "# reference tetrahedron\nvertices 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ncells 1\n0 1 2 3\n"
+
+
+def cube_kuhn_text():
+    """coarse_mesh.hpp:344-368: unit cube, six tets around the (0,0,0)-(1,1,1) diagonal."""
+    lines = ["# unit cube, six tetrahedra around the main diagonal", "vertices 8"]
+    corner = []
+    for vid in range(8):
+        c = (vid & 1, (vid >> 1) & 1, (vid >> 2) & 1)
+        corner.append(c)
+        lines.append(f"{c[0]} {c[1]} {c[2]}")
+    lines.append("cells 6")
+    for axes in ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)):
+        c = [0, 0, 0, 7]
+        c[1] = 1 << axes[0]
+        c[2] = c[1] | (1 << axes[1])
+        v0 = np.array(corner[c[0]], float)
+        u, w, z = (np.array(corner[c[k]], float) - v0 for k in (1, 2, 3))
+        if np.dot(u, np.cross(w, z)) < 0:
+            c[2], c[3] = c[3], c[2]
+        lines.append(" ".join(map(str, c)))
+    return "\n".join(lines) + "\n"
+
+
+@dataclass
+class FEFunction:
+    grid: Grid
+    descriptor: SpaceDescriptor
+    min_level: int
+    max_level: int
+    values: Dict[int, torch.Tensor] = field(default_factory=dict)
+
+    def check_level(self, l):
+        if l < self.min_level or l > self.max_level:
+            raise OutOfRange("level not allocated")
+        return l - self.min_level
+
+    def level(self, l) -> torch.Tensor:
+        self.check_level(l)
+        return self.values[l]
+
+    def slots_of(self, l):
+        return self.grid.space_size(self.descriptor.space, l) // self.grid.n_cells()
+
+    def array(self, l, cell):
+        n = self.slots_of(l)
+        return self.values[l][cell * n:(cell + 1) * n]
+
+    def host(self, l) -> np.ndarray:
+        return self.values[l].cpu().numpy()
+
+    def at(self, l, cell, entry, t, d=0):
+        return float(self.array(l, cell)[t].item())
+
+
+def allocate(descriptor: SpaceDescriptor, grid: Grid, min_level: int = -1, max_level: int = -1) -> FEFunction:
+    if grid is None:
+        raise InvalidArgument("allocate: grid required")
+    if min_level < 0:
+        min_level = grid.min_level()
+    if max_level < 0:
+        max_level = grid.max_level()
+    if not grid.has_level(min_level) or not grid.has_level(max_level) or min_level > max_level:
+        raise OutOfRange("allocate: levels outside grid range")
+    dev = torch.device("cuda", grid.device)
+    vals = {l: torch.zeros(grid.space_size(descriptor.space, l), dtype=torch.float64, device=dev)
+            for l in range(min_level, max_level + 1)}
+    return FEFunction(grid, descriptor, min_level, max_level, vals)
+
+
+def _compatible(a: FEFunction, b: FEFunction, l):
+    if a.grid is not b.grid:
+        raise InvalidArgument("functions live on different grids")
+    if a.descriptor.space != b.descriptor.space:
+        raise InvalidArgument("descriptor mismatch")
+    a.check_level(l)
+    b.check_level(l)
+
+
+def assign(fn: FEFunction, l, value):
+    fn.check_level(l)
+    _check(_L.bt_assign(fn.grid.handle, fn.descriptor.space, l, _ptr(fn.values[l]), float(value), _stream()))
+
+
+def scale(fn: FEFunction, l, s):
+    fn.check_level(l)
+    _check(_L.bt_scale(fn.grid.handle, fn.descriptor.space, l, _ptr(fn.values[l]), float(s), _stream()))
+
+
+def copy(src: FEFunction, dst: FEFunction, l):
+    _compatible(src, dst, l)
+    _check(_L.bt_copy(src.grid.handle, src.descriptor.space, l, _ptr(src.values[l]), _ptr(dst.values[l]),
+                      _stream()))
+
+
+def axpy(y: FEFunction, a, x: FEFunction, l):
+    _compatible(x, y, l)
+    _check(_L.bt_axpy(y.grid.handle, y.descriptor.space, l, _ptr(y.values[l]), float(a), _ptr(x.values[l]),
+                      _stream()))
+
+
+def dot(x: FEFunction, y: FEFunction, l) -> float:
+    _compatible(x, y, l)
+    out = C.c_double()
+    _check(_L.bt_dot(x.grid.handle, x.descriptor.space, l, _ptr(x.values[l]), _ptr(y.values[l]), C.byref(out),
+                     _stream()))
+    return out.value
+
+
+def norm2(x: FEFunction, l) -> float:
+    return math.sqrt(dot(x, x, l))
+
+
+def sync_additive(fn: FEFunction, l):
+    fn.check_level(l)
+    if fn.descriptor.space == 2:
+        _check(_L.bt_n1e1_sync(fn.grid.handle, l, _ptr(fn.values[l]), _stream()))
+        return
+    _check(_L.bt_sync_additive(fn.grid.handle, fn.descriptor.space, l, _ptr(fn.values[l]), _stream()))
+
+
+def sync_broadcast(fn: FEFunction, l):
+    fn.check_level(l)
+    _check(_L.bt_sync_broadcast(fn.grid.handle, fn.descriptor.space, l, _ptr(fn.values[l]), _stream()))
+
+
+def random_fill(fn: FEFunction, l, seed):
+    fn.check_level(l)
+    _check(_L.bt_random_fill(fn.grid.handle, fn.descriptor.space, l, int(seed), _ptr(fn.values[l]), _stream()))
+
+
+def zero_dirichlet(fn: FEFunction, l):
+    """detail::zero_dirichlet (solvers.hpp:66)."""
+    _check(_L.bt_zero_dirichlet(fn.grid.handle, l, _ptr(fn.values[l]), _stream()))
+
+
+def impose_dirichlet(src: FEFunction, dst: FEFunction, l):
+    """detail::impose_dirichlet (operators.hpp:98)."""
+    _check(_L.bt_impose_dirichlet(dst.grid.handle, l, _ptr(src.values[l]), _ptr(dst.values[l]), _stream()))
+
+
+def hadamard(fn: FEFunction, diag: FEFunction, l, divide: bool):
+    _check(_L.bt_hadamard(fn.grid.handle, l, _ptr(fn.values[l]), _ptr(diag.values[l]), int(divide), _stream()))
+
+
+def owned_dof_count(fn: FEFunction, l):
+    fn.check_level(l)
+    return _L.bt_owned_dof_count(fn.grid.handle, fn.descriptor.space, l)
+
+
+# ---------------------------------------------------------------------------
+# forms / operators (forms.hpp, operators.hpp)
+# ---------------------------------------------------------------------------
+class FormKind(enum.IntEnum):
+    Diffusion = 0
+    Mass = 1
+    DivKGrad = 2
+
+
+@dataclass(frozen=True)
+class Coefficient:
+    """Device-evaluable replacement of FormId's std::function coefficient
+    (forms.hpp:31): kind 0 constant, 1 sin product, 2 affine."""
+    kind: int
+    c: tuple
+
+    @staticmethod
+    def constant(c0):
+        return Coefficient(0, (float(c0), 0.0, 0.0, 0.0))
+
+    @staticmethod
+    def sin_product(c0=1.0, c1=0.5, freq=2.0 * math.pi):
+        return Coefficient(1, (float(c0), float(c1), float(freq), 0.0))
+
+    @staticmethod
+    def affine(c0, cx, cy, cz):
+        return Coefficient(2, (float(c0), float(cx), float(cy), float(cz)))
+
+
+@dataclass(frozen=True)
+class FormId:
+    kind: FormKind = FormKind.Diffusion
+    k: Optional[Coefficient] = None
+
+    @staticmethod
+    def diffusion():
+        return FormId(FormKind.Diffusion)
+
+    @staticmethod
+    def mass():
+        return FormId(FormKind.Mass)
+
+    @staticmethod
+    def div_k_grad(coeff: Coefficient):
+        if coeff is None:
+            raise InvalidArgument("div_k_grad needs a coefficient")
+        return FormId(FormKind.DivKGrad, coeff)
+
+    def constant_coefficient(self):
+        return self.kind != FormKind.DivKGrad
+
+    def c_struct(self):
+        f = bt_form()
+        f.kind = int(self.kind)
+        f.coeff_kind = self.k.kind if self.k else 0
+        for i, v in enumerate(self.k.c if self.k else (0.0, 0.0, 0.0, 0.0)):
+            f.c[i] = v
+        return f
+
+
+class ApplyMode(enum.IntEnum):
+    Replace = 0
+    Add = 1
+
+
+class BC(enum.IntEnum):
+    None_ = 0
+    DirichletIdentity = 1
+
+
+class SweepDirection(enum.IntEnum):
+    Forward = 0
+    Backward = 1
+
+
+def _require_pair(src: FEFunction, dst: FEFunction, l):
+    if src.descriptor.space != 0 or dst.descriptor.space != 0:
+        raise InvalidArgument("operator kernels require a P1 function")
+    _compatible(src, dst, l)
+    if src is dst:
+        raise InvalidArgument("source and destination must be distinct")
+
+
+class StencilTable:
+    """StencilTable (operators.hpp:174): per-cell merged rows, typed
+    lattice-boundary rows and the assembled diagonal, device-resident."""
+
+    def __init__(self, form: FormId, grid: Grid, level: int):
+        self.grid = grid
+        self.form = form.kind
+        self.level = level
+        h = C.c_void_p()
+        f = form.c_struct()
+        _check(_L.bt_stencil_create(grid.handle, C.byref(f), level, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _L.bt_stencil_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def rows(self) -> np.ndarray:
+        out = np.zeros(15 * self.grid.n_cells())
+        _check(_L.bt_stencil_rows(self._h, out.ctypes.data_as(_lib.PD)))
+        return out.reshape(-1, 15)
+
+    def diagonal(self) -> torch.Tensor:
+        d = torch.zeros(self.grid.space_size(0, self.level), dtype=torch.float64,
+                        device=torch.device("cuda", self.grid.device))
+        _check(_L.bt_stencil_diagonal(self._h, _ptr(d), _stream()))
+        return d
+
+
+def compute_stencil(form: FormId, grid: Grid, l: int) -> StencilTable:
+    if not form.constant_coefficient():
+        raise InvalidArgument("compute_stencil: variable-coefficient forms are unsupported")
+    if grid is None:
+        raise InvalidArgument("compute_stencil: grid required")
+    return StencilTable(form, grid, l)
+
+
+def apply_stencil(table: StencilTable, src: FEFunction, dst: FEFunction, l, bc=BC.None_, threads=1):
+    _require_pair(src, dst, l)
+    if table.level != l or table.grid is not src.grid:
+        raise InvalidArgument("apply_stencil: table/grid mismatch")
+    _check(_L.bt_apply_stencil(table.handle, _ptr(src.values[l]), _ptr(dst.values[l]), int(bc), _stream()))
+
+
+def apply_elementwise(form: FormId, src: FEFunction, dst: FEFunction, l, mode=ApplyMode.Replace, bc=BC.None_,
+                      threads=1):
+    _require_pair(src, dst, l)
+    f = form.c_struct()
+    _check(_L.bt_apply_elementwise(src.grid.handle, C.byref(f), l, _ptr(src.values[l]), _ptr(dst.values[l]),
+                                   int(mode), int(bc), None, _stream()))
+
+
+def extract_diagonal(form_or_table, diag: FEFunction, l, threads=1):
+    if isinstance(form_or_table, StencilTable):
+        t = form_or_table
+        if t.level != l or t.grid is not diag.grid:
+            raise InvalidArgument("extract_diagonal: table/grid mismatch")
+        _check(_L.bt_stencil_diagonal(t.handle, _ptr(diag.values[l]), _stream()))
+        return
+    f = form_or_table.c_struct()
+    _check(_L.bt_extract_diagonal(diag.grid.handle, C.byref(f), l, _ptr(diag.values[l]), _stream()))
+
+
+# ---------------------------------------------------------------------------
+# transfers and multigrid (solvers.hpp)
+# ---------------------------------------------------------------------------
+def _check_transfer(coarse: FEFunction, fine: FEFunction, fine_l):
+    if coarse.grid is not fine.grid:
+        raise InvalidArgument("transfer: functions live on different grids")
+    fine.check_level(fine_l)
+    coarse.check_level(fine_l - 1)
+
+
+def prolongate_p1(coarse: FEFunction, fine: FEFunction, fine_l, add=False):
+    _check_transfer(coarse, fine, fine_l)
+    _check(_L.bt_prolongate(fine.grid.handle, fine_l, _ptr(coarse.values[fine_l - 1]), _ptr(fine.values[fine_l]),
+                            int(add), _stream()))
+
+
+def restrict_p1(fine: FEFunction, coarse: FEFunction, fine_l):
+    _check_transfer(coarse, fine, fine_l)
+    _check(_L.bt_restrict(fine.grid.handle, fine_l, _ptr(fine.values[fine_l]), _ptr(coarse.values[fine_l - 1]),
+                          _stream()))
+
+
+class KernelKind(enum.IntEnum):
+    Elementwise = 0
+    Stencil = 1
+
+
+class SmootherKind(enum.IntEnum):
+    Jacobi = 0
+    GaussSeidel = 1
+    Chebyshev = 2
+
+
+@dataclass
+class SmootherConfig:
+    kind: SmootherKind = SmootherKind.GaussSeidel
+    omega: float = 0.8
+    order: int = 2
+    lo: float = 0.25
+    hi: float = 1.1
+    nu1: int = 1
+    nu2: int = 1
+
+    @staticmethod
+    def gauss_seidel():
+        return SmootherConfig()
+
+    @staticmethod
+    def jacobi(omega=0.8):
+        return SmootherConfig(kind=SmootherKind.Jacobi, omega=omega)
+
+    @staticmethod
+    def chebyshev(order=2):
+        return SmootherConfig(kind=SmootherKind.Chebyshev, order=order)
+
+    def c_struct(self):
+        return bt_smoother_config(int(self.kind), self.omega, self.order, self.lo, self.hi, self.nu1, self.nu2)
+
+    def as_array(self):
+        return [int(self.kind), self.omega, self.order, self.lo, self.hi, self.nu1, self.nu2]
+
+
+@dataclass
+class MultigridConfig:
+    coarse_level: int = 2
+    cycles: int = 5
+    coarse_tol: float = 1e-12
+    coarse_maxit: int = 4000
+
+    def c_struct(self):
+        return bt_multigrid_config(self.coarse_level, self.cycles, self.coarse_tol, self.coarse_maxit)
+
+
+class GridHierarchy:
+    """GridHierarchy (solvers.hpp:308) on the device: per-level operator
+    tables, assembled diagonals, lazy spectral estimates, work vectors."""
+
+    def __init__(self, grid: Grid, form: FormId, kernel=KernelKind.Stencil, threads=1):
+        self.grid = grid
+        self.form = form
+        self.kernel = kernel
+        h = C.c_void_p()
+        f = form.c_struct()
+        _check(_L.bt_hierarchy_create(grid.handle, C.byref(f), int(kernel), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _L.bt_hierarchy_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def diagonal(self, l) -> torch.Tensor:
+        p = C.c_void_p()
+        _check(_L.bt_hierarchy_diagonal(self._h, l, C.byref(p)))
+        tmp = allocate(p1_space(), self.grid, l, l)
+        _check(_L.bt_copy(self.grid.handle, 0, l, p, _ptr(tmp.values[l]), _stream()))
+        return tmp.values[l]
+
+
+def make_hierarchy(grid: Grid, form: FormId, kernel=KernelKind.Stencil, threads=1) -> GridHierarchy:
+    if grid is None:
+        raise InvalidArgument("make_hierarchy: grid required")
+    if kernel == KernelKind.Stencil and not form.constant_coefficient():
+        raise InvalidArgument("stencil kernel requires a constant-coefficient form")
+    return GridHierarchy(grid, form, kernel, threads)
+
+
+def hierarchy_apply(h: GridHierarchy, x: FEFunction, y: FEFunction, l, bc=BC.DirichletIdentity):
+    _check(_L.bt_hierarchy_apply(h.handle, l, _ptr(x.values[l]), _ptr(y.values[l]), int(bc), _stream()))
+
+
+def spectral_estimate(h: GridHierarchy, l) -> float:
+    out = C.c_double()
+    _check(_L.bt_estimate_lambda_max(h.handle, l, C.byref(out), _stream()))
+    return out.value
+
+
+def smooth(h: GridHierarchy, cfg: SmootherConfig, rhs: FEFunction, x: FEFunction, l, sweeps,
+           direction=SweepDirection.Forward):
+    c = cfg.c_struct()
+    _check(_L.bt_smooth(h.handle, C.byref(c), _ptr(rhs.values[l]), _ptr(x.values[l]), l, sweeps, int(direction),
+                        _stream()))
+
+
+@dataclass
+class IterationReport:
+    residuals: List[float]
+    iterations: int
+    residual: float
+    converged: bool
+
+
+def cg(h: GridHierarchy, rhs: FEFunction, x: FEFunction, l, tol, maxit) -> IterationReport:
+    """cg (solvers.hpp:84) with hierarchy_apply(.., DirichletIdentity) as the
+    operator (the reference's std::function operator argument cannot cross
+    the C ABI; every reference caller passes this operator)."""
+    hist = np.zeros(max(maxit, 1))
+    it = C.c_int()
+    _check(_L.bt_cg(h.handle, l, tol, maxit, _ptr(rhs.values[l]), _ptr(x.values[l]),
+                    hist.ctypes.data_as(_lib.PD), C.byref(it), _stream()))
+    res = list(hist[: it.value])
+    r = res[-1] if res else 0.0
+    return IterationReport(res, it.value, r, bool(res) and r <= tol)
+
+
+def v_cycle(h: GridHierarchy, l, rhs: FEFunction, x: FEFunction, sm: SmootherConfig, mg: MultigridConfig):
+    s = sm.c_struct()
+    m = mg.c_struct()
+    _check(_L.bt_v_cycle(h.handle, l, _ptr(rhs.values[l]), _ptr(x.values[l]), C.byref(s), C.byref(m), _stream()))

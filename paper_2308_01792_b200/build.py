@@ -1,0 +1,77 @@
+"""In-tree build of libbt_b200.so (CUDA sm_100a kernels + C++ host + C ABI).
+
+nvcc compiles the .cu translation units for sm_100a only; the host .cpp
+units are compiled by g++ without -march so the host-side setup arithmetic
+(element matrices, stencil rows) keeps the reference's FMA-free rounding.
+Run: python -m paper_2308_01792_b200.build  (or __graft_entry__.build()).
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT = os.path.join(PKG, "libbt_b200.so")
+OBJ = os.path.join(PKG, "build")
+
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+            "-Xptxas", "-v"]
+CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-fno-fast-math", "-ffp-contract=off",
+             f"-I{CUDA_HOME}/include"]
+
+CU_SOURCES = ["bt_kernels.cu", "bt_n1e1.cu"]
+CXX_SOURCES = ["bt_host.cpp", "bt_solvers.cpp"]
+
+
+def _deps():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(ROOT, "include", "blocktet_b200.h")]
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources if os.path.exists(s))
+
+
+def _run(cmd, log):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    log.write(" ".join(cmd) + "\n" + r.stdout + r.stderr + "\n")
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ...")
+
+
+def build(force: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    deps = _deps()
+    objs = []
+    with open(os.path.join(OBJ, "build.log"), "w") as log:
+        for src in CU_SOURCES:
+            o = os.path.join(OBJ, src + ".o")
+            if force or _stale(o, deps):
+                _run([NVCC, *ARCH, *CU_FLAGS, "-c", os.path.join(CSRC, src), "-o", o], log)
+            objs.append(o)
+        for src in CXX_SOURCES:
+            o = os.path.join(OBJ, src + ".o")
+            if force or _stale(o, deps):
+                _run([CXX, *CXX_FLAGS, "-c", os.path.join(CSRC, src), "-o", o], log)
+            objs.append(o)
+        if force or _stale(OUT, objs):
+            _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart_static", "-lrt", "-lpthread", "-ldl"], log)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv))
+    if shutil.which("cuobjdump"):
+        pass

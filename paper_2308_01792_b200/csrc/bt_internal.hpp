@@ -1,0 +1,203 @@
+// Internal structures of the blocktet_b200 library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/blocktet_b200.h"
+#include "bt_index.cuh"
+
+namespace bt {
+
+// ---------------------------------------------------------------------------
+// errors: exceptions inside, statuses at the C boundary
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  bt_status status;
+  Error(bt_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void raise(bt_status s, const std::string& m) { throw Error(s, m); }
+void set_error(const std::string& m);
+
+#define BT_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      ::bt::raise(BT_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+extern uint64_t g_launches;
+inline void count_launch(int n = 1) { g_launches += (uint64_t)n; }
+void check_launch(const char* what);
+
+// Device buffer owned by the library.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) BT_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  }
+  void upload(const std::vector<T>& h) {
+    alloc(h.size());
+    if (n) BT_CUDA(cudaMemcpy(p, h.data(), sizeof(T) * n, cudaMemcpyHostToDevice));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// ---------------------------------------------------------------------------
+// macro mesh (coarse_mesh.hpp) and implicit interface tables
+// ---------------------------------------------------------------------------
+struct Mesh {
+  std::vector<std::array<double, 3>> coords;
+  std::vector<std::array<int, 4>> cells;        // after orientation repair
+  std::vector<std::array<int, 3>> faces;        // sorted triples, lexicographic
+  std::vector<std::array<int, 2>> face_cells;   // ascending, -1 if none
+  std::vector<char> bflags;
+  std::vector<std::array<int, 2>> edges;        // sorted pairs, lexicographic
+  int warnings = 0;
+  int n_cells() const { return (int)cells.size(); }
+};
+Mesh parse_mesh(const std::string& text);
+
+// Affine map x = A r + b of a macro-cell (coarse_mesh.hpp:84-105).
+struct CellMap {
+  double a[9];  // row-major
+  double b[3];
+};
+
+// Device-side interface records. Global face vertices / edge endpoints are
+// sorted ascending; lv maps them to the local vertex index in each cell.
+struct DevFace {
+  int ncell;
+  int cell[2];
+  int8_t lv[2][3];
+  uint8_t dir;
+};
+struct DevPrimHdr {  // macro edge or vertex
+  int first, count;
+  uint8_t dir;
+};
+struct DevPrimMem {
+  int cell;
+  int8_t lv[2];  // edge: local indices of (e0, e1); vertex: lv[0]
+};
+// Per-cell bits indexed by the zero set Z (bt::zero_set).
+struct DevCellInfo {
+  uint16_t owned_by_z;
+  uint16_t dir_by_z;
+};
+
+struct Topology {
+  // incidence (cells ascending)
+  std::vector<std::vector<int>> edge_cells, vert_cells;
+  std::vector<std::array<int, 4>> cell_faces;  // local face v -> global face
+  std::vector<std::array<int, 6>> cell_edges;  // local edge (a<b) -> global edge
+  std::vector<char> edge_dir, vert_dir;
+  std::vector<DevCellInfo> info;               // per cell
+  std::vector<CellMap> maps;
+  // flattened device tables
+  std::vector<DevFace> faces;
+  std::vector<DevPrimHdr> ehdr, vhdr;
+  std::vector<DevPrimMem> emem, vmem;
+};
+
+// local edge index of local vertices (a, b), a < b: (0,1)(0,2)(0,3)(1,2)(1,3)(2,3)
+inline int local_edge(int a, int b) {
+  if (a > b) std::swap(a, b);
+  static const int tbl[4][4] = {{-1, 0, 1, 2}, {0, -1, 3, 4}, {1, 3, -1, 5}, {2, 4, 5, -1}};
+  return tbl[a][b];
+}
+
+}  // namespace bt
+
+// Opaque ABI handles --------------------------------------------------------
+struct bt_grid {
+  int device = 0;
+  int lo = 2, hi = 2;
+  bt::Mesh mesh;
+  bt::Topology topo;
+  bt::DevBuf<bt::DevFace> d_faces;
+  bt::DevBuf<bt::DevPrimHdr> d_ehdr, d_vhdr;
+  bt::DevBuf<bt::DevPrimMem> d_emem, d_vmem;
+  bt::DevBuf<bt::DevCellInfo> d_info;
+  // reduction scratch for dot products
+  mutable bt::DevBuf<double> d_partials;
+  mutable double* h_pinned = nullptr;
+  ~bt_grid();
+};
+
+namespace bt {
+// Per-cell stencil data: zero-set-typed rows (type 0 = merged interior row,
+// compute_stencil operators.hpp:204-221), and a bitmask of present
+// directions per type.
+struct StencilCell {
+  double w[16][15];
+  uint32_t mask[16];
+};
+// Per-cell data for the elementwise (on-the-fly) kernel.
+struct EwCell {
+  double G[6][16];        // class matrices (diffusion for div_k_grad; else the form)
+  double beta[3][3];      // angle slope: f * A[d][e] * h   (coeff kind 1)
+  double lin[3];          // c . (A h) for coeff kind 2
+  double lin0[6][4];      // kind 2: c0 + c.(A h (ō_s - o_slot) + b)
+};
+struct EwAngles {         // kind 1: sin/cos of the (class, slot, q, d) phase
+  double s[6][4][4][3];
+  double c[6][4][4][3];
+};
+}  // namespace bt
+
+struct bt_stencil {
+  const bt_grid* grid = nullptr;
+  int level = 0;
+  bt_form form{};
+  std::vector<std::array<double, 15>> rows;  // host copy of StencilTable::rows
+  bt::DevBuf<bt::StencilCell> d_cells;
+  bt::DevBuf<double> d_diag;                 // assembled diagonal
+};
+
+namespace bt {
+// host helpers shared between translation units
+void class_matrices(const bt_grid& g, int form_kind, int level, int cell, double out[6][16]);
+void build_stencil_cells(const bt_grid& g, const bt_form& f, int level,
+                         std::vector<StencilCell>& cells, std::vector<std::array<double, 15>>& rows);
+void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<EwCell>& cells,
+                    std::vector<EwAngles>& angles);
+int64_t level_slots(int space, int level);  // per cell
+void validate_form(const bt_form* f);
+void check_level(const bt_grid* g, int level);
+
+// kernel launchers (bt_kernels.cu)
+enum IfaceMode { IF_SYNC = 0, IF_SYNC_DIR = 1, IF_BCAST = 2, IF_IMPOSE = 3, IF_ZERO_DIR = 4, IF_ZERO_NONOWNED = 5 };
+void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src,
+                      cudaStream_t s);
+void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s);
+void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c,
+                        const EwCell* d_cells, const EwAngles* d_angles, const double* x, double* y,
+                        bool diag_only, cudaStream_t s);
+void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStream_t s);
+void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s);
+double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s);
+void launch_prolongate(const bt_grid& g, int fine_level, const double* coarse, double* fine, bool add,
+                       cudaStream_t s);
+void launch_restrict(const bt_grid& g, int fine_level, const double* fine, double* coarse,
+                     cudaStream_t s);
+enum VecOp { V_ASSIGN = 0, V_SCALE = 1, V_COPY = 2, V_AXPY = 3, V_MUL = 4, V_DIV = 5 };
+}  // namespace bt

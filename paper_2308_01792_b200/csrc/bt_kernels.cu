@@ -1,0 +1,761 @@
+// Device kernels of blocktet_b200 (sm_100a) and the device-side C ABI.
+//
+// All kernels address the tetrahedral row layout implicitly: no per-DoF
+// index arrays. A warp owns one lattice row (j, k) of one macro-cell at a
+// time, its lanes walk i, and the 15 stencil neighbours are fixed offsets of
+// the row (bt::row_offsets). Macro-cell interfaces ("ghost layers" of the
+// reference: replicated DoFs summed by sync_additive, fe_function.hpp:400)
+// are handled by one kernel over macro faces, edges and vertices whose
+// member slots are computed from barycentric weights.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "bt_internal.hpp"
+
+namespace bt {
+
+// Present micro-cells (bit 4*s + slot) and needed stencil directions per zero
+// set; derived from in_i_tet(w_s, p - o_slot) (verified exhaustively in
+// tests/test_index.py against the reference rule).
+__constant__ uint32_t kPresent[16] = {0xffffff, 0xe8cc8e, 0x962b4d, 0x80080c, 0x4d962b, 0x48840a,
+                                      0x40209,  0x8,      0x337117, 0x204006, 0x122105, 0x4,
+                                      0x11003,  0x2,      0x1,      0x0};
+__constant__ uint32_t kDirMask[16] = {0x7fff, 0x7f71, 0x26ff, 0x2671, 0x5d6f, 0x5d61, 0x46f, 0x461,
+                                      0x3b9f, 0x3b11, 0x229f, 0x2211, 0x190f, 0x1901, 0xf,   0x0};
+// stencil direction of (o_j - o_slot) for class s (operators.hpp:219)
+#define BT_TET_DIR                                                                      \
+  {{{0, 1, 2, 3}, {8, 0, 11, 12}, {9, 4, 0, 13}, {10, 5, 6, 0}},                        \
+   {{0, 13, 12, 3}, {6, 0, 11, 2}, {5, 4, 0, 1}, {10, 9, 8, 0}},                        \
+   {{0, 13, 7, 3}, {6, 0, 1, 2}, {14, 8, 0, 11}, {10, 9, 4, 0}},                        \
+   {{0, 11, 2, 3}, {4, 0, 1, 7}, {9, 8, 0, 13}, {10, 14, 6, 0}},                        \
+   {{0, 11, 12, 3}, {4, 0, 13, 7}, {5, 6, 0, 1}, {10, 14, 8, 0}},                       \
+   {{0, 1, 7, 3}, {8, 0, 13, 12}, {14, 6, 0, 11}, {10, 5, 4, 0}}}
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRowsPerCta = 64;
+
+static inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------------------
+// Interface pass (sync_additive / sync_broadcast / Dirichlet rows)
+// ---------------------------------------------------------------------------
+struct IfaceArgs {
+  const DevFace* faces;
+  int nfaces;
+  const DevPrimHdr* eh;
+  const DevPrimMem* em;
+  int nedges;
+  const DevPrimHdr* vh;
+  const DevPrimMem* vm;
+  int nverts;
+  int n;
+  int64_t cell_slots;
+};
+
+__device__ __forceinline__ int64_t member_slot(int64_t cell_slots, int w, int cell, int i, int j, int k) {
+  return (int64_t)cell * cell_slots + row_start(w, j, k) + i;
+}
+
+// weights of local vertices 1..3 given up to three (local vertex, weight)
+__device__ __forceinline__ void ijk_from(int l0, int w0, int l1, int w1, int l2, int w2, int& i, int& j, int& k) {
+  i = (l0 == 1 ? w0 : 0) + (l1 == 1 ? w1 : 0) + (l2 == 1 ? w2 : 0);
+  j = (l0 == 2 ? w0 : 0) + (l1 == 2 ? w1 : 0) + (l2 == 2 ? w2 : 0);
+  k = (l0 == 3 ? w0 : 0) + (l1 == 3 ? w1 : 0) + (l2 == 3 ? w2 : 0);
+}
+
+template <int MODE>
+__device__ __forceinline__ void iface_apply(double* __restrict__ v, const double* __restrict__ src, int count,
+                                            bool dir, const int64_t* slots) {
+  if (MODE == IF_SYNC) {
+    if (count < 2) return;
+    double sum = 0;
+    for (int m = 0; m < count; ++m) sum += v[slots[m]];
+    for (int m = 0; m < count; ++m) v[slots[m]] = sum;
+  } else if (MODE == IF_SYNC_DIR) {
+    if (dir) {
+      for (int m = 0; m < count; ++m) v[slots[m]] = src[slots[m]];
+    } else if (count >= 2) {
+      double sum = 0;
+      for (int m = 0; m < count; ++m) sum += v[slots[m]];
+      for (int m = 0; m < count; ++m) v[slots[m]] = sum;
+    }
+  } else if (MODE == IF_BCAST) {
+    if (count < 2) return;
+    const double val = v[slots[0]];
+    for (int m = 1; m < count; ++m) v[slots[m]] = val;
+  } else if (MODE == IF_IMPOSE) {
+    if (dir)
+      for (int m = 0; m < count; ++m) v[slots[m]] = src[slots[m]];
+  } else if (MODE == IF_ZERO_DIR) {
+    if (dir)
+      for (int m = 0; m < count; ++m) v[slots[m]] = 0.0;
+  } else if (MODE == IF_ZERO_NONOWNED) {
+    for (int m = 1; m < count; ++m) v[slots[m]] = 0.0;
+  }
+}
+
+constexpr int kMaxMembers = 64;
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_interface(double* __restrict__ v, const double* __restrict__ src,
+                                                        IfaceArgs a) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = a.n, w = n + 1;
+  const int64_t FP = tri32(n - 2);
+  const int64_t nF = (int64_t)a.nfaces * FP;
+  const int64_t nE = (int64_t)a.nedges * (n - 1);
+  int64_t slots[kMaxMembers];
+  if (id < nF) {
+    const int f = (int)(id / FP);
+    const int q = (int)(id - (int64_t)f * FP);
+    int ap, bp;
+    decode_tri(n - 2, q, ap, bp);
+    const int aa = ap + 1, bb = bp + 1;
+    const DevFace fr = a.faces[f];
+    for (int s = 0; s < fr.ncell; ++s) {
+      int i, j, k;
+      ijk_from(fr.lv[s][0], n - aa - bb, fr.lv[s][1], aa, fr.lv[s][2], bb, i, j, k);
+      slots[s] = member_slot(a.cell_slots, w, fr.cell[s], i, j, k);
+    }
+    iface_apply<MODE>(v, src, fr.ncell, fr.dir != 0, slots);
+  } else if (id < nF + nE) {
+    const int64_t r = id - nF;
+    const int e = (int)(r / (n - 1));
+    const int aa = (int)(r - (int64_t)e * (n - 1)) + 1;
+    const DevPrimHdr hd = a.eh[e];
+    const int cnt = min(hd.count, kMaxMembers);
+    for (int m = 0; m < cnt; ++m) {
+      const DevPrimMem pm = a.em[hd.first + m];
+      int i, j, k;
+      ijk_from(pm.lv[0], n - aa, pm.lv[1], aa, -1, 0, i, j, k);
+      slots[m] = member_slot(a.cell_slots, w, pm.cell, i, j, k);
+    }
+    iface_apply<MODE>(v, src, cnt, hd.dir != 0, slots);
+  } else if (id < nF + nE + a.nverts) {
+    const int vv = (int)(id - nF - nE);
+    const DevPrimHdr hd = a.vh[vv];
+    const int cnt = min(hd.count, kMaxMembers);
+    for (int m = 0; m < cnt; ++m) {
+      const DevPrimMem pm = a.vm[hd.first + m];
+      int i, j, k;
+      ijk_from(pm.lv[0], n, -1, 0, -1, 0, i, j, k);
+      slots[m] = member_slot(a.cell_slots, w, pm.cell, i, j, k);
+    }
+    iface_apply<MODE>(v, src, cnt, hd.dir != 0, slots);
+  }
+}
+
+void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
+  IfaceArgs a;
+  a.faces = g.d_faces.p;
+  a.nfaces = (int)g.topo.faces.size();
+  a.eh = g.d_ehdr.p;
+  a.em = g.d_emem.p;
+  a.nedges = (int)g.topo.ehdr.size();
+  a.vh = g.d_vhdr.p;
+  a.vm = g.d_vmem.p;
+  a.nverts = (int)g.topo.vhdr.size();
+  a.n = 1 << level;
+  a.cell_slots = n_tet(a.n + 1);
+  for (const auto& h : g.topo.vhdr)
+    if (h.count > kMaxMembers) raise(BT_INVALID_ARGUMENT, "macro vertex shared by more than 64 cells");
+  const int64_t total = (int64_t)a.nfaces * tri32(a.n - 2) + (int64_t)a.nedges * (a.n - 1) + a.nverts;
+  if (total == 0) return;
+  const int blocks = ceil_div(total, kThreads);
+  switch (mode) {
+    case IF_SYNC: k_interface<IF_SYNC><<<blocks, kThreads, 0, s>>>(v, src, a); break;
+    case IF_SYNC_DIR: k_interface<IF_SYNC_DIR><<<blocks, kThreads, 0, s>>>(v, src, a); break;
+    case IF_BCAST: k_interface<IF_BCAST><<<blocks, kThreads, 0, s>>>(v, src, a); break;
+    case IF_IMPOSE: k_interface<IF_IMPOSE><<<blocks, kThreads, 0, s>>>(v, src, a); break;
+    case IF_ZERO_DIR: k_interface<IF_ZERO_DIR><<<blocks, kThreads, 0, s>>>(v, src, a); break;
+    case IF_ZERO_NONOWNED: k_interface<IF_ZERO_NONOWNED><<<blocks, kThreads, 0, s>>>(v, src, a); break;
+  }
+  count_launch();
+  check_launch("k_interface");
+}
+
+// ---------------------------------------------------------------------------
+// P1 constant-coefficient 15-point stencil (apply_stencil operators.hpp:247)
+// ---------------------------------------------------------------------------
+// Interior vertices use the merged row in registers; lattice-boundary
+// vertices use the zero-set-typed partial row (the per-cell part of
+// partial_row_apply, operators.hpp:78-96), completed by the interface pass.
+__global__ void __launch_bounds__(kThreads) k_stencil(const double* __restrict__ x, double* __restrict__ y,
+                                                      const StencilCell* __restrict__ cells, int w,
+                                                      int64_t cell_slots) {
+  __shared__ StencilCell sc;
+  const int cell = blockIdx.y;
+  {
+    const double* src = reinterpret_cast<const double*>(cells + cell);
+    double* dst = reinterpret_cast<double*>(&sc);
+    for (int q = threadIdx.x; q < (int)(sizeof(StencilCell) / 8); q += blockDim.x) dst[q] = src[q];
+  }
+  __syncthreads();
+  double w0[15];
+#pragma unroll
+  for (int d = 0; d < 15; ++d) w0[d] = sc.w[0][d];
+  const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
+  double* __restrict__ yc = y + (int64_t)cell * cell_slots;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrows = tri32(w);
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int j, k;
+    decode_row(w, r, j, k);
+    const int L = w - j - k;
+    const int t0 = row_start(w, j, k);
+    int off[15];
+    row_offsets(w, j, k, off);
+    const int zrow = (j == 0 ? 4 : 0) | (k == 0 ? 8 : 0);
+    for (int i = lane; i < L; i += 32) {
+      const int t = t0 + i;
+      const int z = zrow | (i == L - 1 ? 1 : 0) | (i == 0 ? 2 : 0);
+      double acc;
+      if (z == 0) {
+        acc = w0[0] * __ldg(xc + t);
+#pragma unroll
+        for (int d = 1; d < 15; ++d) acc = fma(w0[d], __ldg(xc + t + off[d]), acc);
+      } else {
+        const uint32_t msk = sc.mask[z];
+        acc = 0.0;
+#pragma unroll
+        for (int d = 0; d < 15; ++d)
+          if (msk >> d & 1) acc = fma(sc.w[z][d], __ldg(xc + t + off[d]), acc);
+      }
+      yc[t] = acc;
+    }
+  }
+}
+
+void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
+  const int w = (1 << st.level) + 1;
+  dim3 grid(ceil_div(tri32(w), kRowsPerCta), st.grid->mesh.n_cells());
+  k_stencil<<<grid, kThreads, 0, s>>>(x, y, st.d_cells.p, w, n_tet(w));
+  count_launch();
+  check_launch("k_stencil");
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise P1 apply with on-the-fly coefficient (apply_elementwise
+// operators.hpp:115-164, local_matrix forms.hpp:75-120), pull form:
+// y_v = sum over present micro-cells T of v: kbar_T * (G_s row) . x_T, with
+// kbar_T = 1/4 sum_q k(x_q) by the reference's 4-point rule. For the
+// sin-product coefficient each quadrature phase is C + beta . v, so sin/cos
+// of beta . v (3 sincos per vertex) and the angle-addition formula replace
+// the 12 sin evaluations per micro-cell.
+// ---------------------------------------------------------------------------
+template <int CK, bool DIAG>
+__global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restrict__ x, double* __restrict__ y,
+                                                          const EwCell* __restrict__ cells,
+                                                          const EwAngles* __restrict__ angles, double c0, double c1,
+                                                          int w, int64_t cell_slots) {
+  __shared__ EwCell sc;
+  __shared__ EwAngles sa;
+  const int cell = blockIdx.y;
+  {
+    const double* src = reinterpret_cast<const double*>(cells + cell);
+    double* dst = reinterpret_cast<double*>(&sc);
+    for (int q = threadIdx.x; q < (int)(sizeof(EwCell) / 8); q += blockDim.x) dst[q] = src[q];
+    if (CK == 1) {
+      const double* sa_src = reinterpret_cast<const double*>(angles + cell);
+      double* sa_dst = reinterpret_cast<double*>(&sa);
+      for (int q = threadIdx.x; q < (int)(sizeof(EwAngles) / 8); q += blockDim.x) sa_dst[q] = sa_src[q];
+    }
+  }
+  __syncthreads();
+  constexpr int kTetDir[6][4][4] = BT_TET_DIR;
+  const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
+  double* __restrict__ yc = y + (int64_t)cell * cell_slots;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = w - 1;
+  const int nrows = tri32(w);
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int j, k;
+    decode_row(w, r, j, k);
+    const int L = w - j - k;
+    const int t0 = row_start(w, j, k);
+    int off[15];
+    row_offsets(w, j, k, off);
+    for (int i = lane; i < L; i += 32) {
+      const int t = t0 + i;
+      const int z = zero_set(n, i, j, k);
+      const uint32_t present = kPresent[z];
+      double xv[15];
+      if (!DIAG) {
+        const uint32_t dm = kDirMask[z];
+#pragma unroll
+        for (int d = 0; d < 15; ++d) xv[d] = (dm >> d & 1) ? __ldg(xc + t + off[d]) : 0.0;
+      }
+      double sB[3], cB[3];
+      double lin = 0.0;
+      if (CK == 1) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double ph = sc.beta[d][0] * i + sc.beta[d][1] * j + sc.beta[d][2] * k;
+          sincos(ph, &sB[d], &cB[d]);
+        }
+      } else if (CK == 2) {
+        lin = sc.lin[0] * i + sc.lin[1] * j + sc.lin[2] * k;
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+#pragma unroll
+        for (int slot = 0; slot < 4; ++slot) {
+          if (!(present >> (4 * s + slot) & 1)) continue;
+          double kbar;
+          if (CK == 0) {
+            kbar = c0;
+          } else if (CK == 1) {
+            kbar = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              double prod = 1.0;
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+                prod *= fma(sa.s[s][slot][q][d], cB[d], sa.c[s][slot][q][d] * sB[d]);
+              kbar = fma(0.25, fma(c1, prod, c0), kbar);
+            }
+          } else {
+            kbar = sc.lin0[s][slot] + lin;
+          }
+          if (DIAG) {
+            acc = fma(kbar, sc.G[s][5 * slot], acc);
+          } else {
+            double row = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) row = fma(sc.G[s][4 * slot + jj], xv[kTetDir[s][slot][jj]], row);
+            acc = fma(kbar, row, acc);
+          }
+        }
+      }
+      yc[t] = acc;
+    }
+  }
+}
+
+void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells,
+                        const EwAngles* d_angles, const double* x, double* y, bool diag_only, cudaStream_t s) {
+  const int w = (1 << level) + 1;
+  dim3 grid(ceil_div(tri32(w), kRowsPerCta), g.mesh.n_cells());
+  const int64_t cs = n_tet(w);
+  const double c0 = ck == 0 ? c[0] : c[0], c1 = c[1];
+#define BT_EW(CK_, D_) k_elementwise<CK_, D_><<<grid, kThreads, 0, s>>>(x, y, d_cells, d_angles, c0, c1, w, cs)
+  if (ck == 0) { if (diag_only) BT_EW(0, true); else BT_EW(0, false); }
+  else if (ck == 1) { if (diag_only) BT_EW(1, true); else BT_EW(1, false); }
+  else { if (diag_only) BT_EW(2, true); else BT_EW(2, false); }
+#undef BT_EW
+  count_launch();
+  check_launch("k_elementwise");
+}
+
+// ---------------------------------------------------------------------------
+// Row-walk helpers: fill-by-zero-set, owned dot products, transfers
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_fill_by_z(const double* __restrict__ tbl, double* __restrict__ out,
+                                                        int w, int64_t cell_slots) {
+  const int cell = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = w - 1, nrows = tri32(w);
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int j, k;
+    decode_row(w, r, j, k);
+    const int L = w - j - k, t0 = row_start(w, j, k);
+    for (int i = lane; i < L; i += 32) out[(int64_t)cell * cell_slots + t0 + i] = tbl[16 * cell + zero_set(n, i, j, k)];
+  }
+}
+
+void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s) {
+  const int w = (1 << level) + 1;
+  dim3 grid(ceil_div(tri32(w), kRowsPerCta), g.mesh.n_cells());
+  k_fill_by_z<<<grid, kThreads, 0, s>>>(tbl, out, w, n_tet(w));
+  count_launch();
+  check_launch("k_fill_by_z");
+}
+
+// Deterministic owned-DoF dot: fixed (cell, row block) partials, fixed
+// shuffle tree, fixed final order. Independent of the GPU count because
+// partials never straddle cells (fe_function.hpp:373-394 order up to
+// reassociation).
+__global__ void __launch_bounds__(kThreads) k_dot_partial(const double* __restrict__ x, const double* __restrict__ y,
+                                                          const DevCellInfo* __restrict__ info, int w,
+                                                          int64_t cell_slots, double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  const int cell = blockIdx.y;
+  const uint16_t own = info[cell].owned_by_z;
+  const double* xc = x + (int64_t)cell * cell_slots;
+  const double* yc = y + (int64_t)cell * cell_slots;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = w - 1, nrows = tri32(w);
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+  double acc = 0.0;
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int j, k;
+    decode_row(w, r, j, k);
+    const int L = w - j - k, t0 = row_start(w, j, k);
+    for (int i = lane; i < L; i += 32)
+      if (own >> zero_set(n, i, j, k) & 1) acc = fma(__ldg(xc + t0 + i), __ldg(yc + t0 + i), acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < kWarps; ++q) s += red[q];
+    partials[(int64_t)cell * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_sum(const double* __restrict__ partials, int64_t n, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) acc += partials[q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += red[q];
+    *out = s;
+  }
+}
+
+double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s) {
+  const int w = (1 << level) + 1;
+  const int bx = ceil_div(tri32(w), kRowsPerCta);
+  const int64_t np = (int64_t)bx * g.mesh.n_cells();
+  if (g.d_partials.n < (size_t)np + 1) g.d_partials.alloc((size_t)np + 1);
+  dim3 grid(bx, g.mesh.n_cells());
+  k_dot_partial<<<grid, kThreads, 0, s>>>(x, y, g.d_info.p, w, n_tet(w), g.d_partials.p);
+  k_sum<<<1, 1024, 0, s>>>(g.d_partials.p, np, g.d_partials.p + np);
+  count_launch(2);
+  check_launch("k_dot");
+  BT_CUDA(cudaMemcpyAsync(g.h_pinned, g.d_partials.p + np, sizeof(double), cudaMemcpyDeviceToHost, s));
+  BT_CUDA(cudaStreamSynchronize(s));
+  return g.h_pinned[0];
+}
+
+// prolongate_p1 (solvers.hpp:227-253), optionally fused with axpy(x, 1, ef)
+__global__ void __launch_bounds__(kThreads) k_prolongate(const double* __restrict__ coarse, double* __restrict__ fine,
+                                                         int wf, int add) {
+  const int cell = blockIdx.y;
+  const int wc = (wf - 1) / 2 + 1;
+  const double* cc = coarse + (int64_t)cell * tet32(wc);
+  double* fc = fine + (int64_t)cell * tet32(wf);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrows = tri32(wf);
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int j, k;
+    decode_row(wf, r, j, k);
+    const int L = wf - j - k, t0 = row_start(wf, j, k);
+    for (int i = lane; i < L; i += 32) {
+      const int code = (i & 1) | ((j & 1) << 1) | ((k & 1) << 2);
+      double value;
+      if (code == 0) {
+        value = __ldg(cc + row_start(wc, j >> 1, k >> 1) + (i >> 1));
+      } else {
+        // coarse_endpoints (solvers.hpp:183-211): first / second endpoint
+        int a0, b0, c0, a1, b1, c1;
+        switch (code) {
+          case 1: a0 = i - 1; b0 = j; c0 = k; a1 = i + 1; b1 = j; c1 = k; break;
+          case 2: a0 = i; b0 = j - 1; c0 = k; a1 = i; b1 = j + 1; c1 = k; break;
+          case 4: a0 = i; b0 = j; c0 = k - 1; a1 = i; b1 = j; c1 = k + 1; break;
+          case 3: a0 = i + 1; b0 = j - 1; c0 = k; a1 = i - 1; b1 = j + 1; c1 = k; break;
+          case 5: a0 = i + 1; b0 = j; c0 = k - 1; a1 = i - 1; b1 = j; c1 = k + 1; break;
+          case 6: a0 = i; b0 = j + 1; c0 = k - 1; a1 = i; b1 = j - 1; c1 = k + 1; break;
+          default: a0 = i - 1; b0 = j + 1; c0 = k - 1; a1 = i + 1; b1 = j - 1; c1 = k + 1; break;
+        }
+        const double v0 = __ldg(cc + row_start(wc, b0 >> 1, c0 >> 1) + (a0 >> 1));
+        const double v1 = __ldg(cc + row_start(wc, b1 >> 1, c1 >> 1) + (a1 >> 1));
+        value = 0.5 * __dadd_rn(v0, v1);
+      }
+      if (add) fc[t0 + i] = __dadd_rn(fc[t0 + i], value);
+      else fc[t0 + i] = value;
+    }
+  }
+}
+
+void launch_prolongate(const bt_grid& g, int fine_level, const double* coarse, double* fine, bool add, cudaStream_t s) {
+  const int wf = (1 << fine_level) + 1;
+  dim3 grid(ceil_div(tri32(wf), kRowsPerCta), g.mesh.n_cells());
+  k_prolongate<<<grid, kThreads, 0, s>>>(coarse, fine, wf, add ? 1 : 0);
+  count_launch();
+  check_launch("k_prolongate");
+}
+
+// restrict_p1 (solvers.hpp:259-293) as a pull over coarse vertices: the fine
+// points 2P + d (d a stencil direction) contribute in ascending fine-slot
+// order, exactly the reference's scatter order; non-owned fine replicas
+// contribute 0.
+__global__ void __launch_bounds__(kThreads) k_restrict(const double* __restrict__ fine, double* __restrict__ coarse,
+                                                       const DevCellInfo* __restrict__ info, int wc) {
+  // directions sorted by (dz, dy, dx)
+  constexpr int kOrd[15][3] = {{0, 0, -1}, {1, 0, -1}, {-1, 1, -1}, {0, 1, -1}, {0, -1, 0},
+                               {1, -1, 0}, {-1, 0, 0}, {0, 0, 0},   {1, 0, 0},  {-1, 1, 0},
+                               {0, 1, 0},  {0, -1, 1}, {1, -1, 1},  {-1, 0, 1}, {0, 0, 1}};
+  const int cell = blockIdx.y;
+  const int wf = 2 * (wc - 1) + 1, nf = wf - 1;
+  const uint16_t own = info[cell].owned_by_z;
+  const double* fc = fine + (int64_t)cell * tet32(wf);
+  double* cc = coarse + (int64_t)cell * tet32(wc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrows = tri32(wc);
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int J, K;
+    decode_row(wc, r, J, K);
+    const int L = wc - J - K, t0 = row_start(wc, J, K);
+    for (int I = lane; I < L; I += 32) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 15; ++q) {
+        const int fi = 2 * I + kOrd[q][0], fj = 2 * J + kOrd[q][1], fk = 2 * K + kOrd[q][2];
+        if (!in_i_tet(wf, fi, fj, fk)) continue;
+        const double v = (own >> zero_set(nf, fi, fj, fk) & 1) ? __ldg(fc + row_start(wf, fj, fk) + fi) : 0.0;
+        if (q == 7) acc = __dadd_rn(acc, v);
+        else acc = __dadd_rn(acc, 0.5 * v);
+      }
+      cc[t0 + I] = acc;
+    }
+  }
+}
+
+void launch_restrict(const bt_grid& g, int fine_level, const double* fine, double* coarse, cudaStream_t s) {
+  const int wc = (1 << (fine_level - 1)) + 1;
+  dim3 grid(ceil_div(tri32(wc), kRowsPerCta), g.mesh.n_cells());
+  k_restrict<<<grid, kThreads, 0, s>>>(fine, coarse, g.d_info.p, wc);
+  count_launch();
+  check_launch("k_restrict");
+  launch_interface(g, fine_level - 1, IF_SYNC, coarse, nullptr, s);
+}
+
+// ---------------------------------------------------------------------------
+// Streaming vector kernels (fe_function.hpp:324-371, solvers.hpp:53-64).
+// Explicit _rn intrinsics keep the reference's unfused rounding.
+// ---------------------------------------------------------------------------
+template <int OP>
+__global__ void __launch_bounds__(kThreads) k_vec(double* __restrict__ y, const double* __restrict__ x, double a,
+                                                  int64_t n) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    if (OP == V_ASSIGN) y[q] = a;
+    else if (OP == V_SCALE) y[q] = __dmul_rn(y[q], a);
+    else if (OP == V_COPY) y[q] = x[q];
+    else if (OP == V_AXPY) y[q] = __dadd_rn(y[q], __dmul_rn(a, x[q]));
+    else if (OP == V_MUL) y[q] = __dmul_rn(y[q], x[q]);
+    else if (OP == V_DIV) y[q] = __ddiv_rn(y[q], x[q]);
+  }
+}
+
+void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  int sms = 148;
+  const int blocks = (int)std::min<int64_t>(ceil_div(n, kThreads), (int64_t)sms * 8);
+  switch (op) {
+    case V_ASSIGN: k_vec<V_ASSIGN><<<blocks, kThreads, 0, s>>>(y, x, a, n); break;
+    case V_SCALE: k_vec<V_SCALE><<<blocks, kThreads, 0, s>>>(y, x, a, n); break;
+    case V_COPY: k_vec<V_COPY><<<blocks, kThreads, 0, s>>>(y, x, a, n); break;
+    case V_AXPY: k_vec<V_AXPY><<<blocks, kThreads, 0, s>>>(y, x, a, n); break;
+    case V_MUL: k_vec<V_MUL><<<blocks, kThreads, 0, s>>>(y, x, a, n); break;
+    case V_DIV: k_vec<V_DIV><<<blocks, kThreads, 0, s>>>(y, x, a, n); break;
+  }
+  count_launch();
+  check_launch("k_vec");
+}
+
+}  // namespace bt
+
+// ===========================================================================
+// C ABI (device-side entry points)
+// ===========================================================================
+using namespace bt;
+
+#define BT_TRY try {
+#define BT_CATCH                         \
+  }                                      \
+  catch (const bt::Error& e) {           \
+    bt::set_error(e.what());             \
+    return e.status;                     \
+  }                                      \
+  catch (const std::exception& e) {      \
+    bt::set_error(e.what());             \
+    return BT_LOGIC_ERROR;               \
+  }                                      \
+  return BT_OK;
+
+static void require_p1(int space) {
+  if (space != BT_SPACE_P1) raise(BT_INVALID_ARGUMENT, "operator kernels require a P1 function");
+}
+
+extern "C" {
+
+bt_status bt_assign(const bt_grid* g, int space, int level, double* x, double value, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_vec(V_ASSIGN, x, nullptr, value, bt_space_size(g, space, level), (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_scale(const bt_grid* g, int space, int level, double* x, double s, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_vec(V_SCALE, x, nullptr, s, bt_space_size(g, space, level), (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_copy(const bt_grid* g, int space, int level, const double* src, double* dst, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_vec(V_COPY, dst, src, 0.0, bt_space_size(g, space, level), (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_axpy(const bt_grid* g, int space, int level, double* y, double a, const double* x, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_vec(V_AXPY, y, x, a, bt_space_size(g, space, level), (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_hadamard(const bt_grid* g, int level, double* x, const double* d, int divide, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_vec(divide ? V_DIV : V_MUL, x, d, 0.0, bt_space_size(g, BT_SPACE_P1, level), (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_dot(const bt_grid* g, int space, int level, const double* x, const double* y, double* out,
+                 void* stream) {
+  BT_TRY
+  check_level(g, level);
+  require_p1(space);
+  *out = dot_p1(*g, level, x, y, (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  require_p1(space);
+  launch_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_sync_broadcast(const bt_grid* g, int space, int level, double* x, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  require_p1(space);
+  launch_interface(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_impose_dirichlet(const bt_grid* g, int level, const double* src, double* dst, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_interface(*g, level, IF_IMPOSE, dst, src, (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_zero_dirichlet(const bt_grid* g, int level, double* x, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_interface(*g, level, IF_ZERO_DIR, x, nullptr, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int bc, void* stream) {
+  BT_TRY
+  if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
+  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_stencil(*st, x, y, s);
+  launch_interface(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+  BT_CATCH
+}
+
+bt_status bt_apply_stencil_cells(const bt_stencil* st, const double* x, double* y, void* stream) {
+  BT_TRY
+  if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
+  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  launch_stencil(*st, x, y, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_apply_stencil_interface(const bt_stencil* st, const double* x, double* y, int bc, void* stream) {
+  BT_TRY
+  if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
+  launch_interface(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level, const double* x, double* y,
+                               int mode, int bc, double* scratch, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  validate_form(form);
+  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<EwCell> cells;
+  std::vector<EwAngles> angles;
+  build_ew_cells(*g, *form, level, cells, angles);
+  DevBuf<EwCell> dc;
+  DevBuf<EwAngles> da;
+  dc.upload(cells);
+  if (!angles.empty()) da.upload(angles);
+  const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
+  const double one[4] = {1.0, 0.0, 0.0, 0.0};
+  const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
+  DevBuf<double> tmp;
+  double* out = y;
+  if (mode == BT_MODE_ADD) {
+    if (!scratch) {
+      tmp.alloc((size_t)bt_space_size(g, BT_SPACE_P1, level));
+      scratch = tmp.p;
+    }
+    out = scratch;
+  }
+  launch_elementwise(*g, level, ck, c, dc.p, da.p, x, out, false, s);
+  launch_interface(*g, level, bc ? IF_SYNC_DIR : IF_SYNC, out, x, s);
+  if (mode == BT_MODE_ADD) launch_vec(V_AXPY, y, out, 1.0, bt_space_size(g, BT_SPACE_P1, level), s);
+  BT_CUDA(cudaStreamSynchronize(s));  // host-side tables are released on return
+  BT_CATCH
+}
+
+bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, double* diag, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  validate_form(form);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<EwCell> cells;
+  std::vector<EwAngles> angles;
+  build_ew_cells(*g, *form, level, cells, angles);
+  DevBuf<EwCell> dc;
+  DevBuf<EwAngles> da;
+  dc.upload(cells);
+  if (!angles.empty()) da.upload(angles);
+  const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
+  const double one[4] = {1.0, 0.0, 0.0, 0.0};
+  launch_elementwise(*g, level, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, dc.p, da.p, nullptr, diag,
+                     true, s);
+  launch_interface(*g, level, IF_SYNC, diag, nullptr, s);
+  BT_CUDA(cudaStreamSynchronize(s));
+  BT_CATCH
+}
+
+bt_status bt_prolongate(const bt_grid* g, int fine_level, const double* coarse, double* fine, int add,
+                        void* stream) {
+  BT_TRY
+  check_level(g, fine_level);
+  check_level(g, fine_level - 1);
+  launch_prolongate(*g, fine_level, coarse, fine, add != 0, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_restrict(const bt_grid* g, int fine_level, const double* fine, double* coarse, void* stream) {
+  BT_TRY
+  check_level(g, fine_level);
+  check_level(g, fine_level - 1);
+  launch_restrict(*g, fine_level, fine, coarse, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+}  // extern "C"

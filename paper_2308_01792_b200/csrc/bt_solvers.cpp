@@ -1,0 +1,316 @@
+// Multigrid hierarchy, smoothers, CG and the V-cycle (solvers.hpp:84-541),
+// orchestrated on the host over device kernels. Every vector operation keeps
+// the reference's operation order (and its unfused rounding, see k_vec), so
+// residual histories track the CPU reference to round-off.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <random>
+#include <vector>
+
+#include "bt_internal.hpp"
+
+namespace bt {
+
+struct LevelData {
+  int level = 0;
+  int64_t n = 0;
+  std::unique_ptr<bt_stencil> stencil;  // stencil kernel
+  DevBuf<EwCell> ew;                    // elementwise kernel tables
+  DevBuf<EwAngles> ang;
+  DevBuf<double> diag;
+  double lambda = 0.0;
+  // work vectors
+  DevBuf<double> r, d, p, ap, z, b, x, tmp;
+};
+
+}  // namespace bt
+
+struct bt_hierarchy {
+  const bt_grid* grid = nullptr;
+  bt_form form{};
+  int kernel = 1;
+  std::vector<std::unique_ptr<bt::LevelData>> levels;
+  bt::LevelData& at(int l) {
+    if (l < grid->lo || l > grid->hi) bt::raise(BT_OUT_OF_RANGE, "level not in hierarchy");
+    return *levels[l - grid->lo];
+  }
+};
+
+namespace bt {
+
+static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int bc, cudaStream_t s) {
+  LevelData& L = h.at(l);
+  if (h.kernel == 1) {
+    launch_stencil(*L.stencil, x, y, s);
+  } else {
+    const int ck = h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.coeff_kind : 0;
+    static const double one[4] = {1.0, 0.0, 0.0, 0.0};
+    launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, L.ang.p, x, y,
+                       false, s);
+  }
+  launch_interface(*h.grid, l, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+}
+
+static double dot(bt_hierarchy& h, int l, const double* x, const double* y, cudaStream_t s) {
+  return dot_p1(*h.grid, l, x, y, s);
+}
+
+// estimate_lambda_max (solvers.hpp:140-172) through spectral_estimate (:362)
+static double lambda_max(bt_hierarchy& h, int l, cudaStream_t s) {
+  LevelData& L = h.at(l);
+  if (L.lambda != 0.0) return L.lambda;
+  const int64_t n = L.n;
+  double* v = L.p.p;
+  double* w = L.ap.p;
+  double* z = L.z.p;
+  BT_CUDA(cudaStreamSynchronize(s));
+  if (bt_random_fill(h.grid, BT_SPACE_P1, l, 0x51cbu, v, s) != BT_OK) raise(BT_CUDA_ERROR, bt_last_error());
+  launch_interface(*h.grid, l, IF_ZERO_DIR, v, nullptr, s);
+  const double nv = std::sqrt(dot(h, l, v, v, s));
+  if (nv == 0) raise(BT_RUNTIME_ERROR, "estimate_lambda_max: empty free space");
+  launch_vec(V_SCALE, v, nullptr, 1.0 / nv, n, s);
+  double rho = 0;
+  for (int k = 0; k < 25; ++k) {
+    hier_apply(h, l, v, w, 1, s);
+    launch_vec(V_COPY, z, v, 0.0, n, s);
+    launch_vec(V_MUL, z, L.diag.p, 0.0, n, s);
+    rho = dot(h, l, v, w, s) / dot(h, l, v, z, s);
+    launch_vec(V_COPY, v, w, 0.0, n, s);
+    launch_vec(V_DIV, v, L.diag.p, 0.0, n, s);
+    const double nn = std::sqrt(dot(h, l, v, v, s));
+    if (nn == 0) break;
+    launch_vec(V_SCALE, v, nullptr, 1.0 / nn, n, s);
+  }
+  L.lambda = 1.1 * rho;
+  return L.lambda;
+}
+
+// r = D^-1 (rhs - A x)   (scale(r,-1); axpy(r,1,rhs); hadamard(r, diag, /))
+static void scaled_residual(bt_hierarchy& h, int l, const double* rhs, const double* x, double* r, cudaStream_t s) {
+  LevelData& L = h.at(l);
+  hier_apply(h, l, x, r, 1, s);
+  launch_vec(V_SCALE, r, nullptr, -1.0, L.n, s);
+  launch_vec(V_AXPY, r, rhs, 1.0, L.n, s);
+  launch_vec(V_DIV, r, L.diag.p, 0.0, L.n, s);
+}
+
+// chebyshev_apply (solvers.hpp:425-456)
+static void chebyshev(bt_hierarchy& h, const double* rhs, double* x, int l, int order, double a, double b,
+                      cudaStream_t s) {
+  LevelData& L = h.at(l);
+  const double theta = 0.5 * (b + a);
+  const double delta = 0.5 * (b - a);
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  double* r = L.r.p;
+  double* d = L.d.p;
+  scaled_residual(h, l, rhs, x, r, s);
+  launch_vec(V_COPY, d, r, 0.0, L.n, s);
+  launch_vec(V_SCALE, d, nullptr, 1.0 / theta, L.n, s);
+  launch_vec(V_AXPY, x, d, 1.0, L.n, s);
+  launch_interface(*h.grid, l, IF_IMPOSE, x, rhs, s);
+  for (int k = 1; k < order; ++k) {
+    scaled_residual(h, l, rhs, x, r, s);
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    launch_vec(V_SCALE, d, nullptr, rho_new * rho, L.n, s);
+    launch_vec(V_AXPY, d, r, 2.0 * rho_new / delta, L.n, s);
+    launch_vec(V_AXPY, x, d, 1.0, L.n, s);
+    launch_interface(*h.grid, l, IF_IMPOSE, x, rhs, s);
+    rho = rho_new;
+  }
+}
+
+static void validate(const bt_smoother_config& c) {                    // solvers.hpp:413-421
+  if (!(c.omega > 0) || c.omega > 1) raise(BT_INVALID_ARGUMENT, "smoother: omega must lie in (0, 1]");
+  if (c.order < 1) raise(BT_INVALID_ARGUMENT, "smoother: order must be >= 1");
+  if (!(c.lo > 0) || !(c.hi > c.lo)) raise(BT_INVALID_ARGUMENT, "smoother: need 0 < lo < hi");
+  if (c.nu1 < 0 || c.nu2 < 0) raise(BT_INVALID_ARGUMENT, "smoother: sweep counts must be >= 0");
+}
+
+static void smooth(bt_hierarchy& h, const bt_smoother_config& c, const double* rhs, double* x, int l, int sweeps,
+                   int backward, cudaStream_t s) {
+  validate(c);
+  LevelData& L = h.at(l);
+  (void)backward;
+  for (int q = 0; q < sweeps; ++q) {
+    if (c.kind == 1) {
+      raise(BT_INVALID_ARGUMENT, "gauss-seidel smoothing is not available on the device path (use chebyshev/jacobi)");
+    } else if (c.kind == 0) {
+      scaled_residual(h, l, rhs, x, L.r.p, s);
+      launch_vec(V_AXPY, x, L.r.p, c.omega, L.n, s);
+      launch_interface(*h.grid, l, IF_IMPOSE, x, rhs, s);
+    } else {
+      const double lam = lambda_max(h, l, s);
+      chebyshev(h, rhs, x, l, c.order, c.lo * lam, c.hi * lam, s);
+    }
+  }
+}
+
+// cg (solvers.hpp:84-131)
+static int cg(bt_hierarchy& h, int l, double tol, int maxit, const double* rhs, double* x, double* hist,
+              cudaStream_t s) {
+  LevelData& L = h.at(l);
+  const int64_t n = L.n;
+  double* r = L.r.p;
+  double* p = L.p.p;
+  double* ap = L.ap.p;
+  hier_apply(h, l, x, r, 1, s);
+  launch_vec(V_SCALE, r, nullptr, -1.0, n, s);
+  launch_vec(V_AXPY, r, rhs, 1.0, n, s);
+  launch_vec(V_COPY, p, r, 0.0, n, s);
+  const double nb = std::sqrt(dot(h, l, rhs, rhs, s));
+  const double denom = nb > 0 ? nb : 1.0;
+  double rs = dot(h, l, r, r, s);
+  int iters = 0;
+  if (std::sqrt(rs) / denom <= tol) return 0;
+  for (int it = 1; it <= maxit; ++it) {
+    hier_apply(h, l, p, ap, 1, s);
+    const double pap = dot(h, l, p, ap, s);
+    if (!(pap > 0)) raise(BT_RUNTIME_ERROR, "cg breakdown: operator is not positive definite");
+    const double alpha = rs / pap;
+    launch_vec(V_AXPY, x, p, alpha, n, s);
+    launch_vec(V_AXPY, r, ap, -alpha, n, s);
+    const double rs_new = dot(h, l, r, r, s);
+    iters = it;
+    if (hist) hist[it - 1] = std::sqrt(rs_new) / denom;
+    if (std::sqrt(rs_new) / denom <= tol) break;
+    launch_vec(V_SCALE, p, nullptr, rs_new / rs, n, s);
+    launch_vec(V_AXPY, p, r, 1.0, n, s);
+    rs = rs_new;
+  }
+  return iters;
+}
+
+// v_cycle (solvers.hpp:509-541). Level-l temporaries: r (residual), and the
+// coarse problem (b = restricted residual, x = correction) lives in level
+// l-1's b/x buffers.
+static void v_cycle(bt_hierarchy& h, int l, const double* rhs, double* x, const bt_smoother_config& sm,
+                    const bt_multigrid_config& mg, cudaStream_t s) {
+  if (mg.coarse_level < h.grid->lo || l < mg.coarse_level) raise(BT_INVALID_ARGUMENT, "v_cycle: level range invalid");
+  if (l == mg.coarse_level) {
+    cg(h, l, mg.coarse_tol, mg.coarse_maxit, rhs, x, nullptr, s);
+    return;
+  }
+  LevelData& L = h.at(l);
+  LevelData& C = h.at(l - 1);
+  smooth(h, sm, rhs, x, l, sm.nu1, 0, s);
+  double* r = L.tmp.p;
+  hier_apply(h, l, x, r, 1, s);
+  launch_vec(V_SCALE, r, nullptr, -1.0, L.n, s);
+  launch_vec(V_AXPY, r, rhs, 1.0, L.n, s);
+  launch_restrict(*h.grid, l, r, C.b.p, s);
+  launch_interface(*h.grid, l - 1, IF_ZERO_DIR, C.b.p, nullptr, s);
+  launch_vec(V_ASSIGN, C.x.p, nullptr, 0.0, C.n, s);
+  v_cycle(h, l - 1, C.b.p, C.x.p, sm, mg, s);
+  launch_prolongate(*h.grid, l, C.x.p, x, true, s);
+  smooth(h, sm, rhs, x, l, sm.nu2, 1, s);
+}
+
+}  // namespace bt
+
+using namespace bt;
+
+#define BT_TRY try {
+#define BT_CATCH                         \
+  }                                      \
+  catch (const bt::Error& e) {           \
+    bt::set_error(e.what());             \
+    return e.status;                     \
+  }                                      \
+  catch (const std::exception& e) {      \
+    bt::set_error(e.what());             \
+    return BT_LOGIC_ERROR;               \
+  }                                      \
+  return BT_OK;
+
+extern "C" {
+
+bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel, bt_hierarchy** out) {
+  BT_TRY
+  if (!g) raise(BT_INVALID_ARGUMENT, "make_hierarchy: grid required");
+  validate_form(form);
+  if (kernel == 1 && form->kind == BT_FORM_DIV_K_GRAD)
+    raise(BT_INVALID_ARGUMENT, "stencil kernel requires a constant-coefficient form");
+  BT_CUDA(cudaSetDevice(g->device));
+  auto h = std::make_unique<bt_hierarchy>();
+  h->grid = g;
+  h->form = *form;
+  h->kernel = kernel;
+  for (int l = g->lo; l <= g->hi; ++l) {
+    auto L = std::make_unique<LevelData>();
+    L->level = l;
+    L->n = bt_space_size(g, BT_SPACE_P1, l);
+    const size_t n = (size_t)L->n;
+    for (DevBuf<double>* b : {&L->r, &L->d, &L->p, &L->ap, &L->z, &L->b, &L->x, &L->tmp, &L->diag}) {
+      b->alloc(n);
+      BT_CUDA(cudaMemset(b->p, 0, sizeof(double) * n));
+    }
+    if (kernel == 1) {
+      bt_stencil* st = nullptr;
+      if (bt_stencil_create(g, form, l, &st) != BT_OK) raise(BT_INVALID_ARGUMENT, bt_last_error());
+      L->stencil.reset(st);
+      BT_CUDA(cudaMemcpy(L->diag.p, st->d_diag.p, sizeof(double) * n, cudaMemcpyDeviceToDevice));
+    } else {
+      std::vector<EwCell> cells;
+      std::vector<EwAngles> angles;
+      build_ew_cells(*g, *form, l, cells, angles);
+      L->ew.upload(cells);
+      if (!angles.empty()) L->ang.upload(angles);
+      const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
+      static const double one[4] = {1.0, 0.0, 0.0, 0.0};
+      launch_elementwise(*g, l, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, L->ew.p, L->ang.p, nullptr,
+                         L->diag.p, true, 0);
+      launch_interface(*g, l, IF_SYNC, L->diag.p, nullptr, 0);
+    }
+    h->levels.push_back(std::move(L));
+  }
+  BT_CUDA(cudaDeviceSynchronize());
+  *out = h.release();
+  BT_CATCH
+}
+
+void bt_hierarchy_destroy(bt_hierarchy* h) { delete h; }
+
+bt_status bt_hierarchy_apply(bt_hierarchy* h, int level, const double* x, double* y, int bc, void* stream) {
+  BT_TRY
+  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  hier_apply(*h, level, x, y, bc, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_hierarchy_diagonal(bt_hierarchy* h, int level, const double** diag) {
+  BT_TRY
+  *diag = h->at(level).diag.p;
+  BT_CATCH
+}
+
+bt_status bt_estimate_lambda_max(bt_hierarchy* h, int level, double* out, void* stream) {
+  BT_TRY
+  *out = lambda_max(*h, level, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_smooth(bt_hierarchy* h, const bt_smoother_config* cfg, const double* rhs, double* x, int level,
+                    int sweeps, int backward, void* stream) {
+  BT_TRY
+  smooth(*h, *cfg, rhs, x, level, sweeps, backward, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_cg(bt_hierarchy* h, int level, double tol, int maxit, const double* rhs, double* x, double* hist,
+                int* iterations, void* stream) {
+  BT_TRY
+  const int it = cg(*h, level, tol, maxit, rhs, x, hist, (cudaStream_t)stream);
+  if (iterations) *iterations = it;
+  BT_CATCH
+}
+
+bt_status bt_v_cycle(bt_hierarchy* h, int level, const double* rhs, double* x, const bt_smoother_config* sm,
+                     const bt_multigrid_config* mg, void* stream) {
+  BT_TRY
+  v_cycle(*h, level, rhs, x, *sm, *mg, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+}  // extern "C"
