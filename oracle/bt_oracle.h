@@ -127,6 +127,9 @@ int bo_n1e1_apply(const bo_grid* g, int l, double alpha, double beta, int bc,
                   const double* x, double* y);
 void bo_n1e1_sync(const bo_grid* g, int l, double* v);
 void bo_n1e1_signs(const bo_grid* g, int l, int8_t* sign_of_member);
+void bo_n1e1_random_fill(const bo_grid* g, int l, uint64_t seed, double* out);
+void bo_n1e1_gradient(const bo_grid* g, int l, const double* phi, double* u);
+void bo_n1e1_constant_field(const bo_grid* g, int l, const double* c3, double* u);
 
 const char* bo_last_error(void);
 

@@ -107,13 +107,13 @@ def load_oracle():
     lib.bo_delinearize.argtypes = [C.c_int, C.c_int64, _PI32]
     lib.bo_width_formula.argtypes = [C.c_int, C.c_int]
     lib.bo_subgroup_offsets.argtypes = [C.c_int, _PI32]
-    for name in ("bo_n1e1_apply", "bo_n1e1_local", "bo_n1e1_sync", "bo_n1e1_signs"):
-        if not hasattr(lib, name):
-            continue
-    if hasattr(lib, "bo_n1e1_apply"):
-        lib.bo_n1e1_apply.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, _P, _P]
-        lib.bo_n1e1_local.argtypes = [_P, C.c_double, C.c_double, _P]
-        lib.bo_n1e1_sync.argtypes = [C.c_void_p, C.c_int, _P]
+    lib.bo_n1e1_apply.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, _P, _P]
+    lib.bo_n1e1_local.argtypes = [_P, C.c_double, C.c_double, _P]
+    lib.bo_n1e1_sync.argtypes = [C.c_void_p, C.c_int, _P]
+    lib.bo_n1e1_signs.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int8)]
+    lib.bo_n1e1_random_fill.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _P]
+    lib.bo_n1e1_gradient.argtypes = [C.c_void_p, C.c_int, _P, _P]
+    lib.bo_n1e1_constant_field.argtypes = [C.c_void_p, C.c_int, _P, _P]
     return lib
 
 
@@ -346,6 +346,32 @@ class Oracle(_Base):
         v = np.array(v, dtype=np.float64)
         self.lib.bo_n1e1_sync(self.h, level, _dp(v))
         return v
+
+    def n1e1_random_fill(self, level, seed):
+        v = self.zeros(level, space=2)
+        self.lib.bo_n1e1_random_fill(self.h, level, seed, _dp(v))
+        return v
+
+    def n1e1_gradient(self, level, phi):
+        u = self.zeros(level, space=2)
+        self.lib.bo_n1e1_gradient(self.h, level, _dp(np.ascontiguousarray(phi)), _dp(u))
+        return u
+
+    def n1e1_constant_field(self, level, c3):
+        u = self.zeros(level, space=2)
+        self.lib.bo_n1e1_constant_field(self.h, level, _dp(np.asarray(c3, np.float64)), _dp(u))
+        return u
+
+    def n1e1_signs(self, level):
+        off, cell, g, t = self.groups(level)
+        s = np.zeros(len(cell), np.int8)
+        self.lib.bo_n1e1_signs(self.h, level, s.ctypes.data_as(C.POINTER(C.c_int8)))
+        return s
+
+    def n1e1_local(self, corners, alpha=1.0, beta=1.0):
+        out = np.zeros(36)
+        self._chk(self.lib.bo_n1e1_local(_dp(np.asarray(corners, np.float64).ravel().copy()), alpha, beta, _dp(out)))
+        return out.reshape(6, 6)
 
 
 class Reference(_Base):

@@ -650,6 +650,18 @@ bt_status bt_grid_create(const char* text, int lo, int hi, int device, bt_grid**
   g->d_vhdr.upload(g->topo.vhdr);
   g->d_vmem.upload(g->topo.vmem);
   g->d_info.upload(g->topo.info);
+  for (int f = 0; f < (int)g->topo.faces.size(); ++f) {
+    if (g->topo.faces[f].ncell == 2) g->face_shared.push_back(f);
+    else if (g->topo.faces[f].dir) g->face_bdir.push_back(f);
+  }
+  for (int e = 0; e < (int)g->topo.ehdr.size(); ++e)
+    if (g->topo.ehdr[e].count >= 2 || g->topo.ehdr[e].dir) g->edge_act.push_back(e);
+  for (int v = 0; v < (int)g->topo.vhdr.size(); ++v)
+    if (g->topo.vhdr[v].count >= 2 || g->topo.vhdr[v].dir) g->vert_act.push_back(v);
+  g->d_face_shared.upload(g->face_shared);
+  g->d_face_bdir.upload(g->face_bdir);
+  g->d_edge_act.upload(g->edge_act);
+  g->d_vert_act.upload(g->vert_act);
   BT_CUDA(cudaMallocHost(&g->h_pinned, sizeof(double) * 8));
   *out = g.release();
   BT_CATCH
@@ -817,6 +829,7 @@ bt_status bt_stencil_create(const bt_grid* g, const bt_form* form, int level, bt
   std::vector<StencilCell> cells;
   build_stencil_cells(*g, *form, level, cells, st->rows);
   st->d_cells.upload(cells);
+  init_stencil_tasks(*st);
   // assembled diagonal: zero-set-typed partial diagonals, then additive sync
   const int nc = g->mesh.n_cells();
   std::vector<double> tbl(16 * (size_t)nc);

@@ -1,0 +1,158 @@
+// Interface pass: the reference's replica synchronisation
+// (sync_additive fe_function.hpp:400-423, sync_broadcast :425-446) and
+// Dirichlet rows (impose_dirichlet operators.hpp:98-104, zero_dirichlet
+// solvers.hpp:66-72) for P1 vertex DoFs, organised by macro primitive.
+//
+// Every lattice point on a macro face / edge / vertex is parametrised by its
+// barycentric weights on the primitive's sorted global vertices; each member
+// cell maps them to its own (i, j, k) through the local-vertex table lv, so
+// replica slots are computed, never stored. Members are visited in ascending
+// cell order — the reference's group order — so replica sums are bitwise
+// those of the reference.
+#include <cuda_runtime.h>
+
+#include "bt_internal.hpp"
+
+namespace bt {
+
+namespace {
+constexpr int kT = 256;
+
+struct FaceArgs {
+  const DevFace* faces;
+  const int* list;
+  int n;
+  int64_t cs;
+};
+struct PrimArgs {
+  const DevPrimHdr* eh;
+  const DevPrimMem* em;
+  const int* elist;
+  int ne;
+  const DevPrimHdr* vh;
+  const DevPrimMem* vm;
+  const int* vlist;
+  int nv;
+  int n;
+  int64_t cs;
+};
+
+__device__ __forceinline__ int64_t slot_of(int64_t cs, int w, int cell, int l0, int w0, int l1, int w1, int l2,
+                                           int w2) {
+  const int i = (l0 == 1 ? w0 : 0) + (l1 == 1 ? w1 : 0) + (l2 == 1 ? w2 : 0);
+  const int j = (l0 == 2 ? w0 : 0) + (l1 == 2 ? w1 : 0) + (l2 == 2 ? w2 : 0);
+  const int k = (l0 == 3 ? w0 : 0) + (l1 == 3 ? w1 : 0) + (l2 == 3 ? w2 : 0);
+  return (int64_t)cell * cs + row_start(w, j, k) + i;
+}
+
+// mode semantics for one replica group with slot function S(m), m < count
+template <int MODE, class S>
+__device__ __forceinline__ void apply_group(double* __restrict__ v, const double* __restrict__ src, int count,
+                                            bool dir, S slot) {
+  if (MODE == IF_SYNC || (MODE == IF_SYNC_DIR && !dir)) {
+    if (count < 2) return;
+    double sum = 0;
+    for (int m = 0; m < count; ++m) sum += v[slot(m)];
+    for (int m = 0; m < count; ++m) v[slot(m)] = sum;
+  } else if (MODE == IF_SYNC_DIR || MODE == IF_IMPOSE) {
+    if (!dir) return;
+    for (int m = 0; m < count; ++m) {
+      const int64_t t = slot(m);
+      v[t] = src[t];
+    }
+  } else if (MODE == IF_ZERO_DIR) {
+    if (!dir) return;
+    for (int m = 0; m < count; ++m) v[slot(m)] = 0.0;
+  } else if (MODE == IF_BCAST) {
+    if (count < 2) return;
+    const double val = v[slot(0)];
+    for (int m = 1; m < count; ++m) v[slot(m)] = val;
+  } else if (MODE == IF_ZERO_NONOWNED) {
+    for (int m = 1; m < count; ++m) v[slot(m)] = 0.0;
+  }
+}
+
+// Face-interior points (a, b), a, b >= 1, a + b <= n - 1, weights
+// (n - a - b, a, b) on the face's sorted global vertices.
+template <int MODE>
+__global__ void __launch_bounds__(kT) k_iface_faces(double* __restrict__ v, const double* __restrict__ src,
+                                                    FaceArgs a) {
+  const int n = a.n, w = n + 1;
+  const int q = blockIdx.x * kT + threadIdx.x;
+  if (q >= tri32(n - 2)) return;
+  const DevFace f = a.faces[a.list[blockIdx.y]];
+  int ap, bp;
+  decode_tri(n - 2, q, ap, bp);
+  const int aa = ap + 1, bb = bp + 1, cc = n - aa - bb;
+  const int64_t s0 = slot_of(a.cs, w, f.cell[0], f.lv[0][0], cc, f.lv[0][1], aa, f.lv[0][2], bb);
+  const int64_t s1 = f.ncell == 2 ? slot_of(a.cs, w, f.cell[1], f.lv[1][0], cc, f.lv[1][1], aa, f.lv[1][2], bb) : 0;
+  apply_group<MODE>(v, src, f.ncell, f.dir != 0, [&](int m) { return m == 0 ? s0 : s1; });
+}
+
+// Macro-edge interior points a = 1..n-1 (weights (n - a, a)) on blockIdx.y <
+// ne, then macro vertices.
+template <int MODE>
+__global__ void __launch_bounds__(kT) k_iface_prims(double* __restrict__ v, const double* __restrict__ src,
+                                                    PrimArgs a) {
+  const int n = a.n, w = n + 1;
+  if ((int)blockIdx.y < a.ne) {
+    const int aa = blockIdx.x * kT + threadIdx.x + 1;
+    if (aa > n - 1) return;
+    const DevPrimHdr h = a.eh[a.elist[blockIdx.y]];
+    const DevPrimMem* mem = a.em + h.first;
+    apply_group<MODE>(v, src, h.count, h.dir != 0, [&](int m) {
+      const DevPrimMem pm = mem[m];
+      return slot_of(a.cs, w, pm.cell, pm.lv[0], n - aa, pm.lv[1], aa, -1, 0);
+    });
+  } else {
+    if (blockIdx.x != 0) return;
+    const int vi = (blockIdx.y - a.ne) * kT + threadIdx.x;
+    if (vi >= a.nv) return;
+    const DevPrimHdr h = a.vh[a.vlist[vi]];
+    const DevPrimMem* mem = a.vm + h.first;
+    apply_group<MODE>(v, src, h.count, h.dir != 0, [&](int m) {
+      const DevPrimMem pm = mem[m];
+      return slot_of(a.cs, w, pm.cell, pm.lv[0], n, -1, 0, -1, 0);
+    });
+  }
+}
+
+template <int MODE>
+void launch_mode(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s) {
+  const int n = 1 << level;
+  const int64_t cs = n_tet(n + 1);
+  const int fp = tri32(n - 2);
+  auto faces = [&](const DevBuf<int>& list, size_t cnt) {
+    if (!cnt || !fp) return;
+    FaceArgs fa{g.d_faces.p, list.p, n, cs};
+    k_iface_faces<MODE><<<dim3((fp + kT - 1) / kT, (unsigned)cnt), kT, 0, s>>>(v, src, fa);
+    count_launch();
+  };
+  const bool sync_like = MODE == IF_SYNC || MODE == IF_BCAST || MODE == IF_ZERO_NONOWNED || MODE == IF_SYNC_DIR;
+  const bool dir_like = MODE == IF_SYNC_DIR || MODE == IF_IMPOSE || MODE == IF_ZERO_DIR;
+  if (sync_like) faces(g.d_face_shared, g.face_shared.size());
+  if (dir_like) faces(g.d_face_bdir, g.face_bdir.size());
+  const int ne = (int)g.edge_act.size(), nv = (int)g.vert_act.size();
+  if (ne + nv) {
+    PrimArgs pa{g.d_ehdr.p, g.d_emem.p, g.d_edge_act.p, ne, g.d_vhdr.p, g.d_vmem.p, g.d_vert_act.p, nv, n, cs};
+    const unsigned gy = (unsigned)(ne + (nv + kT - 1) / kT);
+    k_iface_prims<MODE><<<dim3((n - 1 + kT - 1) / kT, gy), kT, 0, s>>>(v, src, pa);
+    count_launch();
+  }
+  check_launch("k_interface");
+}
+
+}  // namespace
+
+void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
+  switch (mode) {
+    case IF_SYNC: launch_mode<IF_SYNC>(g, level, v, src, s); break;
+    case IF_SYNC_DIR: launch_mode<IF_SYNC_DIR>(g, level, v, src, s); break;
+    case IF_BCAST: launch_mode<IF_BCAST>(g, level, v, src, s); break;
+    case IF_IMPOSE: launch_mode<IF_IMPOSE>(g, level, v, src, s); break;
+    case IF_ZERO_DIR: launch_mode<IF_ZERO_DIR>(g, level, v, src, s); break;
+    case IF_ZERO_NONOWNED: launch_mode<IF_ZERO_NONOWNED>(g, level, v, src, s); break;
+  }
+}
+
+}  // namespace bt

@@ -137,6 +137,10 @@ struct bt_grid {
   bt::DevBuf<bt::DevPrimHdr> d_ehdr, d_vhdr;
   bt::DevBuf<bt::DevPrimMem> d_emem, d_vmem;
   bt::DevBuf<bt::DevCellInfo> d_info;
+  // interface work lists: shared faces (2 cells), constrained boundary faces,
+  // edges / vertices that are shared or constrained
+  std::vector<int> face_shared, face_bdir, edge_act, vert_act;
+  bt::DevBuf<int> d_face_shared, d_face_bdir, d_edge_act, d_vert_act;
   // reduction scratch for dot products
   mutable bt::DevBuf<double> d_partials;
   mutable double* h_pinned = nullptr;
@@ -171,6 +175,8 @@ struct bt_stencil {
   std::vector<std::array<double, 15>> rows;  // host copy of StencilTable::rows
   bt::DevBuf<bt::StencilCell> d_cells;
   bt::DevBuf<double> d_diag;                 // assembled diagonal
+  bt::DevBuf<int4> d_tasks;                  // warp march schedule (level-only, see k_stencil)
+  int ntasks = 0;
 };
 
 namespace bt {
@@ -189,6 +195,7 @@ enum IfaceMode { IF_SYNC = 0, IF_SYNC_DIR = 1, IF_BCAST = 2, IF_IMPOSE = 3, IF_Z
 void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src,
                       cudaStream_t s);
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s);
+void init_stencil_tasks(bt_stencil& st);
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c,
                         const EwCell* d_cells, const EwAngles* d_angles, const double* x, double* y,
                         bool diag_only, cudaStream_t s);

@@ -41,200 +41,126 @@ constexpr int kRowsPerCta = 64;
 static inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // ---------------------------------------------------------------------------
-// Interface pass (sync_additive / sync_broadcast / Dirichlet rows)
-// ---------------------------------------------------------------------------
-struct IfaceArgs {
-  const DevFace* faces;
-  int nfaces;
-  const DevPrimHdr* eh;
-  const DevPrimMem* em;
-  int nedges;
-  const DevPrimHdr* vh;
-  const DevPrimMem* vm;
-  int nverts;
-  int n;
-  int64_t cell_slots;
-};
-
-__device__ __forceinline__ int64_t member_slot(int64_t cell_slots, int w, int cell, int i, int j, int k) {
-  return (int64_t)cell * cell_slots + row_start(w, j, k) + i;
-}
-
-// weights of local vertices 1..3 given up to three (local vertex, weight)
-__device__ __forceinline__ void ijk_from(int l0, int w0, int l1, int w1, int l2, int w2, int& i, int& j, int& k) {
-  i = (l0 == 1 ? w0 : 0) + (l1 == 1 ? w1 : 0) + (l2 == 1 ? w2 : 0);
-  j = (l0 == 2 ? w0 : 0) + (l1 == 2 ? w1 : 0) + (l2 == 2 ? w2 : 0);
-  k = (l0 == 3 ? w0 : 0) + (l1 == 3 ? w1 : 0) + (l2 == 3 ? w2 : 0);
-}
-
-template <int MODE>
-__device__ __forceinline__ void iface_apply(double* __restrict__ v, const double* __restrict__ src, int count,
-                                            bool dir, const int64_t* slots) {
-  if (MODE == IF_SYNC) {
-    if (count < 2) return;
-    double sum = 0;
-    for (int m = 0; m < count; ++m) sum += v[slots[m]];
-    for (int m = 0; m < count; ++m) v[slots[m]] = sum;
-  } else if (MODE == IF_SYNC_DIR) {
-    if (dir) {
-      for (int m = 0; m < count; ++m) v[slots[m]] = src[slots[m]];
-    } else if (count >= 2) {
-      double sum = 0;
-      for (int m = 0; m < count; ++m) sum += v[slots[m]];
-      for (int m = 0; m < count; ++m) v[slots[m]] = sum;
-    }
-  } else if (MODE == IF_BCAST) {
-    if (count < 2) return;
-    const double val = v[slots[0]];
-    for (int m = 1; m < count; ++m) v[slots[m]] = val;
-  } else if (MODE == IF_IMPOSE) {
-    if (dir)
-      for (int m = 0; m < count; ++m) v[slots[m]] = src[slots[m]];
-  } else if (MODE == IF_ZERO_DIR) {
-    if (dir)
-      for (int m = 0; m < count; ++m) v[slots[m]] = 0.0;
-  } else if (MODE == IF_ZERO_NONOWNED) {
-    for (int m = 1; m < count; ++m) v[slots[m]] = 0.0;
-  }
-}
-
-constexpr int kMaxMembers = 64;
-
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_interface(double* __restrict__ v, const double* __restrict__ src,
-                                                        IfaceArgs a) {
-  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int n = a.n, w = n + 1;
-  const int64_t FP = tri32(n - 2);
-  const int64_t nF = (int64_t)a.nfaces * FP;
-  const int64_t nE = (int64_t)a.nedges * (n - 1);
-  int64_t slots[kMaxMembers];
-  if (id < nF) {
-    const int f = (int)(id / FP);
-    const int q = (int)(id - (int64_t)f * FP);
-    int ap, bp;
-    decode_tri(n - 2, q, ap, bp);
-    const int aa = ap + 1, bb = bp + 1;
-    const DevFace fr = a.faces[f];
-    for (int s = 0; s < fr.ncell; ++s) {
-      int i, j, k;
-      ijk_from(fr.lv[s][0], n - aa - bb, fr.lv[s][1], aa, fr.lv[s][2], bb, i, j, k);
-      slots[s] = member_slot(a.cell_slots, w, fr.cell[s], i, j, k);
-    }
-    iface_apply<MODE>(v, src, fr.ncell, fr.dir != 0, slots);
-  } else if (id < nF + nE) {
-    const int64_t r = id - nF;
-    const int e = (int)(r / (n - 1));
-    const int aa = (int)(r - (int64_t)e * (n - 1)) + 1;
-    const DevPrimHdr hd = a.eh[e];
-    const int cnt = min(hd.count, kMaxMembers);
-    for (int m = 0; m < cnt; ++m) {
-      const DevPrimMem pm = a.em[hd.first + m];
-      int i, j, k;
-      ijk_from(pm.lv[0], n - aa, pm.lv[1], aa, -1, 0, i, j, k);
-      slots[m] = member_slot(a.cell_slots, w, pm.cell, i, j, k);
-    }
-    iface_apply<MODE>(v, src, cnt, hd.dir != 0, slots);
-  } else if (id < nF + nE + a.nverts) {
-    const int vv = (int)(id - nF - nE);
-    const DevPrimHdr hd = a.vh[vv];
-    const int cnt = min(hd.count, kMaxMembers);
-    for (int m = 0; m < cnt; ++m) {
-      const DevPrimMem pm = a.vm[hd.first + m];
-      int i, j, k;
-      ijk_from(pm.lv[0], n, -1, 0, -1, 0, i, j, k);
-      slots[m] = member_slot(a.cell_slots, w, pm.cell, i, j, k);
-    }
-    iface_apply<MODE>(v, src, cnt, hd.dir != 0, slots);
-  }
-}
-
-void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
-  IfaceArgs a;
-  a.faces = g.d_faces.p;
-  a.nfaces = (int)g.topo.faces.size();
-  a.eh = g.d_ehdr.p;
-  a.em = g.d_emem.p;
-  a.nedges = (int)g.topo.ehdr.size();
-  a.vh = g.d_vhdr.p;
-  a.vm = g.d_vmem.p;
-  a.nverts = (int)g.topo.vhdr.size();
-  a.n = 1 << level;
-  a.cell_slots = n_tet(a.n + 1);
-  for (const auto& h : g.topo.vhdr)
-    if (h.count > kMaxMembers) raise(BT_INVALID_ARGUMENT, "macro vertex shared by more than 64 cells");
-  const int64_t total = (int64_t)a.nfaces * tri32(a.n - 2) + (int64_t)a.nedges * (a.n - 1) + a.nverts;
-  if (total == 0) return;
-  const int blocks = ceil_div(total, kThreads);
-  switch (mode) {
-    case IF_SYNC: k_interface<IF_SYNC><<<blocks, kThreads, 0, s>>>(v, src, a); break;
-    case IF_SYNC_DIR: k_interface<IF_SYNC_DIR><<<blocks, kThreads, 0, s>>>(v, src, a); break;
-    case IF_BCAST: k_interface<IF_BCAST><<<blocks, kThreads, 0, s>>>(v, src, a); break;
-    case IF_IMPOSE: k_interface<IF_IMPOSE><<<blocks, kThreads, 0, s>>>(v, src, a); break;
-    case IF_ZERO_DIR: k_interface<IF_ZERO_DIR><<<blocks, kThreads, 0, s>>>(v, src, a); break;
-    case IF_ZERO_NONOWNED: k_interface<IF_ZERO_NONOWNED><<<blocks, kThreads, 0, s>>>(v, src, a); break;
-  }
-  count_launch();
-  check_launch("k_interface");
-}
-
-// ---------------------------------------------------------------------------
 // P1 constant-coefficient 15-point stencil (apply_stencil operators.hpp:247)
 // ---------------------------------------------------------------------------
-// Interior vertices use the merged row in registers; lattice-boundary
-// vertices use the zero-set-typed partial row (the per-cell part of
+// Register sliding-window march. A warp owns 30 consecutive columns i of one
+// layer k (lanes 0 and 31 are halo columns) and marches up to kMarchRows rows
+// j. Per step it loads three new rows at its own column — A(j+1) of layer k,
+// B(j) of layer k+1, C(j+1) of layer k-1, each a coalesced 256 B access —
+// and obtains the i-1 / i+1 neighbours by warp shuffles, so every x value is
+// loaded once per layer it touches instead of 15 times. Out-of-lattice
+// neighbours load as 0, so lattice-boundary vertices use the same 15-term
+// form with their zero-set-typed partial row (per-cell part of
 // partial_row_apply, operators.hpp:78-96), completed by the interface pass.
-__global__ void __launch_bounds__(kThreads) k_stencil(const double* __restrict__ x, double* __restrict__ y,
-                                                      const StencilCell* __restrict__ cells, int w,
-                                                      int64_t cell_slots) {
-  __shared__ StencilCell sc;
+constexpr int kMarchRows = 32;
+constexpr int kMarchCols = 30;
+
+__global__ void __launch_bounds__(kThreads, 2) k_stencil(const double* __restrict__ x, double* __restrict__ y,
+                                                         const StencilCell* __restrict__ cells,
+                                                         const int4* __restrict__ tasks, int ntasks, int w,
+                                                         int64_t cell_slots) {
+  __shared__ double sw[16][15];
   const int cell = blockIdx.y;
   {
-    const double* src = reinterpret_cast<const double*>(cells + cell);
-    double* dst = reinterpret_cast<double*>(&sc);
-    for (int q = threadIdx.x; q < (int)(sizeof(StencilCell) / 8); q += blockDim.x) dst[q] = src[q];
+    const double* src = cells[cell].w[0];
+    for (int q = threadIdx.x; q < 16 * 15; q += blockDim.x) sw[q / 15][q % 15] = src[q];
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int task = blockIdx.x * kWarps + warp;
+  if (task >= ntasks) return;
   double w0[15];
 #pragma unroll
-  for (int d = 0; d < 15; ++d) w0[d] = sc.w[0][d];
+  for (int d = 0; d < 15; ++d) w0[d] = sw[0][d];
+  const int4 tk = tasks[task];
+  const int k = tk.x, j0 = tk.z, j1 = tk.w;
+  const int n = w - 1;
+  const int i = kMarchCols * tk.y + lane - 1;
+  const bool out_lane = lane >= 1 && lane <= kMarchCols;
   const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
   double* __restrict__ yc = y + (int64_t)cell * cell_slots;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nrows = tri32(w);
-  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
-  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
-    int j, k;
-    decode_row(w, r, j, k);
-    const int L = w - j - k;
-    const int t0 = row_start(w, j, k);
-    int off[15];
-    row_offsets(w, j, k, off);
-    const int zrow = (j == 0 ? 4 : 0) | (k == 0 ? 8 : 0);
-    for (int i = lane; i < L; i += 32) {
-      const int t = t0 + i;
-      const int z = zrow | (i == L - 1 ? 1 : 0) | (i == 0 ? 2 : 0);
-      double acc;
-      if (z == 0) {
-        acc = w0[0] * __ldg(xc + t);
-#pragma unroll
-        for (int d = 1; d < 15; ++d) acc = fma(w0[d], __ldg(xc + t + off[d]), acc);
-      } else {
-        const uint32_t msk = sc.mask[z];
-        acc = 0.0;
-#pragma unroll
-        for (int d = 0; d < 15; ++d)
-          if (msk >> d & 1) acc = fma(sc.w[z][d], __ldg(xc + t + off[d]), acc);
-      }
-      yc[t] = acc;
+  const bool up = k + 1 <= n, dn = k >= 1;
+  // predicated column load of a row with start rs and length len
+  auto ld = [&](bool ok, int rs, int len) -> double { return (ok && i >= 0 && i < len) ? __ldg(xc + rs + i) : 0.0; };
+  // window at step j0: A(j0-1), A(j0), B(j0-1), C(j0)
+  double Am1 = j0 >= 1 ? ld(true, row_start(w, j0 - 1, k), w - k - j0 + 1) : 0.0;
+  double A0 = ld(true, row_start(w, j0, k), w - k - j0);
+  double Bm1 = j0 >= 1 ? ld(up, up ? row_start(w, j0 - 1, k + 1) : 0, w - k - j0) : 0.0;
+  double C0 = ld(dn, dn ? row_start(w, j0, k - 1) : 0, w - k - j0 + 1);
+  double Am1p = __shfl_down_sync(0xffffffffu, Am1, 1);
+  double A0p = __shfl_down_sync(0xffffffffu, A0, 1);
+  double A0m = __shfl_up_sync(0xffffffffu, A0, 1);
+  double Bm1p = __shfl_down_sync(0xffffffffu, Bm1, 1);
+  double C0p = __shfl_down_sync(0xffffffffu, C0, 1);
+  // row cursors for the rows loaded at step j: A(j+1), B(j), C(j+1)
+  int sA = row_start(w, j0 + 1, k), LA = w - k - j0 - 1;
+  int sB = up ? row_start(w, j0, k + 1) : 0, LB = w - k - 1 - j0;
+  int sC = dn ? row_start(w, j0 + 1, k - 1) : 0, LC = w - k - j0;
+  int sY = row_start(w, j0, k), LY = w - k - j0;
+  double nA = ld(true, sA, LA), nB = ld(up, sB, LB), nC = ld(dn, sC, LC);
+  for (int j = j0; j < j1; ++j) {
+    const double A1 = nA, B0 = nB, C1 = nC;
+    sA += LA; --LA;
+    sB += LB; --LB;
+    sC += LC; --LC;
+    if (j + 1 < j1) {  // prefetch the next step's rows
+      nA = ld(true, sA, LA);
+      nB = ld(up, sB, LB);
+      nC = ld(dn, sC, LC);
     }
+    const double A1m = __shfl_up_sync(0xffffffffu, A1, 1);
+    const double A1p = __shfl_down_sync(0xffffffffu, A1, 1);
+    const double B0m = __shfl_up_sync(0xffffffffu, B0, 1);
+    const double B0p = __shfl_down_sync(0xffffffffu, B0, 1);
+    const double C1m = __shfl_up_sync(0xffffffffu, C1, 1);
+    const double C1p = __shfl_down_sync(0xffffffffu, C1, 1);
+    if (out_lane && i < LY) {
+      // kStencilDirs order (operators.hpp:22-26)
+      const double v[15] = {A0, A0p, A1, B0, Am1p, C0p, C1, Bm1p, A0m, Am1, C0, A1m, B0m, Bm1, C1m};
+      const bool interior = i >= 1 && i <= LY - 2 && j >= 1 && k >= 1;
+      double acc;
+      if (interior) {
+        acc = w0[0] * v[0];
+#pragma unroll
+        for (int d = 1; d < 15; ++d) acc = fma(w0[d], v[d], acc);
+      } else {
+        const int z = (i == LY - 1 ? 1 : 0) | (i == 0 ? 2 : 0) | (j == 0 ? 4 : 0) | (k == 0 ? 8 : 0);
+        acc = sw[z][0] * v[0];
+#pragma unroll
+        for (int d = 1; d < 15; ++d) acc = fma(sw[z][d], v[d], acc);
+      }
+      yc[sY + i] = acc;
+    }
+    sY += LY;
+    --LY;
+    Am1 = A0;
+    Am1p = A0p;
+    A0 = A1;
+    A0p = A1p;
+    A0m = A1m;
+    Bm1 = B0;
+    Bm1p = B0p;
+    C0 = C1;
+    C0p = C1p;
   }
+}
+
+void init_stencil_tasks(bt_stencil& st) {
+  const int w = (1 << st.level) + 1;
+  std::vector<int4> t;
+  for (int k = 0; k < w; ++k)
+    for (int b = 0; kMarchCols * b < w - k; ++b) {
+      const int jmax = w - k - kMarchCols * b;
+      for (int j0 = 0; j0 < jmax; j0 += kMarchRows) t.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, jmax)));
+    }
+  st.ntasks = (int)t.size();
+  st.d_tasks.upload(t);
 }
 
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
   const int w = (1 << st.level) + 1;
-  dim3 grid(ceil_div(tri32(w), kRowsPerCta), st.grid->mesh.n_cells());
-  k_stencil<<<grid, kThreads, 0, s>>>(x, y, st.d_cells.p, w, n_tet(w));
+  dim3 grid(ceil_div(st.ntasks, kWarps), st.grid->mesh.n_cells());
+  k_stencil<<<grid, kThreads, 0, s>>>(x, y, st.d_cells.p, st.d_tasks.p, st.ntasks, w, n_tet(w));
   count_launch();
   check_launch("k_stencil");
 }
