@@ -688,3 +688,38 @@ def v_cycle(h: GridHierarchy, l, rhs: FEFunction, x: FEFunction, sm: SmootherCon
     s = sm.c_struct()
     m = mg.c_struct()
     _check(_L.bt_v_cycle(h.handle, l, _ptr(rhs.values[l]), _ptr(x.values[l]), C.byref(s), C.byref(m), _stream()))
+
+
+# ---------------------------------------------------------------------------
+# Nedelec N1E1 curl-curl + mass (no reference implementation)
+# ---------------------------------------------------------------------------
+class N1E1Operator:
+    """alpha curl curl + beta identity on the lowest-order edge space of one
+    level (7 edge subgroups per macro-cell), device-resident."""
+
+    def __init__(self, grid: Grid, level: int, alpha: float = 1.0, beta: float = 1.0):
+        self.grid = grid
+        self.level = level
+        h = C.c_void_p()
+        _check(_L.bt_n1e1_create(grid.handle, level, float(alpha), float(beta), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _L.bt_n1e1_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+
+def apply_n1e1(op: N1E1Operator, src: FEFunction, dst: FEFunction, l=None, bc=BC.DirichletIdentity):
+    l = op.level if l is None else l
+    if src.descriptor.space != 2 or dst.descriptor.space != 2:
+        raise InvalidArgument("N1E1 operator requires edge-space functions")
+    _compatible(src, dst, l)
+    if src is dst:
+        raise InvalidArgument("source and destination must be distinct")
+    _check(_L.bt_apply_n1e1(op.handle, _ptr(src.values[l]), _ptr(dst.values[l]), int(bc), _stream()))

@@ -793,7 +793,11 @@ int64_t bt_cubes_mesh_text(int n, double perturb, uint64_t seed, char* buf, int6
 bt_status bt_random_fill(const bt_grid* g, int space, int level, uint64_t seed, double* x, void* stream) {
   BT_TRY
   check_level(g, level);
-  if (space != BT_SPACE_P1) raise(BT_INVALID_ARGUMENT, "bt_random_fill: P1 space only (edge spaces: N1E1 path)");
+  if (space == BT_SPACE_EDGES) {
+    random_fill_edges(*g, level, seed, x, (cudaStream_t)stream);
+    return BT_OK;
+  }
+  if (space != BT_SPACE_P1) raise(BT_INVALID_ARGUMENT, "bt_random_fill: P1 or edge space expected");
   // fe_function.hpp:479-497: owned slots in canonical (cell, entry, t) order
   const int n = 1 << level, w = n + 1;
   const int64_t per = n_tet(w), total = per * g->mesh.n_cells();

@@ -202,6 +202,11 @@ void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const doubl
 void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStream_t s);
 void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s);
 double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s);
+// edge space (N1E1, bt_n1e1.cu): signed replica sync / broadcast, Dirichlet rows
+void launch_edge_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src,
+                           cudaStream_t s);
+double dot_edges(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s);
+void random_fill_edges(const bt_grid& g, int level, uint64_t seed, double* x, cudaStream_t s);
 void launch_prolongate(const bt_grid& g, int fine_level, const double* coarse, double* fine, bool add,
                        cudaStream_t s);
 void launch_restrict(const bt_grid& g, int fine_level, const double* fine, double* coarse,

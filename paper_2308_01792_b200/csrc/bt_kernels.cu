@@ -41,131 +41,6 @@ constexpr int kRowsPerCta = 64;
 static inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // ---------------------------------------------------------------------------
-// P1 constant-coefficient 15-point stencil (apply_stencil operators.hpp:247)
-// ---------------------------------------------------------------------------
-// Register sliding-window march. A warp owns 30 consecutive columns i of one
-// layer k (lanes 0 and 31 are halo columns) and marches up to kMarchRows rows
-// j. Per step it loads three new rows at its own column — A(j+1) of layer k,
-// B(j) of layer k+1, C(j+1) of layer k-1, each a coalesced 256 B access —
-// and obtains the i-1 / i+1 neighbours by warp shuffles, so every x value is
-// loaded once per layer it touches instead of 15 times. Out-of-lattice
-// neighbours load as 0, so lattice-boundary vertices use the same 15-term
-// form with their zero-set-typed partial row (per-cell part of
-// partial_row_apply, operators.hpp:78-96), completed by the interface pass.
-constexpr int kMarchRows = 32;
-constexpr int kMarchCols = 30;
-
-__global__ void __launch_bounds__(kThreads, 2) k_stencil(const double* __restrict__ x, double* __restrict__ y,
-                                                         const StencilCell* __restrict__ cells,
-                                                         const int4* __restrict__ tasks, int ntasks, int w,
-                                                         int64_t cell_slots) {
-  __shared__ double sw[16][15];
-  const int cell = blockIdx.y;
-  {
-    const double* src = cells[cell].w[0];
-    for (int q = threadIdx.x; q < 16 * 15; q += blockDim.x) sw[q / 15][q % 15] = src[q];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int task = blockIdx.x * kWarps + warp;
-  if (task >= ntasks) return;
-  double w0[15];
-#pragma unroll
-  for (int d = 0; d < 15; ++d) w0[d] = sw[0][d];
-  const int4 tk = tasks[task];
-  const int k = tk.x, j0 = tk.z, j1 = tk.w;
-  const int n = w - 1;
-  const int i = kMarchCols * tk.y + lane - 1;
-  const bool out_lane = lane >= 1 && lane <= kMarchCols;
-  const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
-  double* __restrict__ yc = y + (int64_t)cell * cell_slots;
-  const bool up = k + 1 <= n, dn = k >= 1;
-  // predicated column load of a row with start rs and length len
-  auto ld = [&](bool ok, int rs, int len) -> double { return (ok && i >= 0 && i < len) ? __ldg(xc + rs + i) : 0.0; };
-  // window at step j0: A(j0-1), A(j0), B(j0-1), C(j0)
-  double Am1 = j0 >= 1 ? ld(true, row_start(w, j0 - 1, k), w - k - j0 + 1) : 0.0;
-  double A0 = ld(true, row_start(w, j0, k), w - k - j0);
-  double Bm1 = j0 >= 1 ? ld(up, up ? row_start(w, j0 - 1, k + 1) : 0, w - k - j0) : 0.0;
-  double C0 = ld(dn, dn ? row_start(w, j0, k - 1) : 0, w - k - j0 + 1);
-  double Am1p = __shfl_down_sync(0xffffffffu, Am1, 1);
-  double A0p = __shfl_down_sync(0xffffffffu, A0, 1);
-  double A0m = __shfl_up_sync(0xffffffffu, A0, 1);
-  double Bm1p = __shfl_down_sync(0xffffffffu, Bm1, 1);
-  double C0p = __shfl_down_sync(0xffffffffu, C0, 1);
-  // row cursors for the rows loaded at step j: A(j+1), B(j), C(j+1)
-  int sA = row_start(w, j0 + 1, k), LA = w - k - j0 - 1;
-  int sB = up ? row_start(w, j0, k + 1) : 0, LB = w - k - 1 - j0;
-  int sC = dn ? row_start(w, j0 + 1, k - 1) : 0, LC = w - k - j0;
-  int sY = row_start(w, j0, k), LY = w - k - j0;
-  double nA = ld(true, sA, LA), nB = ld(up, sB, LB), nC = ld(dn, sC, LC);
-  for (int j = j0; j < j1; ++j) {
-    const double A1 = nA, B0 = nB, C1 = nC;
-    sA += LA; --LA;
-    sB += LB; --LB;
-    sC += LC; --LC;
-    if (j + 1 < j1) {  // prefetch the next step's rows
-      nA = ld(true, sA, LA);
-      nB = ld(up, sB, LB);
-      nC = ld(dn, sC, LC);
-    }
-    const double A1m = __shfl_up_sync(0xffffffffu, A1, 1);
-    const double A1p = __shfl_down_sync(0xffffffffu, A1, 1);
-    const double B0m = __shfl_up_sync(0xffffffffu, B0, 1);
-    const double B0p = __shfl_down_sync(0xffffffffu, B0, 1);
-    const double C1m = __shfl_up_sync(0xffffffffu, C1, 1);
-    const double C1p = __shfl_down_sync(0xffffffffu, C1, 1);
-    if (out_lane && i < LY) {
-      // kStencilDirs order (operators.hpp:22-26)
-      const double v[15] = {A0, A0p, A1, B0, Am1p, C0p, C1, Bm1p, A0m, Am1, C0, A1m, B0m, Bm1, C1m};
-      const bool interior = i >= 1 && i <= LY - 2 && j >= 1 && k >= 1;
-      double acc;
-      if (interior) {
-        acc = w0[0] * v[0];
-#pragma unroll
-        for (int d = 1; d < 15; ++d) acc = fma(w0[d], v[d], acc);
-      } else {
-        const int z = (i == LY - 1 ? 1 : 0) | (i == 0 ? 2 : 0) | (j == 0 ? 4 : 0) | (k == 0 ? 8 : 0);
-        acc = sw[z][0] * v[0];
-#pragma unroll
-        for (int d = 1; d < 15; ++d) acc = fma(sw[z][d], v[d], acc);
-      }
-      yc[sY + i] = acc;
-    }
-    sY += LY;
-    --LY;
-    Am1 = A0;
-    Am1p = A0p;
-    A0 = A1;
-    A0p = A1p;
-    A0m = A1m;
-    Bm1 = B0;
-    Bm1p = B0p;
-    C0 = C1;
-    C0p = C1p;
-  }
-}
-
-void init_stencil_tasks(bt_stencil& st) {
-  const int w = (1 << st.level) + 1;
-  std::vector<int4> t;
-  for (int k = 0; k < w; ++k)
-    for (int b = 0; kMarchCols * b < w - k; ++b) {
-      const int jmax = w - k - kMarchCols * b;
-      for (int j0 = 0; j0 < jmax; j0 += kMarchRows) t.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, jmax)));
-    }
-  st.ntasks = (int)t.size();
-  st.d_tasks.upload(t);
-}
-
-void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
-  const int w = (1 << st.level) + 1;
-  dim3 grid(ceil_div(st.ntasks, kWarps), st.grid->mesh.n_cells());
-  k_stencil<<<grid, kThreads, 0, s>>>(x, y, st.d_cells.p, st.d_tasks.p, st.ntasks, w, n_tet(w));
-  count_launch();
-  check_launch("k_stencil");
-}
-
-// ---------------------------------------------------------------------------
 // Elementwise P1 apply with on-the-fly coefficient (apply_elementwise
 // operators.hpp:115-164, local_matrix forms.hpp:75-120), pull form:
 // y_v = sum over present micro-cells T of v: kbar_T * (G_s row) . x_T, with
@@ -557,6 +432,10 @@ bt_status bt_dot(const bt_grid* g, int space, int level, const double* x, const 
                  void* stream) {
   BT_TRY
   check_level(g, level);
+  if (space == BT_SPACE_EDGES) {
+    *out = dot_edges(*g, level, x, y, (cudaStream_t)stream);
+    return BT_OK;
+  }
   require_p1(space);
   *out = dot_p1(*g, level, x, y, (cudaStream_t)stream);
   BT_CATCH
@@ -564,6 +443,10 @@ bt_status bt_dot(const bt_grid* g, int space, int level, const double* x, const 
 bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, void* stream) {
   BT_TRY
   check_level(g, level);
+  if (space == BT_SPACE_EDGES) {
+    launch_edge_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
+    return BT_OK;
+  }
   require_p1(space);
   launch_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
   BT_CATCH
@@ -571,6 +454,10 @@ bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, vo
 bt_status bt_sync_broadcast(const bt_grid* g, int space, int level, double* x, void* stream) {
   BT_TRY
   check_level(g, level);
+  if (space == BT_SPACE_EDGES) {
+    launch_edge_interface(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
+    return BT_OK;
+  }
   require_p1(space);
   launch_interface(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
   BT_CATCH

@@ -1,19 +1,573 @@
-// Nédélec N1E1 curl-curl + mass operator (no reference implementation;
-// SPEC.md:8). Placeholder entry points until the kernel lands.
+// Nédélec N1E1 (lowest-order Whitney edge element) curl-curl + mass
+// operator, alpha curl curl u + beta u, applied matrix-free over the seven
+// micro-edge orientations (x, y, z, xy, xz, yz, xyz) of the reference's edge
+// storage (micro_index.hpp:220-228). The reference has no N1E1 operator
+// (SPEC.md:8); conventions are documented in oracle/bt_oracle_n1e1.c and
+// DESIGN.md, and the oracle there is the checker.
+//
+// Layout: the edge space of one level is cells outer, then the 7 edge
+// subgroups (widths 2^l, ..., 2^l - 1), then lattice slots (Code-1 order).
+// Kernels walk the rows of each subgroup lattice; an interior edge uses the
+// merged per-(cell, orientation) stencil of 19 or 13 coupled edges, a
+// lattice-boundary edge sums the element rows of its present micro-tets.
+// Replicated edges on macro faces/edges are summed with orientation signs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <vector>
+
 #include "bt_internal.hpp"
 
+namespace bt {
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int kW = kT / 32;
+constexpr int kRows = 64;
+
+static const int hOffEdge[7][2][3] = BT_EDGE_OFFSETS;
+static const int hOffCell[6][4][3] = BT_CELL_OFFSETS;
+static const int hLoc[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+
+struct IncTet {  // a micro-tet containing an edge of subgroup g
+  int s, le, sigma;
+  int dq[3];     // tet anchor - edge anchor
+  int nb[6];     // neighbour index of the tet's local edge j
+};
+struct Nb {      // coupled edge: subgroup and anchor offset
+  int g, d[3];
+};
+struct N1e1Static {
+  int ninc[8];
+  IncTet inc[8][6];
+  int nnb[8];
+  Nb nb[8][19];
+  int emap_g[6][6], emap_sigma[6][6];
+  int dir_g[27], dir_sigma[27];  // lattice direction code -> (subgroup, sign)
+};
+__constant__ N1e1Static cS;
+static N1e1Static hS;
+static bool hS_ready = false;
+
+int dcode(int dx, int dy, int dz) { return (dx + 1) * 9 + (dy + 1) * 3 + (dz + 1); }
+
+void build_static() {
+  if (hS_ready) return;
+  std::memset(&hS, 0, sizeof hS);
+  for (int c = 0; c < 27; ++c) hS.dir_g[c] = -1;
+  for (int g = 1; g <= 7; ++g) {
+    int e[3];
+    for (int a = 0; a < 3; ++a) e[a] = hOffEdge[g - 1][1][a] - hOffEdge[g - 1][0][a];
+    hS.dir_g[dcode(e[0], e[1], e[2])] = g;
+    hS.dir_sigma[dcode(e[0], e[1], e[2])] = 1;
+    hS.dir_g[dcode(-e[0], -e[1], -e[2])] = g;
+    hS.dir_sigma[dcode(-e[0], -e[1], -e[2])] = -1;
+  }
+  int emap_d[6][6][3];
+  for (int s = 0; s < 6; ++s)
+    for (int le = 0; le < 6; ++le) {
+      const int* oa = hOffCell[s][hLoc[le][0]];
+      const int* ob = hOffCell[s][hLoc[le][1]];
+      const int c = dcode(ob[0] - oa[0], ob[1] - oa[1], ob[2] - oa[2]);
+      const int g = hS.dir_g[c], sg = hS.dir_sigma[c];
+      hS.emap_g[s][le] = g;
+      hS.emap_sigma[s][le] = sg;
+      const int* from = sg > 0 ? oa : ob;
+      for (int a = 0; a < 3; ++a) emap_d[s][le][a] = from[a] - hOffEdge[g - 1][0][a];
+    }
+  for (int s = 0; s < 6; ++s)
+    for (int le = 0; le < 6; ++le) {
+      const int g = hS.emap_g[s][le];
+      IncTet& it = hS.inc[g][hS.ninc[g]++];
+      it.s = s;
+      it.le = le;
+      it.sigma = hS.emap_sigma[s][le];
+      for (int a = 0; a < 3; ++a) it.dq[a] = -emap_d[s][le][a];
+      for (int j = 0; j < 6; ++j) {
+        Nb nb{hS.emap_g[s][j], {it.dq[0] + emap_d[s][j][0], it.dq[1] + emap_d[s][j][1], it.dq[2] + emap_d[s][j][2]}};
+        int m = 0;
+        for (; m < hS.nnb[g]; ++m)
+          if (hS.nb[g][m].g == nb.g && hS.nb[g][m].d[0] == nb.d[0] && hS.nb[g][m].d[1] == nb.d[1] &&
+              hS.nb[g][m].d[2] == nb.d[2])
+            break;
+        if (m == hS.nnb[g]) hS.nb[g][hS.nnb[g]++] = nb;
+        it.nb[j] = m;
+      }
+    }
+  BT_CUDA(cudaMemcpyToSymbol(cS, &hS, sizeof hS));
+  hS_ready = true;
+}
+
+int64_t entry_off(int g, int l) {
+  int64_t o = 0;
+  for (int q = 1; q < g; ++q) o += n_tet(width_formula(q, l));
+  return o;
+}
+
+// alpha K + beta M on the tet with corners X (same formulas as the oracle)
+void local_n1e1(const double X[4][3], double alpha, double beta, double out[36]) {
+  double a[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) a[3 * r + c] = X[c + 1][r] - X[0][r];
+  const double det = a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+                     a[2] * (a[3] * a[7] - a[4] * a[6]);
+  if (det == 0.0 || !std::isfinite(det)) raise(BT_INVALID_ARGUMENT, "n1e1: degenerate element");
+  const double vol = std::abs(det) / 6.0, d = det;
+  const double inv[9] = {(a[4] * a[8] - a[5] * a[7]) / d, (a[2] * a[7] - a[1] * a[8]) / d,
+                         (a[1] * a[5] - a[2] * a[4]) / d, (a[5] * a[6] - a[3] * a[8]) / d,
+                         (a[0] * a[8] - a[2] * a[6]) / d, (a[2] * a[3] - a[0] * a[5]) / d,
+                         (a[3] * a[7] - a[4] * a[6]) / d, (a[1] * a[6] - a[0] * a[7]) / d,
+                         (a[0] * a[4] - a[1] * a[3]) / d};
+  double gr[4][3], G[4][4], C[6][3];
+  for (int c = 0; c < 3; ++c) {
+    gr[1][c] = inv[c];
+    gr[2][c] = inv[3 + c];
+    gr[3][c] = inv[6 + c];
+    gr[0][c] = -gr[1][c] - gr[2][c] - gr[3][c];
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) G[i][j] = gr[i][0] * gr[j][0] + gr[i][1] * gr[j][1] + gr[i][2] * gr[j][2];
+  for (int e = 0; e < 6; ++e) {
+    const double* u = gr[hLoc[e][0]];
+    const double* v = gr[hLoc[e][1]];
+    C[e][0] = u[1] * v[2] - u[2] * v[1];
+    C[e][1] = u[2] * v[0] - u[0] * v[2];
+    C[e][2] = u[0] * v[1] - u[1] * v[0];
+  }
+  auto mm = [&](int i, int j) { return vol * (i == j ? 2.0 : 1.0) / 20.0; };
+  for (int e = 0; e < 6; ++e)
+    for (int f = 0; f < 6; ++f) {
+      const int ea = hLoc[e][0], eb = hLoc[e][1], fc = hLoc[f][0], fd = hLoc[f][1];
+      const double K = 4.0 * vol * (C[e][0] * C[f][0] + C[e][1] * C[f][1] + C[e][2] * C[f][2]);
+      const double M = mm(ea, fc) * G[eb][fd] - mm(ea, fd) * G[eb][fc] - mm(eb, fc) * G[ea][fd] + mm(eb, fd) * G[ea][fc];
+      out[6 * e + f] = alpha * K + beta * M;
+    }
+}
+
+}  // namespace
+
+struct N1e1Cell {
+  double A[6][36];  // class element matrices
+  double W[8][19];  // merged interior stencil per orientation (index g = 1..7)
+};
+
+}  // namespace bt
+
+struct bt_n1e1 {
+  const bt_grid* grid = nullptr;
+  int level = 0;
+  double alpha = 1, beta = 1;
+  bt::DevBuf<bt::N1e1Cell> d_cells;
+};
+
+namespace bt {
+namespace {
+
+// ---------------------------------------------------------------------------
+// operator kernel: grid (row blocks, cells, 7 orientations)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_n1e1(const double* __restrict__ x, double* __restrict__ y,
+                                             const N1e1Cell* __restrict__ cells, int n, int64_t cs) {
+  __shared__ double sW[19];
+  __shared__ double sA[6][36];
+  const int g = blockIdx.z + 1;
+  const int cell = blockIdx.y;
+  for (int q = threadIdx.x; q < 19; q += kT) sW[q] = cells[cell].W[g][q];
+  for (int q = threadIdx.x; q < 216; q += kT) sA[q / 36][q % 36] = cells[cell].A[q / 36][q % 36];
+  __syncthreads();
+  const int wg = g == 7 ? n - 1 : n;  // subgroup width: 2^l, xyz 2^l - 1
+  const int nrows = tri32(wg);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRows);
+  int eoff[8];
+  {
+    int o = 0;
+    for (int q = 1; q <= 7; ++q) {
+      eoff[q] = o;
+      o += tet32(q == 7 ? n - 1 : n);
+    }
+  }
+  const double* __restrict__ xc = x + (int64_t)cell * cs;
+  double* __restrict__ yc = y + (int64_t)cell * cs + eoff[g];
+  const int nnb = cS.nnb[g], ninc = cS.ninc[g];
+  for (int r = blockIdx.x * kRows + warp; r < rend; r += kW) {
+    int j, k;
+    decode_row(wg, r, j, k);
+    const int L = wg - j - k, t0 = row_start(wg, j, k);
+    int base[19];
+#pragma unroll
+    for (int m = 0; m < 19; ++m) {
+      if (m < nnb) {
+        const Nb nb = cS.nb[g][m];
+        const int w2 = nb.g == 7 ? n - 1 : n;
+        base[m] = eoff[nb.g] + row_start(w2, j + nb.d[1], k + nb.d[2]) + nb.d[0];
+      } else {
+        base[m] = 0;
+      }
+    }
+    for (int i = lane; i < L; i += 32) {
+      // presence of the incident micro-tets (anchor in I_tet(w_s))
+      unsigned pres = 0;
+      for (int q = 0; q < ninc; ++q) {
+        const IncTet& it = cS.inc[g][q];
+        const int ws = it.s == 0 ? n : (it.s == 1 ? n - 2 : n - 1);
+        if (in_i_tet(ws, i + it.dq[0], j + it.dq[1], k + it.dq[2])) pres |= 1u << q;
+      }
+      double acc = 0.0;
+      if (pres == (1u << ninc) - 1) {
+#pragma unroll
+        for (int m = 0; m < 19; ++m)
+          if (m < nnb) acc = fma(sW[m], __ldg(xc + base[m] + i), acc);
+      } else {
+        for (int q = 0; q < ninc; ++q) {
+          if (!(pres >> q & 1)) continue;
+          const IncTet& it = cS.inc[g][q];
+          double row = 0.0;
+          for (int jj = 0; jj < 6; ++jj)
+            row = fma(sA[it.s][6 * it.le + jj] * cS.emap_sigma[it.s][jj], __ldg(xc + base[it.nb[jj]] + i), row);
+          acc = fma((double)it.sigma, row, acc);
+        }
+      }
+      yc[t0 + i] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// signed edge-interface pass
+// ---------------------------------------------------------------------------
+struct EdgeIfaceArgs {
+  const DevFace* faces;
+  const int* flist;
+  const DevPrimHdr* eh;
+  const DevPrimMem* em;
+  const int* elist;
+  int ne;
+  int n;
+  int64_t cs;
+};
+
+// slot and sign of the micro-edge P0 -> P1 (cell lattice coordinates)
+__device__ __forceinline__ int64_t edge_slot(int n, int64_t cs, int cell, int i0, int j0, int k0, int i1, int j1,
+                                             int k1, int& sigma) {
+  const int c = (i1 - i0 + 1) * 9 + (j1 - j0 + 1) * 3 + (k1 - k0 + 1);
+  const int g = cS.dir_g[c];
+  sigma = cS.dir_sigma[c];
+  int ai = sigma > 0 ? i0 : i1, aj = sigma > 0 ? j0 : j1, ak = sigma > 0 ? k0 : k1;
+  // anchor = first canonical endpoint - offs[g][0]
+  const int o0 = g == 4 || g == 7 ? 1 : 0;  // y-offset of offs[g][0] for xy, xyz
+  const int o2 = g == 5 || g == 6 ? 1 : 0;  // z-offset for xz, yz
+  aj -= o0;
+  ak -= o2;
+  int eoff = 0;
+  for (int q = 1; q < g; ++q) eoff += tet32(q == 7 ? n - 1 : n);
+  const int wg = g == 7 ? n - 1 : n;
+  return (int64_t)cell * cs + eoff + row_start(wg, aj, ak) + ai;
+}
+
+__device__ __forceinline__ void ijk3(const int8_t* lv, int w0, int w1, int w2, int& i, int& j, int& k) {
+  i = (lv[0] == 1 ? w0 : 0) + (lv[1] == 1 ? w1 : 0) + (lv[2] == 1 ? w2 : 0);
+  j = (lv[0] == 2 ? w0 : 0) + (lv[1] == 2 ? w1 : 0) + (lv[2] == 2 ? w2 : 0);
+  k = (lv[0] == 3 ? w0 : 0) + (lv[1] == 3 ? w1 : 0) + (lv[2] == 3 ? w2 : 0);
+}
+
+template <int MODE, class S>
+__device__ __forceinline__ void signed_group(double* __restrict__ v, const double* __restrict__ src, int count,
+                                             bool dir, S slot) {
+  int sg;
+  if (MODE == IF_SYNC || (MODE == IF_SYNC_DIR && !dir)) {
+    if (count < 2) return;
+    double sum = 0;
+    for (int m = 0; m < count; ++m) {
+      const int64_t t = slot(m, sg);
+      sum += sg > 0 ? v[t] : -v[t];
+    }
+    for (int m = 0; m < count; ++m) {
+      const int64_t t = slot(m, sg);
+      v[t] = sg > 0 ? sum : -sum;
+    }
+  } else if (MODE == IF_SYNC_DIR || MODE == IF_IMPOSE) {
+    if (!dir) return;
+    for (int m = 0; m < count; ++m) {
+      const int64_t t = slot(m, sg);
+      v[t] = src[t];
+    }
+  } else if (MODE == IF_ZERO_DIR) {
+    if (!dir) return;
+    for (int m = 0; m < count; ++m) v[slot(m, sg)] = 0.0;
+  } else if (MODE == IF_BCAST) {
+    if (count < 2) return;
+    int64_t t = slot(0, sg);
+    const double u = sg > 0 ? v[t] : -v[t];
+    for (int m = 1; m < count; ++m) {
+      t = slot(m, sg);
+      v[t] = sg > 0 ? u : -u;
+    }
+  }
+}
+
+// face-interior micro-edges: tau in {0,1,2} x (a, b) with a + b <= n - 1
+template <int MODE>
+__global__ void __launch_bounds__(kT) k_edge_faces(double* __restrict__ v, const double* __restrict__ src,
+                                                   EdgeIfaceArgs a) {
+  const int n = a.n;
+  const int per = tri32(n);
+  const int q = blockIdx.x * kT + threadIdx.x;
+  if (q >= 3 * per) return;
+  const int tau = q / per;
+  int aa, bb;
+  decode_tri(n, q - tau * per, aa, bb);
+  if ((tau == 0 && bb == 0) || (tau == 1 && aa == 0) || (tau == 2 && aa + bb + 1 == n)) return;  // on a macro edge
+  int a0 = aa, b0 = bb, a1 = aa, b1 = bb;
+  if (tau == 0) a1 = aa + 1;
+  else if (tau == 1) b1 = bb + 1;
+  else { a0 = aa + 1; b1 = bb + 1; }
+  const DevFace f = a.faces[a.flist[blockIdx.y]];
+  signed_group<MODE>(v, src, f.ncell, f.dir != 0, [&](int m, int& sg) {
+    int i0, j0, k0, i1, j1, k1;
+    ijk3(f.lv[m], n - a0 - b0, a0, b0, i0, j0, k0);
+    ijk3(f.lv[m], n - a1 - b1, a1, b1, i1, j1, k1);
+    return edge_slot(n, a.cs, f.cell[m], i0, j0, k0, i1, j1, k1, sg);
+  });
+}
+
+// micro-edges along macro edges: a = 0..n-1, (n - a, a) -> (n - a - 1, a + 1)
+template <int MODE>
+__global__ void __launch_bounds__(kT) k_edge_edges(double* __restrict__ v, const double* __restrict__ src,
+                                                   EdgeIfaceArgs a) {
+  const int n = a.n;
+  const int aa = blockIdx.x * kT + threadIdx.x;
+  if (aa >= n) return;
+  const DevPrimHdr h = a.eh[a.elist[blockIdx.y]];
+  const DevPrimMem* mem = a.em + h.first;
+  signed_group<MODE>(v, src, h.count, h.dir != 0, [&](int m, int& sg) {
+    const DevPrimMem pm = mem[m];
+    const int8_t lv[3] = {pm.lv[0], pm.lv[1], -1};
+    int i0, j0, k0, i1, j1, k1;
+    ijk3(lv, n - aa, aa, 0, i0, j0, k0);
+    ijk3(lv, n - aa - 1, aa + 1, 0, i1, j1, k1);
+    return edge_slot(n, a.cs, pm.cell, i0, j0, k0, i1, j1, k1, sg);
+  });
+}
+
+template <int MODE>
+void edge_iface(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s) {
+  build_static();
+  const int n = 1 << level;
+  EdgeIfaceArgs a{g.d_faces.p, nullptr, g.d_ehdr.p, g.d_emem.p, g.d_edge_act.p, (int)g.edge_act.size(), n,
+                  level_slots(BT_SPACE_EDGES, level)};
+  const int per = 3 * tri32(n);
+  const bool sync_like = MODE == IF_SYNC || MODE == IF_BCAST || MODE == IF_SYNC_DIR;
+  const bool dir_like = MODE == IF_SYNC_DIR || MODE == IF_IMPOSE || MODE == IF_ZERO_DIR;
+  if (sync_like && !g.face_shared.empty()) {
+    a.flist = g.d_face_shared.p;
+    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.face_shared.size()), kT, 0, s>>>(v, src, a);
+    count_launch();
+  }
+  if (dir_like && !g.face_bdir.empty()) {
+    a.flist = g.d_face_bdir.p;
+    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.face_bdir.size()), kT, 0, s>>>(v, src, a);
+    count_launch();
+  }
+  if (a.ne) {
+    k_edge_edges<MODE><<<dim3((n + kT - 1) / kT, (unsigned)a.ne), kT, 0, s>>>(v, src, a);
+    count_launch();
+  }
+  check_launch("k_edge_iface");
+}
+
+// owned-DoF dot over the edge space: deterministic (cell, orientation, row block) partials
+__global__ void __launch_bounds__(kT) k_edge_dot(const double* __restrict__ x, const double* __restrict__ y,
+                                                 const DevCellInfo* __restrict__ info, int n, int64_t cs,
+                                                 double* __restrict__ partials) {
+  __shared__ double red[kW];
+  const int g = blockIdx.z + 1, cell = blockIdx.y;
+  const int wg = g == 7 ? n - 1 : n;
+  int eoff = 0;
+  for (int q = 1; q < g; ++q) eoff += tet32(q == 7 ? n - 1 : n);
+  const uint16_t own = info[cell].owned_by_z;
+  const double* xc = x + (int64_t)cell * cs + eoff;
+  const double* yc = y + (int64_t)cell * cs + eoff;
+  const int o[7][2][3] = BT_EDGE_OFFSETS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrows = tri32(wg);
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRows);
+  double acc = 0.0;
+  for (int r = blockIdx.x * kRows + warp; r < rend; r += kW) {
+    int j, k;
+    decode_row(wg, r, j, k);
+    const int L = wg - j - k, t0 = row_start(wg, j, k);
+    for (int i = lane; i < L; i += 32) {
+      const int z = zero_set(n, i + o[g - 1][0][0], j + o[g - 1][0][1], k + o[g - 1][0][2]) &
+                    zero_set(n, i + o[g - 1][1][0], j + o[g - 1][1][1], k + o[g - 1][1][2]);
+      if (own >> z & 1) acc = fma(__ldg(xc + t0 + i), __ldg(yc + t0 + i), acc);
+    }
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int q = 0; q < kW; ++q) s += red[q];
+    partials[((int64_t)blockIdx.z * gridDim.y + cell) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_edge_sum(const double* __restrict__ p, int64_t n, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) acc += p[q];
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int q = 0; q < 32; ++q) s += red[q];
+    *out = s;
+  }
+}
+
+}  // namespace
+
+void launch_edge_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src,
+                           cudaStream_t s) {
+  switch (mode) {
+    case IF_SYNC: edge_iface<IF_SYNC>(g, level, v, src, s); break;
+    case IF_SYNC_DIR: edge_iface<IF_SYNC_DIR>(g, level, v, src, s); break;
+    case IF_BCAST: edge_iface<IF_BCAST>(g, level, v, src, s); break;
+    case IF_IMPOSE: edge_iface<IF_IMPOSE>(g, level, v, src, s); break;
+    case IF_ZERO_DIR: edge_iface<IF_ZERO_DIR>(g, level, v, src, s); break;
+    default: raise(BT_INVALID_ARGUMENT, "edge interface: unsupported mode");
+  }
+}
+
+double dot_edges(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s) {
+  const int n = 1 << level;
+  const int bx = (tri32(n) + kRows - 1) / kRows;
+  const int64_t np = (int64_t)bx * g.mesh.n_cells() * 7;
+  if (g.d_partials.n < (size_t)np + 1) g.d_partials.alloc((size_t)np + 1);
+  k_edge_dot<<<dim3(bx, g.mesh.n_cells(), 7), kT, 0, s>>>(x, y, g.d_info.p, n, level_slots(BT_SPACE_EDGES, level),
+                                                          g.d_partials.p);
+  k_edge_sum<<<1, 1024, 0, s>>>(g.d_partials.p, np, g.d_partials.p + np);
+  count_launch(2);
+  check_launch("k_edge_dot");
+  BT_CUDA(cudaMemcpyAsync(g.h_pinned, g.d_partials.p + np, sizeof(double), cudaMemcpyDeviceToHost, s));
+  BT_CUDA(cudaStreamSynchronize(s));
+  return g.h_pinned[0];
+}
+
+// mt19937_64 over owned edge slots in canonical (cell, orientation, t) order,
+// then a signed broadcast so replicas carry the same oriented field.
+void random_fill_edges(const bt_grid& g, int level, uint64_t seed, double* x, cudaStream_t s) {
+  const int n = 1 << level;
+  const int64_t cs = level_slots(BT_SPACE_EDGES, level);
+  std::vector<double> h((size_t)(cs * g.mesh.n_cells()), 0.0);
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  for (int c = 0; c < g.mesh.n_cells(); ++c) {
+    const uint16_t own = g.topo.info[c].owned_by_z;
+    int64_t t = cs * c;
+    for (int e = 1; e <= 7; ++e) {
+      const int w = width_formula(e, level);
+      const int* a = hOffEdge[e - 1][0];
+      const int* b = hOffEdge[e - 1][1];
+      for (int k = 0; k < w; ++k)
+        for (int j = 0; j < w - k; ++j)
+          for (int i = 0; i < w - k - j; ++i, ++t) {
+            const int z = zero_set(n, i + a[0], j + a[1], k + a[2]) & zero_set(n, i + b[0], j + b[1], k + b[2]);
+            if (own >> z & 1) h[t] = dist(rng);
+          }
+    }
+  }
+  BT_CUDA(cudaMemcpyAsync(x, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
+  launch_edge_interface(g, level, IF_BCAST, x, nullptr, s);
+  BT_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace bt
+
+using namespace bt;
+
+#define BT_TRY try {
+#define BT_CATCH                         \
+  }                                      \
+  catch (const bt::Error& e) {           \
+    bt::set_error(e.what());             \
+    return e.status;                     \
+  }                                      \
+  catch (const std::exception& e) {      \
+    bt::set_error(e.what());             \
+    return BT_LOGIC_ERROR;               \
+  }                                      \
+  return BT_OK;
+
 extern "C" {
-bt_status bt_n1e1_create(const bt_grid*, int, double, double, bt_n1e1**) {
-  bt::set_error("N1E1 operator not built in this version");
-  return BT_LOGIC_ERROR;
+
+bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta, bt_n1e1** out) {
+  BT_TRY
+  check_level(g, level);
+  BT_CUDA(cudaSetDevice(g->device));
+  build_static();
+  auto op = std::make_unique<bt_n1e1>();
+  op->grid = g;
+  op->level = level;
+  op->alpha = alpha;
+  op->beta = beta;
+  const int nc = g->mesh.n_cells();
+  std::vector<N1e1Cell> cells(nc);
+  const double h = 1.0 / (double)(1 << level);
+  for (int c = 0; c < nc; ++c) {
+    N1e1Cell& cc = cells[c];
+    std::memset(&cc, 0, sizeof cc);
+    const CellMap& mp = g->topo.maps[c];
+    for (int s = 0; s < 6; ++s) {
+      double X[4][3];
+      for (int v = 0; v < 4; ++v) {
+        const double r[3] = {h * hOffCell[s][v][0], h * hOffCell[s][v][1], h * hOffCell[s][v][2]};
+        for (int d = 0; d < 3; ++d) X[v][d] = (mp.a[3 * d] * r[0] + mp.a[3 * d + 1] * r[1] + mp.a[3 * d + 2] * r[2]) + mp.b[d];
+      }
+      local_n1e1(X, alpha, beta, cc.A[s]);
+    }
+    for (int gg = 1; gg <= 7; ++gg)
+      for (int q = 0; q < hS.ninc[gg]; ++q) {
+        const IncTet& it = hS.inc[gg][q];
+        for (int j = 0; j < 6; ++j)
+          cc.W[gg][it.nb[j]] += it.sigma * hS.emap_sigma[it.s][j] * cc.A[it.s][6 * it.le + j];
+      }
+  }
+  op->d_cells.upload(cells);
+  *out = op.release();
+  BT_CATCH
 }
-void bt_n1e1_destroy(bt_n1e1*) {}
-bt_status bt_apply_n1e1(const bt_n1e1*, const double*, double*, int, void*) {
-  bt::set_error("N1E1 operator not built in this version");
-  return BT_LOGIC_ERROR;
+
+void bt_n1e1_destroy(bt_n1e1* op) { delete op; }
+
+bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, void* stream) {
+  BT_TRY
+  if (!op) raise(BT_INVALID_ARGUMENT, "apply_n1e1: operator required");
+  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  const bt_grid& g = *op->grid;
+  const int n = 1 << op->level;
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((tri32(n) + kRows - 1) / kRows, g.mesh.n_cells(), 7);
+  k_n1e1<<<grid, kT, 0, s>>>(x, y, op->d_cells.p, n, level_slots(BT_SPACE_EDGES, op->level));
+  count_launch();
+  check_launch("k_n1e1");
+  launch_edge_interface(g, op->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+  BT_CATCH
 }
-bt_status bt_n1e1_sync(const bt_grid*, int, double*, void*) {
-  bt::set_error("N1E1 operator not built in this version");
-  return BT_LOGIC_ERROR;
+
+bt_status bt_n1e1_sync(const bt_grid* g, int level, double* x, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  launch_edge_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
+  BT_CATCH
 }
-}
+
+}  // extern "C"
