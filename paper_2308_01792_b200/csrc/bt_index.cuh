@@ -17,7 +17,8 @@ BT_HD int64_t n_tri(int64_t w) { return w > 0 ? w * (w + 1) / 2 : 0; }
 BT_HD int64_t n_tet(int64_t w) { return w > 0 ? w * (w + 1) * (w + 2) / 6 : 0; }
 // 32-bit variants for in-cell offsets (level <= 10 keeps n_tet(1025) < 2^31)
 BT_HD int tri32(int w) { return w > 0 ? w * (w + 1) / 2 : 0; }
-BT_HD int tet32(int w) { return w > 0 ? (int)((int64_t)w * (w + 1) * (w + 2) / 6) : 0; }
+// w (w + 1) (w + 2) < 2^31 for w <= 1025 (level 10)
+BT_HD int tet32(int w) { return w > 0 ? w * (w + 1) * (w + 2) / 6 : 0; }
 
 // Subgroup ids follow enum Subgroup (micro_index.hpp:22-28).
 BT_HD int width_formula(int g, int level) {
