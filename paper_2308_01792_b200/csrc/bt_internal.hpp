@@ -177,6 +177,7 @@ struct bt_stencil {
   bt::DevBuf<double> d_diag;                 // assembled diagonal
   bt::DevBuf<int4> d_tasks;                  // warp march schedule (level-only, see k_stencil)
   int ntasks = 0;
+  bool symmetric = false;                    // merged rows satisfy W[d] == W[-d] bitwise
 };
 
 namespace bt {
