@@ -175,9 +175,14 @@ struct bt_stencil {
   std::vector<std::array<double, 15>> rows;  // host copy of StencilTable::rows
   bt::DevBuf<bt::StencilCell> d_cells;
   bt::DevBuf<double> d_diag;                 // assembled diagonal
-  bt::DevBuf<int4> d_tasks;                  // warp march schedule (level-only, see k_stencil)
+  bt::DevBuf<int4> d_tasks;                  // warp march schedule, fast rows (see bt_stencil.cu)
   int ntasks = 0;
-  bool symmetric = false;                    // merged rows satisfy W[d] == W[-d] bitwise
+  bt::DevBuf<int4> d_gtasks;                 // general rows (layer 0, row 0, corner rows)
+  int ngtasks = 0;
+  bt::DevBuf<int4> d_atasks;                 // all rows (general-kernel fallback)
+  int natasks = 0;
+  bool symmetric = false;                    // fast-path preconditions hold (see bt_stencil.cu)
+  std::vector<double> fast;                  // per cell: 8 symmetric weights, 7 + 7 face corrections
 };
 
 namespace bt {
