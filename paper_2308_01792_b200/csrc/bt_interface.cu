@@ -117,28 +117,83 @@ __global__ void __launch_bounds__(kT) k_iface_prims(double* __restrict__ v, cons
   }
 }
 
+// All primitives of one mode in a single launch: a 1-D grid whose leading
+// blocks cover up to two face lists (xb blocks per face) and whose trailing
+// blocks cover macro edges (eb blocks per edge) and vertices.
+struct AllArgs {
+  FaceArgs f1, f2;
+  int nf1, nf2, xb;
+  PrimArgs p;
+  int eb;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kT) k_interface(double* __restrict__ v, const double* __restrict__ src, AllArgs a) {
+  const int n = a.p.n, w = n + 1;
+  int b = blockIdx.x;
+  const int nfb1 = a.nf1 * a.xb, nfb2 = a.nf2 * a.xb;
+  if (b < nfb1 + nfb2) {
+    const FaceArgs& fa = b < nfb1 ? a.f1 : a.f2;
+    if (b >= nfb1) b -= nfb1;
+    const int q = (b % a.xb) * kT + threadIdx.x;
+    if (q >= tri32(n - 2)) return;
+    const DevFace f = fa.faces[fa.list[b / a.xb]];
+    int ap, bp;
+    decode_tri(n - 2, q, ap, bp);
+    const int aa = ap + 1, bb = bp + 1, cc = n - aa - bb;
+    const int64_t s0 = slot_of(fa.cs, w, f.cell[0], f.lv[0][0], cc, f.lv[0][1], aa, f.lv[0][2], bb);
+    const int64_t s1 = f.ncell == 2 ? slot_of(fa.cs, w, f.cell[1], f.lv[1][0], cc, f.lv[1][1], aa, f.lv[1][2], bb) : 0;
+    apply_group<MODE>(v, src, f.ncell, f.dir != 0, [&](int m) { return m == 0 ? s0 : s1; });
+    return;
+  }
+  b -= nfb1 + nfb2;
+  const PrimArgs& pa = a.p;
+  if (b < pa.ne * a.eb) {
+    const int aa = (b % a.eb) * kT + threadIdx.x + 1;
+    if (aa > n - 1) return;
+    const DevPrimHdr h = pa.eh[pa.elist[b / a.eb]];
+    const DevPrimMem* mem = pa.em + h.first;
+    apply_group<MODE>(v, src, h.count, h.dir != 0, [&](int m) {
+      const DevPrimMem pm = mem[m];
+      return slot_of(pa.cs, w, pm.cell, pm.lv[0], n - aa, pm.lv[1], aa, -1, 0);
+    });
+    return;
+  }
+  b -= pa.ne * a.eb;
+  const int vi = b * kT + threadIdx.x;
+  if (vi >= pa.nv) return;
+  const DevPrimHdr h = pa.vh[pa.vlist[vi]];
+  const DevPrimMem* mem = pa.vm + h.first;
+  apply_group<MODE>(v, src, h.count, h.dir != 0, [&](int m) {
+    const DevPrimMem pm = mem[m];
+    return slot_of(pa.cs, w, pm.cell, pm.lv[0], n, -1, 0, -1, 0);
+  });
+}
+
 template <int MODE>
 void launch_mode(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s) {
   const int n = 1 << level;
   const int64_t cs = n_tet(n + 1);
   const int fp = tri32(n - 2);
-  auto faces = [&](const DevBuf<int>& list, size_t cnt) {
-    if (!cnt || !fp) return;
-    FaceArgs fa{g.d_faces.p, list.p, n, cs};
-    k_iface_faces<MODE><<<dim3((fp + kT - 1) / kT, (unsigned)cnt), kT, 0, s>>>(v, src, fa);
-    count_launch();
-  };
   const bool sync_like = MODE == IF_SYNC || MODE == IF_BCAST || MODE == IF_ZERO_NONOWNED || MODE == IF_SYNC_DIR;
   const bool dir_like = MODE == IF_SYNC_DIR || MODE == IF_IMPOSE || MODE == IF_ZERO_DIR;
-  if (sync_like) faces(g.d_face_shared, g.face_shared.size());
-  if (dir_like) faces(g.d_face_bdir, g.face_bdir.size());
-  const int ne = (int)g.edge_act.size(), nv = (int)g.vert_act.size();
-  if (ne + nv) {
-    PrimArgs pa{g.d_ehdr.p, g.d_emem.p, g.d_edge_act.p, ne, g.d_vhdr.p, g.d_vmem.p, g.d_vert_act.p, nv, n, cs};
-    const unsigned gy = (unsigned)(ne + (nv + kT - 1) / kT);
-    k_iface_prims<MODE><<<dim3((n - 1 + kT - 1) / kT, gy), kT, 0, s>>>(v, src, pa);
-    count_launch();
+  AllArgs a{};
+  a.xb = (fp + kT - 1) / kT;
+  if (sync_like && fp) {
+    a.f1 = FaceArgs{g.d_faces.p, g.d_face_shared.p, n, cs};
+    a.nf1 = (int)g.face_shared.size();
   }
+  if (dir_like && fp) {
+    a.f2 = FaceArgs{g.d_faces.p, g.d_face_bdir.p, n, cs};
+    a.nf2 = (int)g.face_bdir.size();
+  }
+  const int ne = (int)g.edge_act.size(), nv = (int)g.vert_act.size();
+  a.p = PrimArgs{g.d_ehdr.p, g.d_emem.p, g.d_edge_act.p, ne, g.d_vhdr.p, g.d_vmem.p, g.d_vert_act.p, nv, n, cs};
+  a.eb = (n - 1 + kT - 1) / kT;
+  const int64_t blocks = (int64_t)(a.nf1 + a.nf2) * a.xb + (int64_t)ne * a.eb + (nv + kT - 1) / kT;
+  if (!blocks) return;
+  k_interface<MODE><<<(unsigned)blocks, kT, 0, s>>>(v, src, a);
+  count_launch();
   check_launch("k_interface");
 }
 

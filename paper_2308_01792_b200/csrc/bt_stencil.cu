@@ -2,14 +2,15 @@
 // operators.hpp:247-271), per-cell phase. The interface phase (replica sums
 // and Dirichlet rows) is bt_interface.cu.
 //
-// Data path. A warp owns 30 consecutive columns i of one layer k of one
-// macro-cell (lanes 0 and 31 are halo columns) and marches up to kMarchRows
-// rows j. Each step needs three new rows at its columns — A(j+1) of layer k,
-// B(j) of layer k+1 and C(j+1) of layer k-1, each one coalesced 256 B
-// segment — loaded two steps early into registers (predicated to 0 outside
-// the lattice, so lattice-boundary vertices need no special loads);
-// neighbours i-1 / i+1 come from warp shuffles. The march is unrolled by two
-// over two alternating window sets, so the sliding window costs no moves.
+// Data path (k_stencil_fast). A warp owns 60 consecutive columns i of one
+// layer k of one macro-cell — two adjacent columns per lane, lanes 0 and 31
+// carry halo columns — and marches up to kMarchRows rows j. Each step needs
+// three new rows at its columns — A(j+1) of layer k, B(j) of layer k+1 and
+// C(j+1) of layer k-1, each one coalesced 512 B segment — loaded one step
+// early into registers (predicated to 0 outside the lattice, so
+// lattice-boundary vertices need no special loads); the i-1 / i+2 columns
+// of a lane come from two warp shuffles per row. The march is unrolled by
+// two over alternating window sets, so the sliding window costs no moves.
 // Every x value is read from L2 once per layer that needs it (3x) and from
 // HBM once.
 //
@@ -21,11 +22,11 @@
 // 8-weight form (W[d] == W[-d] bitwise, checked on the host) and switches the
 // two face vertices to their zero-set-typed partial rows (per-cell part of
 // partial_row_apply, operators.hpp:78-96) by 7-term corrections selected per
-// lane — no per-lane branches. All weights are kernel parameters, so they
-// reach the DFMAs as uniform-register operands. General rows (layer 0, row
-// 0, the last two rows of column block 0) go through k_stencil_general, which
-// reads the typed rows from shared memory; it is also the fallback for
-// tables that fail the fast-path checks.
+// lane; the corrections only run in warps that contain such a vertex. All
+// weights are kernel parameters, so they reach the DFMAs as uniform-register
+// operands. General rows (layer 0, row 0, the last two rows of column 0) go
+// through k_stencil_general, which reads the typed rows from shared memory;
+// it is also the fallback for tables that fail the fast-path checks.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,7 +40,8 @@ namespace {
 constexpr int kT = 256;
 constexpr int kW = kT / 32;
 constexpr int kMarchRows = 48;
-constexpr int kMarchCols = 30;
+constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
+constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
 
 // directions whose weight differs between the interior row and the typed row
 // of the diagonal face (zero set {0}) / the face i = 0 (zero set {1});
@@ -55,12 +57,20 @@ struct FastParams {
 };
 constexpr int kMaxCells = 176;  // 176 * 22 * 8 B = 30 KB of kernel parameters
 
-struct Win {  // row j of layer k (a), row j-1 of layer k+1 (b), row j of layer k-1 (c)
-  double a, ap, am, b, bp, c, cp;
+// One row at a lane's two columns (c0 = v0, c1 = v1) with the neighbours
+// l = column c0 - 1 and r = column c1 + 1.
+struct Row4 {
+  double l, v0, v1, r;
+};
+struct Win {  // A(j) of layer k, B(j-1) of layer k+1, C(j) of layer k-1
+  Row4 a, b, c;
 };
 
+__device__ __forceinline__ double shup(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
 template <int kMaxC>
-__global__ void __launch_bounds__(kT, 3) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
+__global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
                                                         int64_t cell_slots, int cell0,
                                                         const __grid_constant__ FastParams<kMaxC> fp) {
@@ -74,121 +84,141 @@ __global__ void __launch_bounds__(kT, 3) k_stencil_fast(const double* __restrict
   const int4 tk = tasks[task];
   const int k = tk.x, blk = tk.y, j0 = tk.z, j1 = tk.w;  // k >= 1, j0 >= 1 by construction
   const int n = w - 1;
-  const int i = kMarchCols * blk + lane - 1;
-  const bool out_lane = lane >= 1 && lane <= kMarchCols && i >= 0;
-  const bool col_ok = i >= 0;
-  const double* __restrict__ xc = x + (int64_t)cell * cell_slots + i;  // column i of every row
+  const int c0 = kFastCols * blk + 2 * lane - 2;  // this lane's columns c0, c0 + 1
+  const bool out_lane = lane >= 1 && lane <= kFastCols / 2;
   const bool up = k + 1 <= n;
+  // column pointers: entry t of row r is xc[row_start(r) + t]
+  const double* __restrict__ xc = x + (int64_t)cell * cell_slots + c0;
 
-  // load cursors (lane's column) for the rows consumed at row j: A(j+1),
-  // B(j), C(j+1); remaining lengths <= 0 (or an absent layer k+1) load 0.
+  // predicated pair load of a row with start rs and length len at columns c0, c0 + 1
+  auto ld2 = [&](const double* p, int len, double& v0, double& v1) {
+    v0 = (c0 >= 0 && c0 < len) ? __ldg(p) : 0.0;
+    v1 = (c0 + 1 >= 0 && c0 + 1 < len) ? __ldg(p + 1) : 0.0;
+  };
+  auto make_row = [&](double v0, double v1) {
+    Row4 q;
+    q.v0 = v0;
+    q.v1 = v1;
+    q.l = shup(v1);
+    q.r = shdn(v0);
+    return q;
+  };
+
+  // prefetch cursors for the rows consumed at row j: A(j+1), B(j), C(j+1).
+  // len(A(j+1)) = len(B(j)) = r, len(C(j+1)) = r + 1, r = w - k - j - 1.
+  int r = w - k - j0 - 1;
   const double* __restrict__ qA = xc + row_start(w, j0 + 1, k);
   const double* __restrict__ qB = xc + (up ? row_start(w, j0, k + 1) : 0);
   const double* __restrict__ qC = xc + row_start(w, j0 + 1, k - 1);
-  int rA = w - k - j0 - 1, rB = w - k - 1 - j0, rC = w - k - j0;  // row lengths
-  int LA = col_ok ? rA - i : -1;
-  int LB = (col_ok && up) ? rB - i : -1;
-  int LC = col_ok ? rC - i : -1;
-  auto load3 = [&](double& pa, double& pb, double& pc, bool live) {
-    pa = (live && LA > 0) ? __ldg(qA) : 0.0;
-    pb = (live && LB > 0) ? __ldg(qB) : 0.0;
-    pc = (live && LC > 0) ? __ldg(qC) : 0.0;
-    qA += rA;
-    qB += rB;
-    qC += rC;
-    --rA;
-    --rB;
-    --rC;
-    --LA;
-    --LB;
-    --LC;
+  double na0, na1, nb0, nb1, nc0, nc1;
+  auto prefetch = [&](bool live) {
+    const int ra = live ? r : 0, rb = (live && up) ? r : 0, rc = live ? r + 1 : 0;
+    ld2(qA, ra, na0, na1);
+    ld2(qB, rb, nb0, nb1);
+    ld2(qC, rc, nc0, nc1);
+    qA += r;
+    qB += r;
+    qC += r + 1;
+    --r;
   };
-  double pa0, pb0, pc0, pa1, pb1, pc1;
-  load3(pa0, pb0, pc0, true);
-  load3(pa1, pb1, pc1, j0 + 1 < j1);
+  prefetch(true);
 
-  // window sets: X = row j0 (current), Y = row j0 - 1 (previous)
-  Win X, Y;
+  // window at row j0: A(j0), B(j0 - 1), C(j0); plus A(j0 - 1) (only v0, v1, r used)
+  Win X;
+  Row4 Am1;
   {
-    double am1 = 0.0, a0 = 0.0, bm1 = 0.0, c0 = 0.0;
-    if (col_ok) {
-      if (i < w - k - j0 + 1) am1 = __ldg(xc + row_start(w, j0 - 1, k));
-      if (i < w - k - j0) a0 = __ldg(xc + row_start(w, j0, k));
-      if (up && i < w - k - j0) bm1 = __ldg(xc + row_start(w, j0 - 1, k + 1));
-      if (i < w - k - j0 + 1) c0 = __ldg(xc + row_start(w, j0, k - 1));
-    }
-    X.a = a0;
-    X.ap = __shfl_down_sync(0xffffffffu, a0, 1);
-    X.am = __shfl_up_sync(0xffffffffu, a0, 1);
-    X.b = bm1;
-    X.bp = __shfl_down_sync(0xffffffffu, bm1, 1);
-    X.c = c0;
-    X.cp = __shfl_down_sync(0xffffffffu, c0, 1);
-    Y.a = am1;
-    Y.ap = __shfl_down_sync(0xffffffffu, am1, 1);
+    double a0, a1, b0, b1, e0, e1, m0, m1;
+    ld2(xc + row_start(w, j0, k), w - k - j0, a0, a1);
+    ld2(xc + (up ? row_start(w, j0 - 1, k + 1) : 0), up ? w - k - j0 : 0, b0, b1);
+    ld2(xc + row_start(w, j0, k - 1), w - k - j0 + 1, e0, e1);
+    ld2(xc + row_start(w, j0 - 1, k), w - k - j0 + 1, m0, m1);
+    X.a = make_row(a0, a1);
+    X.b = make_row(b0, b1);
+    X.c = make_row(e0, e1);
+    Am1 = make_row(m0, m1);
   }
+  Win Y;  // the second window set (written by the first step)
+  Row4 Am1y;
 
   int LY = w - k - j0;  // length of the output row
-  double* __restrict__ py = y + (int64_t)cell * cell_slots + i + row_start(w, j0, k);
+  double* __restrict__ py = y + (int64_t)cell * cell_slots + c0 + row_start(w, j0, k);
+  const int colend = kFastCols * blk + kFastCols;  // LY <= colend: the row ends in this warp
   const bool blk0 = blk == 0;
-  const int colend = kMarchCols * blk + kMarchCols;  // LY <= colend: the row ends inside this warp
   int j = j0;
-#define BT_STEP(cur, prv, pa, pb, pc)                                                               \
+
+  // One step: output row j at columns c0 (p = 0) and c0 + 1 (p = 1).
+  // cur: A(j), B(j-1), C(j); am1: A(j-1); new rows A1 = A(j+1), B0 = B(j),
+  // C1 = C(j+1). kStencilDirs pairs (d, d + 7):
+  //   (1,0,0)/(-1,0,0)  A(j) at i+1 / i-1      (0,1,0)/(0,-1,0)  A(j+1) / A(j-1)
+  //   (0,0,1)/(0,0,-1)  B(j) / C(j)            (1,-1,0)/(-1,1,0) A(j-1) i+1 / A(j+1) i-1
+  //   (1,0,-1)/(-1,0,1) C(j) i+1 / B(j) i-1    (0,1,-1)/(0,-1,1) C(j+1) / B(j-1)
+  //   (1,-1,1)/(-1,1,-1) B(j-1) i+1 / C(j+1) i-1
+#define BT_STEP(cur, nxt, am1, am1n)                                                                \
   {                                                                                                 \
-    const double A1 = pa, B0 = pb, C1 = pc;                                                         \
-    const double A1m = __shfl_up_sync(0xffffffffu, A1, 1);                                          \
-    const double A1p = __shfl_down_sync(0xffffffffu, A1, 1);                                        \
-    const double B0m = __shfl_up_sync(0xffffffffu, B0, 1);                                          \
-    const double B0p = __shfl_down_sync(0xffffffffu, B0, 1);                                        \
-    const double C1m = __shfl_up_sync(0xffffffffu, C1, 1);                                          \
-    const double C1p = __shfl_down_sync(0xffffffffu, C1, 1);                                        \
-    if (out_lane && i < LY) {                                                                       \
-      double acc = W[0] * cur.a;                                                                    \
-      acc = fma(W[1], cur.ap + cur.am, acc);                                                        \
-      acc = fma(W[2], A1 + prv.a, acc);                                                             \
-      acc = fma(W[3], B0 + cur.c, acc);                                                             \
-      acc = fma(W[4], prv.ap + A1m, acc);                                                           \
-      acc = fma(W[5], cur.cp + B0m, acc);                                                           \
-      acc = fma(W[6], C1 + cur.b, acc);                                                             \
-      acc = fma(W[7], cur.bp + C1m, acc);                                                           \
+    const Row4 A1 = make_row(na0, na1), B0 = make_row(nb0, nb1), C1 = make_row(nc0, nc1);           \
+    prefetch(j + 1 < j1); /* rows for step j + 1 */                                                 \
+    if (out_lane) {                                                                                 \
+      /* column c0: left neighbours are the .l values, right ones .v1 */                           \
+      double s0 = W[0] * cur.a.v0;                                                                  \
+      s0 = fma(W[1], cur.a.v1 + cur.a.l, s0);                                                       \
+      s0 = fma(W[2], A1.v0 + am1.v0, s0);                                                           \
+      s0 = fma(W[3], B0.v0 + cur.c.v0, s0);                                                         \
+      s0 = fma(W[4], am1.v1 + A1.l, s0);                                                            \
+      s0 = fma(W[5], cur.c.v1 + B0.l, s0);                                                          \
+      s0 = fma(W[6], C1.v0 + cur.b.v0, s0);                                                         \
+      s0 = fma(W[7], cur.b.v1 + C1.l, s0);                                                          \
+      /* column c0 + 1: left neighbours .v0, right ones .r */                                      \
+      double s1 = W[0] * cur.a.v1;                                                                  \
+      s1 = fma(W[1], cur.a.r + cur.a.v0, s1);                                                       \
+      s1 = fma(W[2], A1.v1 + am1.v1, s1);                                                           \
+      s1 = fma(W[3], B0.v1 + cur.c.v1, s1);                                                         \
+      s1 = fma(W[4], am1.r + A1.v0, s1);                                                            \
+      s1 = fma(W[5], cur.c.r + B0.v0, s1);                                                          \
+      s1 = fma(W[6], C1.v1 + cur.b.v1, s1);                                                         \
+      s1 = fma(W[7], cur.b.r + C1.v0, s1);                                                          \
       if (LY <= colend) { /* row end in this warp: diagonal face, dirs 0, 4, 5, 6, 11, 12, 13 */     \
-        double dg = fma(DD[0], cur.a, acc);                                                         \
-        dg = fma(DD[1], prv.ap, dg);                                                                \
-        dg = fma(DD[2], cur.cp, dg);                                                                \
-        dg = fma(DD[3], C1, dg);                                                                    \
-        dg = fma(DD[4], A1m, dg);                                                                   \
-        dg = fma(DD[5], B0m, dg);                                                                   \
-        dg = fma(DD[6], cur.b, dg);                                                                 \
-        acc = (i == LY - 1) ? dg : acc;                                                             \
+        double d0 = fma(DD[0], cur.a.v0, s0);                                                       \
+        d0 = fma(DD[1], am1.v1, d0);                                                                \
+        d0 = fma(DD[2], cur.c.v1, d0);                                                              \
+        d0 = fma(DD[3], C1.v0, d0);                                                                 \
+        d0 = fma(DD[4], A1.l, d0);                                                                  \
+        d0 = fma(DD[5], B0.l, d0);                                                                  \
+        d0 = fma(DD[6], cur.b.v0, d0);                                                              \
+        double d1 = fma(DD[0], cur.a.v1, s1);                                                       \
+        d1 = fma(DD[1], am1.r, d1);                                                                 \
+        d1 = fma(DD[2], cur.c.r, d1);                                                               \
+        d1 = fma(DD[3], C1.v1, d1);                                                                 \
+        d1 = fma(DD[4], A1.v0, d1);                                                                 \
+        d1 = fma(DD[5], B0.v0, d1);                                                                 \
+        d1 = fma(DD[6], cur.b.v1, d1);                                                              \
+        s0 = (c0 == LY - 1) ? d0 : s0;                                                              \
+        s1 = (c0 + 1 == LY - 1) ? d1 : s1;                                                          \
       }                                                                                             \
-      if (blk0) { /* face i = 0 (zero set {1}): dirs 0, 2, 3, 6, 9, 10, 13 */                       \
-        double f0 = fma(DI[0], cur.a, acc);                                                         \
-        f0 = fma(DI[1], A1, f0);                                                                    \
-        f0 = fma(DI[2], B0, f0);                                                                    \
-        f0 = fma(DI[3], C1, f0);                                                                    \
-        f0 = fma(DI[4], prv.a, f0);                                                                 \
-        f0 = fma(DI[5], cur.c, f0);                                                                 \
-        f0 = fma(DI[6], cur.b, f0);                                                                 \
-        acc = (i == 0) ? f0 : acc;                                                                  \
+      if (blk0) { /* face i = 0 at column c0 of lane 1: dirs 0, 2, 3, 6, 9, 10, 13 */                \
+        double f0 = fma(DI[0], cur.a.v0, s0);                                                       \
+        f0 = fma(DI[1], A1.v0, f0);                                                                 \
+        f0 = fma(DI[2], B0.v0, f0);                                                                 \
+        f0 = fma(DI[3], C1.v0, f0);                                                                 \
+        f0 = fma(DI[4], am1.v0, f0);                                                                \
+        f0 = fma(DI[5], cur.c.v0, f0);                                                              \
+        f0 = fma(DI[6], cur.b.v0, f0);                                                              \
+        s0 = (c0 == 0) ? f0 : s0;                                                                   \
       }                                                                                             \
-      *py = acc;                                                                                    \
+      if (c0 < LY) py[0] = s0;                                                                      \
+      if (c0 + 1 < LY) py[1] = s1;                                                                  \
     }                                                                                               \
     py += LY;                                                                                       \
     --LY;                                                                                           \
     ++j;                                                                                            \
-    prv.a = A1;                                                                                     \
-    prv.ap = A1p;                                                                                   \
-    prv.am = A1m;                                                                                   \
-    prv.b = B0;                                                                                     \
-    prv.bp = B0p;                                                                                   \
-    prv.c = C1;                                                                                     \
-    prv.cp = C1p;                                                                                   \
-    load3(pa, pb, pc, j + 1 < j1); /* refill for row j + 2 once A1/B0/C1 are dead */                \
+    am1n = cur.a;                                                                                   \
+    nxt.a = A1;                                                                                     \
+    nxt.b = B0;                                                                                     \
+    nxt.c = C1;                                                                                     \
   }
   while (true) {
-    BT_STEP(X, Y, pa0, pb0, pc0)
+    BT_STEP(X, Y, Am1, Am1y)
     if (j >= j1) break;
-    BT_STEP(Y, X, pa1, pb1, pc1)
+    BT_STEP(Y, X, Am1y, Am1)
     if (j >= j1) break;
   }
 #undef BT_STEP
@@ -212,8 +242,8 @@ __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict
   if (task >= ntasks) return;
   const int4 tk = tasks[task];
   const int k = tk.x, j0 = tk.z, j1 = tk.w, n = w - 1;
-  const int i = kMarchCols * tk.y + lane - 1;
-  const bool out_lane = lane >= 1 && lane <= kMarchCols && i >= 0;
+  const int i = kGenCols * tk.y + lane - 1;
+  const bool out_lane = lane >= 1 && lane <= kGenCols && i >= 0;
   const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
   double* __restrict__ yc = y + (int64_t)cell * cell_slots;
   auto at = [&](int jj, int kk) -> double {  // x at column i of row (jj, kk), 0 outside
@@ -223,10 +253,8 @@ __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict
   for (int j = j0; j < j1; ++j) {
     const double A0 = at(j, k), Am1 = at(j - 1, k), A1 = at(j + 1, k), B0 = at(j, k + 1), Bm1 = at(j - 1, k + 1);
     const double C0 = at(j, k - 1), C1 = at(j + 1, k - 1);
-    const double A0p = __shfl_down_sync(0xffffffffu, A0, 1), A0m = __shfl_up_sync(0xffffffffu, A0, 1);
-    const double Am1p = __shfl_down_sync(0xffffffffu, Am1, 1), A1m = __shfl_up_sync(0xffffffffu, A1, 1);
-    const double B0m = __shfl_up_sync(0xffffffffu, B0, 1), Bm1p = __shfl_down_sync(0xffffffffu, Bm1, 1);
-    const double C0p = __shfl_down_sync(0xffffffffu, C0, 1), C1m = __shfl_up_sync(0xffffffffu, C1, 1);
+    const double A0p = shdn(A0), A0m = shup(A0), Am1p = shdn(Am1), A1m = shup(A1);
+    const double B0m = shup(B0), Bm1p = shdn(Bm1), C0p = shdn(C0), C1m = shup(C1);
     const int LY = w - k - j;
     if (out_lane && i < LY) {
       const double v[15] = {A0, A0p, A1, B0, Am1p, C0p, C1, Bm1p, A0m, Am1, C0, A1m, B0m, Bm1, C1m};
@@ -245,22 +273,31 @@ __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict
 void init_stencil_tasks(bt_stencil& st) {
   const int w = (1 << st.level) + 1;
   std::vector<int4> fast, gen, all;
-  auto push = [](std::vector<int4>& v, int k, int b, int a, int e) {
-    for (int j0 = a; j0 < e; j0 += kMarchRows) v.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, e)));
+  // general rows are unprefetched: one row per task keeps them parallel
+  auto push1 = [](std::vector<int4>& v, int k, int b, int a, int e) {
+    for (int j = a; j < e; ++j) v.push_back(make_int4(k, b, j, j + 1));
   };
-  for (int k = 0; k < w; ++k)
-    for (int b = 0; kMarchCols * b < w - k; ++b) {
-      const int jmax = w - k - kMarchCols * b;  // rows of this column block
-      push(all, k, b, 0, jmax);
+  for (int k = 0; k < w; ++k) {
+    // general-kernel column blocks (30 wide): layer 0, row 0, and rows of
+    // length <= 2 (columns 0, 1: block 0)
+    for (int b = 0; kGenCols * b < w - k; ++b) {
+      const int jmax = w - k - kGenCols * b;
+      push1(all, k, b, 0, jmax);
       if (k == 0) {
-        push(gen, k, b, 0, jmax);
-        continue;
+        push1(gen, k, b, 0, jmax);
+      } else {
+        push1(gen, k, b, 0, 1);
+        if (b == 0) push1(gen, k, b, std::max(1, w - k - 2), jmax);
       }
-      push(gen, k, b, 0, 1);                                        // row 0
-      const int fe = b == 0 ? std::max(1, std::min(jmax, w - k - 2)) : jmax;  // block 0: row length >= 3
-      push(fast, k, b, 1, fe);
-      push(gen, k, b, fe, jmax);
     }
+    if (k == 0) continue;
+    // fast column blocks (60 wide): rows 1 .. (block 0: row length >= 3)
+    for (int b = 0; kFastCols * b < w - k; ++b) {
+      const int jmax = w - k - kFastCols * b;
+      const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;
+      for (int j0 = 1; j0 < fe; j0 += kMarchRows) fast.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, fe)));
+    }
+  }
   st.ntasks = (int)fast.size();
   st.d_tasks.upload(fast);
   st.ngtasks = (int)gen.size();
@@ -277,22 +314,22 @@ void init_stencil_tasks(bt_stencil& st) {
   static const int kOutside[3][4] = {{0, 0, 0, 0}, {1, 2, 3, 7}, {8, 11, 12, 14}};
   st.fast.assign(22 * (size_t)nc, 0.0);
   for (int c = 0; c < nc; ++c) {
-    const auto& r = st.rows[c];
-    for (int d = 1; d <= 7; ++d) st.symmetric = st.symmetric && r[d] == r[d + 7];
+    const auto& rw = st.rows[c];
+    for (int d = 1; d <= 7; ++d) st.symmetric = st.symmetric && rw[d] == rw[d + 7];
     for (int z : {1, 2}) {
       const int* dirs = z == 1 ? kDiagDirs : kI0Dirs;
       for (int d = 0; d < 15; ++d) {
         bool exempt = false;
         for (int q = 0; q < 7; ++q) exempt = exempt || dirs[q] == d;
         for (int q = 0; q < 4; ++q) exempt = exempt || kOutside[z][q] == d;
-        if (!exempt && cells[c].w[z][d] != r[d]) st.symmetric = false;
+        if (!exempt && cells[c].w[z][d] != rw[d]) st.symmetric = false;
       }
     }
     double* f = &st.fast[22 * (size_t)c];
-    for (int d = 0; d < 8; ++d) f[d] = r[d];
+    for (int d = 0; d < 8; ++d) f[d] = rw[d];
     for (int q = 0; q < 7; ++q) {
-      f[8 + q] = cells[c].w[1][kDiagDirs[q]] - r[kDiagDirs[q]];
-      f[15 + q] = cells[c].w[2][kI0Dirs[q]] - r[kI0Dirs[q]];
+      f[8 + q] = cells[c].w[1][kDiagDirs[q]] - rw[kDiagDirs[q]];
+      f[15 + q] = cells[c].w[2][kI0Dirs[q]] - rw[kI0Dirs[q]];
     }
   }
 }
