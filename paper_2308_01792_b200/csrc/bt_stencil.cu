@@ -66,6 +66,24 @@ struct Win {  // A(j) of layer k, B(j-1) of layer k+1, C(j) of layer k-1
   Row4 a, b, c;
 };
 
+// per-warp cp.async ring: kStages stages x 3 staged rows; a row holds the
+// warp's 64 columns at offset kRowOff (slack on both sides for the l / r reads)
+constexpr int kStages = 4;
+constexpr int kRowOff = 2;
+constexpr int kRowD = 68;                  // doubles per staged row (16 B multiple)
+constexpr int kStageD = 3 * kRowD;
+constexpr int kRingD = kStages * kStageD;  // doubles per warp
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
@@ -74,6 +92,7 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
                                                         const int4* __restrict__ tasks, int ntasks, int w,
                                                         int64_t cell_slots, int cell0,
                                                         const __grid_constant__ FastParams<kMaxC> fp) {
+  extern __shared__ __align__(16) double ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int task = blockIdx.x * kW + warp;
   if (task >= ntasks) return;
@@ -87,10 +106,38 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
   const int c0 = kFastCols * blk + 2 * lane - 2;  // this lane's columns c0, c0 + 1
   const bool out_lane = lane >= 1 && lane <= kFastCols / 2;
   const bool up = k + 1 <= n;
-  // column pointers: entry t of row r is xc[row_start(r) + t]
-  const double* __restrict__ xc = x + (int64_t)cell * cell_slots + c0;
+  const double* __restrict__ xc = x + (int64_t)cell * cell_slots + c0;  // column c0 of every row
+  double* ring = ring_all + warp * kRingD;
+  const int me = kRowOff + 2 * lane;  // this lane's pair inside a staged row
 
-  // predicated pair load of a row with start rs and length len at columns c0, c0 + 1
+  // ---- producer: stage rows A(j+1), B(j), C(j+1) of step j into the ring.
+  // len(A(j+1)) = len(B(j)) = r, len(C(j+1)) = r + 1 with r = w - k - j - 1.
+  int r = w - k - j0 - 1;
+  const double* __restrict__ qA = xc + row_start(w, j0 + 1, k);
+  const double* __restrict__ qB = xc + (up ? row_start(w, j0, k + 1) : 0);
+  const double* __restrict__ qC = xc + row_start(w, j0 + 1, k - 1);
+  auto stage_rows = [&](int stage, bool live) {
+    double* st = ring + stage * kStageD + me;
+    const bool a0 = live && c0 >= 0 && c0 < r, a1 = live && c0 + 1 >= 0 && c0 + 1 < r;
+    const bool b0 = a0 && up, b1 = a1 && up;
+    const bool e0 = live && c0 >= 0 && c0 <= r, e1 = live && c0 + 1 >= 0 && c0 + 1 <= r;
+    cp_async8(st, a0 ? qA : x, a0);
+    cp_async8(st + 1, a1 ? qA + 1 : x, a1);
+    cp_async8(st + kRowD, b0 ? qB : x, b0);
+    cp_async8(st + kRowD + 1, b1 ? qB + 1 : x, b1);
+    cp_async8(st + 2 * kRowD, e0 ? qC : x, e0);
+    cp_async8(st + 2 * kRowD + 1, e1 ? qC + 1 : x, e1);
+    cp_commit();
+    qA += r;
+    qB += r;
+    qC += r + 1;
+    --r;
+  };
+  const int nsteps = j1 - j0;
+#pragma unroll
+  for (int q = 0; q < kStages - 1; ++q) stage_rows(q, q < nsteps);
+
+  // window at row j0: A(j0), B(j0 - 1), C(j0) and A(j0 - 1), loaded directly
   auto ld2 = [&](const double* p, int len, double& v0, double& v1) {
     v0 = (c0 >= 0 && c0 < len) ? __ldg(p) : 0.0;
     v1 = (c0 + 1 >= 0 && c0 + 1 < len) ? __ldg(p + 1) : 0.0;
@@ -103,29 +150,8 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
     q.r = shdn(v0);
     return q;
   };
-
-  // prefetch cursors for the rows consumed at row j: A(j+1), B(j), C(j+1).
-  // len(A(j+1)) = len(B(j)) = r, len(C(j+1)) = r + 1, r = w - k - j - 1.
-  int r = w - k - j0 - 1;
-  const double* __restrict__ qA = xc + row_start(w, j0 + 1, k);
-  const double* __restrict__ qB = xc + (up ? row_start(w, j0, k + 1) : 0);
-  const double* __restrict__ qC = xc + row_start(w, j0 + 1, k - 1);
-  double na0, na1, nb0, nb1, nc0, nc1;
-  auto prefetch = [&](bool live) {
-    const int ra = live ? r : 0, rb = (live && up) ? r : 0, rc = live ? r + 1 : 0;
-    ld2(qA, ra, na0, na1);
-    ld2(qB, rb, nb0, nb1);
-    ld2(qC, rc, nc0, nc1);
-    qA += r;
-    qB += r;
-    qC += r + 1;
-    --r;
-  };
-  prefetch(true);
-
-  // window at row j0: A(j0), B(j0 - 1), C(j0); plus A(j0 - 1) (only v0, v1, r used)
-  Win X;
-  Row4 Am1;
+  Win X, Y;
+  Row4 Am1, Am1y;
   {
     double a0, a1, b0, b1, e0, e1, m0, m1;
     ld2(xc + row_start(w, j0, k), w - k - j0, a0, a1);
@@ -137,17 +163,15 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
     X.c = make_row(e0, e1);
     Am1 = make_row(m0, m1);
   }
-  Win Y;  // the second window set (written by the first step)
-  Row4 Am1y;
 
   int LY = w - k - j0;  // length of the output row
   double* __restrict__ py = y + (int64_t)cell * cell_slots + c0 + row_start(w, j0, k);
   const int colend = kFastCols * blk + kFastCols;  // LY <= colend: the row ends in this warp
   const bool blk0 = blk == 0;
-  int j = j0;
+  int j = j0, q = 0;
 
-  // One step: output row j at columns c0 (p = 0) and c0 + 1 (p = 1).
-  // cur: A(j), B(j-1), C(j); am1: A(j-1); new rows A1 = A(j+1), B0 = B(j),
+  // One step: output row j at columns c0 (s0) and c0 + 1 (s1).
+  // cur: A(j), B(j-1), C(j); am1: A(j-1); staged rows A1 = A(j+1), B0 = B(j),
   // C1 = C(j+1). kStencilDirs pairs (d, d + 7):
   //   (1,0,0)/(-1,0,0)  A(j) at i+1 / i-1      (0,1,0)/(0,-1,0)  A(j+1) / A(j-1)
   //   (0,0,1)/(0,0,-1)  B(j) / C(j)            (1,-1,0)/(-1,1,0) A(j-1) i+1 / A(j+1) i-1
@@ -155,10 +179,24 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
   //   (1,-1,1)/(-1,1,-1) B(j-1) i+1 / C(j+1) i-1
 #define BT_STEP(cur, nxt, am1, am1n)                                                                \
   {                                                                                                 \
-    const Row4 A1 = make_row(na0, na1), B0 = make_row(nb0, nb1), C1 = make_row(nc0, nc1);           \
-    prefetch(j + 1 < j1); /* rows for step j + 1 */                                                 \
+    cp_wait<kStages - 2>();                                                                         \
+    __syncwarp();                                                                                   \
+    const double* sg = ring + (q % kStages) * kStageD + me;                                         \
+    Row4 A1, B0, C1;                                                                                \
+    A1.l = sg[-1];                                                                                  \
+    A1.v0 = sg[0];                                                                                  \
+    A1.v1 = sg[1];                                                                                  \
+    A1.r = sg[2];                                                                                   \
+    B0.l = sg[kRowD - 1];                                                                           \
+    B0.v0 = sg[kRowD];                                                                              \
+    B0.v1 = sg[kRowD + 1];                                                                          \
+    B0.r = sg[kRowD + 2];                                                                           \
+    C1.l = sg[2 * kRowD - 1];                                                                       \
+    C1.v0 = sg[2 * kRowD];                                                                          \
+    C1.v1 = sg[2 * kRowD + 1];                                                                      \
+    C1.r = sg[2 * kRowD + 2];                                                                       \
+    stage_rows((q + kStages - 1) % kStages, q + kStages - 1 < nsteps);                              \
     if (out_lane) {                                                                                 \
-      /* column c0: left neighbours are the .l values, right ones .v1 */                           \
       double s0 = W[0] * cur.a.v0;                                                                  \
       s0 = fma(W[1], cur.a.v1 + cur.a.l, s0);                                                       \
       s0 = fma(W[2], A1.v0 + am1.v0, s0);                                                           \
@@ -167,7 +205,6 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
       s0 = fma(W[5], cur.c.v1 + B0.l, s0);                                                          \
       s0 = fma(W[6], C1.v0 + cur.b.v0, s0);                                                         \
       s0 = fma(W[7], cur.b.v1 + C1.l, s0);                                                          \
-      /* column c0 + 1: left neighbours .v0, right ones .r */                                      \
       double s1 = W[0] * cur.a.v1;                                                                  \
       s1 = fma(W[1], cur.a.r + cur.a.v0, s1);                                                       \
       s1 = fma(W[2], A1.v1 + am1.v1, s1);                                                           \
@@ -210,6 +247,7 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
     py += LY;                                                                                       \
     --LY;                                                                                           \
     ++j;                                                                                            \
+    ++q;                                                                                            \
     am1n = cur.a;                                                                                   \
     nxt.a = A1;                                                                                     \
     nxt.b = B0;                                                                                     \
@@ -222,6 +260,7 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
     if (j >= j1) break;
   }
 #undef BT_STEP
+  cp_wait<0>();
 }
 
 // Any rows of the march schedule, every row read from the zero-set-typed
@@ -361,8 +400,14 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
         fp.di[c][q] = f[15 + q];
       }
     }
-    k_stencil_fast<kMaxCells><<<dim3((st.ntasks + kW - 1) / kW, cnt), kT, 0, s>>>(x, y, st.d_tasks.p, st.ntasks, w,
-                                                                                 cs, c0, fp);
+    const size_t smem = sizeof(double) * kW * kRingD;
+    static bool attr = false;
+    if (!attr) {
+      BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_stencil_fast<kMaxCells><<<dim3((st.ntasks + kW - 1) / kW, cnt), kT, smem, s>>>(x, y, st.d_tasks.p, st.ntasks,
+                                                                                    w, cs, c0, fp);
     count_launch();
   }
   check_launch("k_stencil");
