@@ -2,31 +2,32 @@
 // operators.hpp:247-271), per-cell phase. The interface phase (replica sums
 // and Dirichlet rows) is bt_interface.cu.
 //
-// Data path (k_stencil_fast). A warp owns 60 consecutive columns i of one
-// layer k of one macro-cell — two adjacent columns per lane, lanes 0 and 31
-// carry halo columns — and marches up to kMarchRows rows j. Each step needs
-// three new rows at its columns — A(j+1) of layer k, B(j) of layer k+1 and
-// C(j+1) of layer k-1, each one coalesced 512 B segment — loaded one step
-// early into registers (predicated to 0 outside the lattice, so
-// lattice-boundary vertices need no special loads); the i-1 / i+2 columns
-// of a lane come from two warp shuffles per row. The march is unrolled by
-// two over alternating window sets, so the sliding window costs no moves.
-// Every x value is read from L2 once per layer that needs it (3x) and from
-// HBM once.
+// Data path (k_stencil_fast). A warp owns 62 consecutive output columns i of
+// one layer k of one macro-cell and marches up to kMarchRows rows j. Each
+// step needs three new rows — A(j+1) of layer k, B(j) of layer k+1 and C(j+1)
+// of layer k-1 — over the warp's 64 staged columns [base - 1, base + 63).
+// Lane 0 stages them with TMA bulk copies (cp.async.bulk, 528 B each, 16 B
+// aligned with a per-row shift) into a per-warp kStages-deep shared-memory
+// ring completed on mbarriers, so the copies cost no LSU wavefronts and no
+// registers. Lanes read two contiguous 32-column halves (columns base-1+l and
+// base+31+l) plus their i-1 / i+1 neighbours from the ring; values reused by
+// later rows stay in registers (window sets alternate, no moves). Every x
+// value is read from L2 once per layer that needs it (3x) and from HBM once.
 //
 // Rows. The host splits every (layer, column block) march into fast rows and
-// a few general rows. Fast rows (k >= 1, j >= 1, and row length >= 3 in
-// column block 0) contain interior vertices plus at most the diagonal-face
-// vertex (i = row end) and the i = 0 vertex; k_stencil_fast evaluates the
-// merged row (compute_stencil operators.hpp:204-221) in its symmetric
-// 8-weight form (W[d] == W[-d] bitwise, checked on the host) and switches the
-// two face vertices to their zero-set-typed partial rows (per-cell part of
-// partial_row_apply, operators.hpp:78-96) by 7-term corrections selected per
-// lane; the corrections only run in warps that contain such a vertex. All
-// weights are kernel parameters, so they reach the DFMAs as uniform-register
-// operands. General rows (layer 0, row 0, the last two rows of column 0) go
-// through k_stencil_general, which reads the typed rows from shared memory;
-// it is also the fallback for tables that fail the fast-path checks.
+// a few general rows. Fast rows (1 <= k <= n-2, j >= 1, row length >= 3 in
+// column block 0) hold interior vertices, evaluated with the merged row
+// (compute_stencil operators.hpp:204-221) in its symmetric 8-weight form
+// (W[d] == W[-d] bitwise, checked on the host), plus at most the
+// diagonal-face vertex (i = row end) and the i = 0 vertex, evaluated with
+// their zero-set-typed partial rows (per-cell part of partial_row_apply,
+// operators.hpp:78-96) over their 11 present neighbours only — so nothing
+// outside the lattice is ever used and the staged rows need no masking. All
+// weights are kernel parameters: they reach the DFMAs as uniform-register
+// operands. General rows (layers 0, n-1, n, row 0, the last two rows of
+// column 0) go through k_stencil_general, which reads the typed rows from
+// shared memory; it is also the fallback for tables that fail the fast-path
+// checks.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,210 +41,225 @@ namespace {
 constexpr int kT = 256;
 constexpr int kW = kT / 32;
 constexpr int kMarchRows = 48;
-constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
+constexpr int kFastCols = 62;  // output columns per warp in k_stencil_fast
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
 
-// directions whose weight differs between the interior row and the typed row
-// of the diagonal face (zero set {0}) / the face i = 0 (zero set {1});
-// structural (which micro-cells are missing), verified on the host.
-constexpr int kDiagDirs[7] = {0, 4, 5, 6, 11, 12, 13};
-constexpr int kI0Dirs[7] = {0, 2, 3, 6, 9, 10, 13};
+// present neighbour directions (kStencilDirs indices) of a diagonal-face
+// vertex (zero set {0}) and of an i = 0 vertex (zero set {1})
+constexpr int kDiagPresent[11] = {0, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14};
+constexpr int kI0Present[11] = {0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 13};
 
 template <int kMaxC>
 struct FastParams {
-  double w[kMaxC][8];   // symmetric interior row: centre + 7 direction pairs
-  double dd[kMaxC][7];  // diagonal-face correction on kDiagDirs
-  double di[kMaxC][7];  // i = 0 face correction on kI0Dirs
+  double w[kMaxC][8];    // symmetric interior row: centre + 7 direction pairs
+  double dg[kMaxC][11];  // diagonal-face typed row on kDiagPresent
+  double f0[kMaxC][11];  // i = 0 face typed row on kI0Present
 };
-constexpr int kMaxCells = 176;  // 176 * 22 * 8 B = 30 KB of kernel parameters
+constexpr int kMaxCells = 128;  // 128 * 30 * 8 B = 30 KB of kernel parameters
 
-// One row at a lane's two columns (c0 = v0, c1 = v1) with the neighbours
-// l = column c0 - 1 and r = column c1 + 1.
-struct Row4 {
-  double l, v0, v1, r;
-};
-struct Win {  // A(j) of layer k, B(j-1) of layer k+1, C(j) of layer k-1
-  Row4 a, b, c;
-};
-
-// per-warp cp.async ring: kStages stages x 3 staged rows; a row holds the
-// warp's 64 columns at offset kRowOff (slack on both sides for the l / r reads)
+// per-warp TMA ring: kStages stages x 3 staged rows of kRowD doubles
 constexpr int kStages = 4;
-constexpr int kRowOff = 2;
-constexpr int kRowD = 68;                  // doubles per staged row (16 B multiple)
+constexpr int kRowD = 72;                  // >= 66 doubles (528 B copy), 16 B multiple
 constexpr int kStageD = 3 * kRowD;
 constexpr int kRingD = kStages * kStageD;  // doubles per warp
+constexpr int kCopyBytes = 528;            // 64 columns + one 16 B alignment chunk
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(valid ? 8 : 0) : "memory");
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_row(double* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
-__device__ __forceinline__ double shup(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-__device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+struct Row3 {  // one row at a lane's two columns: v = value, l = column - 1, r = column + 1
+  double l0, v0, r0, l1, v1, r1;
+};
+struct Win {  // A(j) of layer k, B(j-1) of layer k+1, C(j) of layer k-1
+  Row3 a, b, c;
+};
 
 template <int kMaxC>
 __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
-                                                        int64_t cell_slots, int cell0,
+                                                        int64_t cell_slots, int cell0, const double* x_end,
                                                         const __grid_constant__ FastParams<kMaxC> fp) {
-  extern __shared__ __align__(16) double ring_all[];
+  extern __shared__ __align__(128) double ring_all[];
+  __shared__ __align__(8) uint64_t bars[kW][kStages];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int task = blockIdx.x * kW + warp;
   if (task >= ntasks) return;
   const int cell = cell0 + blockIdx.y;
   const double* W = fp.w[blockIdx.y];
-  const double* DD = fp.dd[blockIdx.y];
-  const double* DI = fp.di[blockIdx.y];
+  const double* DG = fp.dg[blockIdx.y];
+  const double* F0 = fp.f0[blockIdx.y];
   const int4 tk = tasks[task];
-  const int k = tk.x, blk = tk.y, j0 = tk.z, j1 = tk.w;  // k >= 1, j0 >= 1 by construction
-  const int n = w - 1;
-  const int c0 = kFastCols * blk + 2 * lane - 2;  // this lane's columns c0, c0 + 1
-  const bool out_lane = lane >= 1 && lane <= kFastCols / 2;
-  const bool up = k + 1 <= n;
-  const double* __restrict__ xc = x + (int64_t)cell * cell_slots + c0;  // column c0 of every row
+  const int k = tk.x, blk = tk.y, j0 = tk.z, j1 = tk.w;  // k in [1, n-2], j0 >= 1 by construction
+  const int base = kFastCols * blk;
+  const int c0 = base - 1 + lane, c1 = base + 31 + lane;  // this lane's two columns
+  const bool out0 = lane >= 1, out1 = lane <= 30;
+  const double* __restrict__ xcell = x + (int64_t)cell * cell_slots;
   double* ring = ring_all + warp * kRingD;
-  const int me = kRowOff + 2 * lane;  // this lane's pair inside a staged row
+  uint64_t* bar = bars[warp];
+  const uint64_t end16 = ((uint64_t)x_end + 15) & ~(uint64_t)15;
 
-  // ---- producer: stage rows A(j+1), B(j), C(j+1) of step j into the ring.
-  // len(A(j+1)) = len(B(j)) = r, len(C(j+1)) = r + 1 with r = w - k - j - 1.
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+
+  // producer cursors: rows A(j+1), B(j), C(j+1) of step j; offsets of column
+  // base - 1 in each row. len(A(j+1)) = len(B(j)) = r, len(C(j+1)) = r + 1.
   int r = w - k - j0 - 1;
-  const double* __restrict__ qA = xc + row_start(w, j0 + 1, k);
-  const double* __restrict__ qB = xc + (up ? row_start(w, j0, k + 1) : 0);
-  const double* __restrict__ qC = xc + row_start(w, j0 + 1, k - 1);
-  auto stage_rows = [&](int stage, bool live) {
-    double* st = ring + stage * kStageD + me;
-    const bool a0 = live && c0 >= 0 && c0 < r, a1 = live && c0 + 1 >= 0 && c0 + 1 < r;
-    const bool b0 = a0 && up, b1 = a1 && up;
-    const bool e0 = live && c0 >= 0 && c0 <= r, e1 = live && c0 + 1 >= 0 && c0 + 1 <= r;
-    cp_async8(st, a0 ? qA : x, a0);
-    cp_async8(st + 1, a1 ? qA + 1 : x, a1);
-    cp_async8(st + kRowD, b0 ? qB : x, b0);
-    cp_async8(st + kRowD + 1, b1 ? qB + 1 : x, b1);
-    cp_async8(st + 2 * kRowD, e0 ? qC : x, e0);
-    cp_async8(st + 2 * kRowD + 1, e1 ? qC + 1 : x, e1);
-    cp_commit();
-    qA += r;
-    qB += r;
-    qC += r + 1;
+  int oA = row_start(w, j0 + 1, k) + base - 1;
+  int oB = row_start(w, j0, k + 1) + base - 1;
+  int oC = row_start(w, j0 + 1, k - 1) + base - 1;
+  auto produce = [&](int stage) {  // lane 0 only
+    double* st = ring + stage * kStageD;
+    const double* srcs[3] = {xcell + oA, xcell + oB, xcell + oC};
+    uint32_t total = 0, bytes[3];
+    uint64_t al[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      al[q] = (uint64_t)srcs[q] & ~(uint64_t)15;
+      const uint64_t lim = end16 - al[q];
+      bytes[q] = lim < (uint64_t)kCopyBytes ? (uint32_t)lim : (uint32_t)kCopyBytes;
+      total += bytes[q];
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(&bar[stage], total);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) tma_row(st + q * kRowD, (const void*)al[q], bytes[q], &bar[stage]);
+  };
+  auto advance = [&]() {
+    oA += r;
+    oB += r;
+    oC += r + 1;
     --r;
   };
+  // shift (in doubles) of column base - 1 inside a staged row
+  auto shift_of = [&](int o) -> int { return (int)(((uint64_t)(xcell + o) >> 3) & 1); };
   const int nsteps = j1 - j0;
+  // per-stage shifts of the three rows (3 bits per stage), tracked
+  // identically by every lane
+  uint32_t shbits = 0;
+  auto note_shifts = [&](int stage) {
+    const uint32_t b = (uint32_t)(shift_of(oA) | (shift_of(oB) << 1) | (shift_of(oC) << 2));
+    shbits = (shbits & ~(7u << (3 * stage))) | (b << (3 * stage));
+  };
 #pragma unroll
-  for (int q = 0; q < kStages - 1; ++q) stage_rows(q, q < nsteps);
+  for (int q = 0; q < kStages - 1; ++q) {
+    note_shifts(q);
+    if (q < nsteps && lane == 0) produce(q);
+    advance();
+  }
 
   // window at row j0: A(j0), B(j0 - 1), C(j0) and A(j0 - 1), loaded directly
-  auto ld2 = [&](const double* p, int len, double& v0, double& v1) {
-    v0 = (c0 >= 0 && c0 < len) ? __ldg(p) : 0.0;
-    v1 = (c0 + 1 >= 0 && c0 + 1 < len) ? __ldg(p + 1) : 0.0;
-  };
-  auto make_row = [&](double v0, double v1) {
-    Row4 q;
-    q.v0 = v0;
-    q.v1 = v1;
-    q.l = shup(v1);
-    q.r = shdn(v0);
+  auto at = [&](int rs, int len, int c) -> double { return (c >= 0 && c < len) ? __ldg(xcell + rs + c) : 0.0; };
+  auto load_row = [&](int rs, int len) {
+    Row3 q;
+    q.l0 = at(rs, len, c0 - 1);
+    q.v0 = at(rs, len, c0);
+    q.r0 = at(rs, len, c0 + 1);
+    q.l1 = at(rs, len, c1 - 1);
+    q.v1 = at(rs, len, c1);
+    q.r1 = at(rs, len, c1 + 1);
     return q;
   };
   Win X, Y;
-  Row4 Am1, Am1y;
-  {
-    double a0, a1, b0, b1, e0, e1, m0, m1;
-    ld2(xc + row_start(w, j0, k), w - k - j0, a0, a1);
-    ld2(xc + (up ? row_start(w, j0 - 1, k + 1) : 0), up ? w - k - j0 : 0, b0, b1);
-    ld2(xc + row_start(w, j0, k - 1), w - k - j0 + 1, e0, e1);
-    ld2(xc + row_start(w, j0 - 1, k), w - k - j0 + 1, m0, m1);
-    X.a = make_row(a0, a1);
-    X.b = make_row(b0, b1);
-    X.c = make_row(e0, e1);
-    Am1 = make_row(m0, m1);
-  }
+  Row3 Am1, Am1y;
+  X.a = load_row(row_start(w, j0, k), w - k - j0);
+  X.b = load_row(row_start(w, j0 - 1, k + 1), w - k - j0);
+  X.c = load_row(row_start(w, j0, k - 1), w - k - j0 + 1);
+  Am1 = load_row(row_start(w, j0 - 1, k), w - k - j0 + 1);
 
   int LY = w - k - j0;  // length of the output row
-  double* __restrict__ py = y + (int64_t)cell * cell_slots + c0 + row_start(w, j0, k);
-  const int colend = kFastCols * blk + kFastCols;  // LY <= colend: the row ends in this warp
+  double* __restrict__ py = y + (int64_t)cell * cell_slots + row_start(w, j0, k);
+  const int colend = base + kFastCols;  // LY <= colend: the row ends inside this warp
   const bool blk0 = blk == 0;
   int j = j0, q = 0;
 
-  // One step: output row j at columns c0 (s0) and c0 + 1 (s1).
+  auto read_row = [&](const double* row, int sh) {
+    Row3 o;
+    const double* p = row + sh + lane;  // column base - 1 + lane
+    o.l0 = p[-1];
+    o.v0 = p[0];
+    o.r0 = p[1];
+    o.l1 = p[31];
+    o.v1 = p[32];
+    o.r1 = p[33];
+    return o;
+  };
+
+  // One step: output row j at columns c0 (s0) and c1 (s1).
   // cur: A(j), B(j-1), C(j); am1: A(j-1); staged rows A1 = A(j+1), B0 = B(j),
   // C1 = C(j+1). kStencilDirs pairs (d, d + 7):
-  //   (1,0,0)/(-1,0,0)  A(j) at i+1 / i-1      (0,1,0)/(0,-1,0)  A(j+1) / A(j-1)
+  //   (1,0,0)/(-1,0,0)  A(j) i+1 / i-1         (0,1,0)/(0,-1,0)  A(j+1) / A(j-1)
   //   (0,0,1)/(0,0,-1)  B(j) / C(j)            (1,-1,0)/(-1,1,0) A(j-1) i+1 / A(j+1) i-1
   //   (1,0,-1)/(-1,0,1) C(j) i+1 / B(j) i-1    (0,1,-1)/(0,-1,1) C(j+1) / B(j-1)
   //   (1,-1,1)/(-1,1,-1) B(j-1) i+1 / C(j+1) i-1
+#define BT_INTERIOR(cur, am1, s, v, l, r)                                                                     \
+  double s = W[0] * cur.a.v;                                                                        \
+  s = fma(W[1], cur.a.r + cur.a.l, s);                                                              \
+  s = fma(W[2], A1.v + am1.v, s);                                                                   \
+  s = fma(W[3], B0.v + cur.c.v, s);                                                                 \
+  s = fma(W[4], am1.r + A1.l, s);                                                                   \
+  s = fma(W[5], cur.c.r + B0.l, s);                                                                 \
+  s = fma(W[6], C1.v + cur.b.v, s);                                                                 \
+  s = fma(W[7], cur.b.r + C1.l, s);
+  // typed rows over present neighbours (kDiagPresent / kI0Present order)
+#define BT_DIAG(cur, am1, v, l, r)                                                                            \
+  (DG[0] * cur.a.v + DG[1] * am1.r + DG[2] * cur.c.r + DG[3] * C1.v + DG[4] * cur.a.l +             \
+   DG[5] * am1.v + DG[6] * cur.c.v + DG[7] * A1.l + DG[8] * B0.l + DG[9] * cur.b.v + DG[10] * C1.l)
+#define BT_FACE0(cur, am1, v, l, r)                                                                           \
+  (F0[0] * cur.a.v + F0[1] * cur.a.r + F0[2] * A1.v + F0[3] * B0.v + F0[4] * am1.r +                \
+   F0[5] * cur.c.r + F0[6] * C1.v + F0[7] * cur.b.r + F0[8] * am1.v + F0[9] * cur.c.v +             \
+   F0[10] * cur.b.v)
 #define BT_STEP(cur, nxt, am1, am1n)                                                                \
   {                                                                                                 \
-    cp_wait<kStages - 2>();                                                                         \
+    const int sg = q % kStages;                                                                     \
+    mbar_wait(&bar[sg], (uint32_t)((q / kStages) & 1));                                             \
+    const double* st = ring + sg * kStageD;                                                         \
+    const uint32_t sb = shbits >> (3 * sg);                                                         \
+    const Row3 A1 = read_row(st, sb & 1);                                                           \
+    const Row3 B0 = read_row(st + kRowD, (sb >> 1) & 1);                                            \
+    const Row3 C1 = read_row(st + 2 * kRowD, (sb >> 2) & 1);                                        \
     __syncwarp();                                                                                   \
-    const double* sg = ring + (q % kStages) * kStageD + me;                                         \
-    Row4 A1, B0, C1;                                                                                \
-    A1.l = sg[-1];                                                                                  \
-    A1.v0 = sg[0];                                                                                  \
-    A1.v1 = sg[1];                                                                                  \
-    A1.r = sg[2];                                                                                   \
-    B0.l = sg[kRowD - 1];                                                                           \
-    B0.v0 = sg[kRowD];                                                                              \
-    B0.v1 = sg[kRowD + 1];                                                                          \
-    B0.r = sg[kRowD + 2];                                                                           \
-    C1.l = sg[2 * kRowD - 1];                                                                       \
-    C1.v0 = sg[2 * kRowD];                                                                          \
-    C1.v1 = sg[2 * kRowD + 1];                                                                      \
-    C1.r = sg[2 * kRowD + 2];                                                                       \
-    stage_rows((q + kStages - 1) % kStages, q + kStages - 1 < nsteps);                              \
-    if (out_lane) {                                                                                 \
-      double s0 = W[0] * cur.a.v0;                                                                  \
-      s0 = fma(W[1], cur.a.v1 + cur.a.l, s0);                                                       \
-      s0 = fma(W[2], A1.v0 + am1.v0, s0);                                                           \
-      s0 = fma(W[3], B0.v0 + cur.c.v0, s0);                                                         \
-      s0 = fma(W[4], am1.v1 + A1.l, s0);                                                            \
-      s0 = fma(W[5], cur.c.v1 + B0.l, s0);                                                          \
-      s0 = fma(W[6], C1.v0 + cur.b.v0, s0);                                                         \
-      s0 = fma(W[7], cur.b.v1 + C1.l, s0);                                                          \
-      double s1 = W[0] * cur.a.v1;                                                                  \
-      s1 = fma(W[1], cur.a.r + cur.a.v0, s1);                                                       \
-      s1 = fma(W[2], A1.v1 + am1.v1, s1);                                                           \
-      s1 = fma(W[3], B0.v1 + cur.c.v1, s1);                                                         \
-      s1 = fma(W[4], am1.r + A1.v0, s1);                                                            \
-      s1 = fma(W[5], cur.c.r + B0.v0, s1);                                                          \
-      s1 = fma(W[6], C1.v1 + cur.b.v1, s1);                                                         \
-      s1 = fma(W[7], cur.b.r + C1.v0, s1);                                                          \
-      if (LY <= colend) { /* row end in this warp: diagonal face, dirs 0, 4, 5, 6, 11, 12, 13 */     \
-        double d0 = fma(DD[0], cur.a.v0, s0);                                                       \
-        d0 = fma(DD[1], am1.v1, d0);                                                                \
-        d0 = fma(DD[2], cur.c.v1, d0);                                                              \
-        d0 = fma(DD[3], C1.v0, d0);                                                                 \
-        d0 = fma(DD[4], A1.l, d0);                                                                  \
-        d0 = fma(DD[5], B0.l, d0);                                                                  \
-        d0 = fma(DD[6], cur.b.v0, d0);                                                              \
-        double d1 = fma(DD[0], cur.a.v1, s1);                                                       \
-        d1 = fma(DD[1], am1.r, d1);                                                                 \
-        d1 = fma(DD[2], cur.c.r, d1);                                                               \
-        d1 = fma(DD[3], C1.v1, d1);                                                                 \
-        d1 = fma(DD[4], A1.v0, d1);                                                                 \
-        d1 = fma(DD[5], B0.v0, d1);                                                                 \
-        d1 = fma(DD[6], cur.b.v1, d1);                                                              \
-        s0 = (c0 == LY - 1) ? d0 : s0;                                                              \
-        s1 = (c0 + 1 == LY - 1) ? d1 : s1;                                                          \
-      }                                                                                             \
-      if (blk0) { /* face i = 0 at column c0 of lane 1: dirs 0, 2, 3, 6, 9, 10, 13 */                \
-        double f0 = fma(DI[0], cur.a.v0, s0);                                                       \
-        f0 = fma(DI[1], A1.v0, f0);                                                                 \
-        f0 = fma(DI[2], B0.v0, f0);                                                                 \
-        f0 = fma(DI[3], C1.v0, f0);                                                                 \
-        f0 = fma(DI[4], am1.v0, f0);                                                                \
-        f0 = fma(DI[5], cur.c.v0, f0);                                                              \
-        f0 = fma(DI[6], cur.b.v0, f0);                                                              \
-        s0 = (c0 == 0) ? f0 : s0;                                                                   \
-      }                                                                                             \
-      if (c0 < LY) py[0] = s0;                                                                      \
-      if (c0 + 1 < LY) py[1] = s1;                                                                  \
+    {                                                                                               \
+      const int ps = (q + kStages - 1) % kStages;                                                   \
+      note_shifts(ps);                                                                              \
+      if (q + kStages - 1 < nsteps && lane == 0) produce(ps);                                       \
+      advance();                                                                                    \
     }                                                                                               \
+    BT_INTERIOR(cur, am1, s0, v0, l0, r0)                                                                     \
+    BT_INTERIOR(cur, am1, s1, v1, l1, r1)                                                                     \
+    if (LY <= colend) { /* the diagonal-face vertex is in this warp */                              \
+      if (c0 == LY - 1) s0 = BT_DIAG(cur, am1, v0, l0, r0);                                                   \
+      if (c1 == LY - 1) s1 = BT_DIAG(cur, am1, v1, l1, r1);                                                   \
+    }                                                                                               \
+    if (blk0 && c0 == 0) s0 = BT_FACE0(cur, am1, v0, l0, r0); /* lane 1 of block 0 */                         \
+    if (out0 && c0 < LY) py[c0] = s0;                                                               \
+    if (out1 && c1 < LY) py[c1] = s1;                                                               \
     py += LY;                                                                                       \
     --LY;                                                                                           \
     ++j;                                                                                            \
@@ -260,7 +276,9 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
     if (j >= j1) break;
   }
 #undef BT_STEP
-  cp_wait<0>();
+#undef BT_FACE0
+#undef BT_DIAG
+#undef BT_INTERIOR
 }
 
 // Any rows of the march schedule, every row read from the zero-set-typed
@@ -289,6 +307,8 @@ __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict
     if (i < 0 || jj < 0 || kk < 0 || kk > n || i >= w - kk - jj) return 0.0;
     return __ldg(xc + row_start(w, jj, kk) + i);
   };
+  auto shup = [](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
+  auto shdn = [](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
   for (int j = j0; j < j1; ++j) {
     const double A0 = at(j, k), Am1 = at(j - 1, k), A1 = at(j + 1, k), B0 = at(j, k + 1), Bm1 = at(j - 1, k + 1);
     const double C0 = at(j, k - 1), C1 = at(j + 1, k - 1);
@@ -311,27 +331,27 @@ __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict
 
 void init_stencil_tasks(bt_stencil& st) {
   const int w = (1 << st.level) + 1;
+  const int n = w - 1;
   std::vector<int4> fast, gen, all;
   // general rows are unprefetched: one row per task keeps them parallel
   auto push1 = [](std::vector<int4>& v, int k, int b, int a, int e) {
     for (int j = a; j < e; ++j) v.push_back(make_int4(k, b, j, j + 1));
   };
   for (int k = 0; k < w; ++k) {
-    // general-kernel column blocks (30 wide): layer 0, row 0, and rows of
-    // length <= 2 (columns 0, 1: block 0)
-    for (int b = 0; kGenCols * b < w - k; ++b) {
+    // fast rows: 1 <= k <= n - 2, 1 <= j, and in column block 0 row length >= 3
+    const bool fast_layer = k >= 1 && k <= n - 2;
+    for (int b = 0; kGenCols * b < w - k; ++b) {  // general-kernel blocks (30 wide)
       const int jmax = w - k - kGenCols * b;
       push1(all, k, b, 0, jmax);
-      if (k == 0) {
+      if (!fast_layer) {
         push1(gen, k, b, 0, jmax);
       } else {
         push1(gen, k, b, 0, 1);
         if (b == 0) push1(gen, k, b, std::max(1, w - k - 2), jmax);
       }
     }
-    if (k == 0) continue;
-    // fast column blocks (60 wide): rows 1 .. (block 0: row length >= 3)
-    for (int b = 0; kFastCols * b < w - k; ++b) {
+    if (!fast_layer) continue;
+    for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (62 wide)
       const int jmax = w - k - kFastCols * b;
       const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;
       for (int j0 = 1; j0 < fe; j0 += kMarchRows) fast.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, fe)));
@@ -343,32 +363,29 @@ void init_stencil_tasks(bt_stencil& st) {
   st.d_gtasks.upload(gen);
   st.natasks = (int)all.size();
   st.d_atasks.upload(all);
-  // Fast path preconditions: bitwise-symmetric merged rows, and face rows
-  // that differ from them only on the structural correction directions
-  // (neighbours outside the lattice load as 0 and are exempt).
+  // Fast path preconditions: bitwise-symmetric merged rows, and typed face
+  // rows that vanish off their present directions.
   st.symmetric = true;
   const int nc = st.grid->mesh.n_cells();
   std::vector<StencilCell> cells(nc);
   BT_CUDA(cudaMemcpy(cells.data(), st.d_cells.p, sizeof(StencilCell) * nc, cudaMemcpyDeviceToHost));
-  static const int kOutside[3][4] = {{0, 0, 0, 0}, {1, 2, 3, 7}, {8, 11, 12, 14}};
-  st.fast.assign(22 * (size_t)nc, 0.0);
+  st.fast.assign(30 * (size_t)nc, 0.0);
   for (int c = 0; c < nc; ++c) {
     const auto& rw = st.rows[c];
     for (int d = 1; d <= 7; ++d) st.symmetric = st.symmetric && rw[d] == rw[d + 7];
-    for (int z : {1, 2}) {
-      const int* dirs = z == 1 ? kDiagDirs : kI0Dirs;
-      for (int d = 0; d < 15; ++d) {
-        bool exempt = false;
-        for (int q = 0; q < 7; ++q) exempt = exempt || dirs[q] == d;
-        for (int q = 0; q < 4; ++q) exempt = exempt || kOutside[z][q] == d;
-        if (!exempt && cells[c].w[z][d] != rw[d]) st.symmetric = false;
+    for (int d = 0; d < 15; ++d) {
+      bool pd = false, pi = false;
+      for (int q = 0; q < 11; ++q) {
+        pd = pd || kDiagPresent[q] == d;
+        pi = pi || kI0Present[q] == d;
       }
+      if ((!pd && cells[c].w[1][d] != 0.0) || (!pi && cells[c].w[2][d] != 0.0)) st.symmetric = false;
     }
-    double* f = &st.fast[22 * (size_t)c];
+    double* f = &st.fast[30 * (size_t)c];
     for (int d = 0; d < 8; ++d) f[d] = rw[d];
-    for (int q = 0; q < 7; ++q) {
-      f[8 + q] = cells[c].w[1][kDiagDirs[q]] - rw[kDiagDirs[q]];
-      f[15 + q] = cells[c].w[2][kI0Dirs[q]] - rw[kI0Dirs[q]];
+    for (int q = 0; q < 11; ++q) {
+      f[8 + q] = cells[c].w[1][kDiagPresent[q]];
+      f[19 + q] = cells[c].w[2][kI0Present[q]];
     }
   }
 }
@@ -390,24 +407,25 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     count_launch();
   }
   static FastParams<kMaxCells> fp;
+  const size_t smem = sizeof(double) * kW * kRingD;
+  static bool attr = false;
+  if (!attr) {
+    BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const double* x_end = x + cs * nc;
   for (int c0 = 0; c0 < nc && st.ntasks; c0 += kMaxCells) {
     const int cnt = std::min(kMaxCells, nc - c0);
     for (int c = 0; c < cnt; ++c) {
-      const double* f = &st.fast[22 * (size_t)(c0 + c)];
+      const double* f = &st.fast[30 * (size_t)(c0 + c)];
       for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
-      for (int q = 0; q < 7; ++q) {
-        fp.dd[c][q] = f[8 + q];
-        fp.di[c][q] = f[15 + q];
+      for (int q = 0; q < 11; ++q) {
+        fp.dg[c][q] = f[8 + q];
+        fp.f0[c][q] = f[19 + q];
       }
     }
-    const size_t smem = sizeof(double) * kW * kRingD;
-    static bool attr = false;
-    if (!attr) {
-      BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
     k_stencil_fast<kMaxCells><<<dim3((st.ntasks + kW - 1) / kW, cnt), kT, smem, s>>>(x, y, st.d_tasks.p, st.ntasks,
-                                                                                    w, cs, c0, fp);
+                                                                                    w, cs, c0, x_end, fp);
     count_launch();
   }
   check_launch("k_stencil");
