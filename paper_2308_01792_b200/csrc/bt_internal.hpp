@@ -177,6 +177,10 @@ struct bt_stencil {
   bt::DevBuf<double> d_diag;                 // assembled diagonal
   bt::DevBuf<int4> d_tasks;                  // warp march schedule, fast rows (see bt_stencil.cu)
   int ntasks = 0;
+  std::vector<int> chunk_first;              // first task of each 128-cell chunk in d_tasks (+ end)
+  bt::DevBuf<int4> d_xtasks;                 // per-cell general rows (marches that would stage outside x)
+  bt::DevBuf<int> d_xoff;                    // cell c: d_xtasks[d_xoff[c] .. d_xoff[c + 1])
+  int nxtasks = 0, xtask_max = 0;
   bt::DevBuf<int4> d_gtasks;                 // general rows (layer 0, row 0, corner rows)
   int ngtasks = 0;
   bt::DevBuf<int4> d_atasks;                 // all rows (general-kernel fallback)

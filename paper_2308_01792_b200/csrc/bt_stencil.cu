@@ -2,17 +2,19 @@
 // operators.hpp:247-271), per-cell phase. The interface phase (replica sums
 // and Dirichlet rows) is bt_interface.cu.
 //
-// Data path (k_stencil_fast). A warp owns 62 consecutive output columns i of
-// one layer k of one macro-cell and marches up to kMarchRows rows j. Each
-// step needs three new rows — A(j+1) of layer k, B(j) of layer k+1 and C(j+1)
-// of layer k-1 — over the warp's 64 staged columns [base - 1, base + 63).
-// Lane 0 stages them with TMA bulk copies (cp.async.bulk, 528 B each, 16 B
-// aligned with a per-row shift) into a per-warp kStages-deep shared-memory
-// ring completed on mbarriers, so the copies cost no LSU wavefronts and no
-// registers. Lanes read two contiguous 32-column halves (columns base-1+l and
-// base+31+l) plus their i-1 / i+1 neighbours from the ring; values reused by
-// later rows stay in registers (window sets alternate, no moves). Every x
-// value is read from L2 once per layer that needs it (3x) and from HBM once.
+// Data path (k_stencil_fast). A warp owns 60 consecutive output columns i of
+// one layer k of one macro-cell (lane l: the pair c0 = base - 2 + 2l, c0 + 1)
+// and marches up to kMarchRows rows j. Each step needs three new rows — A(j+1)
+// of layer k, B(j) of layer k+1 and C(j+1) of layer k-1 — over the warp's 64
+// staged columns [base - 2, base + 62). Every lane stages its two columns of
+// each row with 8-byte cp.async into a per-warp kStages-deep shared ring (so a
+// row lands at a fixed place whatever its alignment), then reads its pair
+// with one 16-byte shared load and the i-1 / i+1 neighbours by shuffle.
+// Values reused by later rows stay in registers (window sets alternate). The
+// grid is persistent: warps stride over a task list sorted longest first, and
+// the staging stream runs ahead across task boundaries (two phantom steps per
+// march fill the register window). Every x value is read from L2 once per
+// layer that needs it (3x) and from HBM about once.
 //
 // Rows. The host splits every (layer, column block) march into fast rows and
 // a few general rows. Fast rows (1 <= k <= n-2, j >= 1, row length >= 3 in
@@ -31,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "bt_internal.hpp"
@@ -41,7 +44,7 @@ namespace {
 constexpr int kT = 256;
 constexpr int kW = kT / 32;
 constexpr int kMarchRows = 48;
-constexpr int kFastCols = 62;  // output columns per warp in k_stencil_fast
+constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
 
 // present neighbour directions (kStencilDirs indices) of a diagonal-face
@@ -57,245 +60,232 @@ struct FastParams {
 };
 constexpr int kMaxCells = 128;  // 128 * 30 * 8 B = 30 KB of kernel parameters
 
-// per-warp TMA ring: kStages stages x 3 staged rows of kRowD doubles
-constexpr int kStages = 4;
-constexpr int kRowD = 72;                  // >= 66 doubles (528 B copy), 16 B multiple
+// per-warp staging ring: kStages stages x 3 staged rows of kRowD doubles
+constexpr int kStages = 6;
+constexpr int kRowD = 64;  // staged columns [base - 2, base + 62)
 constexpr int kStageD = 3 * kRowD;
 constexpr int kRingD = kStages * kStageD;  // doubles per warp
-constexpr int kCopyBytes = 528;            // 64 columns + one 16 B alignment chunk
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void tma_row(double* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-struct Row3 {  // one row at a lane's two columns: v = value, l = column - 1, r = column + 1
-  double l0, v0, r0, l1, v1, r1;
+struct Row4 {  // one row at a lane's columns (c0, c1 = c0 + 1): l0 = c0 - 1, r1 = c1 + 1
+  double l0, v0, v1, r1;
 };
 struct Win {  // A(j) of layer k, B(j-1) of layer k+1, C(j) of layer k-1
-  Row3 a, b, c;
+  Row4 a, b, c;
 };
 
+// Task word: x = k, y = column block | (cell - cell0) << 16, z = j0, w = j1.
+//
+// Persistent warps: warp g runs tasks g, g + G, g + 2G, ... (the host sorts
+// tasks by length, longest first). Each march of rows j0..j1-1 is preceded by
+// two phantom steps (j0 - 2, j0 - 1) whose staged rows fill the register
+// window, so the staging stream runs through the ring across task boundaries
+// without draining. Lane l stages columns base - 2 + l and base + 30 + l of
+// each row (two 8-byte cp.async, each warp-contiguous), so every row lands at
+// the same place whatever its alignment and lane l reads its pair (c0, c1)
+// with one 16-byte shared load. The host keeps marches that would stage
+// outside x on the general kernel.
 template <int kMaxC>
 __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
-                                                        int64_t cell_slots, int cell0, const double* x_end,
-                                                        const __grid_constant__ FastParams<kMaxC> fp) {
+                                                        int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
   extern __shared__ __align__(128) double ring_all[];
-  __shared__ __align__(8) uint64_t bars[kW][kStages];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int task = blockIdx.x * kW + warp;
-  if (task >= ntasks) return;
-  const int cell = cell0 + blockIdx.y;
-  const double* W = fp.w[blockIdx.y];
-  const double* DG = fp.dg[blockIdx.y];
-  const double* F0 = fp.f0[blockIdx.y];
-  const int4 tk = tasks[task];
-  const int k = tk.x, blk = tk.y, j0 = tk.z, j1 = tk.w;  // k in [1, n-2], j0 >= 1 by construction
-  const int base = kFastCols * blk;
-  const int c0 = base - 1 + lane, c1 = base + 31 + lane;  // this lane's two columns
-  const bool out0 = lane >= 1, out1 = lane <= 30;
-  const double* __restrict__ xcell = x + (int64_t)cell * cell_slots;
-  double* ring = ring_all + warp * kRingD;
-  uint64_t* bar = bars[warp];
-  const uint64_t end16 = ((uint64_t)x_end + 15) & ~(uint64_t)15;
+  const int G = gridDim.x * kW;
+  const int t0 = blockIdx.x * kW + warp;
+  if (t0 >= ntasks) return;
+  const double* ring = ring_all + warp * kRingD;
+  const uint32_t my_s = smem_u32(ring) + 8u * lane;
 
-  if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncwarp();
-
-  // producer cursors: rows A(j+1), B(j), C(j+1) of step j; offsets of column
-  // base - 1 in each row. len(A(j+1)) = len(B(j)) = r, len(C(j+1)) = r + 1.
-  int r = w - k - j0 - 1;
-  int oA = row_start(w, j0 + 1, k) + base - 1;
-  int oB = row_start(w, j0, k + 1) + base - 1;
-  int oC = row_start(w, j0 + 1, k - 1) + base - 1;
-  auto produce = [&](int stage) {  // lane 0 only
-    double* st = ring + stage * kStageD;
-    const double* srcs[3] = {xcell + oA, xcell + oB, xcell + oC};
-    uint32_t total = 0, bytes[3];
-    uint64_t al[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      al[q] = (uint64_t)srcs[q] & ~(uint64_t)15;
-      const uint64_t lim = end16 - al[q];
-      bytes[q] = lim < (uint64_t)kCopyBytes ? (uint32_t)lim : (uint32_t)kCopyBytes;
-      total += bytes[q];
+  // ---- producer (every lane copies its two columns of each staged row) ----
+  // element offsets (within the cell) of column base - 2 + lane in rows
+  // A(j+1), B(j), C(j+1) of the producer's next step j; r = len(A(j+1)) =
+  // len(B(j)); pleft = steps left in the producer's task
+  int pt = t0, pA = 0, pB = 0, pC = 0, pr = 0, pleft = 0;
+  const double* pcell = x;
+  int4 pnext = tasks[t0];
+  auto p_start = [&]() {
+    const int4 tk = pnext;
+    const int k = tk.x, base = kFastCols * (tk.y & 0xffff), cl = tk.y >> 16;
+    const int j = tk.z - 2, cb = base - 2 + lane;
+    pcell = x + (int64_t)cl * cell_slots;
+    pA = cb + row_start(w, j + 1, k);
+    pB = cb + row_start(w, j, k + 1);
+    pC = cb + row_start(w, j + 1, k - 1);
+    pr = w - k - j - 1;
+    pleft = tk.w - tk.z + 2;
+    if (pt + G < ntasks) pnext = tasks[pt + G];
+  };
+  p_start();
+  int ps = 0;  // producer stage
+  auto produce = [&]() {  // one (possibly empty) group of copies
+    if (pleft > 0) {
+      const uint32_t d = my_s + (uint32_t)(ps * kStageD * 8);
+      const double *a = pcell + pA, *b = pcell + pB, *c = pcell + pC;
+      cp8(d, a);
+      cp8(d + 256, a + 32);
+      cp8(d + kRowD * 8, b);
+      cp8(d + kRowD * 8 + 256, b + 32);
+      cp8(d + 2 * kRowD * 8, c);
+      cp8(d + 2 * kRowD * 8 + 256, c + 32);
+      ps = ps == kStages - 1 ? 0 : ps + 1;
+      pA += pr;
+      pB += pr;
+      pC += pr + 1;
+      --pr;
+      if (--pleft == 0) {
+        pt += G;
+        if (pt < ntasks) p_start();
+      }
     }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_expect_tx(&bar[stage], total);
+    cp_commit();
+  };
+#pragma unroll 1
+  for (int q = 0; q < kStages - 1; ++q) produce();
+
+  // ---- consumer ----
+  int cs = 0;
+  auto consume = [&](Row4& A1, Row4& B0, Row4& C1) {
+    cp_wait<kStages - 2>();
+    __syncwarp();
+    const double2* st = reinterpret_cast<const double2*>(ring + cs * kStageD) + lane;
+    const double2 a = st[0], b = st[kRowD / 2], c = st[kRowD];
+    A1.v0 = a.x;
+    A1.v1 = a.y;
+    B0.v0 = b.x;
+    B0.v1 = b.y;
+    C1.v0 = c.x;
+    C1.v1 = c.y;
+    A1.l0 = __shfl_up_sync(0xffffffffu, a.y, 1);
+    A1.r1 = __shfl_down_sync(0xffffffffu, a.x, 1);
+    B0.l0 = __shfl_up_sync(0xffffffffu, b.y, 1);
+    B0.r1 = __shfl_down_sync(0xffffffffu, b.x, 1);
+    C1.l0 = __shfl_up_sync(0xffffffffu, c.y, 1);
+    C1.r1 = __shfl_down_sync(0xffffffffu, c.x, 1);
+    cs = cs == kStages - 1 ? 0 : cs + 1;
+    // the stage refilled next is the one every lane read in the previous
+    // step (its values went through the warp-synchronous shuffles)
+    produce();
+  };
+
+#pragma unroll 1
+  for (int t = t0; t < ntasks; t += G) {
+    const int4 tk = tasks[t];
+    const int k = tk.x, blk = tk.y & 0xffff, cl = tk.y >> 16, j0 = tk.z, j1 = tk.w;
+    double W[8];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) tma_row(st + q * kRowD, (const void*)al[q], bytes[q], &bar[stage]);
-  };
-  auto advance = [&]() {
-    oA += r;
-    oB += r;
-    oC += r + 1;
-    --r;
-  };
-  // shift (in doubles) of column base - 1 inside a staged row
-  auto shift_of = [&](int o) -> int { return (int)(((uint64_t)(xcell + o) >> 3) & 1); };
-  const int nsteps = j1 - j0;
-  // per-stage shifts of the three rows (3 bits per stage), tracked
-  // identically by every lane
-  uint32_t shbits = 0;
-  auto note_shifts = [&](int stage) {
-    const uint32_t b = (uint32_t)(shift_of(oA) | (shift_of(oB) << 1) | (shift_of(oC) << 2));
-    shbits = (shbits & ~(7u << (3 * stage))) | (b << (3 * stage));
-  };
-#pragma unroll
-  for (int q = 0; q < kStages - 1; ++q) {
-    note_shifts(q);
-    if (q < nsteps && lane == 0) produce(q);
-    advance();
-  }
+    for (int d = 0; d < 8; ++d) W[d] = fp.w[cl][d];
+    const double* DG = fp.dg[cl];
+    const double* F0 = fp.f0[cl];
+    const int base = kFastCols * blk;
+    const int c0 = base - 2 + 2 * lane, c1 = c0 + 1;  // this lane's two columns
+    const bool out = lane >= 1 && lane <= 30;
+    Win X, Y;
+    Row4 Am1, Am1y, junk0, junk1;
+    consume(Am1, junk0, junk1);  // phantom step j0 - 2: A(j0 - 1)
+    consume(X.a, X.b, X.c);      // phantom step j0 - 1: A(j0), B(j0 - 1), C(j0)
 
-  // window at row j0: A(j0), B(j0 - 1), C(j0) and A(j0 - 1), loaded directly
-  auto at = [&](int rs, int len, int c) -> double { return (c >= 0 && c < len) ? __ldg(xcell + rs + c) : 0.0; };
-  auto load_row = [&](int rs, int len) {
-    Row3 q;
-    q.l0 = at(rs, len, c0 - 1);
-    q.v0 = at(rs, len, c0);
-    q.r0 = at(rs, len, c0 + 1);
-    q.l1 = at(rs, len, c1 - 1);
-    q.v1 = at(rs, len, c1);
-    q.r1 = at(rs, len, c1 + 1);
-    return q;
-  };
-  Win X, Y;
-  Row3 Am1, Am1y;
-  X.a = load_row(row_start(w, j0, k), w - k - j0);
-  X.b = load_row(row_start(w, j0 - 1, k + 1), w - k - j0);
-  X.c = load_row(row_start(w, j0, k - 1), w - k - j0 + 1);
-  Am1 = load_row(row_start(w, j0 - 1, k), w - k - j0 + 1);
+    int LY = w - k - j0;  // length of the output row
+    double* __restrict__ py = y + (int64_t)cl * cell_slots + row_start(w, j0, k);
+    const int colend = base + kFastCols;  // LY <= colend: the row ends inside this warp
+    const bool blk0 = blk == 0;
+    int j = j0;
 
-  int LY = w - k - j0;  // length of the output row
-  double* __restrict__ py = y + (int64_t)cell * cell_slots + row_start(w, j0, k);
-  const int colend = base + kFastCols;  // LY <= colend: the row ends inside this warp
-  const bool blk0 = blk == 0;
-  int j = j0, q = 0;
-
-  auto read_row = [&](const double* row, int sh) {
-    Row3 o;
-    const double* p = row + sh + lane;  // column base - 1 + lane
-    o.l0 = p[-1];
-    o.v0 = p[0];
-    o.r0 = p[1];
-    o.l1 = p[31];
-    o.v1 = p[32];
-    o.r1 = p[33];
-    return o;
-  };
-
-  // One step: output row j at columns c0 (s0) and c1 (s1).
-  // cur: A(j), B(j-1), C(j); am1: A(j-1); staged rows A1 = A(j+1), B0 = B(j),
-  // C1 = C(j+1). kStencilDirs pairs (d, d + 7):
-  //   (1,0,0)/(-1,0,0)  A(j) i+1 / i-1         (0,1,0)/(0,-1,0)  A(j+1) / A(j-1)
-  //   (0,0,1)/(0,0,-1)  B(j) / C(j)            (1,-1,0)/(-1,1,0) A(j-1) i+1 / A(j+1) i-1
-  //   (1,0,-1)/(-1,0,1) C(j) i+1 / B(j) i-1    (0,1,-1)/(0,-1,1) C(j+1) / B(j-1)
-  //   (1,-1,1)/(-1,1,-1) B(j-1) i+1 / C(j+1) i-1
-#define BT_INTERIOR(cur, am1, s, v, l, r)                                                                     \
+    // One step: output row j at columns c0 (s0) and c1 (s1).
+    // cur: A(j), B(j-1), C(j); am1: A(j-1); staged rows A1 = A(j+1), B0 = B(j),
+    // C1 = C(j+1). kStencilDirs pairs (d, d + 7):
+    //   (1,0,0)/(-1,0,0)  A(j) i+1 / i-1         (0,1,0)/(0,-1,0)  A(j+1) / A(j-1)
+    //   (0,0,1)/(0,0,-1)  B(j) / C(j)            (1,-1,0)/(-1,1,0) A(j-1) i+1 / A(j+1) i-1
+    //   (1,0,-1)/(-1,0,1) C(j) i+1 / B(j) i-1    (0,1,-1)/(0,-1,1) C(j+1) / B(j-1)
+    //   (1,-1,1)/(-1,1,-1) B(j-1) i+1 / C(j+1) i-1
+    // Column c0 reads fields (v, r, l) = (v0, v1, l0); column c1 (v1, r1, v0).
+  // two independent accumulation chains per column (latency, not order,
+  // bounds the chain: the fast path is within the 1e-12 parity tolerance)
+#define BT_INTERIOR(cur, am1, s, v, r, l)                                                           \
   double s = W[0] * cur.a.v;                                                                        \
-  s = fma(W[1], cur.a.r + cur.a.l, s);                                                              \
+  double s##b = W[1] * (cur.a.r + cur.a.l);                                                         \
   s = fma(W[2], A1.v + am1.v, s);                                                                   \
-  s = fma(W[3], B0.v + cur.c.v, s);                                                                 \
+  s##b = fma(W[3], B0.v + cur.c.v, s##b);                                                           \
   s = fma(W[4], am1.r + A1.l, s);                                                                   \
-  s = fma(W[5], cur.c.r + B0.l, s);                                                                 \
+  s##b = fma(W[5], cur.c.r + B0.l, s##b);                                                           \
   s = fma(W[6], C1.v + cur.b.v, s);                                                                 \
-  s = fma(W[7], cur.b.r + C1.l, s);
-  // typed rows over present neighbours (kDiagPresent / kI0Present order)
-#define BT_DIAG(cur, am1, v, l, r)                                                                            \
+  s##b = fma(W[7], cur.b.r + C1.l, s##b);                                                           \
+  s += s##b;
+    // typed rows over present neighbours (kDiagPresent / kI0Present order)
+#define BT_DIAG(cur, am1, v, r, l)                                                                  \
   (DG[0] * cur.a.v + DG[1] * am1.r + DG[2] * cur.c.r + DG[3] * C1.v + DG[4] * cur.a.l +             \
    DG[5] * am1.v + DG[6] * cur.c.v + DG[7] * A1.l + DG[8] * B0.l + DG[9] * cur.b.v + DG[10] * C1.l)
-#define BT_FACE0(cur, am1, v, l, r)                                                                           \
+#define BT_FACE0(cur, am1, v, r, l)                                                                 \
   (F0[0] * cur.a.v + F0[1] * cur.a.r + F0[2] * A1.v + F0[3] * B0.v + F0[4] * am1.r +                \
    F0[5] * cur.c.r + F0[6] * C1.v + F0[7] * cur.b.r + F0[8] * am1.v + F0[9] * cur.c.v +             \
    F0[10] * cur.b.v)
 #define BT_STEP(cur, nxt, am1, am1n)                                                                \
   {                                                                                                 \
-    const int sg = q % kStages;                                                                     \
-    mbar_wait(&bar[sg], (uint32_t)((q / kStages) & 1));                                             \
-    const double* st = ring + sg * kStageD;                                                         \
-    const uint32_t sb = shbits >> (3 * sg);                                                         \
-    const Row3 A1 = read_row(st, sb & 1);                                                           \
-    const Row3 B0 = read_row(st + kRowD, (sb >> 1) & 1);                                            \
-    const Row3 C1 = read_row(st + 2 * kRowD, (sb >> 2) & 1);                                        \
-    __syncwarp();                                                                                   \
-    {                                                                                               \
-      const int ps = (q + kStages - 1) % kStages;                                                   \
-      note_shifts(ps);                                                                              \
-      if (q + kStages - 1 < nsteps && lane == 0) produce(ps);                                       \
-      advance();                                                                                    \
-    }                                                                                               \
-    BT_INTERIOR(cur, am1, s0, v0, l0, r0)                                                                     \
-    BT_INTERIOR(cur, am1, s1, v1, l1, r1)                                                                     \
+    Row4 A1, B0, C1;                                                                                \
+    consume(A1, B0, C1);                                                                            \
+    BT_INTERIOR(cur, am1, s0, v0, v1, l0)                                                           \
+    BT_INTERIOR(cur, am1, s1, v1, r1, v0)                                                           \
     if (LY <= colend) { /* the diagonal-face vertex is in this warp */                              \
-      if (c0 == LY - 1) s0 = BT_DIAG(cur, am1, v0, l0, r0);                                                   \
-      if (c1 == LY - 1) s1 = BT_DIAG(cur, am1, v1, l1, r1);                                                   \
+      if (c0 == LY - 1) s0 = BT_DIAG(cur, am1, v0, v1, l0);                                         \
+      if (c1 == LY - 1) s1 = BT_DIAG(cur, am1, v1, r1, v0);                                         \
     }                                                                                               \
-    if (blk0 && c0 == 0) s0 = BT_FACE0(cur, am1, v0, l0, r0); /* lane 1 of block 0 */                         \
-    if (out0 && c0 < LY) py[c0] = s0;                                                               \
-    if (out1 && c1 < LY) py[c1] = s1;                                                               \
+    if (blk0 && c0 == 0) s0 = BT_FACE0(cur, am1, v0, v1, l0); /* lane 1 of block 0 */               \
+    if (out && c0 < LY) py[c0] = s0;                                                                \
+    if (out && c1 < LY) py[c1] = s1;                                                                \
     py += LY;                                                                                       \
     --LY;                                                                                           \
     ++j;                                                                                            \
-    ++q;                                                                                            \
     am1n = cur.a;                                                                                   \
     nxt.a = A1;                                                                                     \
     nxt.b = B0;                                                                                     \
     nxt.c = C1;                                                                                     \
   }
-  while (true) {
-    BT_STEP(X, Y, Am1, Am1y)
-    if (j >= j1) break;
-    BT_STEP(Y, X, Am1y, Am1)
-    if (j >= j1) break;
-  }
+    while (true) {
+      BT_STEP(X, Y, Am1, Am1y)
+      if (j >= j1) break;
+      BT_STEP(Y, X, Am1y, Am1)
+      if (j >= j1) break;
+    }
 #undef BT_STEP
 #undef BT_FACE0
 #undef BT_DIAG
 #undef BT_INTERIOR
+  }
+  cp_wait<0>();
 }
 
 // Any rows of the march schedule, every row read from the zero-set-typed
 // table in shared memory (interior vertices use type 0 = the merged row).
+// With per_cell (nullable) the tasks of cell c are tasks[per_cell[c] ..
+// per_cell[c + 1]); otherwise every cell runs all ntasks tasks.
 __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict__ x, double* __restrict__ y,
                                                         const StencilCell* __restrict__ cells,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
-                                                        int64_t cell_slots) {
+                                                        int64_t cell_slots, const int* __restrict__ per_cell) {
   __shared__ double sw[16][15];
   const int cell = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int task = blockIdx.x * kW + warp;
+  if (per_cell) {
+    const int first = per_cell[cell], last = per_cell[cell + 1];
+    if (first + (int)blockIdx.x * kW >= last) return;  // whole block idle
+    task += first;
+    ntasks = last;
+  }
   {
     const double* src = cells[cell].w[0];
     for (int q = threadIdx.x; q < 16 * 15; q += blockDim.x) sw[q / 15][q % 15] = src[q];
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int task = blockIdx.x * kW + warp;
   if (task >= ntasks) return;
   const int4 tk = tasks[task];
   const int k = tk.x, j0 = tk.z, j1 = tk.w, n = w - 1;
@@ -351,14 +341,52 @@ void init_stencil_tasks(bt_stencil& st) {
       }
     }
     if (!fast_layer) continue;
-    for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (62 wide)
+    for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (60 wide)
       const int jmax = w - k - kFastCols * b;
       const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;
       for (int j0 = 1; j0 < fe; j0 += kMarchRows) fast.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, fe)));
     }
   }
-  st.ntasks = (int)fast.size();
-  st.d_tasks.upload(fast);
+  // Fast tasks of every cell, in chunks of kMaxCells cells (the kernel's
+  // parameter table); longest marches first. A march whose staged columns
+  // would leave x (cell 0's first rows, the last cell's top layers) runs on
+  // the general kernel instead, as single-row tasks of that cell.
+  std::stable_sort(fast.begin(), fast.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
+  const int nc_all = st.grid->mesh.n_cells();
+  const int64_t cs = n_tet(w), total = cs * nc_all;
+  std::vector<int4> all_fast;
+  std::vector<std::vector<int4>> extra(nc_all);
+  st.chunk_first.clear();
+  for (int c0 = 0; c0 < nc_all; c0 += kMaxCells) {
+    st.chunk_first.push_back((int)all_fast.size());
+    const int cnt = std::min(kMaxCells, nc_all - c0);
+    for (const int4& t : fast)
+      for (int c = 0; c < cnt; ++c) {
+        const int64_t cb = (int64_t)(c0 + c) * cs + kFastCols * t.y;
+        const int64_t lo = cb + row_start(w, t.z - 1, t.x - 1) - 2;  // C(j0 - 1), column base - 2
+        const int64_t hi = cb + row_start(w, t.w - 1, t.x + 1) + 61;  // B(j1 - 1), column base + 61
+        if (lo >= 0 && hi < total) {
+          all_fast.push_back(make_int4(t.x, t.y | (c << 16), t.z, t.w));
+        } else {
+          for (int gb = 2 * t.y; gb < 2 * t.y + 2; ++gb)
+            for (int j = t.z; j < t.w && kGenCols * gb < w - t.x - j; ++j) extra[c0 + c].push_back(make_int4(t.x, gb, j, j + 1));
+        }
+      }
+  }
+  st.chunk_first.push_back((int)all_fast.size());
+  st.ntasks = (int)all_fast.size();
+  st.d_tasks.upload(all_fast);
+  std::vector<int4> ex;
+  std::vector<int> exoff(1, 0);
+  for (auto& e : extra) {
+    ex.insert(ex.end(), e.begin(), e.end());
+    exoff.push_back((int)ex.size());
+  }
+  st.nxtasks = (int)ex.size();
+  st.xtask_max = 0;
+  for (auto& e : extra) st.xtask_max = std::max(st.xtask_max, (int)e.size());
+  st.d_xtasks.upload(ex);
+  st.d_xoff.upload(exoff);
   st.ngtasks = (int)gen.size();
   st.d_gtasks.upload(gen);
   st.natasks = (int)all.size();
@@ -396,26 +424,36 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
   const int64_t cs = n_tet(w);
   if (!st.symmetric) {
     k_stencil_general<<<dim3((st.natasks + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
-                                                                          st.natasks, w, cs);
+                                                                          st.natasks, w, cs, nullptr);
     count_launch();
     check_launch("k_stencil_general");
     return;
   }
   if (st.ngtasks) {
     k_stencil_general<<<dim3((st.ngtasks + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_gtasks.p,
-                                                                          st.ngtasks, w, cs);
+                                                                          st.ngtasks, w, cs, nullptr);
+    count_launch();
+  }
+  if (st.nxtasks) {
+    k_stencil_general<<<dim3((st.xtask_max + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_xtasks.p,
+                                                                            st.nxtasks, w, cs, st.d_xoff.p);
     count_launch();
   }
   static FastParams<kMaxCells> fp;
   const size_t smem = sizeof(double) * kW * kRingD;
-  static bool attr = false;
-  if (!attr) {
+  static int grid = 0;
+  if (!grid) {
     BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    int dev = 0, sms = 0, per_sm = 0;
+    BT_CUDA(cudaGetDevice(&dev));
+    BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kT, smem));
+    grid = sms * std::max(1, per_sm);
   }
-  const double* x_end = x + cs * nc;
-  for (int c0 = 0; c0 < nc && st.ntasks; c0 += kMaxCells) {
-    const int cnt = std::min(kMaxCells, nc - c0);
+  for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
+    const int c0 = ch * kMaxCells, cnt = std::min(kMaxCells, nc - c0);
+    const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
+    if (!nt) continue;
     for (int c = 0; c < cnt; ++c) {
       const double* f = &st.fast[30 * (size_t)(c0 + c)];
       for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
@@ -424,8 +462,9 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
         fp.f0[c][q] = f[19 + q];
       }
     }
-    k_stencil_fast<kMaxCells><<<dim3((st.ntasks + kW - 1) / kW, cnt), kT, smem, s>>>(x, y, st.d_tasks.p, st.ntasks,
-                                                                                    w, cs, c0, x_end, fp);
+    const int64_t e0 = (int64_t)c0 * cs;
+    const int blocks = std::min(grid, (nt + kW - 1) / kW);
+    k_stencil_fast<kMaxCells><<<blocks, kT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
     count_launch();
   }
   check_launch("k_stencil");
