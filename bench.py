@@ -10,11 +10,13 @@ the 126 MB L2, so no explicit flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank runs the same per-GPU workload (weak
-scaling, replicas of config 2: its 6 macro-cells do not shard over 8 GPUs);
-times are max over ranks. `--impl reference` times the reference CPU
-implementation (oracle/_ref, the unmodified blocktet headers) on the host
-cores instead.
+Under torchrun (N > 1) the macro-cells are partitioned over the ranks
+(weak scaling: an N x 1 x 1 box of unit cubes, 6 Kuhn macro-tets = one
+config-2-sized block per GPU, level 8). Each step is the per-cell rows
+kernel on the rank's cells plus the interface exchange of the groups that
+span ranks (pack, NCCL allreduce, member-order finish); times are max over
+ranks. `--impl reference` times the reference CPU implementation
+(oracle/_ref, the unmodified blocktet headers) on the host cores instead.
 """
 from __future__ import annotations
 
@@ -181,13 +183,23 @@ def run_ours(args):
     from paper_2308_01792_b200 import _lib
 
     dev = torch.cuda.current_device()
-    grid = bt.Grid(bt.cube_kuhn_text(), LEVEL, LEVEL, device=dev)
+    if ws > 1:
+        text = bt.box_mesh_text(ws, 1, 1)
+        workload = (f"{ws}x1x1 unit cubes x 6 Kuhn macro-tets ({6 * ws} cells, 6 per GPU) L8, P1 const-coeff "
+                    "15-point stencil apply + interface sync (cells partitioned over ranks)")
+    else:
+        text, workload = bt.cube_kuhn_text(), WORKLOAD
+    grid = bt.Grid(text, LEVEL, LEVEL, device=dev)
+    if ws > 1:
+        grid.set_partition(rank, ws)
     table = bt.compute_stencil(bt.FormId.diffusion(), grid, LEVEL)
     x = bt.allocate(bt.p1_space(), grid)
     y = bt.allocate(bt.p1_space(), grid)
     bt.random_fill(x, LEVEL, 0)
-    owned = bt.owned_dof_count(x, LEVEL)
-    slots = grid.space_size(0, LEVEL)
+    owned = bt.owned_dof_count(x, LEVEL)  # whole job
+    cs = bt.n_tet((1 << LEVEL) + 1)
+    _, _, c_begin, c_end = grid.partition()
+    slots = (c_end - c_begin) * cs  # this rank's slots
     L = _lib.lib
     stream = torch.cuda.current_stream()
     sp = bt.api._stream()
@@ -199,7 +211,10 @@ def run_ours(args):
         bt.api._check(L.bt_apply_stencil_cells(table.handle, xp, yp, sp))
         if ev is not None:
             ev[1].record(stream)
-        bt.api._check(L.bt_apply_stencil_interface(table.handle, xp, yp, 0, sp))
+        if ws > 1:
+            bt.api._exchange(y, LEVEL, 0)
+        else:
+            bt.api._check(L.bt_apply_stencil_interface(table.handle, xp, yp, 0, sp))
 
     for _ in range(args.warmup):
         step()
@@ -228,32 +243,34 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_step = total_ms / K
-    value = ws * owned * K / (total_ms * 1e-3) / 1e9
+    value = owned * K / (total_ms * 1e-3) / 1e9
     kmean = float(np.mean(kern_ms))
     peak, peak_kind = measured_peaks()
     alg_bytes = 16.0 * slots  # read x once, write y once
     achieved = alg_bytes / (kmean * 1e-3) / 1e9
 
     # e2e through the public API: pinned host x -> device, apply, device y -> pinned host
+    # (per rank: its own cells' slices; the per-cell rows read x of the rank's cells only)
+    lo, hi = c_begin * cs, c_end * cs
     hx = torch.empty(slots, dtype=torch.float64, pin_memory=True)
-    hx.copy_(x.values[LEVEL].cpu())
+    hx.copy_(x.values[LEVEL][lo:hi].cpu())
     hy = torch.empty(slots, dtype=torch.float64, pin_memory=True)
     xin = bt.allocate(bt.p1_space(), grid)
     yout = bt.allocate(bt.p1_space(), grid)
     e2e_steps = max(3, min(20, K))
     for _ in range(2):
-        xin.values[LEVEL].copy_(hx, non_blocking=True)
+        xin.values[LEVEL][lo:hi].copy_(hx, non_blocking=True)
         bt.apply_stencil(table, xin, yout, LEVEL)
-        hy.copy_(yout.values[LEVEL], non_blocking=True)
+        hy.copy_(yout.values[LEVEL][lo:hi], non_blocking=True)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        xin.values[LEVEL].copy_(hx, non_blocking=True)
+        xin.values[LEVEL][lo:hi].copy_(hx, non_blocking=True)
         bt.apply_stencil(table, xin, yout, LEVEL)
-        hy.copy_(yout.values[LEVEL], non_blocking=True)
+        hy.copy_(yout.values[LEVEL][lo:hi], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -261,8 +278,8 @@ def run_ours(args):
         t = torch.tensor([e2e_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    assert np.array_equal(hy.numpy(), y.values[LEVEL].cpu().numpy()), "e2e result differs from resident run"
-    e2e_value = ws * owned * e2e_steps / (e2e_ms * 1e-3) / 1e9
+    assert np.array_equal(hy.numpy(), y.values[LEVEL][lo:hi].cpu().numpy()), "e2e result differs from resident run"
+    e2e_value = owned * e2e_steps / (e2e_ms * 1e-3) / 1e9
 
     if rank == 0:
         cpu = cpu_baseline_sample() if ws == 1 and not args.no_cpu else None
@@ -270,9 +287,11 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (random_fill seed 0, reference mt19937_64 stream)",
-            "config": {"workload": WORKLOAD, "level": LEVEL, "cells": 6, "slots": slots, "owned_dofs": owned,
-                       "bc": "none", "l2": "inputs larger than L2 (x+y = %.0f MB)" % (alg_bytes / 1e6),
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "config": {"workload": workload, "level": LEVEL, "cells": grid.n_cells(), "slots_per_gpu": slots,
+                       "owned_dofs": owned, "bc": "none",
+                       "l2": "inputs larger than L2 (x+y = %.0f MB per GPU)" % (alg_bytes / 1e6),
+                       "parallelism": f"cells partitioned over {ws} ranks (NCCL interface exchange)"
+                       if ws > 1 else "1 GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "k_stencil",
                          "kernel_ms": kmean, "kernel_share": kmean / ms_step,

@@ -111,6 +111,9 @@ bt_status bt_grid_groups(const bt_grid* g, int level, int space, int64_t* n_grou
  * interior vertices perturbed by U(-perturb h, perturb h) per component from
  * mt19937_64(seed). Writes at most buflen bytes; returns bytes needed. */
 int64_t bt_cubes_mesh_text(int n, double perturb, uint64_t seed, char* buf, int64_t buflen);
+/* nx x ny x nz unit cubes (side 1) x 6 Kuhn tets, same perturbation rule:
+ * the weak-scaling workload of bench.py (6 cells per GPU at N = nx ny nz) */
+int64_t bt_box_mesh_text(int nx, int ny, int nz, double perturb, uint64_t seed, char* buf, int64_t buflen);
 
 /* ---- vectors (fe_function.hpp:324-497, solvers.hpp:53-72) ---------------- */
 /* random_fill (fe_function.hpp:479): mt19937_64 on the host in canonical
@@ -200,6 +203,38 @@ bt_status bt_cg(bt_hierarchy* h, int level, double tol, int maxit, const double*
 bt_status bt_v_cycle(bt_hierarchy* h, int level, const double* rhs, double* x,
                      const bt_smoother_config* sm, const bt_multigrid_config* mg,
                      void* stream);                                     /* :509 */
+
+/* ---- multi-GPU: cell partition --------------------------
+ * One process per GPU, each with its own bt_grid. bt_grid_set_partition
+ * restricts a handle's compute to the contiguous cell block
+ * [rank*nc/nranks, (rank+1)*nc/nranks). Vectors keep the full-size layout;
+ * applies write only this rank's cells. Set the partition before
+ * bt_stencil_create. Interface groups with members on several ranks go
+ * through an exchange buffer of bt_xchg_size doubles:
+ *   bt_apply_stencil_cells(s, x, y)     per-cell rows of this rank's cells
+ *   bt_xchg_pack(g, l, y, buf)          this rank's replica values, zeros elsewhere
+ *   allreduce(buf, sum) over ranks      caller's collective (NCCL / gloo)
+ *   bt_xchg_finish(g, l, mode, y, x, buf)  local groups + member-order sums
+ * mode: 0 sync_additive, 1 sync with Dirichlet identity rows (src = x),
+ * 2 sync_broadcast, 3 impose_dirichlet, 4 zero_dirichlet. Replica sums run
+ * in ascending cell order, so results are bitwise independent of nranks.
+ * Entry points that need a full sync (bt_apply_stencil, bt_sync_*, bt_dot,
+ * elementwise, transfers, hierarchies, N1E1) return BT_LOGIC_ERROR on a
+ * partitioned grid. */
+bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks);
+bt_status bt_grid_partition(const bt_grid* g, int* rank, int* nranks, int* cell_begin, int* cell_end);
+int64_t bt_xchg_size(const bt_grid* g, int level); /* -1 on error */
+bt_status bt_xchg_pack(const bt_grid* g, int level, const double* x, double* buf, void* stream);
+bt_status bt_xchg_finish(const bt_grid* g, int level, int mode, double* x, const double* src, const double* buf,
+                         void* stream);
+/* owned-DoF dot partials per cell (host array of bt_num_cells doubles; cells
+ * of other ranks are 0): sum them in cell order after an allreduce */
+bt_status bt_dot_cells(const bt_grid* g, int space, int level, const double* x, const double* y, double* per_cell,
+                       void* stream);
+/* host-only exchange plan (no CUDA needed): entries of `rank`; NULL arrays
+ * query the count. Returns the entry count, -1 on error. */
+int64_t bt_xchg_plan_host(const char* mesh_text, int level, int rank, int nranks, int64_t* buf_size,
+                          int64_t* slot, int32_t* buf, int32_t* base, int32_t* count, uint8_t* dir);
 
 /* ---- N1E1 curl-curl + mass (no reference implementation) ----- */
 bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta, bt_n1e1** out);

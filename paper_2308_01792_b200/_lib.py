@@ -60,6 +60,7 @@ SIGNATURES = {
     "bt_grid_masks": (I, [P, I, I, I, PU8, PU8]),
     "bt_grid_groups": (I, [P, I, I, PI64, PI64, PI64, PI32, PI32, PI64]),
     "bt_cubes_mesh_text": (I64, [I, D, C.c_uint64, C.c_char_p, I64]),
+    "bt_box_mesh_text": (I64, [I, I, I, D, C.c_uint64, C.c_char_p, I64]),
     "bt_random_fill": (I, [P, I, I, C.c_uint64, P, P]),
     "bt_assign": (I, [P, I, I, P, D, P]),
     "bt_scale": (I, [P, I, I, P, D, P]),
@@ -94,6 +95,13 @@ SIGNATURES = {
     "bt_n1e1_destroy": (None, [P]),
     "bt_apply_n1e1": (I, [P, P, P, I, P]),
     "bt_n1e1_sync": (I, [P, I, P, P]),
+    "bt_grid_set_partition": (I, [P, I, I]),
+    "bt_grid_partition": (I, [P, PI, PI, PI, PI]),
+    "bt_xchg_size": (I64, [P, I]),
+    "bt_xchg_pack": (I, [P, I, P, P, P]),
+    "bt_xchg_finish": (I, [P, I, I, P, P, P, P]),
+    "bt_dot_cells": (I, [P, I, I, P, P, PD, P]),
+    "bt_xchg_plan_host": (I64, [C.c_char_p, I, I, I, PI64, PI64, PI32, PI32, PI32, PU8]),
 }
 
 

@@ -202,6 +202,47 @@ class Grid:
     def space_size(self, space: int, level: int) -> int:
         return _L.bt_space_size(self._h, space, level)
 
+    # ---- multi-GPU cell partition ---------------------------
+    def set_partition(self, rank: int, nranks: int, allreduce=None):
+        """Restrict this handle's compute to the cell block of `rank` out of
+        `nranks` (bt_grid_set_partition). `allreduce(tensor)` sums a device
+        tensor over the ranks in place; default torch.distributed.all_reduce.
+        Call before compute_stencil."""
+        _check(_L.bt_grid_set_partition(self._h, rank, nranks))
+        self._allreduce = allreduce
+        self._xbufs = {}
+
+    def partition(self):
+        """(rank, nranks, cell_begin, cell_end)"""
+        r, n, b, e = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(_L.bt_grid_partition(self._h, C.byref(r), C.byref(n), C.byref(b), C.byref(e)))
+        return r.value, n.value, b.value, e.value
+
+    def partitioned(self) -> bool:
+        return self.partition()[1] > 1
+
+    def allreduce(self, t: torch.Tensor):
+        fn = getattr(self, "_allreduce", None)
+        if fn is not None:
+            fn(t)
+        else:
+            import torch.distributed as dist
+            dist.all_reduce(t)
+
+    def xchg_buffer(self, l) -> Optional[torch.Tensor]:
+        n = _L.bt_xchg_size(self._h, l)
+        if n < 0:
+            _check(4)  # BT_LOGIC_ERROR, message from bt_last_error
+        if n == 0:
+            return None
+        bufs = getattr(self, "_xbufs", None)
+        if bufs is None:
+            bufs = self._xbufs = {}
+        b = bufs.get(l)
+        if b is None or b.numel() != n:
+            b = bufs[l] = torch.zeros(n, dtype=torch.float64, device=f"cuda:{self.device}")
+        return b
+
     def masks(self, level, cell, g):
         n = n_tet(width_formula(g, level))
         o = np.zeros(n, np.uint8)
@@ -227,6 +268,16 @@ def cubes_mesh_text(n: int, perturb: float = 0.1, seed: int = 0) -> str:
     need = _L.bt_cubes_mesh_text(n, perturb, seed, None, 0)
     buf = C.create_string_buffer(need + 1)
     _L.bt_cubes_mesh_text(n, perturb, seed, buf, need + 1)
+    return buf.value.decode()
+
+
+def box_mesh_text(nx: int, ny: int, nz: int, perturb: float = 0.0, seed: int = 0) -> str:
+    """nx x ny x nz unit cubes x 6 Kuhn tets (bt_box_mesh_text)."""
+    need = _L.bt_box_mesh_text(nx, ny, nz, perturb, seed, None, 0)
+    if need < 0:
+        raise InvalidArgument("box_mesh_text: dimensions must be >= 1")
+    buf = C.create_string_buffer(need + 1)
+    _L.bt_box_mesh_text(nx, ny, nz, perturb, seed, buf, need + 1)
     return buf.value.decode()
 
 
@@ -332,8 +383,76 @@ def axpy(y: FEFunction, a, x: FEFunction, l):
                       _stream()))
 
 
+def xchg_plan_host(mesh_text: str, level: int, rank: int, nranks: int) -> dict:
+    """The exchange plan of one rank, built on the host without CUDA
+    (bt_xchg_plan_host): entry arrays slot / buf / base / count / dir and the
+    buffer size. For tests of the partition logic on CPU."""
+    bs = C.c_int64()
+    n = _L.bt_xchg_plan_host(mesh_text.encode(), level, rank, nranks, C.byref(bs), None, None, None, None, None)
+    if n < 0:
+        raise InvalidArgument(_L.bt_last_error().decode())
+    slot = np.zeros(n, np.int64)
+    buf = np.zeros(n, np.int32)
+    base = np.zeros(n, np.int32)
+    count = np.zeros(n, np.int32)
+    d = np.zeros(n, np.uint8)
+    _L.bt_xchg_plan_host(mesh_text.encode(), level, rank, nranks, C.byref(bs), slot.ctypes.data_as(_lib.PI64),
+                         buf.ctypes.data_as(_lib.PI32), base.ctypes.data_as(_lib.PI32),
+                         count.ctypes.data_as(_lib.PI32), d.ctypes.data_as(_lib.PU8))
+    return {"buf_size": bs.value, "slot": slot, "buf": buf, "base": base, "count": count, "dir": d}
+
+
+def partition_range(n_cells: int, rank: int, nranks: int):
+    """Cells [begin, end) of `rank` (bt_grid_set_partition's block partition)."""
+    return n_cells * rank // nranks, n_cells * (rank + 1) // nranks
+
+
+def xchg_pack(fn: FEFunction, l, buf: Optional[torch.Tensor]):
+    """Multi-GPU protocol step 1: this rank's replica values of rank-spanning
+    interface groups into buf (zeros elsewhere)."""
+    fn.check_level(l)
+    if buf is not None:
+        _check(_L.bt_xchg_pack(fn.grid.handle, l, _ptr(fn.values[l]), _ptr(buf), _stream()))
+
+
+def xchg_finish(fn: FEFunction, l, mode: int, buf: Optional[torch.Tensor], src: Optional[FEFunction] = None):
+    """Multi-GPU protocol step 3 (after the caller's allreduce of buf): local
+    groups plus member-order reduction of the rank-spanning ones. mode: 0
+    sync_additive, 1 sync with Dirichlet identity rows from src, 2
+    sync_broadcast, 3 impose_dirichlet (src), 4 zero_dirichlet."""
+    fn.check_level(l)
+    _check(_L.bt_xchg_finish(fn.grid.handle, l, int(mode), _ptr(fn.values[l]),
+                             _ptr(src.values[l]) if src is not None else None,
+                             _ptr(buf) if buf is not None else None, _stream()))
+
+
+def _exchange(fn: FEFunction, l, mode: int, src: Optional[FEFunction] = None):
+    g = fn.grid
+    buf = g.xchg_buffer(l)
+    if buf is not None and mode in (0, 1, 2):
+        xchg_pack(fn, l, buf)
+        g.allreduce(buf)
+    xchg_finish(fn, l, mode, buf, src)
+
+
+def dot_cells(x: FEFunction, y: FEFunction, l) -> np.ndarray:
+    """Owned-DoF dot partial of every cell (0 for other ranks' cells)."""
+    _compatible(x, y, l)
+    out = np.zeros(x.grid.n_cells())
+    _check(_L.bt_dot_cells(x.grid.handle, x.descriptor.space, l, _ptr(x.values[l]), _ptr(y.values[l]),
+                           out.ctypes.data_as(_lib.PD), _stream()))
+    return out
+
+
 def dot(x: FEFunction, y: FEFunction, l) -> float:
     _compatible(x, y, l)
+    if x.grid.partitioned():
+        per = torch.from_numpy(dot_cells(x, y, l)).to(f"cuda:{x.grid.device}")
+        x.grid.allreduce(per)
+        s = 0.0
+        for v in per.cpu().tolist():  # cells in order, as on one GPU
+            s += v
+        return s
     out = C.c_double()
     _check(_L.bt_dot(x.grid.handle, x.descriptor.space, l, _ptr(x.values[l]), _ptr(y.values[l]), C.byref(out),
                      _stream()))
@@ -346,6 +465,9 @@ def norm2(x: FEFunction, l) -> float:
 
 def sync_additive(fn: FEFunction, l):
     fn.check_level(l)
+    if fn.grid.partitioned() and fn.descriptor.space == 0:
+        _exchange(fn, l, 0)
+        return
     if fn.descriptor.space == 2:
         _check(_L.bt_n1e1_sync(fn.grid.handle, l, _ptr(fn.values[l]), _stream()))
         return
@@ -354,6 +476,9 @@ def sync_additive(fn: FEFunction, l):
 
 def sync_broadcast(fn: FEFunction, l):
     fn.check_level(l)
+    if fn.grid.partitioned() and fn.descriptor.space == 0:
+        _exchange(fn, l, 2)
+        return
     _check(_L.bt_sync_broadcast(fn.grid.handle, fn.descriptor.space, l, _ptr(fn.values[l]), _stream()))
 
 
@@ -512,6 +637,10 @@ def apply_stencil(table: StencilTable, src: FEFunction, dst: FEFunction, l, bc=B
     _require_pair(src, dst, l)
     if table.level != l or table.grid is not src.grid:
         raise InvalidArgument("apply_stencil: table/grid mismatch")
+    if src.grid.partitioned():  # this rank's cells, then the interface exchange
+        _check(_L.bt_apply_stencil_cells(table.handle, _ptr(src.values[l]), _ptr(dst.values[l]), _stream()))
+        _exchange(dst, l, 1 if int(bc) else 0, src)
+        return
     _check(_L.bt_apply_stencil(table.handle, _ptr(src.values[l]), _ptr(dst.values[l]), int(bc), _stream()))
 
 

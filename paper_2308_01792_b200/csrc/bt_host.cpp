@@ -166,7 +166,7 @@ static int edge_of(const Mesh& m, std::array<int, 2> e) {
   return (int)(it - m.edges.begin());
 }
 
-static void build_topology(const Mesh& m, Topology& t) {
+void build_topology(const Mesh& m, Topology& t) {
   const int nc = m.n_cells(), nv = (int)m.coords.size();
   const int ne = (int)m.edges.size(), nf = (int)m.faces.size();
   t.edge_cells.assign(ne, {});
@@ -461,40 +461,43 @@ void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<E
 // ---------------------------------------------------------------------------
 // Builder mesh generator, shared with oracle/bt_oracle.c
 // ---------------------------------------------------------------------------
-std::string cubes_mesh_text(int n, double perturb, uint64_t seed) {
-  const int nv1 = n + 1, nverts = nv1 * nv1 * nv1;
-  const double h = 1.0 / n;
+// nx x ny x nz cubes of side h, each split into 6 Kuhn tets (positive
+// orientation); vertices not on the box boundary perturbed per component by
+// U(-perturb h, perturb h) from mt19937_64(seed) in vertex order.
+static std::string box_text(int nx, int ny, int nz, double h, double perturb, uint64_t seed, const char* header) {
+  const int vx = nx + 1, vy = ny + 1, vz = nz + 1, nverts = vx * vy * vz;
+  const int dims[3] = {nx, ny, nz};
   std::vector<double> xyz(3 * (size_t)nverts);
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> dist(-perturb * h, perturb * h);
-  for (int c = 0; c <= n; ++c)
-    for (int b = 0; b <= n; ++b)
-      for (int a = 0; a <= n; ++a) {
-        const int id = a + nv1 * (b + nv1 * c);
+  for (int c = 0; c <= nz; ++c)
+    for (int b = 0; b <= ny; ++b)
+      for (int a = 0; a <= nx; ++a) {
+        const int id = a + vx * (b + vy * c);
         const int idx[3] = {a, b, c};
         for (int d = 0; d < 3; ++d) {
           const double off = dist(rng);
-          const bool on_bdry = idx[d] == 0 || idx[d] == n;
+          const bool on_bdry = idx[d] == 0 || idx[d] == dims[d];
           xyz[3 * id + d] = idx[d] * h + (perturb > 0 && !on_bdry ? off : 0.0);
         }
       }
   static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-  std::string out;
+  std::string out = header;
   char tmp[256];
-  snprintf(tmp, sizeof tmp, "# %d^3 unit cubes x 6 Kuhn tets, perturb %.17g, seed %llu\n", n, perturb,
-           (unsigned long long)seed);
-  out += tmp;
   snprintf(tmp, sizeof tmp, "vertices %d\n", nverts);
   out += tmp;
   for (int i = 0; i < nverts; ++i) {
     snprintf(tmp, sizeof tmp, "%.17g %.17g %.17g\n", xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
     out += tmp;
   }
-  snprintf(tmp, sizeof tmp, "cells %d\n", 6 * n * n * n);
+  snprintf(tmp, sizeof tmp, "cells %d\n", 6 * nx * ny * nz);
   out += tmp;
-  for (int c = 0; c < n; ++c)
-    for (int b = 0; b < n; ++b)
-      for (int a = 0; a < n; ++a)
+  auto vid = [&](int a, int b, int c, int bits) {
+    return (a + (bits & 1)) + vx * ((b + ((bits >> 1) & 1)) + vy * (c + ((bits >> 2) & 1)));
+  };
+  for (int c = 0; c < nz; ++c)
+    for (int b = 0; b < ny; ++b)
+      for (int a = 0; a < nx; ++a)
         for (const auto& pm : perms) {
           int loc[4] = {0, 0, 0, 7};
           loc[1] = 1 << pm[0];
@@ -511,14 +514,25 @@ std::string cubes_mesh_text(int n, double perturb, uint64_t seed) {
           const double vol = u[0] * (w[1] * z[2] - w[2] * z[1]) + u[1] * (w[2] * z[0] - w[0] * z[2]) +
                              u[2] * (w[0] * z[1] - w[1] * z[0]);
           if (vol < 0) std::swap(loc[2], loc[3]);
-          snprintf(tmp, sizeof tmp, "%d %d %d %d\n",
-                   (a + (loc[0] & 1)) + nv1 * ((b + ((loc[0] >> 1) & 1)) + nv1 * (c + ((loc[0] >> 2) & 1))),
-                   (a + (loc[1] & 1)) + nv1 * ((b + ((loc[1] >> 1) & 1)) + nv1 * (c + ((loc[1] >> 2) & 1))),
-                   (a + (loc[2] & 1)) + nv1 * ((b + ((loc[2] >> 1) & 1)) + nv1 * (c + ((loc[2] >> 2) & 1))),
-                   (a + (loc[3] & 1)) + nv1 * ((b + ((loc[3] >> 1) & 1)) + nv1 * (c + ((loc[3] >> 2) & 1))));
+          snprintf(tmp, sizeof tmp, "%d %d %d %d\n", vid(a, b, c, loc[0]), vid(a, b, c, loc[1]), vid(a, b, c, loc[2]),
+                   vid(a, b, c, loc[3]));
           out += tmp;
         }
   return out;
+}
+
+std::string cubes_mesh_text(int n, double perturb, uint64_t seed) {
+  char header[256];
+  snprintf(header, sizeof header, "# %d^3 unit cubes x 6 Kuhn tets, perturb %.17g, seed %llu\n", n, perturb,
+           (unsigned long long)seed);
+  return box_text(n, n, n, 1.0 / n, perturb, seed, header);
+}
+
+std::string box_mesh_text(int nx, int ny, int nz, double perturb, uint64_t seed) {
+  char header[256];
+  snprintf(header, sizeof header, "# %dx%dx%d unit cubes x 6 Kuhn tets, perturb %.17g, seed %llu\n", nx, ny, nz,
+           perturb, (unsigned long long)seed);
+  return box_text(nx, ny, nz, 1.0, perturb, seed, header);
 }
 
 // Zero set of an edge micro-primitive = intersection of its endpoints' sets.
@@ -537,25 +551,53 @@ static int prim_zero_set(int g, int n, int i, int j, int k) {
 // ===========================================================================
 using namespace bt;
 
-#define BT_TRY try {
-#define BT_CATCH                                     \
-  }                                                  \
-  catch (const bt::Error& e) {                       \
-    bt::set_error(e.what());                         \
-    return e.status;                                 \
-  }                                                  \
-  catch (const std::bad_alloc&) {                    \
-    bt::set_error("out of host memory");             \
-    return BT_RUNTIME_ERROR;                         \
-  }                                                  \
-  catch (const std::exception& e) {                  \
-    bt::set_error(e.what());                         \
-    return BT_LOGIC_ERROR;                           \
-  }                                                  \
-  return BT_OK;
 
 bt_grid::~bt_grid() {
   if (h_pinned) cudaFreeHost(h_pinned);
+}
+
+// Interface work lists of the groups whose members all lie in cells
+// [begin, end) (every group when the range covers the mesh).
+static void interface_lists(const bt_grid& g, int begin, int end, IfaceLists& L) {
+  auto in = [&](int c) { return c >= begin && c < end; };
+  L.face_shared.clear();
+  L.face_bdir.clear();
+  L.edge_act.clear();
+  L.vert_act.clear();
+  for (int f = 0; f < (int)g.topo.faces.size(); ++f) {
+    const DevFace& F = g.topo.faces[f];
+    if (F.ncell == 2) {
+      if (in(F.cell[0]) && in(F.cell[1])) L.face_shared.push_back(f);
+    } else if (F.dir && in(F.cell[0])) {
+      L.face_bdir.push_back(f);
+    }
+  }
+  auto all_in = [&](const DevPrimHdr& h, const std::vector<DevPrimMem>& mem) {
+    for (int m = 0; m < h.count; ++m)
+      if (!in(mem[h.first + m].cell)) return false;
+    return true;
+  };
+  for (int e = 0; e < (int)g.topo.ehdr.size(); ++e) {
+    const DevPrimHdr& h = g.topo.ehdr[e];
+    if ((h.count >= 2 || h.dir) && all_in(h, g.topo.emem)) L.edge_act.push_back(e);
+  }
+  for (int v = 0; v < (int)g.topo.vhdr.size(); ++v) {
+    const DevPrimHdr& h = g.topo.vhdr[v];
+    if ((h.count >= 2 || h.dir) && all_in(h, g.topo.vmem)) L.vert_act.push_back(v);
+  }
+  L.upload();
+}
+
+void bt::require_unpartitioned(const bt_grid* g, const char* what) {
+  if (g && g->part_nranks > 1)
+    raise(BT_LOGIC_ERROR, std::string(what) +
+                              ": not available on a partitioned grid (rank-spanning groups need the exchange; see "
+                              "bt_xchg_pack / bt_xchg_finish)");
+}
+
+void bt::partition_range(int nc, int rank, int nranks, int& begin, int& end) {
+  begin = (int)((int64_t)nc * rank / nranks);
+  end = (int)((int64_t)nc * (rank + 1) / nranks);
 }
 
 extern "C" {
@@ -650,24 +692,28 @@ bt_status bt_grid_create(const char* text, int lo, int hi, int device, bt_grid**
   g->d_vhdr.upload(g->topo.vhdr);
   g->d_vmem.upload(g->topo.vmem);
   g->d_info.upload(g->topo.info);
-  for (int f = 0; f < (int)g->topo.faces.size(); ++f) {
-    if (g->topo.faces[f].ncell == 2) g->face_shared.push_back(f);
-    else if (g->topo.faces[f].dir) g->face_bdir.push_back(f);
-  }
-  for (int e = 0; e < (int)g->topo.ehdr.size(); ++e)
-    if (g->topo.ehdr[e].count >= 2 || g->topo.ehdr[e].dir) g->edge_act.push_back(e);
-  for (int v = 0; v < (int)g->topo.vhdr.size(); ++v)
-    if (g->topo.vhdr[v].count >= 2 || g->topo.vhdr[v].dir) g->vert_act.push_back(v);
-  g->d_face_shared.upload(g->face_shared);
-  g->d_face_bdir.upload(g->face_bdir);
-  g->d_edge_act.upload(g->edge_act);
-  g->d_vert_act.upload(g->vert_act);
+  g->part_end = g->mesh.n_cells();
+  interface_lists(*g, 0, g->mesh.n_cells(), g->full);
+  interface_lists(*g, 0, g->mesh.n_cells(), g->loc);
   BT_CUDA(cudaMallocHost(&g->h_pinned, sizeof(double) * 8));
   *out = g.release();
   BT_CATCH
 }
 
 void bt_grid_destroy(bt_grid* g) { delete g; }
+
+bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks) {
+  BT_TRY
+  if (!g) raise(BT_INVALID_ARGUMENT, "bt_grid_set_partition: grid required");
+  if (nranks < 1 || rank < 0 || rank >= nranks) raise(BT_INVALID_ARGUMENT, "bt_grid_set_partition: bad rank");
+  BT_CUDA(cudaSetDevice(g->device));
+  g->part_rank = rank;
+  g->part_nranks = nranks;
+  partition_range(g->mesh.n_cells(), rank, nranks, g->part_begin, g->part_end);
+  interface_lists(*g, g->part_begin, g->part_end, g->loc);
+  for (auto& p : g->xplan) p.reset();
+  BT_CATCH
+}
 int bt_num_cells(const bt_grid* g) { return g ? g->mesh.n_cells() : 0; }
 int bt_grid_min_level(const bt_grid* g) { return g->lo; }
 int bt_grid_max_level(const bt_grid* g) { return g->hi; }
@@ -780,6 +826,17 @@ bt_status bt_grid_groups(const bt_grid* g, int level, int space, int64_t* n_grou
   BT_CATCH
 }
 
+int64_t bt_box_mesh_text(int nx, int ny, int nz, double perturb, uint64_t seed, char* buf, int64_t buflen) {
+  if (nx < 1 || ny < 1 || nz < 1) return -1;
+  const std::string s = box_mesh_text(nx, ny, nz, perturb, seed);
+  if (buf && buflen > 0) {
+    const int64_t k = std::min<int64_t>((int64_t)s.size(), buflen - 1);
+    std::memcpy(buf, s.data(), (size_t)k);
+    buf[k] = 0;
+  }
+  return (int64_t)s.size();
+}
+
 int64_t bt_cubes_mesh_text(int n, double perturb, uint64_t seed, char* buf, int64_t buflen) {
   const std::string s = cubes_mesh_text(n, perturb, seed);
   if (buf && buflen > 0) {
@@ -814,7 +871,7 @@ bt_status bt_random_fill(const bt_grid* g, int space, int level, uint64_t seed, 
   }
   cudaStream_t s = (cudaStream_t)stream;
   BT_CUDA(cudaMemcpyAsync(x, h.data(), sizeof(double) * (size_t)total, cudaMemcpyHostToDevice, s));
-  launch_interface(*g, level, IF_BCAST, x, nullptr, s);
+  launch_interface(*g, level, IF_BCAST, x, nullptr, s, /*full=*/true);
   BT_CUDA(cudaStreamSynchronize(s));
   BT_CATCH
 }
@@ -846,7 +903,7 @@ bt_status bt_stencil_create(const bt_grid* g, const bt_form* form, int level, bt
   d_tbl.upload(tbl);
   st->d_diag.alloc((size_t)bt_space_size(g, BT_SPACE_P1, level));
   launch_fill_by_z(*g, level, d_tbl.p, st->d_diag.p, 0);
-  launch_interface(*g, level, IF_SYNC, st->d_diag.p, nullptr, 0);
+  launch_interface(*g, level, IF_SYNC, st->d_diag.p, nullptr, 0, /*full=*/true);
   BT_CUDA(cudaStreamSynchronize(0));
   *out = st.release();
   BT_CATCH

@@ -72,51 +72,6 @@ __device__ __forceinline__ void apply_group(double* __restrict__ v, const double
   }
 }
 
-// Face-interior points (a, b), a, b >= 1, a + b <= n - 1, weights
-// (n - a - b, a, b) on the face's sorted global vertices.
-template <int MODE>
-__global__ void __launch_bounds__(kT) k_iface_faces(double* __restrict__ v, const double* __restrict__ src,
-                                                    FaceArgs a) {
-  const int n = a.n, w = n + 1;
-  const int q = blockIdx.x * kT + threadIdx.x;
-  if (q >= tri32(n - 2)) return;
-  const DevFace f = a.faces[a.list[blockIdx.y]];
-  int ap, bp;
-  decode_tri(n - 2, q, ap, bp);
-  const int aa = ap + 1, bb = bp + 1, cc = n - aa - bb;
-  const int64_t s0 = slot_of(a.cs, w, f.cell[0], f.lv[0][0], cc, f.lv[0][1], aa, f.lv[0][2], bb);
-  const int64_t s1 = f.ncell == 2 ? slot_of(a.cs, w, f.cell[1], f.lv[1][0], cc, f.lv[1][1], aa, f.lv[1][2], bb) : 0;
-  apply_group<MODE>(v, src, f.ncell, f.dir != 0, [&](int m) { return m == 0 ? s0 : s1; });
-}
-
-// Macro-edge interior points a = 1..n-1 (weights (n - a, a)) on blockIdx.y <
-// ne, then macro vertices.
-template <int MODE>
-__global__ void __launch_bounds__(kT) k_iface_prims(double* __restrict__ v, const double* __restrict__ src,
-                                                    PrimArgs a) {
-  const int n = a.n, w = n + 1;
-  if ((int)blockIdx.y < a.ne) {
-    const int aa = blockIdx.x * kT + threadIdx.x + 1;
-    if (aa > n - 1) return;
-    const DevPrimHdr h = a.eh[a.elist[blockIdx.y]];
-    const DevPrimMem* mem = a.em + h.first;
-    apply_group<MODE>(v, src, h.count, h.dir != 0, [&](int m) {
-      const DevPrimMem pm = mem[m];
-      return slot_of(a.cs, w, pm.cell, pm.lv[0], n - aa, pm.lv[1], aa, -1, 0);
-    });
-  } else {
-    if (blockIdx.x != 0) return;
-    const int vi = (blockIdx.y - a.ne) * kT + threadIdx.x;
-    if (vi >= a.nv) return;
-    const DevPrimHdr h = a.vh[a.vlist[vi]];
-    const DevPrimMem* mem = a.vm + h.first;
-    apply_group<MODE>(v, src, h.count, h.dir != 0, [&](int m) {
-      const DevPrimMem pm = mem[m];
-      return slot_of(a.cs, w, pm.cell, pm.lv[0], n, -1, 0, -1, 0);
-    });
-  }
-}
-
 // All primitives of one mode in a single launch: a 1-D grid whose leading
 // blocks cover up to two face lists (xb blocks per face) and whose trailing
 // blocks cover macro edges (eb blocks per edge) and vertices.
@@ -171,7 +126,8 @@ __global__ void __launch_bounds__(kT) k_interface(double* __restrict__ v, const 
 }
 
 template <int MODE>
-void launch_mode(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s) {
+void launch_mode(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s, bool full) {
+  const IfaceLists& L = full ? g.full : g.loc;
   const int n = 1 << level;
   const int64_t cs = n_tet(n + 1);
   const int fp = tri32(n - 2);
@@ -180,15 +136,15 @@ void launch_mode(const bt_grid& g, int level, double* v, const double* src, cuda
   AllArgs a{};
   a.xb = (fp + kT - 1) / kT;
   if (sync_like && fp) {
-    a.f1 = FaceArgs{g.d_faces.p, g.d_face_shared.p, n, cs};
-    a.nf1 = (int)g.face_shared.size();
+    a.f1 = FaceArgs{g.d_faces.p, L.d_face_shared.p, n, cs};
+    a.nf1 = (int)L.face_shared.size();
   }
   if (dir_like && fp) {
-    a.f2 = FaceArgs{g.d_faces.p, g.d_face_bdir.p, n, cs};
-    a.nf2 = (int)g.face_bdir.size();
+    a.f2 = FaceArgs{g.d_faces.p, L.d_face_bdir.p, n, cs};
+    a.nf2 = (int)L.face_bdir.size();
   }
-  const int ne = (int)g.edge_act.size(), nv = (int)g.vert_act.size();
-  a.p = PrimArgs{g.d_ehdr.p, g.d_emem.p, g.d_edge_act.p, ne, g.d_vhdr.p, g.d_vmem.p, g.d_vert_act.p, nv, n, cs};
+  const int ne = (int)L.edge_act.size(), nv = (int)L.vert_act.size();
+  a.p = PrimArgs{g.d_ehdr.p, g.d_emem.p, L.d_edge_act.p, ne, g.d_vhdr.p, g.d_vmem.p, L.d_vert_act.p, nv, n, cs};
   a.eb = (n - 1 + kT - 1) / kT;
   const int64_t blocks = (int64_t)(a.nf1 + a.nf2) * a.xb + (int64_t)ne * a.eb + (nv + kT - 1) / kT;
   if (!blocks) return;
@@ -199,14 +155,15 @@ void launch_mode(const bt_grid& g, int level, double* v, const double* src, cuda
 
 }  // namespace
 
-void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
+void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s,
+                      bool full) {
   switch (mode) {
-    case IF_SYNC: launch_mode<IF_SYNC>(g, level, v, src, s); break;
-    case IF_SYNC_DIR: launch_mode<IF_SYNC_DIR>(g, level, v, src, s); break;
-    case IF_BCAST: launch_mode<IF_BCAST>(g, level, v, src, s); break;
-    case IF_IMPOSE: launch_mode<IF_IMPOSE>(g, level, v, src, s); break;
-    case IF_ZERO_DIR: launch_mode<IF_ZERO_DIR>(g, level, v, src, s); break;
-    case IF_ZERO_NONOWNED: launch_mode<IF_ZERO_NONOWNED>(g, level, v, src, s); break;
+    case IF_SYNC: launch_mode<IF_SYNC>(g, level, v, src, s, full); break;
+    case IF_SYNC_DIR: launch_mode<IF_SYNC_DIR>(g, level, v, src, s, full); break;
+    case IF_BCAST: launch_mode<IF_BCAST>(g, level, v, src, s, full); break;
+    case IF_IMPOSE: launch_mode<IF_IMPOSE>(g, level, v, src, s, full); break;
+    case IF_ZERO_DIR: launch_mode<IF_ZERO_DIR>(g, level, v, src, s, full); break;
+    case IF_ZERO_NONOWNED: launch_mode<IF_ZERO_NONOWNED>(g, level, v, src, s, full); break;
   }
 }
 

@@ -5,6 +5,7 @@
 #include <array>
 #include <cstdint>
 #include <memory>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -30,6 +31,24 @@ void set_error(const std::string& m);
     if (e_ != cudaSuccess)                                                             \
       ::bt::raise(BT_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_));  \
   } while (0)
+
+// C-ABI entry point bodies: exceptions inside, statuses at the boundary.
+#define BT_TRY try {
+#define BT_CATCH                                     \
+  }                                                  \
+  catch (const ::bt::Error& e) {                     \
+    ::bt::set_error(e.what());                       \
+    return e.status;                                 \
+  }                                                  \
+  catch (const std::bad_alloc&) {                    \
+    ::bt::set_error("out of host memory");           \
+    return BT_RUNTIME_ERROR;                         \
+  }                                                  \
+  catch (const std::exception& e) {                  \
+    ::bt::set_error(e.what());                       \
+    return BT_LOGIC_ERROR;                           \
+  }                                                  \
+  return BT_OK;
 
 extern uint64_t g_launches;
 inline void count_launch(int n = 1) { g_launches += (uint64_t)n; }
@@ -75,6 +94,8 @@ struct Mesh {
   int n_cells() const { return (int)cells.size(); }
 };
 Mesh parse_mesh(const std::string& text);
+struct Topology;
+void build_topology(const Mesh& m, Topology& t);
 
 // Affine map x = A r + b of a macro-cell (coarse_mesh.hpp:84-105).
 struct CellMap {
@@ -102,6 +123,46 @@ struct DevPrimMem {
 struct DevCellInfo {
   uint16_t owned_by_z;
   uint16_t dir_by_z;
+};
+
+// Interface work lists (indices into Topology::faces / ehdr / vhdr).
+struct IfaceLists {
+  std::vector<int> face_shared, face_bdir, edge_act, vert_act;
+  DevBuf<int> d_face_shared, d_face_bdir, d_edge_act, d_vert_act;
+  void upload() {
+    d_face_shared.upload(face_shared);
+    d_face_bdir.upload(face_bdir);
+    d_edge_act.upload(edge_act);
+    d_vert_act.upload(vert_act);
+  }
+};
+
+// Exchange plan for interface groups whose members lie on several ranks.
+// The exchange buffer holds, for every such group (faces, then macro edges,
+// then macro vertices in topology order; points in the interface kernel's
+// order), one double per member in ascending cell order. Each rank writes its
+// members' values (bt_xchg_pack), the caller sums the buffers over ranks, and
+// each rank then reduces every group in member order (bt_xchg_combine) — the
+// same order as a single-handle sync, so results do not depend on the rank
+// count. One entry per member on this rank:
+struct XEntry {
+  int64_t slot;   // element index in the full-size vector
+  int32_t buf;    // this member's value in the buffer
+  int32_t base;   // first member of the group
+  int32_t count;  // members in the group
+  int32_t dir;    // group is Dirichlet-constrained
+};
+struct XPlan {
+  bool built = false;
+  int64_t buf_size = 0;
+  std::vector<XEntry> entries;
+  DevBuf<XEntry> d_entries;
+  void reset() {
+    built = false;
+    buf_size = 0;
+    entries.clear();
+    d_entries.release();
+  }
 };
 
 struct Topology {
@@ -138,9 +199,14 @@ struct bt_grid {
   bt::DevBuf<bt::DevPrimMem> d_emem, d_vmem;
   bt::DevBuf<bt::DevCellInfo> d_info;
   // interface work lists: shared faces (2 cells), constrained boundary faces,
-  // edges / vertices that are shared or constrained
-  std::vector<int> face_shared, face_bdir, edge_act, vert_act;
-  bt::DevBuf<int> d_face_shared, d_face_bdir, d_edge_act, d_vert_act;
+  // edges / vertices that are shared or constrained. `full` covers every
+  // cell; `loc` only the groups whose members all lie in this handle's cell
+  // partition (== full when unpartitioned).
+  bt::IfaceLists full, loc;
+  // cell partition (bt_grid_set_partition): this handle computes cells
+  // [part_begin, part_end) of rank part_rank out of part_nranks
+  int part_rank = 0, part_nranks = 1, part_begin = 0, part_end = 0;
+  mutable std::array<bt::XPlan, 11> xplan;  // per level, built on first use
   // reduction scratch for dot products
   mutable bt::DevBuf<double> d_partials;
   mutable double* h_pinned = nullptr;
@@ -177,6 +243,7 @@ struct bt_stencil {
   bt::DevBuf<double> d_diag;                 // assembled diagonal
   bt::DevBuf<int4> d_tasks;                  // warp march schedule, fast rows (see bt_stencil.cu)
   int ntasks = 0;
+  int part_begin = 0, part_end = 0;          // the grid's cell partition when the tasks were built
   std::vector<int> chunk_first;              // first task of each 128-cell chunk in d_tasks (+ end)
   bt::DevBuf<int4> d_xtasks;                 // per-cell general rows (marches that would stage outside x)
   bt::DevBuf<int> d_xoff;                    // cell c: d_xtasks[d_xoff[c] .. d_xoff[c + 1])
@@ -198,12 +265,24 @@ void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<E
                     std::vector<EwAngles>& angles);
 int64_t level_slots(int space, int level);  // per cell
 void validate_form(const bt_form* f);
+// entry points that need every group local (no exchange step) refuse a
+// partitioned grid
+void require_unpartitioned(const bt_grid* g, const char* what);
 void check_level(const bt_grid* g, int level);
 
 // kernel launchers (bt_kernels.cu)
 enum IfaceMode { IF_SYNC = 0, IF_SYNC_DIR = 1, IF_BCAST = 2, IF_IMPOSE = 3, IF_ZERO_DIR = 4, IF_ZERO_NONOWNED = 5 };
+// full = false: the groups local to this handle's partition (g.loc);
+// full = true: every group (setup on full-size vectors, e.g. random_fill)
 void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src,
-                      cudaStream_t s);
+                      cudaStream_t s, bool full = false);
+// exchange for rank-spanning groups (bt_xchg.cu)
+const XPlan& xchg_plan(const bt_grid& g, int level);
+void build_xplan(const Mesh& m, const Topology& t, int level, int rank, int nranks, XPlan& out);
+void launch_xchg_pack(const bt_grid& g, int level, const double* x, double* buf, cudaStream_t s);
+void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x, const double* src,
+                         const double* buf, cudaStream_t s);
+void partition_range(int nc, int rank, int nranks, int& begin, int& end);
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s);
 void init_stencil_tasks(bt_stencil& st);
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c,

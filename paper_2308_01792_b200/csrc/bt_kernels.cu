@@ -186,9 +186,10 @@ void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* ou
 // reassociation).
 __global__ void __launch_bounds__(kThreads) k_dot_partial(const double* __restrict__ x, const double* __restrict__ y,
                                                           const DevCellInfo* __restrict__ info, int w,
-                                                          int64_t cell_slots, double* __restrict__ partials) {
+                                                          int64_t cell_slots, int cell0,
+                                                          double* __restrict__ partials) {
   __shared__ double red[kWarps];
-  const int cell = blockIdx.y;
+  const int cell = cell0 + blockIdx.y;
   const uint16_t own = info[cell].owned_by_z;
   const double* xc = x + (int64_t)cell * cell_slots;
   const double* yc = y + (int64_t)cell * cell_slots;
@@ -229,19 +230,51 @@ __global__ void __launch_bounds__(1024) k_sum(const double* __restrict__ partial
   }
 }
 
-double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s) {
+// Per-cell sums of the row-block partials (fixed order), then the cells in
+// order: the same association on any number of GPUs (bt_dot_cells).
+__global__ void k_cell_sums(const double* __restrict__ partials, int per_cell, int cell0, int ncells,
+                            double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const double* p = partials + (int64_t)(cell0 + c) * per_cell;
+  double s = 0.0;
+  for (int q = 0; q < per_cell; ++q) s += p[q];
+  out[c] = s;
+}
+__global__ void k_ordered_sum(const double* __restrict__ v, int n, double* out) {
+  double s = 0.0;
+  for (int q = 0; q < n; ++q) s += v[q];
+  *out = s;
+}
+
+// owned dot over this handle's cells: per-cell sums into host[cell_begin..cell_end)
+// (total != nullptr: also their ordered sum)
+static void dot_p1_cells(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s,
+                         double* host_cells, double* total) {
   const int w = (1 << level) + 1;
   const int bx = ceil_div(tri32(w), kRowsPerCta);
-  const int64_t np = (int64_t)bx * g.mesh.n_cells();
-  if (g.d_partials.n < (size_t)np + 1) g.d_partials.alloc((size_t)np + 1);
-  dim3 grid(bx, g.mesh.n_cells());
-  k_dot_partial<<<grid, kThreads, 0, s>>>(x, y, g.d_info.p, w, n_tet(w), g.d_partials.p);
-  k_sum<<<1, 1024, 0, s>>>(g.d_partials.p, np, g.d_partials.p + np);
+  const int nc = g.mesh.n_cells(), c0 = g.part_begin, nl = g.part_end - g.part_begin;
+  const int64_t np = (int64_t)bx * nc;
+  if (g.d_partials.n < (size_t)(np + nc + 1)) g.d_partials.alloc((size_t)(np + nc + 1));
+  double* cells = g.d_partials.p + np;
+  k_dot_partial<<<dim3(bx, nl), kThreads, 0, s>>>(x, y, g.d_info.p, w, n_tet(w), c0, g.d_partials.p);
+  k_cell_sums<<<ceil_div(nl, 128), 128, 0, s>>>(g.d_partials.p, bx, c0, nl, cells);
   count_launch(2);
+  if (total) {
+    k_ordered_sum<<<1, 1, 0, s>>>(cells, nl, cells + nc);
+    count_launch();
+  }
   check_launch("k_dot");
-  BT_CUDA(cudaMemcpyAsync(g.h_pinned, g.d_partials.p + np, sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (host_cells) BT_CUDA(cudaMemcpyAsync(host_cells + c0, cells, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
+  if (total) BT_CUDA(cudaMemcpyAsync(g.h_pinned, cells + nc, sizeof(double), cudaMemcpyDeviceToHost, s));
   BT_CUDA(cudaStreamSynchronize(s));
-  return g.h_pinned[0];
+  if (total) *total = g.h_pinned[0];
+}
+
+double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s) {
+  double t = 0.0;
+  dot_p1_cells(g, level, x, y, s, nullptr, &t);
+  return t;
 }
 
 // prolongate_p1 (solvers.hpp:227-253), optionally fused with axpy(x, 1, ef)
@@ -379,18 +412,6 @@ void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStr
 // ===========================================================================
 using namespace bt;
 
-#define BT_TRY try {
-#define BT_CATCH                         \
-  }                                      \
-  catch (const bt::Error& e) {           \
-    bt::set_error(e.what());             \
-    return e.status;                     \
-  }                                      \
-  catch (const std::exception& e) {      \
-    bt::set_error(e.what());             \
-    return BT_LOGIC_ERROR;               \
-  }                                      \
-  return BT_OK;
 
 static void require_p1(int space) {
   if (space != BT_SPACE_P1) raise(BT_INVALID_ARGUMENT, "operator kernels require a P1 function");
@@ -437,11 +458,23 @@ bt_status bt_dot(const bt_grid* g, int space, int level, const double* x, const 
     return BT_OK;
   }
   require_p1(space);
+  require_unpartitioned(g, "dot (use bt_dot_cells and sum the cells in order)");
   *out = dot_p1(*g, level, x, y, (cudaStream_t)stream);
+  BT_CATCH
+}
+bt_status bt_dot_cells(const bt_grid* g, int space, int level, const double* x, const double* y, double* per_cell,
+                       void* stream) {
+  BT_TRY
+  check_level(g, level);
+  require_p1(space);
+  if (!per_cell) raise(BT_INVALID_ARGUMENT, "bt_dot_cells: output required");
+  for (int c = 0; c < g->mesh.n_cells(); ++c) per_cell[c] = 0.0;
+  dot_p1_cells(*g, level, x, y, (cudaStream_t)stream, per_cell, nullptr);
   BT_CATCH
 }
 bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, void* stream) {
   BT_TRY
+  require_unpartitioned(g, "sync_additive");
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
     launch_edge_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
@@ -453,6 +486,7 @@ bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, vo
 }
 bt_status bt_sync_broadcast(const bt_grid* g, int space, int level, double* x, void* stream) {
   BT_TRY
+  require_unpartitioned(g, "sync_broadcast");
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
     launch_edge_interface(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
@@ -466,17 +500,20 @@ bt_status bt_impose_dirichlet(const bt_grid* g, int level, const double* src, do
   BT_TRY
   check_level(g, level);
   launch_interface(*g, level, IF_IMPOSE, dst, src, (cudaStream_t)stream);
+  if (g->part_nranks > 1) launch_xchg_combine(*g, level, IF_IMPOSE, dst, src, nullptr, (cudaStream_t)stream);
   BT_CATCH
 }
 bt_status bt_zero_dirichlet(const bt_grid* g, int level, double* x, void* stream) {
   BT_TRY
   check_level(g, level);
   launch_interface(*g, level, IF_ZERO_DIR, x, nullptr, (cudaStream_t)stream);
+  if (g->part_nranks > 1) launch_xchg_combine(*g, level, IF_ZERO_DIR, x, nullptr, nullptr, (cudaStream_t)stream);
   BT_CATCH
 }
 
 bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int bc, void* stream) {
   BT_TRY
+  require_unpartitioned(st ? st->grid : nullptr, "apply_stencil");
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   cudaStream_t s = (cudaStream_t)stream;
@@ -495,6 +532,7 @@ bt_status bt_apply_stencil_cells(const bt_stencil* st, const double* x, double* 
 
 bt_status bt_apply_stencil_interface(const bt_stencil* st, const double* x, double* y, int bc, void* stream) {
   BT_TRY
+  require_unpartitioned(st ? st->grid : nullptr, "apply_stencil_interface");
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
   launch_interface(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, (cudaStream_t)stream);
   BT_CATCH
@@ -503,6 +541,7 @@ bt_status bt_apply_stencil_interface(const bt_stencil* st, const double* x, doub
 bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level, const double* x, double* y,
                                int mode, int bc, double* scratch, void* stream) {
   BT_TRY
+  require_unpartitioned(g, "apply_elementwise");
   check_level(g, level);
   validate_form(form);
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
@@ -535,6 +574,7 @@ bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level,
 
 bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, double* diag, void* stream) {
   BT_TRY
+  require_unpartitioned(g, "extract_diagonal");
   check_level(g, level);
   validate_form(form);
   cudaStream_t s = (cudaStream_t)stream;
@@ -557,6 +597,7 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
 bt_status bt_prolongate(const bt_grid* g, int fine_level, const double* coarse, double* fine, int add,
                         void* stream) {
   BT_TRY
+  require_unpartitioned(g, "prolongate_p1");
   check_level(g, fine_level);
   check_level(g, fine_level - 1);
   launch_prolongate(*g, fine_level, coarse, fine, add != 0, (cudaStream_t)stream);
@@ -565,6 +606,7 @@ bt_status bt_prolongate(const bt_grid* g, int fine_level, const double* coarse, 
 
 bt_status bt_restrict(const bt_grid* g, int fine_level, const double* fine, double* coarse, void* stream) {
   BT_TRY
+  require_unpartitioned(g, "restrict_p1");
   check_level(g, fine_level);
   check_level(g, fine_level - 1);
   launch_restrict(*g, fine_level, fine, coarse, (cudaStream_t)stream);

@@ -358,19 +358,19 @@ template <int MODE>
 void edge_iface(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s) {
   build_static();
   const int n = 1 << level;
-  EdgeIfaceArgs a{g.d_faces.p, nullptr, g.d_ehdr.p, g.d_emem.p, g.d_edge_act.p, (int)g.edge_act.size(), n,
+  EdgeIfaceArgs a{g.d_faces.p, nullptr, g.d_ehdr.p, g.d_emem.p, g.full.d_edge_act.p, (int)g.full.edge_act.size(), n,
                   level_slots(BT_SPACE_EDGES, level)};
   const int per = 3 * tri32(n);
   const bool sync_like = MODE == IF_SYNC || MODE == IF_BCAST || MODE == IF_SYNC_DIR;
   const bool dir_like = MODE == IF_SYNC_DIR || MODE == IF_IMPOSE || MODE == IF_ZERO_DIR;
-  if (sync_like && !g.face_shared.empty()) {
-    a.flist = g.d_face_shared.p;
-    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.face_shared.size()), kT, 0, s>>>(v, src, a);
+  if (sync_like && !g.full.face_shared.empty()) {
+    a.flist = g.full.d_face_shared.p;
+    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.full.face_shared.size()), kT, 0, s>>>(v, src, a);
     count_launch();
   }
-  if (dir_like && !g.face_bdir.empty()) {
-    a.flist = g.d_face_bdir.p;
-    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.face_bdir.size()), kT, 0, s>>>(v, src, a);
+  if (dir_like && !g.full.face_bdir.empty()) {
+    a.flist = g.full.d_face_bdir.p;
+    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.full.face_bdir.size()), kT, 0, s>>>(v, src, a);
     count_launch();
   }
   if (a.ne) {
@@ -494,23 +494,12 @@ void random_fill_edges(const bt_grid& g, int level, uint64_t seed, double* x, cu
 
 using namespace bt;
 
-#define BT_TRY try {
-#define BT_CATCH                         \
-  }                                      \
-  catch (const bt::Error& e) {           \
-    bt::set_error(e.what());             \
-    return e.status;                     \
-  }                                      \
-  catch (const std::exception& e) {      \
-    bt::set_error(e.what());             \
-    return BT_LOGIC_ERROR;               \
-  }                                      \
-  return BT_OK;
 
 extern "C" {
 
 bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta, bt_n1e1** out) {
   BT_TRY
+  require_unpartitioned(g, "N1E1 operator");
   check_level(g, level);
   BT_CUDA(cudaSetDevice(g->device));
   build_static();

@@ -211,23 +211,12 @@ static void v_cycle(bt_hierarchy& h, int l, const double* rhs, double* x, const 
 
 using namespace bt;
 
-#define BT_TRY try {
-#define BT_CATCH                         \
-  }                                      \
-  catch (const bt::Error& e) {           \
-    bt::set_error(e.what());             \
-    return e.status;                     \
-  }                                      \
-  catch (const std::exception& e) {      \
-    bt::set_error(e.what());             \
-    return BT_LOGIC_ERROR;               \
-  }                                      \
-  return BT_OK;
 
 extern "C" {
 
 bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel, bt_hierarchy** out) {
   BT_TRY
+  require_unpartitioned(g, "make_hierarchy");
   if (!g) raise(BT_INVALID_ARGUMENT, "make_hierarchy: grid required");
   validate_form(form);
   if (kernel == 1 && form->kind == BT_FORM_DIV_K_GRAD)

@@ -265,18 +265,19 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
 
 // Any rows of the march schedule, every row read from the zero-set-typed
 // table in shared memory (interior vertices use type 0 = the merged row).
-// With per_cell (nullable) the tasks of cell c are tasks[per_cell[c] ..
-// per_cell[c + 1]); otherwise every cell runs all ntasks tasks.
+// Block row y works on cell cell0 + y. With per_cell (nullable) its tasks are
+// tasks[per_cell[y] .. per_cell[y + 1]); otherwise every cell runs all ntasks.
 __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict__ x, double* __restrict__ y,
                                                         const StencilCell* __restrict__ cells,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
-                                                        int64_t cell_slots, const int* __restrict__ per_cell) {
+                                                        int64_t cell_slots, const int* __restrict__ per_cell,
+                                                        int cell0) {
   __shared__ double sw[16][15];
-  const int cell = blockIdx.y;
+  const int cell = cell0 + blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int task = blockIdx.x * kW + warp;
   if (per_cell) {
-    const int first = per_cell[cell], last = per_cell[cell + 1];
+    const int first = per_cell[blockIdx.y], last = per_cell[blockIdx.y + 1];  // partition-local cell
     if (first + (int)blockIdx.x * kW >= last) return;  // whole block idle
     task += first;
     ntasks = last;
@@ -354,12 +355,14 @@ void init_stencil_tasks(bt_stencil& st) {
   std::stable_sort(fast.begin(), fast.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
   const int nc_all = st.grid->mesh.n_cells();
   const int64_t cs = n_tet(w), total = cs * nc_all;
+  st.part_begin = st.grid->part_begin;
+  st.part_end = st.grid->part_end;
   std::vector<int4> all_fast;
   std::vector<std::vector<int4>> extra(nc_all);
   st.chunk_first.clear();
-  for (int c0 = 0; c0 < nc_all; c0 += kMaxCells) {
+  for (int c0 = st.part_begin; c0 < st.part_end; c0 += kMaxCells) {
     st.chunk_first.push_back((int)all_fast.size());
-    const int cnt = std::min(kMaxCells, nc_all - c0);
+    const int cnt = std::min(kMaxCells, st.part_end - c0);
     for (const int4& t : fast)
       for (int c = 0; c < cnt; ++c) {
         const int64_t cb = (int64_t)(c0 + c) * cs + kFastCols * t.y;
@@ -377,9 +380,9 @@ void init_stencil_tasks(bt_stencil& st) {
   st.ntasks = (int)all_fast.size();
   st.d_tasks.upload(all_fast);
   std::vector<int4> ex;
-  std::vector<int> exoff(1, 0);
-  for (auto& e : extra) {
-    ex.insert(ex.end(), e.begin(), e.end());
+  std::vector<int> exoff(1, 0);  // per cell of the partition
+  for (int c = st.part_begin; c < st.part_end; ++c) {
+    ex.insert(ex.end(), extra[c].begin(), extra[c].end());
     exoff.push_back((int)ex.size());
   }
   st.nxtasks = (int)ex.size();
@@ -420,23 +423,26 @@ void init_stencil_tasks(bt_stencil& st) {
 
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
   const int w = (1 << st.level) + 1;
-  const int nc = st.grid->mesh.n_cells();
   const int64_t cs = n_tet(w);
+  if (st.part_begin != st.grid->part_begin || st.part_end != st.grid->part_end)
+    raise(BT_LOGIC_ERROR, "apply_stencil: the grid was repartitioned after compute_stencil");
+  const int c0 = st.part_begin, nc = st.part_end - st.part_begin;  // this handle's cells
+  if (!nc) return;
   if (!st.symmetric) {
     k_stencil_general<<<dim3((st.natasks + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
-                                                                          st.natasks, w, cs, nullptr);
+                                                                          st.natasks, w, cs, nullptr, c0);
     count_launch();
     check_launch("k_stencil_general");
     return;
   }
   if (st.ngtasks) {
     k_stencil_general<<<dim3((st.ngtasks + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_gtasks.p,
-                                                                          st.ngtasks, w, cs, nullptr);
+                                                                          st.ngtasks, w, cs, nullptr, c0);
     count_launch();
   }
   if (st.nxtasks) {
     k_stencil_general<<<dim3((st.xtask_max + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_xtasks.p,
-                                                                            st.nxtasks, w, cs, st.d_xoff.p);
+                                                                            st.nxtasks, w, cs, st.d_xoff.p, c0);
     count_launch();
   }
   static FastParams<kMaxCells> fp;
@@ -451,18 +457,18 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     grid = sms * std::max(1, per_sm);
   }
   for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
-    const int c0 = ch * kMaxCells, cnt = std::min(kMaxCells, nc - c0);
+    const int cc0 = c0 + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
     const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
     if (!nt) continue;
     for (int c = 0; c < cnt; ++c) {
-      const double* f = &st.fast[30 * (size_t)(c0 + c)];
+      const double* f = &st.fast[30 * (size_t)(cc0 + c)];
       for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
       for (int q = 0; q < 11; ++q) {
         fp.dg[c][q] = f[8 + q];
         fp.f0[c][q] = f[19 + q];
       }
     }
-    const int64_t e0 = (int64_t)c0 * cs;
+    const int64_t e0 = (int64_t)cc0 * cs;
     const int blocks = std::min(grid, (nt + kW - 1) / kW);
     k_stencil_fast<kMaxCells><<<blocks, kT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
     count_launch();

@@ -1,0 +1,250 @@
+// Cell partition across ranks: the interface groups whose
+// members live on several ranks. The per-cell phase of an apply and the
+// groups local to a rank run as on one GPU; a rank-spanning group goes
+// through an exchange buffer (XPlan, bt_internal.hpp):
+//   bt_xchg_pack     this rank's member values -> buffer (zeros elsewhere)
+//   (caller)         allreduce(sum) of the buffer over ranks (NCCL / gloo)
+//   bt_xchg_finish   local groups + member-order reduction of each spanning
+//                    group from the buffer (sync_additive fe_function.hpp:
+//                    400-423 order, starting from 0.0), so replicas are
+//                    bitwise those of a single-GPU sync for any rank count.
+// Adding the other ranks' zeros is exact, so the allreduce is an allgather.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "bt_internal.hpp"
+
+namespace bt {
+
+namespace {
+constexpr int kT = 256;
+
+// lattice slot of the point with barycentric weights (w0, w1, w2) on the
+// local vertices (l0, l1, l2) of a cell (the interface kernel's slot_of)
+int64_t slot_of(int64_t cs, int w, int cell, int l0, int w0, int l1, int w1, int l2, int w2) {
+  const int i = (l0 == 1 ? w0 : 0) + (l1 == 1 ? w1 : 0) + (l2 == 1 ? w2 : 0);
+  const int j = (l0 == 2 ? w0 : 0) + (l1 == 2 ? w1 : 0) + (l2 == 2 ? w2 : 0);
+  const int k = (l0 == 3 ? w0 : 0) + (l1 == 3 ? w1 : 0) + (l2 == 3 ? w2 : 0);
+  return (int64_t)cell * cs + row_start(w, j, k) + i;
+}
+
+__global__ void __launch_bounds__(kT) k_xpack(const XEntry* __restrict__ e, int n, const double* __restrict__ x,
+                                              double* __restrict__ buf) {
+  const int q = blockIdx.x * kT + threadIdx.x;
+  if (q < n) buf[e[q].buf] = x[e[q].slot];
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kT) k_xcombine(const XEntry* __restrict__ e, int n, double* __restrict__ x,
+                                                 const double* __restrict__ src, const double* __restrict__ buf) {
+  const int q = blockIdx.x * kT + threadIdx.x;
+  if (q >= n) return;
+  const XEntry E = e[q];
+  if (MODE == IF_SYNC || (MODE == IF_SYNC_DIR && !E.dir)) {
+    double sum = 0.0;
+    for (int m = 0; m < E.count; ++m) sum += buf[E.base + m];
+    x[E.slot] = sum;
+  } else if (MODE == IF_SYNC_DIR || MODE == IF_IMPOSE) {
+    if (E.dir) x[E.slot] = src[E.slot];
+  } else if (MODE == IF_ZERO_DIR) {
+    if (E.dir) x[E.slot] = 0.0;
+  } else if (MODE == IF_BCAST) {
+    x[E.slot] = buf[E.base];
+  } else if (MODE == IF_ZERO_NONOWNED) {
+    if (E.buf != E.base) x[E.slot] = 0.0;
+  }
+}
+
+bool needs_buffer(IfaceMode m) { return m == IF_SYNC || m == IF_SYNC_DIR || m == IF_BCAST; }
+
+void check_partitioned_level(const bt_grid* g, int level) {
+  check_level(g, level);
+}
+}  // namespace
+
+void build_xplan(const Mesh& m, const Topology& t, int level, int rank, int nranks, XPlan& out) {
+  const int nc = m.n_cells();
+  const int n = 1 << level, w = n + 1;
+  const int64_t cs = n_tet(w);
+  std::vector<int> owner(nc);
+  for (int r = 0; r < nranks; ++r) {
+    int b, e;
+    partition_range(nc, r, nranks, b, e);
+    for (int c = b; c < e; ++c) owner[c] = r;
+  }
+  out.entries.clear();
+  int64_t off = 0;
+  auto add_group = [&](int count, int dir, auto&& slot_of_member, auto&& cell_of_member) {
+    for (int mm = 0; mm < count; ++mm)
+      if (owner[cell_of_member(mm)] == rank)
+        out.entries.push_back(XEntry{slot_of_member(mm), (int32_t)(off + mm), (int32_t)off, count, dir});
+    off += count;
+  };
+  // shared macro faces: interior points (a, b), weights (n - a - b, a, b)
+  for (const DevFace& F : t.faces) {
+    if (F.ncell != 2 || owner[F.cell[0]] == owner[F.cell[1]]) continue;
+    for (int q = 0; q < tri32(n - 2); ++q) {
+      int ap, bp;
+      decode_tri(n - 2, q, ap, bp);
+      const int aa = ap + 1, bb = bp + 1, cc = n - aa - bb;
+      add_group(
+          2, F.dir,
+          [&](int mm) {
+            return slot_of(cs, w, F.cell[mm], F.lv[mm][0], cc, F.lv[mm][1], aa, F.lv[mm][2], bb);
+          },
+          [&](int mm) { return F.cell[mm]; });
+    }
+  }
+  auto spans = [&](const DevPrimHdr& h, const std::vector<DevPrimMem>& mem) {
+    for (int mm = 1; mm < h.count; ++mm)
+      if (owner[mem[h.first + mm].cell] != owner[mem[h.first].cell]) return true;
+    return false;
+  };
+  // macro edges: points a = 1..n-1, weights (n - a, a)
+  for (const DevPrimHdr& h : t.ehdr) {
+    if (h.count < 2 || !spans(h, t.emem)) continue;
+    for (int aa = 1; aa <= n - 1; ++aa)
+      add_group(
+          h.count, h.dir,
+          [&](int mm) {
+            const DevPrimMem& pm = t.emem[h.first + mm];
+            return slot_of(cs, w, pm.cell, pm.lv[0], n - aa, pm.lv[1], aa, -1, 0);
+          },
+          [&](int mm) { return t.emem[h.first + mm].cell; });
+  }
+  // macro vertices
+  for (const DevPrimHdr& h : t.vhdr) {
+    if (h.count < 2 || !spans(h, t.vmem)) continue;
+    add_group(
+        h.count, h.dir,
+        [&](int mm) {
+          const DevPrimMem& pm = t.vmem[h.first + mm];
+          return slot_of(cs, w, pm.cell, pm.lv[0], n, -1, 0, -1, 0);
+        },
+        [&](int mm) { return t.vmem[h.first + mm].cell; });
+  }
+  if (off > INT32_MAX) raise(BT_OUT_OF_RANGE, "exchange buffer exceeds 2^31 entries");
+  out.buf_size = off;
+  out.built = true;
+}
+
+const XPlan& xchg_plan(const bt_grid& g, int level) {
+  XPlan& p = g.xplan.at(level);
+  if (!p.built) {
+    build_xplan(g.mesh, g.topo, level, g.part_rank, g.part_nranks, p);
+    p.d_entries.upload(p.entries);
+  }
+  return p;
+}
+
+void launch_xchg_pack(const bt_grid& g, int level, const double* x, double* buf, cudaStream_t s) {
+  const XPlan& p = xchg_plan(g, level);
+  if (!p.buf_size) return;
+  BT_CUDA(cudaMemsetAsync(buf, 0, sizeof(double) * (size_t)p.buf_size, s));
+  const int n = (int)p.entries.size();
+  if (!n) return;
+  k_xpack<<<(n + kT - 1) / kT, kT, 0, s>>>(p.d_entries.p, n, x, buf);
+  count_launch();
+  check_launch("k_xpack");
+}
+
+void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x, const double* src,
+                         const double* buf, cudaStream_t s) {
+  const XPlan& p = xchg_plan(g, level);
+  const int n = (int)p.entries.size();
+  if (!n) return;
+  const dim3 grid((n + kT - 1) / kT);
+  const XEntry* e = p.d_entries.p;
+  switch (mode) {
+    case IF_SYNC: k_xcombine<IF_SYNC><<<grid, kT, 0, s>>>(e, n, x, src, buf); break;
+    case IF_SYNC_DIR: k_xcombine<IF_SYNC_DIR><<<grid, kT, 0, s>>>(e, n, x, src, buf); break;
+    case IF_BCAST: k_xcombine<IF_BCAST><<<grid, kT, 0, s>>>(e, n, x, src, buf); break;
+    case IF_IMPOSE: k_xcombine<IF_IMPOSE><<<grid, kT, 0, s>>>(e, n, x, src, buf); break;
+    case IF_ZERO_DIR: k_xcombine<IF_ZERO_DIR><<<grid, kT, 0, s>>>(e, n, x, src, buf); break;
+    case IF_ZERO_NONOWNED: k_xcombine<IF_ZERO_NONOWNED><<<grid, kT, 0, s>>>(e, n, x, src, buf); break;
+  }
+  count_launch();
+  check_launch("k_xcombine");
+}
+
+}  // namespace bt
+
+using namespace bt;
+
+extern "C" {
+
+bt_status bt_grid_partition(const bt_grid* g, int* rank, int* nranks, int* cell_begin, int* cell_end) {
+  BT_TRY
+  if (!g) raise(BT_INVALID_ARGUMENT, "bt_grid_partition: grid required");
+  if (rank) *rank = g->part_rank;
+  if (nranks) *nranks = g->part_nranks;
+  if (cell_begin) *cell_begin = g->part_begin;
+  if (cell_end) *cell_end = g->part_end;
+  BT_CATCH
+}
+
+int64_t bt_xchg_size(const bt_grid* g, int level) {
+  try {
+    check_level(g, level);
+    BT_CUDA(cudaSetDevice(g->device));
+    return xchg_plan(*g, level).buf_size;
+  } catch (const Error& e) {
+    set_error(e.what());
+    return -1;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return -1;
+  }
+}
+
+bt_status bt_xchg_pack(const bt_grid* g, int level, const double* x, double* buf, void* stream) {
+  BT_TRY
+  check_partitioned_level(g, level);
+  launch_xchg_pack(*g, level, x, buf, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_xchg_finish(const bt_grid* g, int level, int mode, double* x, const double* src, const double* buf,
+                         void* stream) {
+  BT_TRY
+  check_partitioned_level(g, level);
+  if (mode < IF_SYNC || mode > IF_ZERO_NONOWNED) raise(BT_INVALID_ARGUMENT, "bt_xchg_finish: bad mode");
+  const IfaceMode m = (IfaceMode)mode;
+  if ((m == IF_SYNC_DIR || m == IF_IMPOSE) && !src) raise(BT_INVALID_ARGUMENT, "bt_xchg_finish: src required");
+  if (needs_buffer(m) && !buf && xchg_plan(*g, level).buf_size)
+    raise(BT_INVALID_ARGUMENT, "bt_xchg_finish: exchange buffer required");
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_interface(*g, level, m, x, src, s);
+  launch_xchg_combine(*g, level, m, x, src, buf, s);
+  BT_CATCH
+}
+
+int64_t bt_xchg_plan_host(const char* mesh_text, int level, int rank, int nranks, int64_t* buf_size,
+                          int64_t* slot, int32_t* buf, int32_t* base, int32_t* count, uint8_t* dir) {
+  try {
+    if (!mesh_text || level < 1 || level > 10 || nranks < 1 || rank < 0 || rank >= nranks)
+      raise(BT_INVALID_ARGUMENT, "bt_xchg_plan_host: bad arguments");
+    const Mesh m = parse_mesh(mesh_text);
+    Topology t;
+    build_topology(m, t);
+    XPlan p;
+    build_xplan(m, t, level, rank, nranks, p);
+    if (buf_size) *buf_size = p.buf_size;
+    for (size_t q = 0; q < p.entries.size(); ++q) {
+      if (slot) slot[q] = p.entries[q].slot;
+      if (buf) buf[q] = p.entries[q].buf;
+      if (base) base[q] = p.entries[q].base;
+      if (count) count[q] = p.entries[q].count;
+      if (dir) dir[q] = (uint8_t)p.entries[q].dir;
+    }
+    return (int64_t)p.entries.size();
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return -1;
+  }
+}
+
+}  // extern "C"
