@@ -253,7 +253,8 @@ struct bt_stencil {
   bt::DevBuf<int4> d_atasks;                 // all rows (general-kernel fallback)
   int natasks = 0;
   bool symmetric = false;                    // fast-path preconditions hold (see bt_stencil.cu)
-  std::vector<double> fast;                  // per cell: 8 symmetric weights, 7 + 7 face corrections
+  std::vector<double> fast;                  // per cell: the 8 symmetric interior weights
+  bt::DevBuf<double> d_ends;                 // per cell: typed rows of the two row ends (11 + 11)
 };
 
 namespace bt {

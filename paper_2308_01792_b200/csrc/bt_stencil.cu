@@ -46,6 +46,11 @@ constexpr int kW = kT / 32;
 constexpr int kMarchRows = 48;
 constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
+// k_stencil_general / k_stencil_ends blocks are small and register-light so
+// that one fits on an SM beside three k_stencil_fast blocks: they run on a
+// side stream concurrently with the fast kernel (launch_stencil).
+constexpr int kGT = 128;
+constexpr int kGW = kGT / 32;
 
 // present neighbour directions (kStencilDirs indices) of a diagonal-face
 // vertex (zero set {0}) and of an i = 0 vertex (zero set {1})
@@ -54,17 +59,18 @@ constexpr int kI0Present[11] = {0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 13};
 
 template <int kMaxC>
 struct FastParams {
-  double w[kMaxC][8];    // symmetric interior row: centre + 7 direction pairs
-  double dg[kMaxC][11];  // diagonal-face typed row on kDiagPresent
-  double f0[kMaxC][11];  // i = 0 face typed row on kI0Present
+  double w[kMaxC][8];  // symmetric interior row: centre + 7 direction pairs
 };
-constexpr int kMaxCells = 128;  // 128 * 30 * 8 B = 30 KB of kernel parameters
+constexpr int kMaxCells = 256;  // 256 * 8 * 8 B = 16 KB of kernel parameters
 
-// per-warp staging ring: kStages stages x 3 staged rows of kRowD doubles
-constexpr int kStages = 6;
+// per-warp staging ring: kStages stages x 4 staged rows of kRowD doubles
+constexpr int kStages = 5;
+constexpr int kRows = 4;   // A(j+1), P(j+1), C(j+1), Q(j)
 constexpr int kRowD = 64;  // staged columns [base - 2, base + 62)
-constexpr int kStageD = 3 * kRowD;
+constexpr int kStageD = kRows * kRowD;
 constexpr int kRingD = kStages * kStageD;  // doubles per warp
+constexpr int kFT = 128;                   // k_stencil_fast block
+constexpr int kFW = kFT / 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
@@ -79,38 +85,52 @@ __device__ __forceinline__ void cp_wait() {
 struct Row4 {  // one row at a lane's columns (c0, c1 = c0 + 1): l0 = c0 - 1, r1 = c1 + 1
   double l0, v0, v1, r1;
 };
-struct Win {  // A(j) of layer k, B(j-1) of layer k+1, C(j) of layer k-1
-  Row4 a, b, c;
+// Register window of a two-layer march at row j: layers k-1 (C), k (A),
+// k+1 (P), k+2 (Q).
+struct Win {
+  Row4 am1, a;  // A(j-1), A(j)
+  Row4 pm1, p;  // P(j-1), P(j)
+  Row4 c;       // C(j)
+  Row4 qm1;     // Q(j-1)
 };
 
-// Task word: x = k, y = column block | (cell - cell0) << 16, z = j0, w = j1.
+// Task word: x = k (first layer of the pair k, k+1), y = column block |
+// (cell - cell0) << 16, z = j0, w = j1.
+//
+// A warp owns 60 output columns of two adjacent layers k, k+1 of one cell and
+// marches rows j0..j1-1 of both (layer k+1's rows end one row earlier; its
+// last-step row is left to the general kernel or is empty). Per step it
+// stages four rows — A(j+1), P(j+1), C(j+1) and Q(j) — which serve both
+// layers: layer k reads A(j-1..j+1), P(j-1..j) as its upper layer and
+// C(j..j+1); layer k+1 reads P(j-1..j+1), Q(j-1..j) and A(j..j+1) as its
+// lower layer.
 //
 // Persistent warps: warp g runs tasks g, g + G, g + 2G, ... (the host sorts
-// tasks by length, longest first). Each march of rows j0..j1-1 is preceded by
-// two phantom steps (j0 - 2, j0 - 1) whose staged rows fill the register
-// window, so the staging stream runs through the ring across task boundaries
-// without draining. Lane l stages columns base - 2 + l and base + 30 + l of
-// each row (two 8-byte cp.async, each warp-contiguous), so every row lands at
-// the same place whatever its alignment and lane l reads its pair (c0, c1)
-// with one 16-byte shared load. The host keeps marches that would stage
-// outside x on the general kernel.
+// tasks by length, longest first). Each march is preceded by two phantom
+// steps (j0 - 2, j0 - 1) whose staged rows fill the register window, so the
+// staging stream runs through the ring across task boundaries without
+// draining. Lane l stages columns base - 2 + l and base + 30 + l of each row
+// (two 8-byte cp.async, each warp-contiguous), so every row lands at the same
+// place whatever its alignment and lane l reads its pair (c0, c1) with one
+// 16-byte shared load. The host keeps marches that would stage outside x on
+// the general kernel.
 template <int kMaxC>
-__global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
+__global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
                                                         int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
   extern __shared__ __align__(128) double ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = gridDim.x * kW;
-  const int t0 = blockIdx.x * kW + warp;
+  const int G = gridDim.x * kFW;
+  const int t0 = blockIdx.x * kFW + warp;
   if (t0 >= ntasks) return;
   const double* ring = ring_all + warp * kRingD;
   const uint32_t my_s = smem_u32(ring) + 8u * lane;
 
   // ---- producer (every lane copies its two columns of each staged row) ----
   // element offsets (within the cell) of column base - 2 + lane in rows
-  // A(j+1), B(j), C(j+1) of the producer's next step j; r = len(A(j+1)) =
-  // len(B(j)); pleft = steps left in the producer's task
-  int pt = t0, pA = 0, pB = 0, pC = 0, pr = 0, pleft = 0;
+  // A(j+1), P(j+1), C(j+1), Q(j) of the producer's next step j;
+  // r = len(A(j+1)) = len(P(j)); pleft = steps left in the producer's task
+  int pt = t0, pA = 0, pP = 0, pC = 0, pQ = 0, pr = 0, pleft = 0;
   const double* pcell = x;
   int4 pnext = tasks[t0];
   auto p_start = [&]() {
@@ -119,8 +139,9 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
     const int j = tk.z - 2, cb = base - 2 + lane;
     pcell = x + (int64_t)cl * cell_slots;
     pA = cb + row_start(w, j + 1, k);
-    pB = cb + row_start(w, j, k + 1);
+    pP = cb + row_start(w, j + 1, k + 1);
     pC = cb + row_start(w, j + 1, k - 1);
+    pQ = cb + row_start(w, j, k + 2);
     pr = w - k - j - 1;
     pleft = tk.w - tk.z + 2;
     if (pt + G < ntasks) pnext = tasks[pt + G];
@@ -130,17 +151,22 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
   auto produce = [&]() {  // one (possibly empty) group of copies
     if (pleft > 0) {
       const uint32_t d = my_s + (uint32_t)(ps * kStageD * 8);
-      const double *a = pcell + pA, *b = pcell + pB, *c = pcell + pC;
+      const double *a = pcell + pA, *p = pcell + pP, *c = pcell + pC, *q = pcell + pQ;
       cp8(d, a);
       cp8(d + 256, a + 32);
-      cp8(d + kRowD * 8, b);
-      cp8(d + kRowD * 8 + 256, b + 32);
+      cp8(d + kRowD * 8, p);
+      cp8(d + kRowD * 8 + 256, p + 32);
       cp8(d + 2 * kRowD * 8, c);
       cp8(d + 2 * kRowD * 8 + 256, c + 32);
+      cp8(d + 3 * kRowD * 8, q);
+      cp8(d + 3 * kRowD * 8 + 256, q + 32);
       ps = ps == kStages - 1 ? 0 : ps + 1;
+      // next rows: A(j+2) = A(j+1) + len(A(j+1)); P(j+2) = P(j+1) + len(P(j+1));
+      // C(j+2) = C(j+1) + len(C(j+1)); Q(j+1) = Q(j) + len(Q(j))
       pA += pr;
-      pB += pr;
+      pP += pr - 1;
       pC += pr + 1;
+      pQ += pr - 1;
       --pr;
       if (--pleft == 0) {
         pt += G;
@@ -154,23 +180,21 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
 
   // ---- consumer ----
   int cs = 0;
-  auto consume = [&](Row4& A1, Row4& B0, Row4& C1) {
+  auto read_row = [&](const double* row, Row4& o) {
+    const double2 v = reinterpret_cast<const double2*>(row)[lane];
+    o.v0 = v.x;
+    o.v1 = v.y;
+    o.l0 = __shfl_up_sync(0xffffffffu, v.y, 1);
+    o.r1 = __shfl_down_sync(0xffffffffu, v.x, 1);
+  };
+  auto consume = [&](Row4& A1, Row4& P1, Row4& C1, Row4& Q0) {
     cp_wait<kStages - 2>();
     __syncwarp();
-    const double2* st = reinterpret_cast<const double2*>(ring + cs * kStageD) + lane;
-    const double2 a = st[0], b = st[kRowD / 2], c = st[kRowD];
-    A1.v0 = a.x;
-    A1.v1 = a.y;
-    B0.v0 = b.x;
-    B0.v1 = b.y;
-    C1.v0 = c.x;
-    C1.v1 = c.y;
-    A1.l0 = __shfl_up_sync(0xffffffffu, a.y, 1);
-    A1.r1 = __shfl_down_sync(0xffffffffu, a.x, 1);
-    B0.l0 = __shfl_up_sync(0xffffffffu, b.y, 1);
-    B0.r1 = __shfl_down_sync(0xffffffffu, b.x, 1);
-    C1.l0 = __shfl_up_sync(0xffffffffu, c.y, 1);
-    C1.r1 = __shfl_down_sync(0xffffffffu, c.x, 1);
+    const double* st = ring + cs * kStageD;
+    read_row(st, A1);
+    read_row(st + kRowD, P1);
+    read_row(st + 2 * kRowD, C1);
+    read_row(st + 3 * kRowD, Q0);
     cs = cs == kStages - 1 ? 0 : cs + 1;
     // the stage refilled next is the one every lane read in the previous
     // step (its values went through the warp-synchronous shuffles)
@@ -184,90 +208,115 @@ __global__ void __launch_bounds__(kT, 2) k_stencil_fast(const double* __restrict
     double W[8];
 #pragma unroll
     for (int d = 0; d < 8; ++d) W[d] = fp.w[cl][d];
-    const double* DG = fp.dg[cl];
-    const double* F0 = fp.f0[cl];
     const int base = kFastCols * blk;
     const int c0 = base - 2 + 2 * lane, c1 = c0 + 1;  // this lane's two columns
     const bool out = lane >= 1 && lane <= 30;
     Win X, Y;
-    Row4 Am1, Am1y, junk0, junk1;
-    consume(Am1, junk0, junk1);  // phantom step j0 - 2: A(j0 - 1)
-    consume(X.a, X.b, X.c);      // phantom step j0 - 1: A(j0), B(j0 - 1), C(j0)
+    Row4 junk0, junk1;
+    consume(X.am1, X.pm1, junk0, junk1);  // phantom step j0 - 2: A(j0-1), P(j0-1)
+    consume(X.a, X.p, X.c, X.qm1);        // phantom step j0 - 1: A(j0), P(j0), C(j0), Q(j0-1)
 
-    int LY = w - k - j0;  // length of the output row
-    double* __restrict__ py = y + (int64_t)cl * cell_slots + row_start(w, j0, k);
-    const int colend = base + kFastCols;  // LY <= colend: the row ends inside this warp
-    const bool blk0 = blk == 0;
+    int LA = w - k - j0;  // length of A(j); P(j) has LA - 1
+    double* __restrict__ pya = y + (int64_t)cl * cell_slots + row_start(w, j0, k);
+    double* __restrict__ pyp = y + (int64_t)cl * cell_slots + row_start(w, j0, k + 1);
+    const int pmin = blk == 0 ? 3 : 0;        // layer k+1 rows shorter than 3 belong to the general kernel
     int j = j0;
 
-    // One step: output row j at columns c0 (s0) and c1 (s1).
-    // cur: A(j), B(j-1), C(j); am1: A(j-1); staged rows A1 = A(j+1), B0 = B(j),
-    // C1 = C(j+1). kStencilDirs pairs (d, d + 7):
-    //   (1,0,0)/(-1,0,0)  A(j) i+1 / i-1         (0,1,0)/(0,-1,0)  A(j+1) / A(j-1)
-    //   (0,0,1)/(0,0,-1)  B(j) / C(j)            (1,-1,0)/(-1,1,0) A(j-1) i+1 / A(j+1) i-1
-    //   (1,0,-1)/(-1,0,1) C(j) i+1 / B(j) i-1    (0,1,-1)/(0,-1,1) C(j+1) / B(j-1)
-    //   (1,-1,1)/(-1,1,-1) B(j-1) i+1 / C(j+1) i-1
+    // One layer's output row at columns c0 (s0) and c1 (s1) from its window:
+    // cur = (a = row j, b = upper layer row j-1, c = lower layer row j),
+    // am1 = row j-1, staged A1 = row j+1, B0 = upper row j, C1 = lower row j+1.
+    // kStencilDirs pairs (d, d + 7):
+    //   (1,0,0)/(-1,0,0)  a i+1 / i-1            (0,1,0)/(0,-1,0)  A1 / am1
+    //   (0,0,1)/(0,0,-1)  B0 / c                 (1,-1,0)/(-1,1,0) am1 i+1 / A1 i-1
+    //   (1,0,-1)/(-1,0,1) c i+1 / B0 i-1         (0,1,-1)/(0,-1,1) C1 / b
+    //   (1,-1,1)/(-1,1,-1) b i+1 / C1 i-1
     // Column c0 reads fields (v, r, l) = (v0, v1, l0); column c1 (v1, r1, v0).
-  // two independent accumulation chains per column (latency, not order,
-  // bounds the chain: the fast path is within the 1e-12 parity tolerance)
-#define BT_INTERIOR(cur, am1, s, v, r, l)                                                           \
-  double s = W[0] * cur.a.v;                                                                        \
-  double s##b = W[1] * (cur.a.r + cur.a.l);                                                         \
+    // Two independent accumulation chains per column (latency, not order,
+    // bounds the chain: the fast path is within the 1e-12 parity tolerance).
+#define BT_INTERIOR(a, b, c, am1, A1, B0, C1, s, v, r, l)                                           \
+  double s = W[0] * a.v;                                                                            \
+  double s##b_ = W[1] * (a.r + a.l);                                                                \
   s = fma(W[2], A1.v + am1.v, s);                                                                   \
-  s##b = fma(W[3], B0.v + cur.c.v, s##b);                                                           \
+  s##b_ = fma(W[3], B0.v + c.v, s##b_);                                                             \
   s = fma(W[4], am1.r + A1.l, s);                                                                   \
-  s##b = fma(W[5], cur.c.r + B0.l, s##b);                                                           \
-  s = fma(W[6], C1.v + cur.b.v, s);                                                                 \
-  s##b = fma(W[7], cur.b.r + C1.l, s##b);                                                           \
-  s += s##b;
-    // typed rows over present neighbours (kDiagPresent / kI0Present order)
-#define BT_DIAG(cur, am1, v, r, l)                                                                  \
-  (DG[0] * cur.a.v + DG[1] * am1.r + DG[2] * cur.c.r + DG[3] * C1.v + DG[4] * cur.a.l +             \
-   DG[5] * am1.v + DG[6] * cur.c.v + DG[7] * A1.l + DG[8] * B0.l + DG[9] * cur.b.v + DG[10] * C1.l)
-#define BT_FACE0(cur, am1, v, r, l)                                                                 \
-  (F0[0] * cur.a.v + F0[1] * cur.a.r + F0[2] * A1.v + F0[3] * B0.v + F0[4] * am1.r +                \
-   F0[5] * cur.c.r + F0[6] * C1.v + F0[7] * cur.b.r + F0[8] * am1.v + F0[9] * cur.c.v +             \
-   F0[10] * cur.b.v)
-#define BT_STEP(cur, nxt, am1, am1n)                                                                \
+  s##b_ = fma(W[5], c.r + B0.l, s##b_);                                                             \
+  s = fma(W[6], C1.v + b.v, s);                                                                     \
+  s##b_ = fma(W[7], b.r + C1.l, s##b_);                                                             \
+  s += s##b_;
+#define BT_LAYER(a, b, c, am1, A1, B0, C1, LY, py, ok)                                              \
   {                                                                                                 \
-    Row4 A1, B0, C1;                                                                                \
-    consume(A1, B0, C1);                                                                            \
-    BT_INTERIOR(cur, am1, s0, v0, v1, l0)                                                           \
-    BT_INTERIOR(cur, am1, s1, v1, r1, v0)                                                           \
-    if (LY <= colend) { /* the diagonal-face vertex is in this warp */                              \
-      if (c0 == LY - 1) s0 = BT_DIAG(cur, am1, v0, v1, l0);                                         \
-      if (c1 == LY - 1) s1 = BT_DIAG(cur, am1, v1, r1, v0);                                         \
-    }                                                                                               \
-    if (blk0 && c0 == 0) s0 = BT_FACE0(cur, am1, v0, v1, l0); /* lane 1 of block 0 */               \
-    if (out && c0 < LY) py[c0] = s0;                                                                \
-    if (out && c1 < LY) py[c1] = s1;                                                                \
-    py += LY;                                                                                       \
-    --LY;                                                                                           \
+    BT_INTERIOR(a, b, c, am1, A1, B0, C1, s0, v0, v1, l0)                                           \
+    BT_INTERIOR(a, b, c, am1, A1, B0, C1, s1, v1, r1, v0)                                           \
+    /* row ends (i = 0, i = LY - 1) are k_stencil_ends' */                                          \
+    if (ok && out && c0 < LY - 1 && c0 > 0) py[c0] = s0;                                            \
+    if (ok && out && c1 < LY - 1) py[c1] = s1;                                                      \
+  }
+#define BT_STEP(cur, nxt)                                                                           \
+  {                                                                                                 \
+    Row4 A1, P1, C1, Q0;                                                                            \
+    consume(A1, P1, C1, Q0);                                                                        \
+    BT_LAYER(cur.a, cur.pm1, cur.c, cur.am1, A1, cur.p, C1, LA, pya, true)                          \
+    BT_LAYER(cur.p, cur.qm1, cur.a, cur.pm1, P1, Q0, A1, LA - 1, pyp, LA - 1 >= pmin)               \
+    pya += LA;                                                                                      \
+    pyp += LA - 1;                                                                                  \
+    --LA;                                                                                           \
     ++j;                                                                                            \
-    am1n = cur.a;                                                                                   \
+    nxt.am1 = cur.a;                                                                                \
     nxt.a = A1;                                                                                     \
-    nxt.b = B0;                                                                                     \
+    nxt.pm1 = cur.p;                                                                                \
+    nxt.p = P1;                                                                                     \
     nxt.c = C1;                                                                                     \
+    nxt.qm1 = Q0;                                                                                   \
   }
     while (true) {
-      BT_STEP(X, Y, Am1, Am1y)
+      BT_STEP(X, Y)
       if (j >= j1) break;
-      BT_STEP(Y, X, Am1y, Am1)
+      BT_STEP(Y, X)
       if (j >= j1) break;
     }
 #undef BT_STEP
-#undef BT_FACE0
-#undef BT_DIAG
+#undef BT_LAYER
 #undef BT_INTERIOR
   }
   cp_wait<0>();
+}
+
+// Both ends of every fast row (1 <= k <= n-2, j >= 1, length L >= 3): the
+// i = 0 vertex (zero set {i = 0}) and the diagonal-face vertex i = L - 1
+// (zero set {S = n}), each from its typed partial row over its 11 present
+// neighbours (per-cell part of partial_row_apply, operators.hpp:78-96). One
+// thread per row; rows of a layer are consecutive threads, whose end vertices
+// are each other's neighbours, so most loads hit L1.
+__global__ void __launch_bounds__(128) k_stencil_ends(const double* __restrict__ x, double* __restrict__ y,
+                                                      const double* __restrict__ ends, int w, int64_t cell_slots,
+                                                      int cell0) {
+  const int n = w - 1;
+  const int k = blockIdx.y + 1, j = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (j > n - 2 - k) return;  // L = w - k - j >= 3
+  const int cell = cell0 + blockIdx.z;
+  const double* __restrict__ e = ends + 22 * (size_t)cell;  // [0, 11): diagonal face, [11, 22): i = 0
+  const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
+  double* __restrict__ yc = y + (int64_t)cell * cell_slots;
+  int off[15];
+  row_offsets(w, j, k, off);
+  const int t0 = row_start(w, j, k), tL = t0 + (w - k - j) - 1;
+  constexpr int dp[11] = {0, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14};  // kDiagPresent
+  constexpr int ip[11] = {0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 13};     // kI0Present
+  double sd = 0.0, s0 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 11; ++q) {
+    sd = fma(__ldg(e + q), __ldg(xc + tL + off[dp[q]]), sd);
+    s0 = fma(__ldg(e + 11 + q), __ldg(xc + t0 + off[ip[q]]), s0);
+  }
+  yc[tL] = sd;
+  yc[t0] = s0;
 }
 
 // Any rows of the march schedule, every row read from the zero-set-typed
 // table in shared memory (interior vertices use type 0 = the merged row).
 // Block row y works on cell cell0 + y. With per_cell (nullable) its tasks are
 // tasks[per_cell[y] .. per_cell[y + 1]); otherwise every cell runs all ntasks.
-__global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict__ x, double* __restrict__ y,
+__global__ void __launch_bounds__(kGT, 9) k_stencil_general(const double* __restrict__ x, double* __restrict__ y,
                                                         const StencilCell* __restrict__ cells,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
                                                         int64_t cell_slots, const int* __restrict__ per_cell,
@@ -275,10 +324,10 @@ __global__ void __launch_bounds__(kT) k_stencil_general(const double* __restrict
   __shared__ double sw[16][15];
   const int cell = cell0 + blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int task = blockIdx.x * kW + warp;
+  int task = blockIdx.x * kGW + warp;
   if (per_cell) {
     const int first = per_cell[blockIdx.y], last = per_cell[blockIdx.y + 1];  // partition-local cell
-    if (first + (int)blockIdx.x * kW >= last) return;  // whole block idle
+    if (first + (int)blockIdx.x * kGW >= last) return;  // whole block idle
     task += first;
     ntasks = last;
   }
@@ -341,10 +390,11 @@ void init_stencil_tasks(bt_stencil& st) {
         if (b == 0) push1(gen, k, b, std::max(1, w - k - 2), jmax);
       }
     }
-    if (!fast_layer) continue;
+    // fast marches cover layer pairs (k, k + 1), k odd (n - 2 fast layers, n = 2^l even)
+    if (!fast_layer || (k & 1) == 0) continue;
     for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (60 wide)
       const int jmax = w - k - kFastCols * b;
-      const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;
+      const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;  // layer k's fast rows
       for (int j0 = 1; j0 < fe; j0 += kMarchRows) fast.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, fe)));
     }
   }
@@ -367,12 +417,17 @@ void init_stencil_tasks(bt_stencil& st) {
       for (int c = 0; c < cnt; ++c) {
         const int64_t cb = (int64_t)(c0 + c) * cs + kFastCols * t.y;
         const int64_t lo = cb + row_start(w, t.z - 1, t.x - 1) - 2;  // C(j0 - 1), column base - 2
-        const int64_t hi = cb + row_start(w, t.w - 1, t.x + 1) + 61;  // B(j1 - 1), column base + 61
+        const int64_t hi = cb + row_start(w, t.w - 1, t.x + 2) + 61;  // Q(j1 - 1), column base + 61
         if (lo >= 0 && hi < total) {
           all_fast.push_back(make_int4(t.x, t.y | (c << 16), t.z, t.w));
         } else {
+          // the march's rows of both layers (layer k + 1 only where they are fast rows)
+          const int k = t.x, pe = t.y == 0 ? w - k - 3 : w - k - 1 - kFastCols * t.y;
           for (int gb = 2 * t.y; gb < 2 * t.y + 2; ++gb)
-            for (int j = t.z; j < t.w && kGenCols * gb < w - t.x - j; ++j) extra[c0 + c].push_back(make_int4(t.x, gb, j, j + 1));
+            for (int j = t.z; j < t.w; ++j) {
+              if (kGenCols * gb < w - k - j) extra[c0 + c].push_back(make_int4(k, gb, j, j + 1));
+              if (j < pe && kGenCols * gb < w - k - 1 - j) extra[c0 + c].push_back(make_int4(k + 1, gb, j, j + 1));
+            }
         }
       }
   }
@@ -400,7 +455,8 @@ void init_stencil_tasks(bt_stencil& st) {
   const int nc = st.grid->mesh.n_cells();
   std::vector<StencilCell> cells(nc);
   BT_CUDA(cudaMemcpy(cells.data(), st.d_cells.p, sizeof(StencilCell) * nc, cudaMemcpyDeviceToHost));
-  st.fast.assign(30 * (size_t)nc, 0.0);
+  st.fast.assign(8 * (size_t)nc, 0.0);
+  std::vector<double> ends(22 * (size_t)nc, 0.0);
   for (int c = 0; c < nc; ++c) {
     const auto& rw = st.rows[c];
     for (int d = 1; d <= 7; ++d) st.symmetric = st.symmetric && rw[d] == rw[d + 7];
@@ -412,14 +468,35 @@ void init_stencil_tasks(bt_stencil& st) {
       }
       if ((!pd && cells[c].w[1][d] != 0.0) || (!pi && cells[c].w[2][d] != 0.0)) st.symmetric = false;
     }
-    double* f = &st.fast[30 * (size_t)c];
+    double* f = &st.fast[8 * (size_t)c];
     for (int d = 0; d < 8; ++d) f[d] = rw[d];
     for (int q = 0; q < 11; ++q) {
-      f[8 + q] = cells[c].w[1][kDiagPresent[q]];
-      f[19 + q] = cells[c].w[2][kI0Present[q]];
+      ends[22 * (size_t)c + q] = cells[c].w[1][kDiagPresent[q]];
+      ends[22 * (size_t)c + 11 + q] = cells[c].w[2][kI0Present[q]];
     }
   }
+  st.d_ends.upload(ends);
 }
+
+namespace {
+// side stream (per device) and fork/join events for the small kernels
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  static SideStream ss[16];
+  int dev = 0;
+  BT_CUDA(cudaGetDevice(&dev));
+  SideStream& r = ss[dev & 15];
+  if (!r.s) {
+    BT_CUDA(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
+    BT_CUDA(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
+    BT_CUDA(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
+  }
+  return r;
+}
+}  // namespace
 
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
   const int w = (1 << st.level) + 1;
@@ -429,31 +506,25 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
   const int c0 = st.part_begin, nc = st.part_end - st.part_begin;  // this handle's cells
   if (!nc) return;
   if (!st.symmetric) {
-    k_stencil_general<<<dim3((st.natasks + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
-                                                                          st.natasks, w, cs, nullptr, c0);
+    k_stencil_general<<<dim3((st.natasks + kGW - 1) / kGW, nc), kGT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
+                                                                            st.natasks, w, cs, nullptr, c0);
     count_launch();
     check_launch("k_stencil_general");
     return;
   }
-  if (st.ngtasks) {
-    k_stencil_general<<<dim3((st.ngtasks + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_gtasks.p,
-                                                                          st.ngtasks, w, cs, nullptr, c0);
-    count_launch();
-  }
-  if (st.nxtasks) {
-    k_stencil_general<<<dim3((st.xtask_max + kW - 1) / kW, nc), kT, 0, s>>>(x, y, st.d_cells.p, st.d_xtasks.p,
-                                                                            st.nxtasks, w, cs, st.d_xoff.p, c0);
-    count_launch();
-  }
+  // fast rows on s; row ends and general rows on the side stream, overlapping
+  // the (latency-bound, persistent) fast kernel on the SMs' spare slots
+  SideStream& ss = side_stream();
+  BT_CUDA(cudaEventRecord(ss.fork, s));
   static FastParams<kMaxCells> fp;
-  const size_t smem = sizeof(double) * kW * kRingD;
+  const size_t smem = sizeof(double) * kFW * kRingD;
   static int grid = 0;
   if (!grid) {
     BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per_sm = 0;
     BT_CUDA(cudaGetDevice(&dev));
     BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kT, smem));
+    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kFT, smem));
     grid = sms * std::max(1, per_sm);
   }
   for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
@@ -461,18 +532,32 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
     if (!nt) continue;
     for (int c = 0; c < cnt; ++c) {
-      const double* f = &st.fast[30 * (size_t)(cc0 + c)];
+      const double* f = &st.fast[8 * (size_t)(cc0 + c)];
       for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
-      for (int q = 0; q < 11; ++q) {
-        fp.dg[c][q] = f[8 + q];
-        fp.f0[c][q] = f[19 + q];
-      }
     }
     const int64_t e0 = (int64_t)cc0 * cs;
-    const int blocks = std::min(grid, (nt + kW - 1) / kW);
-    k_stencil_fast<kMaxCells><<<blocks, kT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
+    const int blocks = std::min(grid, (nt + kFW - 1) / kFW);
+    k_stencil_fast<kMaxCells><<<blocks, kFT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
     count_launch();
   }
+  BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  if (w - 1 >= 4) {
+    const int n = w - 1;
+    k_stencil_ends<<<dim3((n - 3 + 127) / 128, n - 3, nc), 128, 0, ss.s>>>(x, y, st.d_ends.p, w, cs, c0);
+    count_launch();
+  }
+  if (st.ngtasks) {
+    k_stencil_general<<<dim3((st.ngtasks + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(x, y, st.d_cells.p, st.d_gtasks.p,
+                                                                               st.ngtasks, w, cs, nullptr, c0);
+    count_launch();
+  }
+  if (st.nxtasks) {
+    k_stencil_general<<<dim3((st.xtask_max + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(
+        x, y, st.d_cells.p, st.d_xtasks.p, st.nxtasks, w, cs, st.d_xoff.p, c0);
+    count_launch();
+  }
+  BT_CUDA(cudaEventRecord(ss.join, ss.s));
+  BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
   check_launch("k_stencil");
 }
 
