@@ -284,7 +284,13 @@ void launch_xchg_pack(const bt_grid& g, int level, const double* x, double* buf,
 void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x, const double* src,
                          const double* buf, cudaStream_t s);
 void partition_range(int nc, int rank, int nranks, int& begin, int& end);
+// per-cell rows only (no replica sums): interior + row ends + general rows
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s);
+// the whole apply_stencil (replica sums and, bc != 0, Dirichlet identity rows
+// included): interior kernel and fused boundary kernel run concurrently.
+// Available when stencil_fused(st): symmetric tables on an unpartitioned grid.
+bool stencil_fused(const bt_stencil& st);
+void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s);
 void init_stencil_tasks(bt_stencil& st);
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c,
                         const EwCell* d_cells, const EwAngles* d_angles, const double* x, double* y,

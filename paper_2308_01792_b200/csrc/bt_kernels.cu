@@ -517,6 +517,10 @@ bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   cudaStream_t s = (cudaStream_t)stream;
+  if (stencil_fused(*st)) {
+    launch_stencil_fused(*st, x, y, bc, s);
+    return BT_OK;
+  }
   launch_stencil(*st, x, y, s);
   launch_interface(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
   BT_CATCH

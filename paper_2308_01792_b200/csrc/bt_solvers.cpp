@@ -42,6 +42,10 @@ namespace bt {
 static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int bc, cudaStream_t s) {
   LevelData& L = h.at(l);
   if (h.kernel == 1) {
+    if (stencil_fused(*L.stencil)) {
+      launch_stencil_fused(*L.stencil, x, y, bc, s);  // interior and boundary (incl. sync, Dirichlet rows)
+      return;
+    }
     launch_stencil(*L.stencil, x, y, s);
   } else {
     const int ck = h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.coeff_kind : 0;

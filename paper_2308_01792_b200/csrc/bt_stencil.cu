@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -312,6 +313,123 @@ __global__ void __launch_bounds__(128) k_stencil_ends(const double* __restrict__
   yc[t0] = s0;
 }
 
+// Fused boundary pass of apply_stencil (operators.hpp:247-271 with
+// sync_additive fe_function.hpp:400-423 and the Dirichlet identity rows):
+// every lattice point on a macro face, edge or vertex is computed once per
+// interface group. For each member cell (ascending cell order) the point's
+// per-cell partial row — the zero-set-typed row over the cell's micro-tets
+// containing it (partial_row_apply, operators.hpp:78-96) — is evaluated from
+// that cell's x; the partials are summed from 0.0 in member order, exactly
+// the replica sum sync_additive forms from per-cell results, and the sum (or
+// x on Dirichlet groups under BC::DirichletIdentity) is written to every
+// replica. No dependency on the interior kernel: the two run concurrently.
+struct BndArgs {
+  const DevFace* faces;
+  const DevPrimHdr* eh;
+  const DevPrimMem* em;
+  const DevPrimHdr* vh;
+  const DevPrimMem* vm;
+  const StencilCell* cells;
+  int nf, ne, nv, n;
+  int64_t cs;
+};
+
+__device__ __forceinline__ void bary_ijk(const int8_t* lv, int nl, const int* wt, int& i, int& j, int& k) {
+  i = j = k = 0;
+  for (int q = 0; q < nl; ++q) {
+    if (lv[q] == 1) i += wt[q];
+    if (lv[q] == 2) j += wt[q];
+    if (lv[q] == 3) k += wt[q];
+  }
+}
+
+// per-cell partial row at lattice point (i, j, k) of `cell`; returns its slot
+__device__ __forceinline__ double typed_partial(const double* __restrict__ x, const BndArgs& a, int cell, int i,
+                                                int j, int k, int64_t& slot) {
+  const int w = a.n + 1;
+  const int z = zero_set(a.n, i, j, k);
+  const StencilCell& sc = a.cells[cell];
+  const uint32_t mask = __ldg(&sc.mask[z]);
+  slot = (int64_t)cell * a.cs + row_start(w, j, k) + i;
+  const double* __restrict__ xc = x + slot;
+  int off[15];
+  row_offsets(w, j, k, off);
+  double acc = __ldg(&sc.w[z][0]) * __ldg(xc);
+#pragma unroll
+  for (int d = 1; d < 15; ++d) {
+    const double v = (mask >> d) & 1 ? __ldg(xc + off[d]) : 0.0;
+    acc = fma(__ldg(&sc.w[z][d]), v, acc);
+  }
+  return acc;
+}
+
+template <bool kDir>
+__global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, double* __restrict__ y, BndArgs a) {
+  const int n = a.n, w = n + 1;
+  const int fpts = tri32(n - 2);
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // the group: members as (cell, local-vertex map), barycentric weights
+  int count, dir, nl;
+  int wt[3];
+  const DevFace* F = nullptr;
+  const DevPrimMem* mem = nullptr;
+  if (q < (int64_t)a.nf * fpts) {  // face-interior point (a, b), weights (n - a - b, a, b)
+    F = a.faces + q / fpts;
+    int ap, bp;
+    decode_tri(n - 2, (int)(q % fpts), ap, bp);
+    wt[0] = n - (ap + 1) - (bp + 1);
+    wt[1] = ap + 1;
+    wt[2] = bp + 1;
+    count = F->ncell;
+    dir = F->dir;
+    nl = 3;
+  } else {
+    q -= (int64_t)a.nf * fpts;
+    DevPrimHdr h;
+    if (q < (int64_t)a.ne * (n - 1)) {  // macro-edge point a = 1..n-1, weights (n - a, a)
+      h = a.eh[q / (n - 1)];
+      mem = a.em + h.first;
+      wt[1] = (int)(q % (n - 1)) + 1;
+      wt[0] = n - wt[1];
+      nl = 2;
+    } else {  // macro vertex
+      q -= (int64_t)a.ne * (n - 1);
+      if (q >= a.nv) return;
+      h = a.vh[q];
+      mem = a.vm + h.first;
+      wt[0] = n;
+      nl = 1;
+    }
+    count = h.count;
+    dir = h.dir;
+  }
+  auto member = [&](int m, int& cell, int& i, int& j, int& k) {
+    if (F) {
+      cell = F->cell[m];
+      bary_ijk(F->lv[m], 3, wt, i, j, k);
+    } else {
+      const DevPrimMem pm = mem[m];
+      cell = pm.cell;
+      bary_ijk(pm.lv, nl, wt, i, j, k);
+    }
+  };
+  double sum = 0.0, single = 0.0;
+  for (int m = 0; m < count; ++m) {
+    int cell, i, j, k;
+    member(m, cell, i, j, k);
+    int64_t slot;
+    single = typed_partial(x, a, cell, i, j, k, slot);
+    sum += single;
+  }
+  if (count < 2) sum = single;  // no replicas: sync_additive leaves the value alone
+  for (int m = 0; m < count; ++m) {
+    int cell, i, j, k;
+    member(m, cell, i, j, k);
+    const int64_t slot = (int64_t)cell * a.cs + row_start(w, j, k) + i;
+    y[slot] = (kDir && dir) ? __ldg(x + slot) : sum;
+  }
+}
+
 // Any rows of the march schedule, every row read from the zero-set-typed
 // table in shared memory (interior vertices use type 0 = the merged row).
 // Block row y works on cell cell0 + y. With per_cell (nullable) its tasks are
@@ -513,7 +631,12 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     return;
   }
   // fast rows on s; row ends and general rows on the side stream, overlapping
-  // the (latency-bound, persistent) fast kernel on the SMs' spare slots
+  // the (latency-bound, persistent) fast kernel on the SMs' spare slots.
+  // BT_STENCIL_PARTS (profiling only: bit 0 fast, 1 ends, 2 general) drops parts.
+  static const int parts = [] {
+    const char* e = std::getenv("BT_STENCIL_PARTS");
+    return e ? std::atoi(e) : 7;
+  }();
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
   static FastParams<kMaxCells> fp;
@@ -527,7 +650,7 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kFT, smem));
     grid = sms * std::max(1, per_sm);
   }
-  for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
+  for (int ch = 0; (parts & 1) && ch + 1 < (int)st.chunk_first.size(); ++ch) {
     const int cc0 = c0 + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
     const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
     if (!nt) continue;
@@ -541,17 +664,17 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     count_launch();
   }
   BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-  if (w - 1 >= 4) {
+  if ((parts & 2) && w - 1 >= 4) {
     const int n = w - 1;
     k_stencil_ends<<<dim3((n - 3 + 127) / 128, n - 3, nc), 128, 0, ss.s>>>(x, y, st.d_ends.p, w, cs, c0);
     count_launch();
   }
-  if (st.ngtasks) {
+  if ((parts & 4) && st.ngtasks) {
     k_stencil_general<<<dim3((st.ngtasks + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(x, y, st.d_cells.p, st.d_gtasks.p,
                                                                                st.ngtasks, w, cs, nullptr, c0);
     count_launch();
   }
-  if (st.nxtasks) {
+  if ((parts & 4) && st.nxtasks) {
     k_stencil_general<<<dim3((st.xtask_max + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(
         x, y, st.d_cells.p, st.d_xtasks.p, st.nxtasks, w, cs, st.d_xoff.p, c0);
     count_launch();
@@ -559,6 +682,70 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
   BT_CUDA(cudaEventRecord(ss.join, ss.s));
   BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
   check_launch("k_stencil");
+}
+
+bool stencil_fused(const bt_stencil& st) {
+  return st.symmetric && st.grid->part_nranks == 1;
+}
+
+// fast kernel launches (interior rows) for this handle's cells, on stream s
+static void launch_fast(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
+  const int w = (1 << st.level) + 1;
+  const int64_t cs = n_tet(w);
+  static FastParams<kMaxCells> fp;
+  const size_t smem = sizeof(double) * kFW * kRingD;
+  static int grid = 0;
+  if (!grid) {
+    BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 0, per_sm = 0;
+    BT_CUDA(cudaGetDevice(&dev));
+    BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kFT, smem));
+    grid = sms * std::max(1, per_sm);
+  }
+  for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
+    const int cc0 = st.part_begin + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
+    const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
+    if (!nt) continue;
+    for (int c = 0; c < cnt; ++c) {
+      const double* f = &st.fast[8 * (size_t)(cc0 + c)];
+      for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
+    }
+    const int64_t e0 = (int64_t)cc0 * cs;
+    const int blocks = std::min(grid, (nt + kFW - 1) / kFW);
+    k_stencil_fast<kMaxCells><<<blocks, kFT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
+    count_launch();
+  }
+}
+
+void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s) {
+  const bt_grid& g = *st.grid;
+  const int n = 1 << st.level;
+  SideStream& ss = side_stream();
+  BT_CUDA(cudaEventRecord(ss.fork, s));
+  launch_fast(st, x, y, s);  // first, so its persistent blocks are resident first
+  BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
+            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, n_tet(n + 1)};
+  // interior rows of the marches the host kept off the fast kernel (they
+  // would stage outside x) — whole rows; the boundary kernel, next on the
+  // same stream, then writes the final values of their end points
+  if (st.nxtasks) {
+    const int w = n + 1, nc = st.part_end - st.part_begin;
+    k_stencil_general<<<dim3((st.xtask_max + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(
+        x, y, st.d_cells.p, st.d_xtasks.p, st.nxtasks, w, n_tet(w), st.d_xoff.p, st.part_begin);
+    count_launch();
+  }
+  const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
+  const unsigned blocks = (unsigned)((pts + 127) / 128);
+  if (bc)
+    k_boundary<true><<<blocks, 128, 0, ss.s>>>(x, y, a);
+  else
+    k_boundary<false><<<blocks, 128, 0, ss.s>>>(x, y, a);
+  count_launch();
+  BT_CUDA(cudaEventRecord(ss.join, ss.s));
+  BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
+  check_launch("k_stencil_fused");
 }
 
 }  // namespace bt
