@@ -520,7 +520,15 @@ void init_stencil_tasks(bt_stencil& st) {
   // parameter table); longest marches first. A march whose staged columns
   // would leave x (cell 0's first rows, the last cell's top layers) runs on
   // the general kernel instead, as single-row tasks of that cell.
-  std::stable_sort(fast.begin(), fast.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
+  // Task order (BT_STENCIL_ORDER, profiling): 1 = longest march first, cells
+  // interleaved (default: best balance); 0 = spatial, cells outermost (better
+  // L2 reuse of staged rows, but a longer tail: measured slower).
+  static const int order = [] {
+    const char* e = std::getenv("BT_STENCIL_ORDER");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (order == 1)
+    std::stable_sort(fast.begin(), fast.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
   const int nc_all = st.grid->mesh.n_cells();
   const int64_t cs = n_tet(w), total = cs * nc_all;
   st.part_begin = st.grid->part_begin;
@@ -531,8 +539,12 @@ void init_stencil_tasks(bt_stencil& st) {
   for (int c0 = st.part_begin; c0 < st.part_end; c0 += kMaxCells) {
     st.chunk_first.push_back((int)all_fast.size());
     const int cnt = std::min(kMaxCells, st.part_end - c0);
-    for (const int4& t : fast)
-      for (int c = 0; c < cnt; ++c) {
+    // spatial order walks cells outermost (a cell's x + y fits the 126 MB L2)
+    const int64_t ntc = (int64_t)fast.size() * cnt;
+    for (int64_t q = 0; q < ntc; ++q) {
+      const int c = order == 1 ? (int)(q % cnt) : (int)(q / (int64_t)fast.size());
+      const int4& t = fast[order == 1 ? (size_t)(q / cnt) : (size_t)(q % (int64_t)fast.size())];
+      {
         const int64_t cb = (int64_t)(c0 + c) * cs + kFastCols * t.y;
         const int64_t lo = cb + row_start(w, t.z - 1, t.x - 1) - 2;  // C(j0 - 1), column base - 2
         const int64_t hi = cb + row_start(w, t.w - 1, t.x + 2) + 61;  // Q(j1 - 1), column base + 61
@@ -548,6 +560,7 @@ void init_stencil_tasks(bt_stencil& st) {
             }
         }
       }
+    }
   }
   st.chunk_first.push_back((int)all_fast.size());
   st.ntasks = (int)all_fast.size();
@@ -616,6 +629,16 @@ SideStream& side_stream() {
 }
 }  // namespace
 
+// BT_STENCIL_PARTS (profiling only) drops parts of an apply: bit 0 interior
+// kernel, 1 row ends, 2 general rows, 3 fused boundary kernel.
+static int stencil_parts() {
+  static const int parts = [] {
+    const char* e = std::getenv("BT_STENCIL_PARTS");
+    return e ? std::atoi(e) : 15;
+  }();
+  return parts;
+}
+
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
   const int w = (1 << st.level) + 1;
   const int64_t cs = n_tet(w);
@@ -631,12 +654,8 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     return;
   }
   // fast rows on s; row ends and general rows on the side stream, overlapping
-  // the (latency-bound, persistent) fast kernel on the SMs' spare slots.
-  // BT_STENCIL_PARTS (profiling only: bit 0 fast, 1 ends, 2 general) drops parts.
-  static const int parts = [] {
-    const char* e = std::getenv("BT_STENCIL_PARTS");
-    return e ? std::atoi(e) : 7;
-  }();
+  // the (latency-bound, persistent) fast kernel on the SMs' spare slots
+  const int parts = stencil_parts();
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
   static FastParams<kMaxCells> fp;
@@ -721,9 +740,16 @@ static void launch_fast(const bt_stencil& st, const double* x, double* y, cudaSt
 void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s) {
   const bt_grid& g = *st.grid;
   const int n = 1 << st.level;
+  const int parts = stencil_parts();
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
-  launch_fast(st, x, y, s);  // first, so its persistent blocks are resident first
+  if (parts & 1) launch_fast(st, x, y, s);  // first, so its persistent blocks are resident first
+  if (!(parts & 8)) {
+    BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+    BT_CUDA(cudaEventRecord(ss.join, ss.s));
+    BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
+    return;
+  }
   BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
   BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
             (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, n_tet(n + 1)};
