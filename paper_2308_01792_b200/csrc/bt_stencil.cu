@@ -83,16 +83,16 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-struct Row4 {  // one row at a lane's columns (c0, c1 = c0 + 1): l0 = c0 - 1, r1 = c1 + 1
-  double l0, v0, v1, r1;
+struct Row2 {  // one row at a lane's columns c0, c1 = c0 + 1
+  double v0, v1;
 };
 // Register window of a two-layer march at row j: layers k-1 (C), k (A),
 // k+1 (P), k+2 (Q).
 struct Win {
-  Row4 am1, a;  // A(j-1), A(j)
-  Row4 pm1, p;  // P(j-1), P(j)
-  Row4 c;       // C(j)
-  Row4 qm1;     // Q(j-1)
+  Row2 am1, a;  // A(j-1), A(j)
+  Row2 pm1, p;  // P(j-1), P(j)
+  Row2 c;       // C(j)
+  Row2 qm1;     // Q(j-1)
 };
 
 // Task word: x = k (first layer of the pair k, k+1), y = column block |
@@ -116,7 +116,7 @@ struct Win {
 // 16-byte shared load. The host keeps marches that would stage outside x on
 // the general kernel.
 template <int kMaxC>
-__global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
+__global__ void __launch_bounds__(kFT, 4) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
                                                         int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
   extern __shared__ __align__(128) double ring_all[];
@@ -131,13 +131,14 @@ __global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restric
   // element offsets (within the cell) of column base - 2 + lane in rows
   // A(j+1), P(j+1), C(j+1), Q(j) of the producer's next step j;
   // r = len(A(j+1)) = len(P(j)); pleft = steps left in the producer's task
-  int pt = t0, pA = 0, pP = 0, pC = 0, pQ = 0, pr = 0, pleft = 0;
+  int pt = t0, pA = 0, pP = 0, pC = 0, pQ = 0, pr = 0, pleft = 0, pcol = 0;
   const double* pcell = x;
   int4 pnext = tasks[t0];
   auto p_start = [&]() {
     const int4 tk = pnext;
     const int k = tk.x, base = kFastCols * (tk.y & 0xffff), cl = tk.y >> 16;
     const int j = tk.z - 2, cb = base - 2 + lane;
+    pcol = cb;  // this lane's first staged column (the second is pcol + 32)
     pcell = x + (int64_t)cl * cell_slots;
     pA = cb + row_start(w, j + 1, k);
     pP = cb + row_start(w, j + 1, k + 1);
@@ -153,14 +154,17 @@ __global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restric
     if (pleft > 0) {
       const uint32_t d = my_s + (uint32_t)(ps * kStageD * 8);
       const double *a = pcell + pA, *p = pcell + pP, *c = pcell + pC, *q = pcell + pQ;
-      cp8(d, a);
-      cp8(d + 256, a + 32);
-      cp8(d + kRowD * 8, p);
-      cp8(d + kRowD * 8 + 256, p + 32);
-      cp8(d + 2 * kRowD * 8, c);
-      cp8(d + 2 * kRowD * 8 + 256, c + 32);
-      cp8(d + 3 * kRowD * 8, q);
-      cp8(d + 3 * kRowD * 8 + 256, q + 32);
+      // columns past a row's end are never used: those lanes skip the copy
+      // (row lengths: A(j+1) pr, P(j+1) and Q(j) pr - 1, C(j+1) pr + 1)
+      const int c1 = pcol + 32;
+      if (pcol < pr) cp8(d, a);
+      if (c1 < pr) cp8(d + 256, a + 32);
+      if (pcol < pr - 1) cp8(d + kRowD * 8, p);
+      if (c1 < pr - 1) cp8(d + kRowD * 8 + 256, p + 32);
+      if (pcol <= pr) cp8(d + 2 * kRowD * 8, c);
+      if (c1 <= pr) cp8(d + 2 * kRowD * 8 + 256, c + 32);
+      if (pcol < pr - 1) cp8(d + 3 * kRowD * 8, q);
+      if (c1 < pr - 1) cp8(d + 3 * kRowD * 8 + 256, q + 32);
       ps = ps == kStages - 1 ? 0 : ps + 1;
       // next rows: A(j+2) = A(j+1) + len(A(j+1)); P(j+2) = P(j+1) + len(P(j+1));
       // C(j+2) = C(j+1) + len(C(j+1)); Q(j+1) = Q(j) + len(Q(j))
@@ -181,14 +185,12 @@ __global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restric
 
   // ---- consumer ----
   int cs = 0;
-  auto read_row = [&](const double* row, Row4& o) {
+  auto read_row = [&](const double* row, Row2& o) {
     const double2 v = reinterpret_cast<const double2*>(row)[lane];
     o.v0 = v.x;
     o.v1 = v.y;
-    o.l0 = __shfl_up_sync(0xffffffffu, v.y, 1);
-    o.r1 = __shfl_down_sync(0xffffffffu, v.x, 1);
   };
-  auto consume = [&](Row4& A1, Row4& P1, Row4& C1, Row4& Q0) {
+  auto consume = [&](Row2& A1, Row2& P1, Row2& C1, Row2& Q0) {
     cp_wait<kStages - 2>();
     __syncwarp();
     const double* st = ring + cs * kStageD;
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restric
     read_row(st + 3 * kRowD, Q0);
     cs = cs == kStages - 1 ? 0 : cs + 1;
     // the stage refilled next is the one every lane read in the previous
-    // step (its values went through the warp-synchronous shuffles)
+    // step, which the __syncwarp above orders before this refill
     produce();
   };
 
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restric
     const int c0 = base - 2 + 2 * lane, c1 = c0 + 1;  // this lane's two columns
     const bool out = lane >= 1 && lane <= 30;
     Win X, Y;
-    Row4 junk0, junk1;
+    Row2 junk0, junk1;
     consume(X.am1, X.pm1, junk0, junk1);  // phantom step j0 - 2: A(j0-1), P(j0-1)
     consume(X.a, X.p, X.c, X.qm1);        // phantom step j0 - 1: A(j0), P(j0), C(j0), Q(j0-1)
 
@@ -226,35 +228,32 @@ __global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restric
     // One layer's output row at columns c0 (s0) and c1 (s1) from its window:
     // cur = (a = row j, b = upper layer row j-1, c = lower layer row j),
     // am1 = row j-1, staged A1 = row j+1, B0 = upper row j, C1 = lower row j+1.
-    // kStencilDirs pairs (d, d + 7):
-    //   (1,0,0)/(-1,0,0)  a i+1 / i-1            (0,1,0)/(0,-1,0)  A1 / am1
-    //   (0,0,1)/(0,0,-1)  B0 / c                 (1,-1,0)/(-1,1,0) am1 i+1 / A1 i-1
-    //   (1,0,-1)/(-1,0,1) c i+1 / B0 i-1         (0,1,-1)/(0,-1,1) C1 / b
-    //   (1,-1,1)/(-1,1,-1) b i+1 / C1 i-1
-    // Column c0 reads fields (v, r, l) = (v0, v1, l0); column c1 (v1, r1, v0).
-    // Two independent accumulation chains per column (latency, not order,
-    // bounds the chain: the fast path is within the 1e-12 parity tolerance).
-#define BT_INTERIOR(a, b, c, am1, A1, B0, C1, s, v, r, l)                                           \
-  double s = W[0] * a.v;                                                                            \
-  double s##b_ = W[1] * (a.r + a.l);                                                                \
-  s = fma(W[2], A1.v + am1.v, s);                                                                   \
-  s##b_ = fma(W[3], B0.v + c.v, s##b_);                                                             \
-  s = fma(W[4], am1.r + A1.l, s);                                                                   \
-  s##b_ = fma(W[5], c.r + B0.l, s##b_);                                                             \
-  s = fma(W[6], C1.v + b.v, s);                                                                     \
-  s##b_ = fma(W[7], b.r + C1.l, s##b_);                                                             \
-  s += s##b_;
+    // The merged row is bitwise symmetric (W[d] == W[d+7]):
+    //   y_i = W0 a_i + W2 (A1_i + am1_i) + W3 (B0_i + c_i) + W6 (C1_i + b_i)
+    //       + [W1 a + W4 am1 + W5 c + W7 b]_{i+1} + [W1 a + W4 A1 + W5 B0 + W7 C1]_{i-1}
+    // The bracketed sums are formed by the lane that owns column i+1 / i-1 and
+    // shuffled (one double each way per layer), so neighbour values never
+    // cross lanes. Within the 1e-12 parity tolerance of the reference order.
 #define BT_LAYER(a, b, c, am1, A1, B0, C1, LY, py, ok)                                              \
   {                                                                                                 \
-    BT_INTERIOR(a, b, c, am1, A1, B0, C1, s0, v0, v1, l0)                                           \
-    BT_INTERIOR(a, b, c, am1, A1, B0, C1, s1, v1, r1, v0)                                           \
-    /* row ends (i = 0, i = LY - 1) are k_stencil_ends' */                                          \
+    /* this lane's contributions to its neighbours' columns */                                      \
+    const double up = W[1] * a.v1 + W[4] * A1.v1 + W[5] * B0.v1 + W[7] * C1.v1;  /* to c1 + 1 */     \
+    const double dn = W[1] * a.v0 + W[4] * am1.v0 + W[5] * c.v0 + W[7] * b.v0;   /* to c0 - 1 */     \
+    const double lft = __shfl_up_sync(0xffffffffu, up, 1);   /* column c0 - 1's, for c0 */          \
+    const double rgt = __shfl_down_sync(0xffffffffu, dn, 1); /* column c1 + 1's, for c1 */          \
+    double s0 = W[0] * a.v0 + W[2] * (A1.v0 + am1.v0) + W[3] * (B0.v0 + c.v0) + W[6] * (C1.v0 + b.v0); \
+    double s1 = W[0] * a.v1 + W[2] * (A1.v1 + am1.v1) + W[3] * (B0.v1 + c.v1) + W[6] * (C1.v1 + b.v1); \
+    s0 += W[1] * a.v1 + W[4] * am1.v1 + W[5] * c.v1 + W[7] * b.v1; /* i+1 of c0 = own c1 */           \
+    s1 += W[1] * a.v0 + W[4] * A1.v0 + W[5] * B0.v0 + W[7] * C1.v0; /* i-1 of c1 = own c0 */          \
+    s0 += lft;                                                                                      \
+    s1 += rgt;                                                                                      \
+    /* row ends (i = 0, i = LY - 1) are the boundary kernel's */                                    \
     if (ok && out && c0 < LY - 1 && c0 > 0) py[c0] = s0;                                            \
     if (ok && out && c1 < LY - 1) py[c1] = s1;                                                      \
   }
 #define BT_STEP(cur, nxt)                                                                           \
   {                                                                                                 \
-    Row4 A1, P1, C1, Q0;                                                                            \
+    Row2 A1, P1, C1, Q0;                                                                            \
     consume(A1, P1, C1, Q0);                                                                        \
     BT_LAYER(cur.a, cur.pm1, cur.c, cur.am1, A1, cur.p, C1, LA, pya, true)                          \
     BT_LAYER(cur.p, cur.qm1, cur.a, cur.pm1, P1, Q0, A1, LA - 1, pyp, LA - 1 >= pmin)               \
@@ -277,7 +276,6 @@ __global__ void __launch_bounds__(kFT, 3) k_stencil_fast(const double* __restric
     }
 #undef BT_STEP
 #undef BT_LAYER
-#undef BT_INTERIOR
   }
   cp_wait<0>();
 }
