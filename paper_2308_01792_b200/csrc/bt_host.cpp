@@ -535,6 +535,32 @@ std::string box_mesh_text(int nx, int ny, int nz, double perturb, uint64_t seed)
   return box_text(nx, ny, nz, 1.0, perturb, seed, header);
 }
 
+// Elementwise tables are cached on the grid per (form, level): a repeated
+// apply_elementwise launches kernels only.
+const EwTables& ew_tables(const bt_grid& g, const bt_form& f, int level) {
+  auto same = [&](const EwTables& t) {
+    if (t.level != level || t.form.kind != f.kind) return false;
+    if (f.kind != BT_FORM_DIV_K_GRAD) return true;
+    if (t.form.coeff_kind != f.coeff_kind) return false;
+    for (int q = 0; q < 4; ++q)
+      if (t.form.c[q] != f.c[q]) return false;
+    return true;
+  };
+  for (const auto& t : g.ew_cache)
+    if (same(*t)) return *t;
+  auto t = std::make_unique<EwTables>();
+  t->form = f;
+  t->level = level;
+  std::vector<EwCell> cells;
+  std::vector<EwAngles> angles;
+  build_ew_cells(g, f, level, cells, angles);
+  t->cells.upload(cells);
+  if (!angles.empty()) t->angles.upload(angles);
+  if (g.ew_cache.size() >= 16) g.ew_cache.erase(g.ew_cache.begin());
+  g.ew_cache.push_back(std::move(t));
+  return *g.ew_cache.back();
+}
+
 // Zero set of an edge micro-primitive = intersection of its endpoints' sets.
 static int prim_zero_set(int g, int n, int i, int j, int k) {
   static const int kOffEdge[7][2][3] = BT_EDGE_OFFSETS;

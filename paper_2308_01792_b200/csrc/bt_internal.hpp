@@ -165,6 +165,10 @@ struct XPlan {
   }
 };
 
+struct EwCell;
+struct EwAngles;
+struct EwTables;
+
 struct Topology {
   // incidence (cells ascending)
   std::vector<std::vector<int>> edge_cells, vert_cells;
@@ -207,6 +211,9 @@ struct bt_grid {
   // [part_begin, part_end) of rank part_rank out of part_nranks
   int part_rank = 0, part_nranks = 1, part_begin = 0, part_end = 0;
   mutable std::array<bt::XPlan, 11> xplan;  // per level, built on first use
+  // elementwise-kernel tables per (form, level), built on first use
+  mutable std::vector<std::unique_ptr<bt::EwTables>> ew_cache;
+  mutable bt::DevBuf<double> ew_scratch;  // ApplyMode::Add without a caller scratch
   // reduction scratch for dot products
   mutable bt::DevBuf<double> d_partials;
   mutable double* h_pinned = nullptr;
@@ -232,6 +239,13 @@ struct EwAngles {         // kind 1: sin/cos of the (class, slot, q, d) phase
   double s[6][4][4][3];
   double c[6][4][4][3];
 };
+struct EwTables {  // device tables of one (form, level) for the elementwise kernel
+  bt_form form{};
+  int level = 0;
+  DevBuf<EwCell> cells;
+  DevBuf<EwAngles> angles;
+};
+const EwTables& ew_tables(const bt_grid& g, const bt_form& f, int level);
 }  // namespace bt
 
 struct bt_stencil {

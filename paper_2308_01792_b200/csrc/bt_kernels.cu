@@ -550,29 +550,22 @@ bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level,
   validate_form(form);
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   cudaStream_t s = (cudaStream_t)stream;
-  std::vector<EwCell> cells;
-  std::vector<EwAngles> angles;
-  build_ew_cells(*g, *form, level, cells, angles);
-  DevBuf<EwCell> dc;
-  DevBuf<EwAngles> da;
-  dc.upload(cells);
-  if (!angles.empty()) da.upload(angles);
+  const EwTables& t = ew_tables(*g, *form, level);
   const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
   const double one[4] = {1.0, 0.0, 0.0, 0.0};
   const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
-  DevBuf<double> tmp;
   double* out = y;
   if (mode == BT_MODE_ADD) {
     if (!scratch) {
-      tmp.alloc((size_t)bt_space_size(g, BT_SPACE_P1, level));
-      scratch = tmp.p;
+      const size_t n = (size_t)bt_space_size(g, BT_SPACE_P1, level);
+      if (g->ew_scratch.n < n) g->ew_scratch.alloc(n);
+      scratch = g->ew_scratch.p;
     }
     out = scratch;
   }
-  launch_elementwise(*g, level, ck, c, dc.p, da.p, x, out, false, s);
+  launch_elementwise(*g, level, ck, c, t.cells.p, t.angles.p, x, out, false, s);
   launch_interface(*g, level, bc ? IF_SYNC_DIR : IF_SYNC, out, x, s);
   if (mode == BT_MODE_ADD) launch_vec(V_AXPY, y, out, 1.0, bt_space_size(g, BT_SPACE_P1, level), s);
-  BT_CUDA(cudaStreamSynchronize(s));  // host-side tables are released on return
   BT_CATCH
 }
 
@@ -582,19 +575,12 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
   check_level(g, level);
   validate_form(form);
   cudaStream_t s = (cudaStream_t)stream;
-  std::vector<EwCell> cells;
-  std::vector<EwAngles> angles;
-  build_ew_cells(*g, *form, level, cells, angles);
-  DevBuf<EwCell> dc;
-  DevBuf<EwAngles> da;
-  dc.upload(cells);
-  if (!angles.empty()) da.upload(angles);
+  const EwTables& t = ew_tables(*g, *form, level);
   const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
   const double one[4] = {1.0, 0.0, 0.0, 0.0};
-  launch_elementwise(*g, level, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, dc.p, da.p, nullptr, diag,
-                     true, s);
+  launch_elementwise(*g, level, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, t.cells.p, t.angles.p,
+                     nullptr, diag, true, s);
   launch_interface(*g, level, IF_SYNC, diag, nullptr, s);
-  BT_CUDA(cudaStreamSynchronize(s));
   BT_CATCH
 }
 

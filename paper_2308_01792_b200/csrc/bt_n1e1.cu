@@ -27,11 +27,17 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kW = kT / 32;
-constexpr int kRows = 64;
+constexpr int kRows = 256;  // rows per block (per warp: kRows / kW consecutive rows)
 
 static const int hOffEdge[7][2][3] = BT_EDGE_OFFSETS;
 static const int hOffCell[6][4][3] = BT_CELL_OFFSETS;
 static const int hLoc[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+
+// coupled edges / incident micro-tets of orientation g (checked against the
+// tables in build_static): x, z, xy, yz edges have 6 incident micro-tets and
+// couple to 19 edges; y, xz, xyz edges 4 and 13
+__host__ __device__ constexpr int n1e1_nnb(int g) { return g == 2 || g == 5 || g == 7 ? 13 : 19; }
+__host__ __device__ constexpr int n1e1_ninc(int g) { return g == 2 || g == 5 || g == 7 ? 4 : 6; }
 
 struct IncTet {  // a micro-tet containing an edge of subgroup g
   int s, le, sigma;
@@ -48,6 +54,9 @@ struct N1e1Static {
   Nb nb[8][19];
   int emap_g[6][6], emap_sigma[6][6];
   int dir_g[27], dir_sigma[27];  // lattice direction code -> (subgroup, sign)
+  int nbmask[8][19];  // incident tets (bits q) containing coupled edge m
+  int mask_off[8];    // first row of orientation g in a cell's masked-row table
+  int mask_rows;      // rows per cell: sum over g of 2^ninc[g]
 };
 __constant__ N1e1Static cS;
 static N1e1Static hS;
@@ -96,17 +105,22 @@ void build_static() {
             break;
         if (m == hS.nnb[g]) hS.nb[g][hS.nnb[g]++] = nb;
         it.nb[j] = m;
+        hS.nbmask[g][m] |= 1 << (hS.ninc[g] - 1);
       }
     }
+  for (int g = 1; g <= 7; ++g)
+    if (hS.nnb[g] != n1e1_nnb(g) || hS.ninc[g] != n1e1_ninc(g))
+      raise(BT_LOGIC_ERROR, "n1e1: coupling table does not match the per-orientation counts");
+  int rows = 0;
+  for (int g = 1; g <= 7; ++g) {
+    hS.mask_off[g] = rows;
+    rows += 1 << hS.ninc[g];
+  }
+  hS.mask_rows = rows;
   BT_CUDA(cudaMemcpyToSymbol(cS, &hS, sizeof hS));
   hS_ready = true;
 }
 
-int64_t entry_off(int g, int l) {
-  int64_t o = 0;
-  for (int q = 1; q < g; ++q) o += n_tet(width_formula(q, l));
-  return o;
-}
 
 // alpha K + beta M on the tet with corners X (same formulas as the oracle)
 void local_n1e1(const double X[4][3], double alpha, double beta, double out[36]) {
@@ -162,78 +176,118 @@ struct bt_n1e1 {
   int level = 0;
   double alpha = 1, beta = 1;
   bt::DevBuf<bt::N1e1Cell> d_cells;
+  // per cell, per orientation g, per presence mask of the incident micro-tets:
+  // the merged 19-weight row of the present ones (cS.mask_off / mask_rows)
+  bt::DevBuf<double> d_masked;
 };
 
 namespace bt {
 namespace {
 
 // ---------------------------------------------------------------------------
-// operator kernel: grid (row blocks, cells, 7 orientations)
+// operator kernel: grid (row block x 7 orientations, cells)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kT) k_n1e1(const double* __restrict__ x, double* __restrict__ y,
-                                             const N1e1Cell* __restrict__ cells, int n, int64_t cs) {
-  __shared__ double sW[19];
-  __shared__ double sA[6][36];
-  const int g = blockIdx.z + 1;
-  const int cell = blockIdx.y;
-  for (int q = threadIdx.x; q < 19; q += kT) sW[q] = cells[cell].W[g][q];
-  for (int q = threadIdx.x; q < 216; q += kT) sA[q / 36][q % 36] = cells[cell].A[q / 36][q % 36];
-  __syncthreads();
-  const int wg = g == 7 ? n - 1 : n;  // subgroup width: 2^l, xyz 2^l - 1
+
+// Rows [rb * kRows, ...) of orientation G of one cell. Each warp walks a
+// contiguous run of rows; within a layer the neighbour row starts advance by
+// their row lengths (one add per row). Every edge applies one merged row —
+// the row of its present incident micro-tets (presence mask from per-row
+// intervals), from the block's shared table — with straight-line loads: a
+// coupled edge that does not exist reads slot 0 with weight 0.
+template <int G>
+__device__ __forceinline__ void n1e1_rows(const double* __restrict__ x, double* __restrict__ y,
+                                          const double* sM, int cell, int rb, int n, int64_t cs) {
+  constexpr int NNB = n1e1_nnb(G), NINC = n1e1_ninc(G);
+  const int wg = G == 7 ? n - 1 : n;  // subgroup width: 2^l, xyz 2^l - 1
   const int nrows = tri32(wg);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRows);
-  int eoff[8];
-  {
-    int o = 0;
-    for (int q = 1; q <= 7; ++q) {
-      eoff[q] = o;
-      o += tet32(q == 7 ? n - 1 : n);
-    }
-  }
+  const int rend = min(nrows, (rb + 1) * kRows);
+  const int tn = tet32(n);  // entry offsets: subgroups 1..6 have width n, xyz (7) n - 1
+  auto eoff = [&](int q) { return (q - 1) * tn; };
   const double* __restrict__ xc = x + (int64_t)cell * cs;
-  double* __restrict__ yc = y + (int64_t)cell * cs + eoff[g];
-  const int nnb = cS.nnb[g], ninc = cS.ninc[g];
-  for (int r = blockIdx.x * kRows + warp; r < rend; r += kW) {
-    int j, k;
-    decode_row(wg, r, j, k);
-    const int L = wg - j - k, t0 = row_start(wg, j, k);
-    int base[19];
+  double* __restrict__ yc = y + (int64_t)cell * cs + eoff(G);
+  constexpr int kRpw = kRows / kW;
+  int r = rb * kRows + warp * kRpw;
+  const int rlast = min(rend, r + kRpw);
+  if (r >= rlast) return;
+  int j, k;
+  decode_row(wg, r, j, k);
+  int base[NNB];
+  auto full_bases = [&]() {
 #pragma unroll
-    for (int m = 0; m < 19; ++m) {
-      if (m < nnb) {
-        const Nb nb = cS.nb[g][m];
-        const int w2 = nb.g == 7 ? n - 1 : n;
-        base[m] = eoff[nb.g] + row_start(w2, j + nb.d[1], k + nb.d[2]) + nb.d[0];
-      } else {
-        base[m] = 0;
-      }
+    for (int m = 0; m < NNB; ++m) {
+      const Nb nb = cS.nb[G][m];
+      const int w2 = nb.g == 7 ? n - 1 : n;
+      base[m] = eoff(nb.g) + row_start(w2, j + nb.d[1], k + nb.d[2]) + nb.d[0];
+    }
+  };
+  full_bases();
+  for (; r < rlast; ++r) {
+    const int L = wg - j - k, t0 = row_start(wg, j, k);
+    // incident micro-tet q exists (anchor in I_tet(w_s)) for i in [lo_q, hi_q]
+    int lo[NINC], hi[NINC];
+#pragma unroll
+    for (int q = 0; q < NINC; ++q) {
+      const IncTet& it = cS.inc[G][q];
+      const int ws = it.s == 0 ? n : (it.s == 1 ? n - 2 : n - 1);
+      lo[q] = max(0, -it.dq[0]);
+      hi[q] = (j + it.dq[1] < 0 || k + it.dq[2] < 0) ? -1 : ws - 1 - it.dq[0] - (j + it.dq[1]) - (k + it.dq[2]);
     }
     for (int i = lane; i < L; i += 32) {
-      // presence of the incident micro-tets (anchor in I_tet(w_s))
-      unsigned pres = 0;
-      for (int q = 0; q < ninc; ++q) {
-        const IncTet& it = cS.inc[g][q];
-        const int ws = it.s == 0 ? n : (it.s == 1 ? n - 2 : n - 1);
-        if (in_i_tet(ws, i + it.dq[0], j + it.dq[1], k + it.dq[2])) pres |= 1u << q;
-      }
-      double acc = 0.0;
-      if (pres == (1u << ninc) - 1) {
+      unsigned mask = 0;
 #pragma unroll
-        for (int m = 0; m < 19; ++m)
-          if (m < nnb) acc = fma(sW[m], __ldg(xc + base[m] + i), acc);
-      } else {
-        for (int q = 0; q < ninc; ++q) {
-          if (!(pres >> q & 1)) continue;
-          const IncTet& it = cS.inc[g][q];
-          double row = 0.0;
-          for (int jj = 0; jj < 6; ++jj)
-            row = fma(sA[it.s][6 * it.le + jj] * cS.emap_sigma[it.s][jj], __ldg(xc + base[it.nb[jj]] + i), row);
-          acc = fma((double)it.sigma, row, acc);
-        }
-      }
+      for (int q = 0; q < NINC; ++q)
+        if (i >= lo[q] && i <= hi[q]) mask |= 1u << q;
+      const double* wrow = sM + NNB * mask;
+      double v[NNB];
+#pragma unroll
+      for (int m = 0; m < NNB; ++m) v[m] = __ldg(xc + ((cS.nbmask[G][m] & mask) ? base[m] + i : 0));
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < NNB; ++m) acc = fma(wrow[m], v[m], acc);
       yc[t0 + i] = acc;
     }
+    // next row: neighbour m's row (j + dj, k + dk) of width w2 has length
+    // w2 - (k + dk) - (j + dj) = L + (w2 - wg) - dk - dj
+    if (++j < wg - k) {
+#pragma unroll
+      for (int m = 0; m < NNB; ++m) {
+        const Nb nb = cS.nb[G][m];
+        base[m] += L + ((nb.g == 7) - (G == 7)) * -1 - nb.d[2] - nb.d[1];
+      }
+    } else {
+      ++k;
+      j = 0;
+      full_bases();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kT, 3) k_n1e1(const double* __restrict__ x, double* __restrict__ y,
+                                                const double* __restrict__ masked, int n, int64_t cs) {
+  // this block's (cell, orientation): its masked-row table (<= 64 rows)
+  __shared__ double sM[64 * 19];
+  const int g = blockIdx.x % 7 + 1;  // the 7 orientations of a row block are consecutive
+  const int rb = blockIdx.x / 7;     // blocks: they gather the same rows, kept in L2
+  const int cell = blockIdx.y;
+  const int nnb = n1e1_nnb(g);
+  {
+    const double* __restrict__ src = masked + (size_t)cell * cS.mask_rows * 19 + (size_t)cS.mask_off[g] * 19;
+    const int nw = (1 << n1e1_ninc(g)) * 19;
+    for (int q = threadIdx.x; q < nw; q += kT) {
+      const int row = q / 19, m = q % 19;  // repack rows to nnb weights
+      if (m < nnb) sM[row * nnb + m] = src[q];
+    }
+  }
+  __syncthreads();
+  switch (g) {
+    case 1: n1e1_rows<1>(x, y, sM, cell, rb, n, cs); break;
+    case 2: n1e1_rows<2>(x, y, sM, cell, rb, n, cs); break;
+    case 3: n1e1_rows<3>(x, y, sM, cell, rb, n, cs); break;
+    case 4: n1e1_rows<4>(x, y, sM, cell, rb, n, cs); break;
+    case 5: n1e1_rows<5>(x, y, sM, cell, rb, n, cs); break;
+    case 6: n1e1_rows<6>(x, y, sM, cell, rb, n, cs); break;
+    default: n1e1_rows<7>(x, y, sM, cell, rb, n, cs); break;
   }
 }
 
@@ -510,6 +564,7 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
   op->beta = beta;
   const int nc = g->mesh.n_cells();
   std::vector<N1e1Cell> cells(nc);
+  std::vector<double> masked((size_t)nc * hS.mask_rows * 19, 0.0);
   const double h = 1.0 / (double)(1 << level);
   for (int c = 0; c < nc; ++c) {
     N1e1Cell& cc = cells[c];
@@ -523,6 +578,16 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
       }
       local_n1e1(X, alpha, beta, cc.A[s]);
     }
+    double* mt = &masked[(size_t)c * hS.mask_rows * 19];
+    for (int gg = 1; gg <= 7; ++gg)
+      for (int mask = 0; mask < (1 << hS.ninc[gg]); ++mask) {
+        double* row = mt + 19 * (size_t)(hS.mask_off[gg] + mask);
+        for (int q = 0; q < hS.ninc[gg]; ++q) {
+          if (!(mask >> q & 1)) continue;
+          const IncTet& it = hS.inc[gg][q];
+          for (int j = 0; j < 6; ++j) row[it.nb[j]] += it.sigma * hS.emap_sigma[it.s][j] * cc.A[it.s][6 * it.le + j];
+        }
+      }
     for (int gg = 1; gg <= 7; ++gg)
       for (int q = 0; q < hS.ninc[gg]; ++q) {
         const IncTet& it = hS.inc[gg][q];
@@ -531,6 +596,7 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
       }
   }
   op->d_cells.upload(cells);
+  op->d_masked.upload(masked);
   *out = op.release();
   BT_CATCH
 }
@@ -544,8 +610,8 @@ bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, v
   const bt_grid& g = *op->grid;
   const int n = 1 << op->level;
   cudaStream_t s = (cudaStream_t)stream;
-  dim3 grid((tri32(n) + kRows - 1) / kRows, g.mesh.n_cells(), 7);
-  k_n1e1<<<grid, kT, 0, s>>>(x, y, op->d_cells.p, n, level_slots(BT_SPACE_EDGES, op->level));
+  dim3 grid(7 * ((tri32(n) + kRows - 1) / kRows), g.mesh.n_cells());  // x: row block x 7 orientations
+  k_n1e1<<<grid, kT, 0, s>>>(x, y, op->d_masked.p, n, level_slots(BT_SPACE_EDGES, op->level));
   count_launch();
   check_launch("k_n1e1");
   launch_edge_interface(g, op->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);

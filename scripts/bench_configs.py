@@ -1,0 +1,233 @@
+"""Per-config measurements of the §8 rows beyond the headline (bench.py is
+config 2). Run on a GPU box from the repo root:
+
+    python scripts/bench_configs.py [--out gpurun_out/configs.json] [--skip-cpu]
+
+For every BASELINE config it times the device path (CUDA events, warm, many
+repeats), states the algorithmic work per unit and the roofline it implies,
+checks the result against the reference or oracle, and times the reference
+CPU path on the box's host cores beside it (bounded samples, stated).
+Synthetic seeded inputs only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import paper_2308_01792_b200 as bt  # noqa: E402
+import pyoracle  # noqa: E402
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "B200_PROFILING.md fallback"
+
+
+def timed(fn, reps, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e-3  # seconds per call
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def host(f, l):
+    return f.values[l].cpu().numpy()
+
+
+def nproc():
+    return os.cpu_count() or 1
+
+
+def cfg1(res, skip_cpu):
+    """ref-tet L6, zero Dirichlet, 15-point stencil: 1 + 10 applies."""
+    L = 6
+    text = bt.ref_tet_text()
+    g = bt.Grid(text, L, L)
+    x, y = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
+    bt.random_fill(x, L, 0)
+    bt.zero_dirichlet(x, L)
+    t = bt.compute_stencil(bt.FormId.diffusion(), g, L)
+    sec = timed(lambda: bt.apply_stencil(t, x, y, L, bt.BC.DirichletIdentity), 2000)
+    slots = g.space_size(0, L)
+    owned = bt.owned_dof_count(x, L)
+    pk, src = peaks()
+    r = pyoracle.Reference(text, L, L)
+    xr = r.random_fill(L, 0)
+    xr = r.zero_dirichlet(L, xr) if hasattr(r, "zero_dirichlet") else xr
+    yr = r.apply_stencil(L, host(x, L), bc=1)
+    out = {"config": 1, "workload": "ref-tet L6, P1 stencil, Dirichlet identity rows, 1 + 10 applies",
+           "slots": slots, "owned": owned, "gpu_us_per_apply": sec * 1e6, "gpu_gdofs": owned / sec / 1e9,
+           "bytes_per_apply": 16 * slots, "hbm_floor_us": 16 * slots / (pk * 1e9) * 1e6,
+           "note": "0.77 MB fits in L2: launch/latency bound, not HBM",
+           "parity_rel_l2_vs_reference": rel(host(y, L), yr)}
+    if not skip_cpu:
+        cpu = r.time_apply(L, host(x, L), kind=0, form=0, bc=1, reps=11, threads=1)
+        out["cpu_reference"] = {"sec_per_apply": cpu, "gdofs": owned / cpu / 1e9, "threads": 1,
+                                "sample": "median of 11 full applies (1 cell: no parallelism)"}
+    res.append(out)
+
+
+def cfg3(res, skip_cpu):
+    """384 perturbed Kuhn tets, L6, div(k grad) with k = 1 + 0.5 sin sin sin,
+    elementwise over the 6 micro-tet classes."""
+    L = 6
+    text = bt.cubes_mesh_text(4, 0.1, 0)
+    g = bt.Grid(text, L, L)
+    form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
+    x, y = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
+    bt.random_fill(x, L, 0)
+    sec = timed(lambda: bt.apply_elementwise(form, x, y, L), 50)
+    slots = g.space_size(0, L)
+    owned = bt.owned_dof_count(x, L)
+    tets = g.n_cells() * 8 ** L
+    out = {"config": 3, "workload": "4x4x4 cubes x 6 perturbed Kuhn tets (384 cells) L6, div(k grad), "
+                                    "k = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z), elementwise",
+           "slots": slots, "owned": owned, "micro_tets": tets, "gpu_us_per_apply": sec * 1e6,
+           "gpu_gdofs": owned / sec / 1e9, "gpu_micro_tets_per_s": tets / sec,
+           "bound": "FP64 (per vertex: 24 incident micro-tets x (class matrix row + k at 4 quadrature points))"}
+    if not skip_cpu:
+        r = pyoracle.Reference(text, L, L)
+        kp = pyoracle.kparams()
+        yr = r.apply_elementwise(L, host(x, L), form=2, kp=kp, threads=nproc())
+        out["parity_rel_l2_vs_reference"] = rel(host(y, L), yr)
+        cpu = r.time_apply(L, host(x, L), kind=1, form=2, kp=kp, bc=0, reps=1, threads=nproc())
+        out["cpu_reference"] = {"sec_per_apply": cpu, "gdofs": owned / cpu / 1e9, "threads": nproc(),
+                                "sample": "1 full apply"}
+    res.append(out)
+
+
+def cfg4(res, skip_cpu):
+    """384 perturbed tets, L7, N1E1 curl-curl + mass, tangential Dirichlet."""
+    L = 7
+    text = bt.cubes_mesh_text(4, 0.1, 0)
+    g = bt.Grid(text, L, L)
+    op = bt.N1E1Operator(g, L)
+    x, y = bt.allocate(bt.edge_space(), g, L, L), bt.allocate(bt.edge_space(), g, L, L)
+    bt.random_fill(x, L, 0)
+    sec = timed(lambda: bt.apply_n1e1(op, x, y, L), 20)
+    slots = g.space_size(2, L)
+    owned = bt.owned_dof_count(x, L)
+    pk, src = peaks()
+    alg = 16.0 * slots
+    out = {"config": 4, "workload": "4x4x4 cubes x 6 perturbed Kuhn tets (384 cells) L7, N1E1 curl-curl + mass, "
+                                    "tangential Dirichlet identity rows",
+           "edge_slots": slots, "owned": owned, "gpu_us_per_apply": sec * 1e6, "gpu_gdofs": owned / sec / 1e9,
+           "bytes_per_apply": alg, "achieved_gbs": alg / sec / 1e9, "peak_gbs": pk, "peak_source": src,
+           "roofline_frac": alg / sec / 1e9 / pk}
+    del x, y
+    torch.cuda.empty_cache()
+    if not skip_cpu:
+        Ls = 4  # CPU sample: the oracle port (there is no reference N1E1), one thread
+        o = pyoracle.Oracle(text, Ls, Ls)
+        xs = o.n1e1_random_fill(Ls, 0)
+        t0 = time.perf_counter()
+        o.n1e1_apply(Ls, xs)
+        cpu = time.perf_counter() - t0
+        owned_s = o.owned_count(Ls, space=2)
+        out["cpu_port"] = {"sec_per_apply": cpu, "gdofs": owned_s / cpu / 1e9, "threads": 1,
+                           "sample": f"same mesh at L{Ls} ({owned_s} owned edges), oracle restatement (no reference "
+                                     "N1E1 exists)"}
+    res.append(out)
+
+
+def cfg5(res, skip_cpu):
+    """V(2,2) Chebyshev(2)-Jacobi multigrid, var-coeff P1 elementwise, linear
+    transfers, 50 coarse CG iterations (coarse_tol 0), 5 cycles. Full size
+    (3072 cells, L8: 70 GB per vector) needs several GPUs' memory; measured
+    here on reduced instances (stated)."""
+    sm = bt.SmootherConfig.chebyshev(2)
+    sm.nu1 = sm.nu2 = 2
+    form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
+    runs = []
+    for n, lo, hi, cpu_ok in [(2, 2, 5, True), (8, 2, 6, False)]:
+        text = bt.cubes_mesh_text(n, 0.1, 0)
+        g = bt.Grid(text, lo, hi)
+        h = bt.make_hierarchy(g, form, bt.KernelKind.Elementwise)
+        rhs = bt.allocate(bt.p1_space(), g)
+        xx = bt.allocate(bt.p1_space(), g)
+        bt.random_fill(rhs, hi, 0)
+        bt.zero_dirichlet(rhs, hi)
+        mg = bt.MultigridConfig(coarse_level=lo, cycles=5, coarse_tol=0.0, coarse_maxit=50)
+        bt.v_cycle(h, hi, rhs, xx, sm, mg)  # warm-up (also fills the spectral estimates)
+        bt.assign(xx, hi, 0.0)
+        torch.cuda.synchronize()
+        hist = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        r = bt.allocate(bt.p1_space(), g, hi, hi)
+        for c in range(5):
+            e0.record()
+            bt.v_cycle(h, hi, rhs, xx, sm, mg)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+            bt.hierarchy_apply(h, xx, r, hi)
+            r.values[hi].mul_(-1.0).add_(rhs.values[hi])
+            hist.append(bt.norm2(r, hi) / bt.norm2(rhs, hi))
+        slots = g.space_size(0, hi)
+        run = {"mesh": f"{n}x{n}x{n} cubes x 6 perturbed Kuhn tets ({6 * n ** 3} cells)", "levels": f"{lo}->{hi}",
+               "fine_slots": slots, "gpu_sec_per_cycle": float(np.median(ts)), "residual_history": hist}
+        if cpu_ok and not skip_cpu:
+            rr = pyoracle.Reference(text, lo, hi)
+            rr.make_hierarchy(form=2, kp=pyoracle.kparams(), kernel=0, threads=nproc())
+            secs = np.zeros(5)
+            _, href = rr.vcycles(hi, sm.as_array(), host(rhs, hi), np.zeros(slots), 5, lo, 0.0, 50, seconds=secs)
+            run["reference_residual_history"] = [float(v) for v in href[1:]]
+            run["residual_history_rel_diff"] = rel(hist, href[1:])
+            run["cpu_reference"] = {"sec_per_cycle": float(np.median(secs)), "threads": nproc(),
+                                    "sample": "the same 5 cycles"}
+        runs.append(run)
+        del g, h, rhs, xx, r
+        torch.cuda.empty_cache()
+    res.append({"config": 5, "workload": "V(2,2) Chebyshev(2), var-coeff P1 elementwise, 50 coarse CG its, 5 cycles "
+                                         "(reduced instances; full size = 70 GB/vector, multi-GPU)", "runs": runs})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--only", default="1,3,4,5")
+    a = ap.parse_args()
+    res = []
+    for c in a.only.split(","):
+        t0 = time.time()
+        try:
+            {"1": cfg1, "3": cfg3, "4": cfg4, "5": cfg5}[c](res, a.skip_cpu)
+        except Exception as e:  # keep the other configs
+            res.append({"config": int(c), "error": repr(e)})
+        print(f"config {c}: {time.time() - t0:.1f} s", flush=True)
+        os.makedirs(os.path.dirname(a.out), exist_ok=True)
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
