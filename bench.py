@@ -251,6 +251,12 @@ def run_ours(args):
     value = owned * K / (total_ms * 1e-3) / 1e9
     kmean = float(np.mean(kern_ms))
     peak, peak_kind = measured_peaks()
+    traffic = None  # DRAM bytes per apply from the committed ncu capture (profiles/r1_traffic.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            traffic = float(json.load(f)["apply_total"]) if ws == 1 else None
+    except Exception:
+        traffic = None
     alg_bytes = 16.0 * slots  # read x once, write y once
     achieved = alg_bytes / (kmean * 1e-3) / 1e9
 
@@ -298,7 +304,7 @@ def run_ours(args):
                        "parallelism": f"cells partitioned over {ws} ranks (NCCL interface exchange)"
                        if ws > 1 else "1 GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_stencil_fast || k_boundary" if ws == 1 else "k_stencil (per-cell rows)",
                          "kernel_ms": kmean, "kernel_share": kmean / ms_step,
                          "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs (copy)",
