@@ -164,9 +164,8 @@ void local_n1e1(const double X[4][3], double alpha, double beta, double out[36])
 
 }  // namespace
 
-struct N1e1Cell {
+struct N1e1Cell {    // host-side setup of one cell
   double A[6][36];  // class element matrices
-  double W[8][19];  // merged interior stencil per orientation (index g = 1..7)
 };
 
 }  // namespace bt
@@ -175,7 +174,6 @@ struct bt_n1e1 {
   const bt_grid* grid = nullptr;
   int level = 0;
   double alpha = 1, beta = 1;
-  bt::DevBuf<bt::N1e1Cell> d_cells;
   // per cell, per orientation g, per presence mask of the incident micro-tets:
   // the merged 19-weight row of the present ones (cS.mask_off / mask_rows)
   bt::DevBuf<double> d_masked;
@@ -588,14 +586,7 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
           for (int j = 0; j < 6; ++j) row[it.nb[j]] += it.sigma * hS.emap_sigma[it.s][j] * cc.A[it.s][6 * it.le + j];
         }
       }
-    for (int gg = 1; gg <= 7; ++gg)
-      for (int q = 0; q < hS.ninc[gg]; ++q) {
-        const IncTet& it = hS.inc[gg][q];
-        for (int j = 0; j < 6; ++j)
-          cc.W[gg][it.nb[j]] += it.sigma * hS.emap_sigma[it.s][j] * cc.A[it.s][6 * it.le + j];
-      }
   }
-  op->d_cells.upload(cells);
   op->d_masked.upload(masked);
   *out = op.release();
   BT_CATCH

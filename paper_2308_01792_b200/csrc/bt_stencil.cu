@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -613,8 +614,10 @@ struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
+// per host thread and device, so concurrent host threads never share the
+// fork/join events
 SideStream& side_stream() {
-  static SideStream ss[16];
+  static thread_local SideStream ss[16];
   int dev = 0;
   BT_CUDA(cudaGetDevice(&dev));
   SideStream& r = ss[dev & 15];
@@ -637,6 +640,45 @@ static int stencil_parts() {
   return parts;
 }
 
+// fast kernel launches (interior rows) for this handle's cells, on stream s
+static void launch_fast(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
+  const int w = (1 << st.level) + 1;
+  const int64_t cs = n_tet(w);
+  const size_t smem = sizeof(double) * kFW * kRingD;
+  // persistent grid: SMs x resident blocks, per device (set up once)
+  static std::mutex mu;
+  static int grids[64] = {0};
+  int dev = 0;
+  BT_CUDA(cudaGetDevice(&dev));
+  int grid;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    int& gr = grids[dev & 63];
+    if (!gr) {
+      BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int sms = 0, per_sm = 0;
+      BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kFT, smem));
+      gr = sms * std::max(1, per_sm);
+    }
+    grid = gr;
+  }
+  FastParams<kMaxCells> fp;  // copied into the launch's parameter buffer
+  for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
+    const int cc0 = st.part_begin + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
+    const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
+    if (!nt) continue;
+    for (int c = 0; c < cnt; ++c) {
+      const double* f = &st.fast[8 * (size_t)(cc0 + c)];
+      for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
+    }
+    const int64_t e0 = (int64_t)cc0 * cs;
+    const int blocks = std::min(grid, (nt + kFW - 1) / kFW);
+    k_stencil_fast<kMaxCells><<<blocks, kFT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
+    count_launch();
+  }
+}
+
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
   const int w = (1 << st.level) + 1;
   const int64_t cs = n_tet(w);
@@ -656,30 +698,7 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
   const int parts = stencil_parts();
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
-  static FastParams<kMaxCells> fp;
-  const size_t smem = sizeof(double) * kFW * kRingD;
-  static int grid = 0;
-  if (!grid) {
-    BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 0, per_sm = 0;
-    BT_CUDA(cudaGetDevice(&dev));
-    BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kFT, smem));
-    grid = sms * std::max(1, per_sm);
-  }
-  for (int ch = 0; (parts & 1) && ch + 1 < (int)st.chunk_first.size(); ++ch) {
-    const int cc0 = c0 + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
-    const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
-    if (!nt) continue;
-    for (int c = 0; c < cnt; ++c) {
-      const double* f = &st.fast[8 * (size_t)(cc0 + c)];
-      for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
-    }
-    const int64_t e0 = (int64_t)cc0 * cs;
-    const int blocks = std::min(grid, (nt + kFW - 1) / kFW);
-    k_stencil_fast<kMaxCells><<<blocks, kFT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
-    count_launch();
-  }
+  if (parts & 1) launch_fast(st, x, y, s);
   BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
   if ((parts & 2) && w - 1 >= 4) {
     const int n = w - 1;
@@ -703,36 +722,6 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
 
 bool stencil_fused(const bt_stencil& st) {
   return st.symmetric && st.grid->part_nranks == 1;
-}
-
-// fast kernel launches (interior rows) for this handle's cells, on stream s
-static void launch_fast(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
-  const int w = (1 << st.level) + 1;
-  const int64_t cs = n_tet(w);
-  static FastParams<kMaxCells> fp;
-  const size_t smem = sizeof(double) * kFW * kRingD;
-  static int grid = 0;
-  if (!grid) {
-    BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 0, per_sm = 0;
-    BT_CUDA(cudaGetDevice(&dev));
-    BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kFT, smem));
-    grid = sms * std::max(1, per_sm);
-  }
-  for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
-    const int cc0 = st.part_begin + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
-    const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
-    if (!nt) continue;
-    for (int c = 0; c < cnt; ++c) {
-      const double* f = &st.fast[8 * (size_t)(cc0 + c)];
-      for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
-    }
-    const int64_t e0 = (int64_t)cc0 * cs;
-    const int blocks = std::min(grid, (nt + kFW - 1) / kFW);
-    k_stencil_fast<kMaxCells><<<blocks, kFT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
-    count_launch();
-  }
 }
 
 void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s) {
