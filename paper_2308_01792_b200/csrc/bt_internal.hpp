@@ -165,6 +165,12 @@ struct XPlan {
   }
 };
 
+// fast-kernel march schedule of one layer-group size (see bt_stencil.cu)
+struct FastTasks {
+  DevBuf<int4> d_tasks;
+  int ntasks = 0;
+  std::vector<int> chunk_first;  // first task of each kMaxCells-cell chunk (+ end)
+};
 struct EwCell;
 struct EwAngles;
 struct EwTables;
@@ -255,10 +261,8 @@ struct bt_stencil {
   std::vector<std::array<double, 15>> rows;  // host copy of StencilTable::rows
   bt::DevBuf<bt::StencilCell> d_cells;
   bt::DevBuf<double> d_diag;                 // assembled diagonal
-  bt::DevBuf<int4> d_tasks;                  // warp march schedule, fast rows (see bt_stencil.cu)
-  int ntasks = 0;
+  bt::FastTasks fast4, fast2;                // fast-kernel marches: 4-layer groups, the 2-layer group
   int part_begin = 0, part_end = 0;          // the grid's cell partition when the tasks were built
-  std::vector<int> chunk_first;              // first task of each 128-cell chunk in d_tasks (+ end)
   bt::DevBuf<int4> d_xtasks;                 // per-cell general rows (marches that would stage outside x)
   bt::DevBuf<int> d_xoff;                    // cell c: d_xtasks[d_xoff[c] .. d_xoff[c + 1])
   int nxtasks = 0, xtask_max = 0;

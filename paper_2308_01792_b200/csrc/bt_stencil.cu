@@ -43,9 +43,8 @@
 namespace bt {
 
 namespace {
-constexpr int kT = 256;
-constexpr int kW = kT / 32;
 constexpr int kMarchRows = 48;
+constexpr int kGroup = 4;  // layers per fast march (plus one 2-layer group)
 constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
 // k_stencil_general / k_stencil_ends blocks are small and register-light so
@@ -65,14 +64,15 @@ struct FastParams {
 };
 constexpr int kMaxCells = 256;  // 256 * 8 * 8 B = 16 KB of kernel parameters
 
-// per-warp staging ring: kStages stages x 4 staged rows of kRowD doubles
-constexpr int kStages = 5;
-constexpr int kRows = 4;   // A(j+1), P(j+1), C(j+1), Q(j)
+// per-warp staging ring: kStages stages x (N + 2) staged rows of kRowD doubles
+constexpr int kStages = 4;
 constexpr int kRowD = 64;  // staged columns [base - 2, base + 62)
-constexpr int kStageD = kRows * kRowD;
-constexpr int kRingD = kStages * kStageD;  // doubles per warp
-constexpr int kFT = 128;                   // k_stencil_fast block
+constexpr int kFT = 128;   // k_stencil_fast block
 constexpr int kFW = kFT / 32;
+template <int N>
+constexpr int ring_doubles() {  // per warp
+  return kStages * (N + 2) * kRowD;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
@@ -87,52 +87,52 @@ __device__ __forceinline__ void cp_wait() {
 struct Row2 {  // one row at a lane's columns c0, c1 = c0 + 1
   double v0, v1;
 };
-// Register window of a two-layer march at row j: layers k-1 (C), k (A),
-// k+1 (P), k+2 (Q).
+// Register window of an N-layer march at row j: layers k .. k+N-1 (rows j-1
+// and j), layer k-1 (row j) below, layer k+N (row j-1) above.
+template <int N>
 struct Win {
-  Row2 am1, a;  // A(j-1), A(j)
-  Row2 pm1, p;  // P(j-1), P(j)
-  Row2 c;       // C(j)
-  Row2 qm1;     // Q(j-1)
+  Row2 am1[N], a[N];
+  Row2 c, qm1;
 };
 
-// Task word: x = k (first layer of the pair k, k+1), y = column block |
+// Task word: x = k (first layer of the march's N layers), y = column block |
 // (cell - cell0) << 16, z = j0, w = j1.
 //
-// A warp owns 60 output columns of two adjacent layers k, k+1 of one cell and
-// marches rows j0..j1-1 of both (layer k+1's rows end one row earlier; its
-// last-step row is left to the general kernel or is empty). Per step it
-// stages four rows — A(j+1), P(j+1), C(j+1) and Q(j) — which serve both
-// layers: layer k reads A(j-1..j+1), P(j-1..j) as its upper layer and
-// C(j..j+1); layer k+1 reads P(j-1..j+1), Q(j-1..j) and A(j..j+1) as its
-// lower layer.
+// A warp owns 60 output columns of N adjacent layers k .. k+N-1 of one cell
+// and marches rows j0..j1-1 of all of them (each layer's rows end one row
+// before the one below; rows that are not interior rows are masked). Per
+// step it stages N + 2 rows — row j+1 of layers k-1 .. k+N-1 and row j of
+// layer k+N — which serve all N layers: N + 2 staged rows per N output rows.
 //
 // Persistent warps: warp g runs tasks g, g + G, g + 2G, ... (the host sorts
 // tasks by length, longest first). Each march is preceded by two phantom
 // steps (j0 - 2, j0 - 1) whose staged rows fill the register window, so the
 // staging stream runs through the ring across task boundaries without
 // draining. Lane l stages columns base - 2 + l and base + 30 + l of each row
-// (two 8-byte cp.async, each warp-contiguous), so every row lands at the same
-// place whatever its alignment and lane l reads its pair (c0, c1) with one
-// 16-byte shared load. The host keeps marches that would stage outside x on
-// the general kernel.
-template <int kMaxC>
-__global__ void __launch_bounds__(kFT, 4) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
+// (two 8-byte cp.async, each warp-contiguous; none past the row's end), so
+// every row lands at the same place whatever its alignment and lane l reads
+// its pair (c0, c1) with one 16-byte shared load. The host keeps marches that
+// would stage outside x on the general kernel.
+template <int N, int kMaxC>
+__global__ void __launch_bounds__(kFT, N <= 2 ? 4 : 3) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
                                                         int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
+  constexpr int NS = N + 2;  // staged rows per step: C (layer k-1), layers k..k+N-1, Q (layer k+N)
+  constexpr int kStageD = NS * kRowD;
   extern __shared__ __align__(128) double ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = gridDim.x * kFW;
   const int t0 = blockIdx.x * kFW + warp;
   if (t0 >= ntasks) return;
-  const double* ring = ring_all + warp * kRingD;
+  const double* ring = ring_all + warp * ring_doubles<N>();
   const uint32_t my_s = smem_u32(ring) + 8u * lane;
 
   // ---- producer (every lane copies its two columns of each staged row) ----
-  // element offsets (within the cell) of column base - 2 + lane in rows
-  // A(j+1), P(j+1), C(j+1), Q(j) of the producer's next step j;
-  // r = len(A(j+1)) = len(P(j)); pleft = steps left in the producer's task
-  int pt = t0, pA = 0, pP = 0, pC = 0, pQ = 0, pr = 0, pleft = 0, pcol = 0;
+  // po[s]: element offset (within the cell) of column base - 2 + lane in the
+  // producer's next step j of stream s: 0 = C(j+1) (layer k-1), 1 + q = row
+  // j+1 of layer k+q, N+1 = Q(j) (layer k+N); pr = len(row j+1 of layer k)
+  int pt = t0, pr = 0, pleft = 0, pcol = 0;
+  int po[NS];
   const double* pcell = x;
   int4 pnext = tasks[t0];
   auto p_start = [&]() {
@@ -141,10 +141,10 @@ __global__ void __launch_bounds__(kFT, 4) k_stencil_fast(const double* __restric
     const int j = tk.z - 2, cb = base - 2 + lane;
     pcol = cb;  // this lane's first staged column (the second is pcol + 32)
     pcell = x + (int64_t)cl * cell_slots;
-    pA = cb + row_start(w, j + 1, k);
-    pP = cb + row_start(w, j + 1, k + 1);
-    pC = cb + row_start(w, j + 1, k - 1);
-    pQ = cb + row_start(w, j, k + 2);
+    po[0] = cb + row_start(w, j + 1, k - 1);
+#pragma unroll
+    for (int q = 0; q < N; ++q) po[1 + q] = cb + row_start(w, j + 1, k + q);
+    po[N + 1] = cb + row_start(w, j, k + N);
     pr = w - k - j - 1;
     pleft = tk.w - tk.z + 2;
     if (pt + G < ntasks) pnext = tasks[pt + G];
@@ -154,25 +154,16 @@ __global__ void __launch_bounds__(kFT, 4) k_stencil_fast(const double* __restric
   auto produce = [&]() {  // one (possibly empty) group of copies
     if (pleft > 0) {
       const uint32_t d = my_s + (uint32_t)(ps * kStageD * 8);
-      const double *a = pcell + pA, *p = pcell + pP, *c = pcell + pC, *q = pcell + pQ;
-      // columns past a row's end are never used: those lanes skip the copy
-      // (row lengths: A(j+1) pr, P(j+1) and Q(j) pr - 1, C(j+1) pr + 1)
-      const int c1 = pcol + 32;
-      if (pcol < pr) cp8(d, a);
-      if (c1 < pr) cp8(d + 256, a + 32);
-      if (pcol < pr - 1) cp8(d + kRowD * 8, p);
-      if (c1 < pr - 1) cp8(d + kRowD * 8 + 256, p + 32);
-      if (pcol <= pr) cp8(d + 2 * kRowD * 8, c);
-      if (c1 <= pr) cp8(d + 2 * kRowD * 8 + 256, c + 32);
-      if (pcol < pr - 1) cp8(d + 3 * kRowD * 8, q);
-      if (c1 < pr - 1) cp8(d + 3 * kRowD * 8 + 256, q + 32);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        // length of stream s's current row; columns past it are never used
+        const int len = s == 0 ? pr + 1 : (s <= N ? pr - (s - 1) : pr + 1 - N);
+        const double* src = pcell + po[s];
+        if (pcol < len) cp8(d + s * kRowD * 8, src);
+        if (pcol + 32 < len) cp8(d + s * kRowD * 8 + 256, src + 32);
+        po[s] += len;  // next row of the stream
+      }
       ps = ps == kStages - 1 ? 0 : ps + 1;
-      // next rows: A(j+2) = A(j+1) + len(A(j+1)); P(j+2) = P(j+1) + len(P(j+1));
-      // C(j+2) = C(j+1) + len(C(j+1)); Q(j+1) = Q(j) + len(Q(j))
-      pA += pr;
-      pP += pr - 1;
-      pC += pr + 1;
-      pQ += pr - 1;
       --pr;
       if (--pleft == 0) {
         pt += G;
@@ -191,14 +182,15 @@ __global__ void __launch_bounds__(kFT, 4) k_stencil_fast(const double* __restric
     o.v0 = v.x;
     o.v1 = v.y;
   };
-  auto consume = [&](Row2& A1, Row2& P1, Row2& C1, Row2& Q0) {
+  // staged rows of one step: C1 = C(j+1), A1[q] = row j+1 of layer k+q, Q0 = Q(j)
+  auto consume = [&](Row2& C1, Row2* A1, Row2& Q0) {
     cp_wait<kStages - 2>();
     __syncwarp();
     const double* st = ring + cs * kStageD;
-    read_row(st, A1);
-    read_row(st + kRowD, P1);
-    read_row(st + 2 * kRowD, C1);
-    read_row(st + 3 * kRowD, Q0);
+    read_row(st, C1);
+#pragma unroll
+    for (int q = 0; q < N; ++q) read_row(st + (1 + q) * kRowD, A1[q]);
+    read_row(st + (N + 1) * kRowD, Q0);
     cs = cs == kStages - 1 ? 0 : cs + 1;
     // the stage refilled next is the one every lane read in the previous
     // step, which the __syncwarp above orders before this refill
@@ -215,57 +207,67 @@ __global__ void __launch_bounds__(kFT, 4) k_stencil_fast(const double* __restric
     const int base = kFastCols * blk;
     const int c0 = base - 2 + 2 * lane, c1 = c0 + 1;  // this lane's two columns
     const bool out = lane >= 1 && lane <= 30;
-    Win X, Y;
-    Row2 junk0, junk1;
-    consume(X.am1, X.pm1, junk0, junk1);  // phantom step j0 - 2: A(j0-1), P(j0-1)
-    consume(X.a, X.p, X.c, X.qm1);        // phantom step j0 - 1: A(j0), P(j0), C(j0), Q(j0-1)
-
-    int LA = w - k - j0;  // length of A(j); P(j) has LA - 1
-    double* __restrict__ pya = y + (int64_t)cl * cell_slots + row_start(w, j0, k);
-    double* __restrict__ pyp = y + (int64_t)cl * cell_slots + row_start(w, j0, k + 1);
-    const int pmin = blk == 0 ? 3 : 0;        // layer k+1 rows shorter than 3 belong to the general kernel
+    Win<N> X, Y;
+    {
+      Row2 cj, qj, a1[N];
+      consume(cj, a1, qj);  // phantom step j0 - 2: rows j0 - 1
+#pragma unroll
+      for (int q = 0; q < N; ++q) X.am1[q] = a1[q];
+      consume(X.c, a1, X.qm1);  // phantom step j0 - 1: rows j0, C(j0), Q(j0 - 1)
+#pragma unroll
+      for (int q = 0; q < N; ++q) X.a[q] = a1[q];
+    }
+    int LA = w - k - j0;  // length of row j of layer k; layer k+q's is LA - q
+    double* __restrict__ py[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) py[q] = y + (int64_t)cl * cell_slots + row_start(w, j0, k + q);
+    const int pmin = blk == 0 ? 3 : 0;  // shorter rows of column block 0 are not interior rows
     int j = j0;
 
     // One layer's output row at columns c0 (s0) and c1 (s1) from its window:
-    // cur = (a = row j, b = upper layer row j-1, c = lower layer row j),
-    // am1 = row j-1, staged A1 = row j+1, B0 = upper row j, C1 = lower row j+1.
-    // The merged row is bitwise symmetric (W[d] == W[d+7]):
+    // a = row j, b = upper layer row j-1, c = lower layer row j, am1 = row
+    // j-1, A1 = row j+1, B0 = upper row j, C1 = lower row j+1. The merged row
+    // is bitwise symmetric (W[d] == W[d+7]):
     //   y_i = W0 a_i + W2 (A1_i + am1_i) + W3 (B0_i + c_i) + W6 (C1_i + b_i)
     //       + [W1 a + W4 am1 + W5 c + W7 b]_{i+1} + [W1 a + W4 A1 + W5 B0 + W7 C1]_{i-1}
     // The bracketed sums are formed by the lane that owns column i+1 / i-1 and
     // shuffled (one double each way per layer), so neighbour values never
     // cross lanes. Within the 1e-12 parity tolerance of the reference order.
-#define BT_LAYER(a, b, c, am1, A1, B0, C1, LY, py, ok)                                              \
-  {                                                                                                 \
-    /* this lane's contributions to its neighbours' columns */                                      \
-    const double up = W[1] * a.v1 + W[4] * A1.v1 + W[5] * B0.v1 + W[7] * C1.v1;  /* to c1 + 1 */     \
-    const double dn = W[1] * a.v0 + W[4] * am1.v0 + W[5] * c.v0 + W[7] * b.v0;   /* to c0 - 1 */     \
-    const double lft = __shfl_up_sync(0xffffffffu, up, 1);   /* column c0 - 1's, for c0 */          \
-    const double rgt = __shfl_down_sync(0xffffffffu, dn, 1); /* column c1 + 1's, for c1 */          \
-    double s0 = W[0] * a.v0 + W[2] * (A1.v0 + am1.v0) + W[3] * (B0.v0 + c.v0) + W[6] * (C1.v0 + b.v0); \
-    double s1 = W[0] * a.v1 + W[2] * (A1.v1 + am1.v1) + W[3] * (B0.v1 + c.v1) + W[6] * (C1.v1 + b.v1); \
-    s0 += W[1] * a.v1 + W[4] * am1.v1 + W[5] * c.v1 + W[7] * b.v1; /* i+1 of c0 = own c1 */           \
-    s1 += W[1] * a.v0 + W[4] * A1.v0 + W[5] * B0.v0 + W[7] * C1.v0; /* i-1 of c1 = own c0 */          \
-    s0 += lft;                                                                                      \
-    s1 += rgt;                                                                                      \
-    /* row ends (i = 0, i = LY - 1) are the boundary kernel's */                                    \
-    if (ok && out && c0 < LY - 1 && c0 > 0) py[c0] = s0;                                            \
-    if (ok && out && c1 < LY - 1) py[c1] = s1;                                                      \
-  }
+    auto layer = [&](const Row2& a, const Row2& b, const Row2& c, const Row2& am1, const Row2& A1, const Row2& B0,
+                     const Row2& C1, int LY, double* py_, bool ok) {
+      const double upv = W[1] * a.v1 + W[4] * A1.v1 + W[5] * B0.v1 + W[7] * C1.v1;  // to column c1 + 1
+      const double dnv = W[1] * a.v0 + W[4] * am1.v0 + W[5] * c.v0 + W[7] * b.v0;   // to column c0 - 1
+      const double lft = __shfl_up_sync(0xffffffffu, upv, 1);    // column c0 - 1's, for c0
+      const double rgt = __shfl_down_sync(0xffffffffu, dnv, 1);  // column c1 + 1's, for c1
+      double s0 = W[0] * a.v0 + W[2] * (A1.v0 + am1.v0) + W[3] * (B0.v0 + c.v0) + W[6] * (C1.v0 + b.v0);
+      double s1 = W[0] * a.v1 + W[2] * (A1.v1 + am1.v1) + W[3] * (B0.v1 + c.v1) + W[6] * (C1.v1 + b.v1);
+      s0 += W[1] * a.v1 + W[4] * am1.v1 + W[5] * c.v1 + W[7] * b.v1;  // i+1 of c0 = own c1
+      s1 += W[1] * a.v0 + W[4] * A1.v0 + W[5] * B0.v0 + W[7] * C1.v0;  // i-1 of c1 = own c0
+      s0 += lft;
+      s1 += rgt;
+      // row ends (i = 0, i = LY - 1) are the boundary kernel's
+      if (ok && out && c0 < LY - 1 && c0 > 0) py_[c0] = s0;
+      if (ok && out && c1 < LY - 1) py_[c1] = s1;
+    };
 #define BT_STEP(cur, nxt)                                                                           \
   {                                                                                                 \
-    Row2 A1, P1, C1, Q0;                                                                            \
-    consume(A1, P1, C1, Q0);                                                                        \
-    BT_LAYER(cur.a, cur.pm1, cur.c, cur.am1, A1, cur.p, C1, LA, pya, true)                          \
-    BT_LAYER(cur.p, cur.qm1, cur.a, cur.pm1, P1, Q0, A1, LA - 1, pyp, LA - 1 >= pmin)               \
-    pya += LA;                                                                                      \
-    pyp += LA - 1;                                                                                  \
+    Row2 C1, Q0, A1[N];                                                                             \
+    consume(C1, A1, Q0);                                                                            \
+    _Pragma("unroll") for (int q = 0; q < N; ++q) {                                                 \
+      const int qu = q < N - 1 ? q + 1 : q, ql = q > 0 ? q - 1 : q; /* in-range indices */          \
+      const Row2& b = q < N - 1 ? cur.am1[qu] : cur.qm1;                                            \
+      const Row2& B0 = q < N - 1 ? cur.a[qu] : Q0;                                                  \
+      const Row2& c = q > 0 ? cur.a[ql] : cur.c;                                                    \
+      const Row2& Cn = q > 0 ? A1[ql] : C1;                                                         \
+      layer(cur.a[q], b, c, cur.am1[q], A1[q], B0, Cn, LA - q, py[q], LA - q >= pmin);              \
+      py[q] += LA - q;                                                                              \
+    }                                                                                               \
     --LA;                                                                                           \
     ++j;                                                                                            \
-    nxt.am1 = cur.a;                                                                                \
-    nxt.a = A1;                                                                                     \
-    nxt.pm1 = cur.p;                                                                                \
-    nxt.p = P1;                                                                                     \
+    _Pragma("unroll") for (int q = 0; q < N; ++q) {                                                 \
+      nxt.am1[q] = cur.a[q];                                                                        \
+      nxt.a[q] = A1[q];                                                                             \
+    }                                                                                               \
     nxt.c = C1;                                                                                     \
     nxt.qm1 = Q0;                                                                                   \
   }
@@ -276,7 +278,6 @@ __global__ void __launch_bounds__(kFT, 4) k_stencil_fast(const double* __restric
       if (j >= j1) break;
     }
 #undef BT_STEP
-#undef BT_LAYER
   }
   cp_wait<0>();
 }
@@ -489,7 +490,7 @@ __global__ void __launch_bounds__(kGT, 9) k_stencil_general(const double* __rest
 void init_stencil_tasks(bt_stencil& st) {
   const int w = (1 << st.level) + 1;
   const int n = w - 1;
-  std::vector<int4> fast, gen, all;
+  std::vector<int4> fast, fast2, gen, all;  // fast: groups of kGroup layers; fast2: the 2-layer group
   // general rows are unprefetched: one row per task keeps them parallel
   auto push1 = [](std::vector<int4>& v, int k, int b, int a, int e) {
     for (int j = a; j < e; ++j) v.push_back(make_int4(k, b, j, j + 1));
@@ -507,14 +508,21 @@ void init_stencil_tasks(bt_stencil& st) {
         if (b == 0) push1(gen, k, b, std::max(1, w - k - 2), jmax);
       }
     }
-    // fast marches cover layer pairs (k, k + 1), k odd (n - 2 fast layers, n = 2^l even)
-    if (!fast_layer || (k & 1) == 0) continue;
+    // fast marches: groups of kGroup layers k .. k+kGroup-1 starting at
+    // k = 1, then one group of 2 (n - 2 fast layers, n - 2 = 2 mod 4)
+    const int ng = (n - 2) / kGroup;
+    const bool start4 = fast_layer && (k - 1) % kGroup == 0 && (k - 1) / kGroup < ng;
+    const bool start2 = fast_layer && k == 1 + ng * kGroup && k + 1 <= n - 2;
+    if (!start4 && !start2) continue;
     for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (60 wide)
       const int jmax = w - k - kFastCols * b;
       const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;  // layer k's fast rows
-      for (int j0 = 1; j0 < fe; j0 += kMarchRows) fast.push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, fe)));
+      for (int j0 = 1; j0 < fe; j0 += kMarchRows)
+        (start4 ? fast : fast2).push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, fe)));
     }
   }
+  if ((n - 2) % kGroup != 0 && (n - 2) % kGroup != 2)
+    raise(BT_LOGIC_ERROR, "stencil: fast layer count must be 2 mod 4");
   // Fast tasks of every cell, in chunks of kMaxCells cells (the kernel's
   // parameter table); longest marches first. A march whose staged columns
   // would leave x (cell 0's first rows, the last cell's top layers) runs on
@@ -526,44 +534,46 @@ void init_stencil_tasks(bt_stencil& st) {
     const char* e = std::getenv("BT_STENCIL_ORDER");
     return e ? std::atoi(e) : 1;
   }();
-  if (order == 1)
-    std::stable_sort(fast.begin(), fast.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
   const int nc_all = st.grid->mesh.n_cells();
   const int64_t cs = n_tet(w), total = cs * nc_all;
   st.part_begin = st.grid->part_begin;
   st.part_end = st.grid->part_end;
-  std::vector<int4> all_fast;
   std::vector<std::vector<int4>> extra(nc_all);
-  st.chunk_first.clear();
-  for (int c0 = st.part_begin; c0 < st.part_end; c0 += kMaxCells) {
-    st.chunk_first.push_back((int)all_fast.size());
-    const int cnt = std::min(kMaxCells, st.part_end - c0);
-    // spatial order walks cells outermost (a cell's x + y fits the 126 MB L2)
-    const int64_t ntc = (int64_t)fast.size() * cnt;
-    for (int64_t q = 0; q < ntc; ++q) {
-      const int c = order == 1 ? (int)(q % cnt) : (int)(q / (int64_t)fast.size());
-      const int4& t = fast[order == 1 ? (size_t)(q / cnt) : (size_t)(q % (int64_t)fast.size())];
-      {
+  auto build = [&](std::vector<int4>& list, int N, FastTasks& out) {
+    if (order == 1)
+      std::stable_sort(list.begin(), list.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
+    std::vector<int4> all_fast;
+    out.chunk_first.clear();
+    for (int c0 = st.part_begin; c0 < st.part_end; c0 += kMaxCells) {
+      out.chunk_first.push_back((int)all_fast.size());
+      const int cnt = std::min(kMaxCells, st.part_end - c0);
+      const int64_t ntc = (int64_t)list.size() * cnt;
+      for (int64_t q = 0; q < ntc; ++q) {
+        const int c = order == 1 ? (int)(q % cnt) : (int)(q / (int64_t)list.size());
+        const int4& t = list[order == 1 ? (size_t)(q / cnt) : (size_t)(q % (int64_t)list.size())];
         const int64_t cb = (int64_t)(c0 + c) * cs + kFastCols * t.y;
         const int64_t lo = cb + row_start(w, t.z - 1, t.x - 1) - 2;  // C(j0 - 1), column base - 2
-        const int64_t hi = cb + row_start(w, t.w - 1, t.x + 2) + 61;  // Q(j1 - 1), column base + 61
+        const int64_t hi = cb + row_start(w, t.w - 1, t.x + N) + 61;  // Q(j1 - 1), column base + 61
         if (lo >= 0 && hi < total) {
           all_fast.push_back(make_int4(t.x, t.y | (c << 16), t.z, t.w));
         } else {
-          // the march's rows of both layers (layer k + 1 only where they are fast rows)
-          const int k = t.x, pe = t.y == 0 ? w - k - 3 : w - k - 1 - kFastCols * t.y;
-          for (int gb = 2 * t.y; gb < 2 * t.y + 2; ++gb)
-            for (int j = t.z; j < t.w; ++j) {
-              if (kGenCols * gb < w - k - j) extra[c0 + c].push_back(make_int4(k, gb, j, j + 1));
-              if (j < pe && kGenCols * gb < w - k - 1 - j) extra[c0 + c].push_back(make_int4(k + 1, gb, j, j + 1));
-            }
+          // the march's interior rows of its N layers
+          for (int q = 0; q < N; ++q) {
+            const int kq = t.x + q;
+            const int fe = t.y == 0 ? w - kq - 2 : w - kq - kFastCols * t.y;
+            for (int gb = 2 * t.y; gb < 2 * t.y + 2; ++gb)
+              for (int j = t.z; j < t.w && j < fe; ++j)
+                if (kGenCols * gb < w - kq - j) extra[c0 + c].push_back(make_int4(kq, gb, j, j + 1));
+          }
         }
       }
     }
-  }
-  st.chunk_first.push_back((int)all_fast.size());
-  st.ntasks = (int)all_fast.size();
-  st.d_tasks.upload(all_fast);
+    out.chunk_first.push_back((int)all_fast.size());
+    out.ntasks = (int)all_fast.size();
+    out.d_tasks.upload(all_fast);
+  };
+  build(fast, kGroup, st.fast4);
+  build(fast2, 2, st.fast2);
   std::vector<int4> ex;
   std::vector<int> exoff(1, 0);  // per cell of the partition
   for (int c = st.part_begin; c < st.part_end; ++c) {
@@ -640,11 +650,15 @@ static int stencil_parts() {
   return parts;
 }
 
-// fast kernel launches (interior rows) for this handle's cells, on stream s
-static void launch_fast(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
+// fast kernel launches (interior rows of the N-layer marches in ft) for this
+// handle's cells, on stream s
+template <int N>
+static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double* x, double* y, cudaStream_t s) {
+  if (!ft.ntasks) return;
   const int w = (1 << st.level) + 1;
   const int64_t cs = n_tet(w);
-  const size_t smem = sizeof(double) * kFW * kRingD;
+  const size_t smem = sizeof(double) * kFW * ring_doubles<N>();
+  auto kern = k_stencil_fast<N, kMaxCells>;
   // persistent grid: SMs x resident blocks, per device (set up once)
   static std::mutex mu;
   static int grids[64] = {0};
@@ -655,18 +669,18 @@ static void launch_fast(const bt_stencil& st, const double* x, double* y, cudaSt
     std::lock_guard<std::mutex> lock(mu);
     int& gr = grids[dev & 63];
     if (!gr) {
-      BT_CUDA(cudaFuncSetAttribute(k_stencil_fast<kMaxCells>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      BT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int sms = 0, per_sm = 0;
       BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_fast<kMaxCells>, kFT, smem));
+      BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFT, smem));
       gr = sms * std::max(1, per_sm);
     }
     grid = gr;
   }
   FastParams<kMaxCells> fp;  // copied into the launch's parameter buffer
-  for (int ch = 0; ch + 1 < (int)st.chunk_first.size(); ++ch) {
+  for (int ch = 0; ch + 1 < (int)ft.chunk_first.size(); ++ch) {
     const int cc0 = st.part_begin + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
-    const int t0 = st.chunk_first[ch], nt = st.chunk_first[ch + 1] - t0;
+    const int t0 = ft.chunk_first[ch], nt = ft.chunk_first[ch + 1] - t0;
     if (!nt) continue;
     for (int c = 0; c < cnt; ++c) {
       const double* f = &st.fast[8 * (size_t)(cc0 + c)];
@@ -674,7 +688,7 @@ static void launch_fast(const bt_stencil& st, const double* x, double* y, cudaSt
     }
     const int64_t e0 = (int64_t)cc0 * cs;
     const int blocks = std::min(grid, (nt + kFW - 1) / kFW);
-    k_stencil_fast<kMaxCells><<<blocks, kFT, smem, s>>>(x + e0, y + e0, st.d_tasks.p + t0, nt, w, cs, fp);
+    kern<<<blocks, kFT, smem, s>>>(x + e0, y + e0, ft.d_tasks.p + t0, nt, w, cs, fp);
     count_launch();
   }
 }
@@ -698,8 +712,9 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
   const int parts = stencil_parts();
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
-  if (parts & 1) launch_fast(st, x, y, s);
+  if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);
   BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s);  // the 2-layer group
   if ((parts & 2) && w - 1 >= 4) {
     const int n = w - 1;
     k_stencil_ends<<<dim3((n - 3 + 127) / 128, n - 3, nc), 128, 0, ss.s>>>(x, y, st.d_ends.p, w, cs, c0);
@@ -730,14 +745,14 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
   const int parts = stencil_parts();
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
-  if (parts & 1) launch_fast(st, x, y, s);  // first, so its persistent blocks are resident first
+  if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);  // first, so its persistent blocks are resident first
+  BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s);  // the 2-layer group, beside the main launch
   if (!(parts & 8)) {
-    BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
     BT_CUDA(cudaEventRecord(ss.join, ss.s));
     BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
     return;
   }
-  BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
   BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
             (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, n_tet(n + 1)};
   // interior rows of the marches the host kept off the fast kernel (they
