@@ -44,7 +44,7 @@ namespace bt {
 
 namespace {
 constexpr int kMarchRows = 48;
-constexpr int kGroup = 4;  // layers per fast march (plus one 2-layer group)
+constexpr int kGroup = 4;  // layers per fast march (plus one 2-layer group); 6 measured slower (2 blocks/SM)
 constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
 // k_stencil_general / k_stencil_ends blocks are small and register-light so
@@ -114,7 +114,7 @@ struct Win {
 // its pair (c0, c1) with one 16-byte shared load. The host keeps marches that
 // would stage outside x on the general kernel.
 template <int N, int kMaxC>
-__global__ void __launch_bounds__(kFT, N <= 2 ? 4 : 3) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
+__global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2)) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
                                                         int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
   constexpr int NS = N + 2;  // staged rows per step: C (layer k-1), layers k..k+N-1, Q (layer k+N)
@@ -522,7 +522,7 @@ void init_stencil_tasks(bt_stencil& st) {
     }
   }
   if ((n - 2) % kGroup != 0 && (n - 2) % kGroup != 2)
-    raise(BT_LOGIC_ERROR, "stencil: fast layer count must be 2 mod 4");
+    raise(BT_LOGIC_ERROR, "stencil: fast layer count must be 0 or 2 mod the group size");
   // Fast tasks of every cell, in chunks of kMaxCells cells (the kernel's
   // parameter table); longest marches first. A march whose staged columns
   // would leave x (cell 0's first rows, the last cell's top layers) runs on
