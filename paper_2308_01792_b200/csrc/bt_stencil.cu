@@ -43,7 +43,7 @@
 namespace bt {
 
 namespace {
-constexpr int kMarchRows = 48;
+constexpr int kMarchRows = 32;
 constexpr int kGroup = 4;  // layers per fast march (plus one 2-layer group); 6 measured slower (2 blocks/SM)
 constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
