@@ -343,24 +343,40 @@ __device__ __forceinline__ void bary_ijk(const int8_t* lv, int nl, const int* wt
   }
 }
 
-// per-cell partial row at lattice point (i, j, k) of `cell`; returns its slot
-__device__ __forceinline__ double typed_partial(const double* __restrict__ x, const BndArgs& a, int cell, int i,
-                                                int j, int k, int64_t& slot) {
+// The 15 neighbour values of lattice point (i, j, k) of `cell` — all loads
+// issued at once (an absent direction, whose typed weight is 0, reads the
+// point itself) — and its slot.
+struct Gather15 {
+  double v[15];
+  const double* wz;  // the zero-set-typed row
+};
+__device__ __forceinline__ int64_t gather15(const double* __restrict__ x, const BndArgs& a, int cell, int i, int j,
+                                            int k, Gather15& gt) {
   const int w = a.n + 1;
   const int z = zero_set(a.n, i, j, k);
   const StencilCell& sc = a.cells[cell];
   const uint32_t mask = __ldg(&sc.mask[z]);
-  slot = (int64_t)cell * a.cs + row_start(w, j, k) + i;
+  const int64_t slot = (int64_t)cell * a.cs + row_start(w, j, k) + i;
   const double* __restrict__ xc = x + slot;
   int off[15];
   row_offsets(w, j, k, off);
-  double acc = __ldg(&sc.w[z][0]) * __ldg(xc);
 #pragma unroll
-  for (int d = 1; d < 15; ++d) {
-    const double v = (mask >> d) & 1 ? __ldg(xc + off[d]) : 0.0;
-    acc = fma(__ldg(&sc.w[z][d]), v, acc);
-  }
+  for (int d = 0; d < 15; ++d) gt.v[d] = __ldg(xc + ((mask >> d) & 1 ? off[d] : 0));
+  gt.wz = sc.w[z];
+  return slot;
+}
+// per-cell partial row (partial_row_apply, operators.hpp:78-96) from a gather
+__device__ __forceinline__ double partial_row(const Gather15& gt) {
+  double acc = __ldg(gt.wz) * gt.v[0];
+#pragma unroll
+  for (int d = 1; d < 15; ++d) acc = fma(__ldg(gt.wz + d), gt.v[d], acc);
   return acc;
+}
+__device__ __forceinline__ double typed_partial(const double* __restrict__ x, const BndArgs& a, int cell, int i,
+                                                int j, int k, int64_t& slot) {
+  Gather15 gt;
+  slot = gather15(x, a, cell, i, j, k, gt);
+  return partial_row(gt);
 }
 
 template <bool kDir>
@@ -414,12 +430,29 @@ __global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, 
     }
   };
   double sum = 0.0, single = 0.0;
-  for (int m = 0; m < count; ++m) {
+  if (F) {  // face point: one or two members, all their loads in flight together
+    Gather15 g0, g1;
     int cell, i, j, k;
-    member(m, cell, i, j, k);
-    int64_t slot;
-    single = typed_partial(x, a, cell, i, j, k, slot);
+    member(0, cell, i, j, k);
+    gather15(x, a, cell, i, j, k, g0);
+    if (count == 2) {
+      member(1, cell, i, j, k);
+      gather15(x, a, cell, i, j, k, g1);
+    }
+    single = partial_row(g0);
     sum += single;
+    if (count == 2) {
+      single = partial_row(g1);
+      sum += single;
+    }
+  } else {
+    for (int m = 0; m < count; ++m) {
+      int cell, i, j, k;
+      member(m, cell, i, j, k);
+      int64_t slot;
+      single = typed_partial(x, a, cell, i, j, k, slot);
+      sum += single;
+    }
   }
   if (count < 2) sum = single;  // no replicas: sync_additive leaves the value alone
   for (int m = 0; m < count; ++m) {
