@@ -365,6 +365,57 @@ __device__ __forceinline__ int64_t gather15(const double* __restrict__ x, const 
   gt.wz = sc.w[z];
   return slot;
 }
+// Face-interior points: the zero set is one bit and the typed row has 11
+// present directions (those not leaving the face's half-space).
+template <int Z>
+__device__ __forceinline__ constexpr int face_dir(int q) {
+  constexpr int dg[11] = {0, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14};  // diagonal face S = n: no dx + dy + dz = +1
+  constexpr int di[11] = {0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 13};     // i = 0: no dx = -1
+  constexpr int dj[11] = {0, 1, 2, 3, 5, 6, 8, 10, 11, 12, 14};    // j = 0: no dy = -1
+  constexpr int dk[11] = {0, 1, 2, 3, 4, 7, 8, 9, 11, 12, 13};     // k = 0: no dz = -1
+  return Z == 1 ? dg[q] : (Z == 2 ? di[q] : (Z == 4 ? dj[q] : dk[q]));
+}
+struct Gather11 {
+  double v[11];
+  const double* wz;
+  int z;
+};
+template <int Z>
+__device__ __forceinline__ void gather11_z(const double* __restrict__ xc, int w, int j, int k, double* v) {
+  int off[15];
+  row_offsets(w, j, k, off);
+#pragma unroll
+  for (int q = 0; q < 11; ++q) v[q] = __ldg(xc + off[face_dir<Z>(q)]);
+}
+__device__ __forceinline__ void gather11(const double* __restrict__ x, const BndArgs& a, int cell, int i, int j, int k,
+                                         Gather11& gt) {
+  const int w = a.n + 1;
+  gt.z = zero_set(a.n, i, j, k);  // one bit
+  gt.wz = a.cells[cell].w[gt.z];
+  const double* __restrict__ xc = x + (int64_t)cell * a.cs + row_start(w, j, k) + i;
+  switch (gt.z) {
+    case 1: gather11_z<1>(xc, w, j, k, gt.v); break;
+    case 2: gather11_z<2>(xc, w, j, k, gt.v); break;
+    case 4: gather11_z<4>(xc, w, j, k, gt.v); break;
+    default: gather11_z<8>(xc, w, j, k, gt.v); break;
+  }
+}
+template <int Z>
+__device__ __forceinline__ double face_row_z(const double* __restrict__ wz, const double* v) {
+  double acc = __ldg(wz) * v[0];  // direction 0 first, then ascending: the typed row's order
+#pragma unroll
+  for (int q = 1; q < 11; ++q) acc = fma(__ldg(wz + face_dir<Z>(q)), v[q], acc);
+  return acc;
+}
+__device__ __forceinline__ double face_row(const Gather11& gt) {
+  switch (gt.z) {
+    case 1: return face_row_z<1>(gt.wz, gt.v);
+    case 2: return face_row_z<2>(gt.wz, gt.v);
+    case 4: return face_row_z<4>(gt.wz, gt.v);
+    default: return face_row_z<8>(gt.wz, gt.v);
+  }
+}
+
 // per-cell partial row (partial_row_apply, operators.hpp:78-96) from a gather
 __device__ __forceinline__ double partial_row(const Gather15& gt) {
   double acc = __ldg(gt.wz) * gt.v[0];
@@ -431,18 +482,18 @@ __global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, 
   };
   double sum = 0.0, single = 0.0;
   if (F) {  // face point: one or two members, all their loads in flight together
-    Gather15 g0, g1;
+    Gather11 g0, g1;
     int cell, i, j, k;
     member(0, cell, i, j, k);
-    gather15(x, a, cell, i, j, k, g0);
+    gather11(x, a, cell, i, j, k, g0);
     if (count == 2) {
       member(1, cell, i, j, k);
-      gather15(x, a, cell, i, j, k, g1);
+      gather11(x, a, cell, i, j, k, g1);
     }
-    single = partial_row(g0);
+    single = face_row(g0);
     sum += single;
     if (count == 2) {
-      single = partial_row(g1);
+      single = face_row(g1);
       sum += single;
     }
   } else {
@@ -640,6 +691,14 @@ void init_stencil_tasks(bt_stencil& st) {
         pi = pi || kI0Present[q] == d;
       }
       if ((!pd && cells[c].w[1][d] != 0.0) || (!pi && cells[c].w[2][d] != 0.0)) st.symmetric = false;
+      // the boundary kernel's face rows use 11 fixed directions per face zero set
+      static const int fdirs[4][11] = {{0, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14}, {0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 13},
+                                       {0, 1, 2, 3, 5, 6, 8, 10, 11, 12, 14}, {0, 1, 2, 3, 4, 7, 8, 9, 11, 12, 13}};
+      for (int f = 0; f < 4; ++f) {
+        bool in = false;
+        for (int q = 0; q < 11; ++q) in = in || fdirs[f][q] == d;
+        if (!in && cells[c].w[1 << f][d] != 0.0) st.symmetric = false;
+      }
     }
     double* f = &st.fast[8 * (size_t)c];
     for (int d = 0; d < 8; ++d) f[d] = rw[d];
