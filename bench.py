@@ -260,35 +260,58 @@ def run_ours(args):
     alg_bytes = 16.0 * slots  # read x once, write y once
     achieved = alg_bytes / (kmean * 1e-3) / 1e9
 
-    # e2e through the public API: pinned host x -> device, apply, device y -> pinned host
+    # e2e through the public API, as a pipelined serving loop: every step
+    # copies its inputs pinned host -> device and its result device -> pinned
+    # host; consecutive steps overlap on three streams (H2D of step s+1, apply
+    # of step s, D2H of step s-1 — PCIe is full duplex), double-buffered.
     # (per rank: its own cells' slices; the per-cell rows read x of the rank's cells only)
     lo, hi = c_begin * cs, c_end * cs
     hx = torch.empty(slots, dtype=torch.float64, pin_memory=True)
     hx.copy_(x.values[LEVEL][lo:hi].cpu())
-    hy = torch.empty(slots, dtype=torch.float64, pin_memory=True)
-    xin = bt.allocate(bt.p1_space(), grid)
-    yout = bt.allocate(bt.p1_space(), grid)
-    e2e_steps = max(3, min(20, K))
-    for _ in range(2):
-        xin.values[LEVEL][lo:hi].copy_(hx, non_blocking=True)
-        bt.apply_stencil(table, xin, yout, LEVEL)
-        hy.copy_(yout.values[LEVEL][lo:hi], non_blocking=True)
+    hys = [torch.empty(slots, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    xs = [bt.allocate(bt.p1_space(), grid) for _ in range(2)]
+    ys = [bt.allocate(bt.p1_space(), grid) for _ in range(2)]
+    s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+
+    def serve(nsteps):
+        for q in range(nsteps):
+            b = q & 1
+            with torch.cuda.stream(s_in):
+                if q >= 2:
+                    s_in.wait_event(ev_cmp[b])  # the apply of step q-2 has read xs[b]
+                xs[b].values[LEVEL][lo:hi].copy_(hx, non_blocking=True)
+                ev_in[b].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in[b])
+                if q >= 2:
+                    s_cmp.wait_event(ev_out[b])  # the D2H of step q-2 has read ys[b]
+                bt.apply_stencil(table, xs[b], ys[b], LEVEL)
+                ev_cmp[b].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[b])
+                hys[b].copy_(ys[b].values[LEVEL][lo:hi], non_blocking=True)
+                ev_out[b].record(s_out)
+
+    e2e_steps = max(4, min(20, K))
+    serve(4)  # warm-up
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        xin.values[LEVEL][lo:hi].copy_(hx, non_blocking=True)
-        bt.apply_stencil(table, xin, yout, LEVEL)
-        hy.copy_(yout.values[LEVEL][lo:hi], non_blocking=True)
-    e1.record(stream)
+    e0.record(s_in)
+    serve(e2e_steps)
+    s_out.wait_event(ev_out[(e2e_steps - 1) & 1])
+    e1.record(s_out)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if ws > 1:
         t = torch.tensor([e2e_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
+    hy = hys[(e2e_steps - 1) & 1]
     assert np.array_equal(hy.numpy(), y.values[LEVEL][lo:hi].cpu().numpy()), "e2e result differs from resident run"
     e2e_value = owned * e2e_steps / (e2e_ms * 1e-3) / 1e9
 
@@ -311,7 +334,8 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * slots,
-                    "d2h_bytes_per_step": 8 * slots, "steps": e2e_steps},
+                    "d2h_bytes_per_step": 8 * slots, "steps": e2e_steps,
+                    "mode": "pipelined serving loop: H2D / apply / D2H of consecutive steps overlap (double-buffered)"},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
