@@ -264,8 +264,9 @@ def run_ours(args):
     # copies its inputs pinned host -> device and its result device -> pinned
     # host; consecutive steps overlap on three streams (H2D of step s+1, apply
     # of step s, D2H of step s-1 — PCIe is full duplex), double-buffered.
-    # (per rank: its own cells' slices; the per-cell rows read x of the rank's cells only)
-    lo, hi = c_begin * cs, c_end * cs
+    # (per rank: its own cells' vector — a partitioned grid stores only those)
+    lo, hi = 0, slots
+    assert x.values[LEVEL].numel() == slots
     hx = torch.empty(slots, dtype=torch.float64, pin_memory=True)
     hx.copy_(x.values[LEVEL][lo:hi].cpu())
     hys = [torch.empty(slots, dtype=torch.float64, pin_memory=True) for _ in range(2)]
@@ -324,7 +325,7 @@ def run_ours(args):
             "config": {"workload": workload, "level": LEVEL, "cells": grid.n_cells(), "slots_per_gpu": slots,
                        "owned_dofs": owned, "bc": "none",
                        "l2": "inputs larger than L2 (x+y = %.0f MB per GPU)" % (alg_bytes / 1e6),
-                       "parallelism": f"cells partitioned over {ws} ranks (NCCL interface exchange)"
+                       "parallelism": f"cells partitioned over {ws} ranks, memory-sharded vectors (NCCL interface exchange)"
                        if ws > 1 else "1 GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

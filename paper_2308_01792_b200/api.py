@@ -207,7 +207,8 @@ class Grid:
         """Restrict this handle's compute to the cell block of `rank` out of
         `nranks` (bt_grid_set_partition). `allreduce(tensor)` sums a device
         tensor over the ranks in place; default torch.distributed.all_reduce.
-        Call before compute_stencil."""
+        Call before allocating vectors and before compute_stencil: vectors of
+        a partitioned grid hold the rank's cells only (space_size is local)."""
         _check(_L.bt_grid_set_partition(self._h, rank, nranks))
         self._allreduce = allreduce
         self._xbufs = {}
@@ -483,8 +484,13 @@ def sync_broadcast(fn: FEFunction, l):
 
 
 def random_fill(fn: FEFunction, l, seed):
+    """On a partitioned grid each rank fills its own cells with their part of
+    the single-GPU stream, then the exchange broadcasts rank-spanning groups
+    (collective: every rank must call it)."""
     fn.check_level(l)
     _check(_L.bt_random_fill(fn.grid.handle, fn.descriptor.space, l, int(seed), _ptr(fn.values[l]), _stream()))
+    if fn.grid.partitioned() and fn.descriptor.space == 0:
+        _exchange(fn, l, 2)
 
 
 def zero_dirichlet(fn: FEFunction, l):

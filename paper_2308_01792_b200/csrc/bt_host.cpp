@@ -261,6 +261,10 @@ void build_topology(const Mesh& m, Topology& t) {
   }
 }
 
+int64_t part_shift(const bt_grid& g, int space, int level) {
+  return g.part_nranks > 1 ? level_slots(space, level) * g.part_begin : 0;
+}
+
 int64_t level_slots(int space, int level) {
   int64_t s = 0;
   if (space == BT_SPACE_P1 || space == BT_SPACE_P2) s += n_tet(width_formula(0, level));
@@ -744,7 +748,8 @@ int bt_num_cells(const bt_grid* g) { return g ? g->mesh.n_cells() : 0; }
 int bt_grid_min_level(const bt_grid* g) { return g->lo; }
 int bt_grid_max_level(const bt_grid* g) { return g->hi; }
 int64_t bt_space_size(const bt_grid* g, int space, int level) {
-  return level_slots(space, level) * g->mesh.n_cells();
+  // a partitioned grid's vectors hold its cell block only
+  return level_slots(space, level) * (g->part_end - g->part_begin);
 }
 
 int64_t bt_owned_dof_count(const bt_grid* g, int space, int level) {
@@ -877,27 +882,49 @@ bt_status bt_random_fill(const bt_grid* g, int space, int level, uint64_t seed, 
   BT_TRY
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
+    require_unpartitioned(g, "random_fill (edge space)");
     random_fill_edges(*g, level, seed, x, (cudaStream_t)stream);
     return BT_OK;
   }
   if (space != BT_SPACE_P1) raise(BT_INVALID_ARGUMENT, "bt_random_fill: P1 or edge space expected");
-  // fe_function.hpp:479-497: owned slots in canonical (cell, entry, t) order
+  // fe_function.hpp:479-497: owned slots in canonical (cell, entry, t) order.
+  // A partitioned grid generates its own cells' values, after discarding the
+  // draws of the owned slots of the cells before its block.
   const int n = 1 << level, w = n + 1;
-  const int64_t per = n_tet(w), total = per * g->mesh.n_cells();
-  std::vector<double> h((size_t)total, 0.0);
+  const int64_t per = n_tet(w);
+  const int cb = g->part_begin, ce = g->part_end;
+  std::vector<double> h((size_t)(per * (ce - cb)), 0.0);
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> dist(-1.0, 1.0);
-  for (int c = 0; c < g->mesh.n_cells(); ++c) {
+  {
+    // lattice points per zero set: interior n_tet(n-3), face tri(n-2), edge n-1, vertex 1
+    auto points = [&](int z) -> int64_t {
+      const int bits = __builtin_popcount((unsigned)z);
+      return bits == 0 ? n_tet(n - 3) : bits == 1 ? n_tri(n - 2) : bits == 2 ? n - 1 : 1;
+    };
+    unsigned long long skip = 0;
+    for (int c = 0; c < cb; ++c)
+      for (int z = 0; z < 15; ++z)
+        if ((g->topo.info[c].owned_by_z >> z) & 1) skip += (unsigned long long)points(z);
+    rng.discard(skip);  // one engine call per value (64-bit engine, generate_canonical<double>)
+  }
+  for (int c = cb; c < ce; ++c) {
     const uint16_t own = g->topo.info[c].owned_by_z;
-    int64_t t = per * c;
+    int64_t t = per * (c - cb);
     for (int k = 0; k < w; ++k)
       for (int j = 0; j < w - k; ++j)
         for (int i = 0; i < w - k - j; ++i, ++t)
           if ((own >> zero_set(n, i, j, k)) & 1) h[t] = dist(rng);
   }
   cudaStream_t s = (cudaStream_t)stream;
-  BT_CUDA(cudaMemcpyAsync(x, h.data(), sizeof(double) * (size_t)total, cudaMemcpyHostToDevice, s));
-  launch_interface(*g, level, IF_BCAST, x, nullptr, s, /*full=*/true);
+  BT_CUDA(cudaMemcpyAsync(x, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
+  // replicas: every group on one handle; on a partitioned grid the groups
+  // local to the rank (the caller completes rank-spanning ones with
+  // bt_xchg_pack / allreduce / bt_xchg_finish(mode 2))
+  if (g->part_nranks > 1)
+    launch_interface(*g, level, IF_BCAST, shifted(x, *g, BT_SPACE_P1, level), nullptr, s);
+  else
+    launch_interface(*g, level, IF_BCAST, x, nullptr, s, /*full=*/true);
   BT_CUDA(cudaStreamSynchronize(s));
   BT_CATCH
 }
@@ -927,7 +954,7 @@ bt_status bt_stencil_create(const bt_grid* g, const bt_form* form, int level, bt
   }
   DevBuf<double> d_tbl;
   d_tbl.upload(tbl);
-  st->d_diag.alloc((size_t)bt_space_size(g, BT_SPACE_P1, level));
+  st->d_diag.alloc((size_t)(level_slots(BT_SPACE_P1, level) * g->mesh.n_cells()));  // every cell (internal)
   launch_fill_by_z(*g, level, d_tbl.p, st->d_diag.p, 0);
   launch_interface(*g, level, IF_SYNC, st->d_diag.p, nullptr, 0, /*full=*/true);
   BT_CUDA(cudaStreamSynchronize(0));

@@ -263,9 +263,6 @@ struct bt_stencil {
   bt::DevBuf<double> d_diag;                 // assembled diagonal
   bt::FastTasks fast4, fast2;                // fast-kernel marches: 4-layer groups, the 2-layer group
   int part_begin = 0, part_end = 0;          // the grid's cell partition when the tasks were built
-  bt::DevBuf<int4> d_xtasks;                 // per-cell general rows (marches that would stage outside x)
-  bt::DevBuf<int> d_xoff;                    // cell c: d_xtasks[d_xoff[c] .. d_xoff[c + 1])
-  int nxtasks = 0, xtask_max = 0;
   bt::DevBuf<int4> d_gtasks;                 // general rows (layer 0, row 0, corner rows)
   int ngtasks = 0;
   bt::DevBuf<int4> d_atasks;                 // all rows (general-kernel fallback)
@@ -283,6 +280,14 @@ void build_stencil_cells(const bt_grid& g, const bt_form& f, int level,
 void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<EwCell>& cells,
                     std::vector<EwAngles>& angles);
 int64_t level_slots(int space, int level);  // per cell
+// Vectors of a partitioned grid hold the rank's cells [part_begin, part_end)
+// only. Kernels index by global cell, so they get the caller's pointer
+// shifted back by part_begin cells (only local cells are ever touched).
+int64_t part_shift(const bt_grid& g, int space, int level);
+template <class T>
+T* shifted(T* p, const bt_grid& g, int space, int level) {
+  return p ? p - part_shift(g, space, level) : p;
+}
 void validate_form(const bt_form* f);
 // entry points that need every group local (no exchange step) refuse a
 // partitioned grid

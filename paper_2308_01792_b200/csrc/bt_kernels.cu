@@ -469,7 +469,8 @@ bt_status bt_dot_cells(const bt_grid* g, int space, int level, const double* x, 
   require_p1(space);
   if (!per_cell) raise(BT_INVALID_ARGUMENT, "bt_dot_cells: output required");
   for (int c = 0; c < g->mesh.n_cells(); ++c) per_cell[c] = 0.0;
-  dot_p1_cells(*g, level, x, y, (cudaStream_t)stream, per_cell, nullptr);
+  dot_p1_cells(*g, level, shifted(x, *g, space, level), shifted(y, *g, space, level), (cudaStream_t)stream, per_cell,
+               nullptr);
   BT_CATCH
 }
 bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, void* stream) {
@@ -499,6 +500,8 @@ bt_status bt_sync_broadcast(const bt_grid* g, int space, int level, double* x, v
 bt_status bt_impose_dirichlet(const bt_grid* g, int level, const double* src, double* dst, void* stream) {
   BT_TRY
   check_level(g, level);
+  src = shifted(src, *g, BT_SPACE_P1, level);
+  dst = shifted(dst, *g, BT_SPACE_P1, level);
   launch_interface(*g, level, IF_IMPOSE, dst, src, (cudaStream_t)stream);
   if (g->part_nranks > 1) launch_xchg_combine(*g, level, IF_IMPOSE, dst, src, nullptr, (cudaStream_t)stream);
   BT_CATCH
@@ -506,6 +509,7 @@ bt_status bt_impose_dirichlet(const bt_grid* g, int level, const double* src, do
 bt_status bt_zero_dirichlet(const bt_grid* g, int level, double* x, void* stream) {
   BT_TRY
   check_level(g, level);
+  x = shifted(x, *g, BT_SPACE_P1, level);
   launch_interface(*g, level, IF_ZERO_DIR, x, nullptr, (cudaStream_t)stream);
   if (g->part_nranks > 1) launch_xchg_combine(*g, level, IF_ZERO_DIR, x, nullptr, nullptr, (cudaStream_t)stream);
   BT_CATCH
@@ -530,7 +534,9 @@ bt_status bt_apply_stencil_cells(const bt_stencil* st, const double* x, double* 
   BT_TRY
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
-  launch_stencil(*st, x, y, (cudaStream_t)stream);
+  const bt_grid& g = *st->grid;
+  launch_stencil(*st, shifted(x, g, BT_SPACE_P1, st->level), shifted(y, g, BT_SPACE_P1, st->level),
+                 (cudaStream_t)stream);
   BT_CATCH
 }
 

@@ -111,8 +111,10 @@ struct Win {
 // draining. Lane l stages columns base - 2 + l and base + 30 + l of each row
 // (two 8-byte cp.async, each warp-contiguous; none past the row's end), so
 // every row lands at the same place whatever its alignment and lane l reads
-// its pair (c0, c1) with one 16-byte shared load. The host keeps marches that
-// would stage outside x on the general kernel.
+// its pair (c0, c1) with one 16-byte shared load. Columns -2, -1 (lanes 0, 1
+// of column block 0) are not staged: they feed only lane 0's outputs and
+// column 0's, which are never stored. So every copy stays inside its row:
+// any march of any cell runs here, whatever the vector's extent.
 template <int N, int kMaxC>
 __global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2)) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2)) k_stencil_
         // length of stream s's current row; columns past it are never used
         const int len = s == 0 ? pr + 1 : (s <= N ? pr - (s - 1) : pr + 1 - N);
         const double* src = pcell + po[s];
-        if (pcol < len) cp8(d + s * kRowD * 8, src);
+        if ((unsigned)pcol < (unsigned)len) cp8(d + s * kRowD * 8, src);
         if (pcol + 32 < len) cp8(d + s * kRowD * 8 + 256, src + 32);
         po[s] += len;  // next row of the stream
       }
@@ -516,23 +518,15 @@ __global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, 
 
 // Any rows of the march schedule, every row read from the zero-set-typed
 // table in shared memory (interior vertices use type 0 = the merged row).
-// Block row y works on cell cell0 + y. With per_cell (nullable) its tasks are
-// tasks[per_cell[y] .. per_cell[y + 1]); otherwise every cell runs all ntasks.
+// Block row y works on cell cell0 + y; every cell runs all ntasks.
 __global__ void __launch_bounds__(kGT, 9) k_stencil_general(const double* __restrict__ x, double* __restrict__ y,
                                                         const StencilCell* __restrict__ cells,
                                                         const int4* __restrict__ tasks, int ntasks, int w,
-                                                        int64_t cell_slots, const int* __restrict__ per_cell,
-                                                        int cell0) {
+                                                        int64_t cell_slots, int cell0) {
   __shared__ double sw[16][15];
   const int cell = cell0 + blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int task = blockIdx.x * kGW + warp;
-  if (per_cell) {
-    const int first = per_cell[blockIdx.y], last = per_cell[blockIdx.y + 1];  // partition-local cell
-    if (first + (int)blockIdx.x * kGW >= last) return;  // whole block idle
-    task += first;
-    ntasks = last;
-  }
+  const int task = blockIdx.x * kGW + warp;
   {
     const double* src = cells[cell].w[0];
     for (int q = threadIdx.x; q < 16 * 15; q += blockDim.x) sw[q / 15][q % 15] = src[q];
@@ -607,10 +601,8 @@ void init_stencil_tasks(bt_stencil& st) {
   }
   if ((n - 2) % kGroup != 0 && (n - 2) % kGroup != 2)
     raise(BT_LOGIC_ERROR, "stencil: fast layer count must be 0 or 2 mod the group size");
-  // Fast tasks of every cell, in chunks of kMaxCells cells (the kernel's
-  // parameter table); longest marches first. A march whose staged columns
-  // would leave x (cell 0's first rows, the last cell's top layers) runs on
-  // the general kernel instead, as single-row tasks of that cell.
+  // Fast tasks of every cell of this handle, in chunks of kMaxCells cells
+  // (the kernel's parameter table); longest marches first.
   // Task order (BT_STENCIL_ORDER, profiling): 1 = longest march first, cells
   // interleaved (default: best balance); 0 = spatial, cells outermost (better
   // L2 reuse of staged rows, but a longer tail: measured slower).
@@ -618,12 +610,9 @@ void init_stencil_tasks(bt_stencil& st) {
     const char* e = std::getenv("BT_STENCIL_ORDER");
     return e ? std::atoi(e) : 1;
   }();
-  const int nc_all = st.grid->mesh.n_cells();
-  const int64_t cs = n_tet(w), total = cs * nc_all;
   st.part_begin = st.grid->part_begin;
   st.part_end = st.grid->part_end;
-  std::vector<std::vector<int4>> extra(nc_all);
-  auto build = [&](std::vector<int4>& list, int N, FastTasks& out) {
+  auto build = [&](std::vector<int4>& list, FastTasks& out) {
     if (order == 1)
       std::stable_sort(list.begin(), list.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
     std::vector<int4> all_fast;
@@ -635,40 +624,15 @@ void init_stencil_tasks(bt_stencil& st) {
       for (int64_t q = 0; q < ntc; ++q) {
         const int c = order == 1 ? (int)(q % cnt) : (int)(q / (int64_t)list.size());
         const int4& t = list[order == 1 ? (size_t)(q / cnt) : (size_t)(q % (int64_t)list.size())];
-        const int64_t cb = (int64_t)(c0 + c) * cs + kFastCols * t.y;
-        const int64_t lo = cb + row_start(w, t.z - 1, t.x - 1) - 2;  // C(j0 - 1), column base - 2
-        const int64_t hi = cb + row_start(w, t.w - 1, t.x + N) + 61;  // Q(j1 - 1), column base + 61
-        if (lo >= 0 && hi < total) {
-          all_fast.push_back(make_int4(t.x, t.y | (c << 16), t.z, t.w));
-        } else {
-          // the march's interior rows of its N layers
-          for (int q = 0; q < N; ++q) {
-            const int kq = t.x + q;
-            const int fe = t.y == 0 ? w - kq - 2 : w - kq - kFastCols * t.y;
-            for (int gb = 2 * t.y; gb < 2 * t.y + 2; ++gb)
-              for (int j = t.z; j < t.w && j < fe; ++j)
-                if (kGenCols * gb < w - kq - j) extra[c0 + c].push_back(make_int4(kq, gb, j, j + 1));
-          }
-        }
+        all_fast.push_back(make_int4(t.x, t.y | (c << 16), t.z, t.w));
       }
     }
     out.chunk_first.push_back((int)all_fast.size());
     out.ntasks = (int)all_fast.size();
     out.d_tasks.upload(all_fast);
   };
-  build(fast, kGroup, st.fast4);
-  build(fast2, 2, st.fast2);
-  std::vector<int4> ex;
-  std::vector<int> exoff(1, 0);  // per cell of the partition
-  for (int c = st.part_begin; c < st.part_end; ++c) {
-    ex.insert(ex.end(), extra[c].begin(), extra[c].end());
-    exoff.push_back((int)ex.size());
-  }
-  st.nxtasks = (int)ex.size();
-  st.xtask_max = 0;
-  for (auto& e : extra) st.xtask_max = std::max(st.xtask_max, (int)e.size());
-  st.d_xtasks.upload(ex);
-  st.d_xoff.upload(exoff);
+  build(fast, st.fast4);
+  build(fast2, st.fast2);
   st.ngtasks = (int)gen.size();
   st.d_gtasks.upload(gen);
   st.natasks = (int)all.size();
@@ -794,7 +758,7 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
   if (!nc) return;
   if (!st.symmetric) {
     k_stencil_general<<<dim3((st.natasks + kGW - 1) / kGW, nc), kGT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
-                                                                            st.natasks, w, cs, nullptr, c0);
+                                                                            st.natasks, w, cs, c0);
     count_launch();
     check_launch("k_stencil_general");
     return;
@@ -814,12 +778,7 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
   }
   if ((parts & 4) && st.ngtasks) {
     k_stencil_general<<<dim3((st.ngtasks + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(x, y, st.d_cells.p, st.d_gtasks.p,
-                                                                               st.ngtasks, w, cs, nullptr, c0);
-    count_launch();
-  }
-  if ((parts & 4) && st.nxtasks) {
-    k_stencil_general<<<dim3((st.xtask_max + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(
-        x, y, st.d_cells.p, st.d_xtasks.p, st.nxtasks, w, cs, st.d_xoff.p, c0);
+                                                                               st.ngtasks, w, cs, c0);
     count_launch();
   }
   BT_CUDA(cudaEventRecord(ss.join, ss.s));
@@ -847,15 +806,6 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
   }
   BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
             (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, n_tet(n + 1)};
-  // interior rows of the marches the host kept off the fast kernel (they
-  // would stage outside x) — whole rows; the boundary kernel, next on the
-  // same stream, then writes the final values of their end points
-  if (st.nxtasks) {
-    const int w = n + 1, nc = st.part_end - st.part_begin;
-    k_stencil_general<<<dim3((st.xtask_max + kGW - 1) / kGW, nc), kGT, 0, ss.s>>>(
-        x, y, st.d_cells.p, st.d_xtasks.p, st.nxtasks, w, n_tet(w), st.d_xoff.p, st.part_begin);
-    count_launch();
-  }
   const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
   const unsigned blocks = (unsigned)((pts + 127) / 128);
   if (bc)

@@ -203,7 +203,7 @@ int64_t bt_xchg_size(const bt_grid* g, int level) {
 bt_status bt_xchg_pack(const bt_grid* g, int level, const double* x, double* buf, void* stream) {
   BT_TRY
   check_partitioned_level(g, level);
-  launch_xchg_pack(*g, level, x, buf, (cudaStream_t)stream);
+  launch_xchg_pack(*g, level, shifted(x, *g, BT_SPACE_P1, level), buf, (cudaStream_t)stream);
   BT_CATCH
 }
 
@@ -217,6 +217,8 @@ bt_status bt_xchg_finish(const bt_grid* g, int level, int mode, double* x, const
   if (needs_buffer(m) && !buf && xchg_plan(*g, level).buf_size)
     raise(BT_INVALID_ARGUMENT, "bt_xchg_finish: exchange buffer required");
   cudaStream_t s = (cudaStream_t)stream;
+  x = shifted(x, *g, BT_SPACE_P1, level);
+  src = shifted(src, *g, BT_SPACE_P1, level);
   launch_interface(*g, level, m, x, src, s);
   launch_xchg_combine(*g, level, m, x, src, buf, s);
   BT_CATCH
