@@ -206,21 +206,39 @@ bt_status bt_v_cycle(bt_hierarchy* h, int level, const double* rhs, double* x,
 
 /* ---- multi-GPU: cell partition --------------------------
  * One process per GPU, each with its own bt_grid. bt_grid_set_partition
- * restricts a handle's compute to the contiguous cell block
- * [rank*nc/nranks, (rank+1)*nc/nranks). Vectors keep the full-size layout;
- * applies write only this rank's cells. Set the partition before
+ * gives a handle the contiguous cell block [rank*nc/nranks,
+ * (rank+1)*nc/nranks). Vectors are memory-sharded: on a partitioned grid
+ * every vector argument holds that block only (bt_space_size is the local
+ * size, same layout). Set the partition before allocating vectors and before
  * bt_stencil_create. Interface groups with members on several ranks go
  * through an exchange buffer of bt_xchg_size doubles:
  *   bt_apply_stencil_cells(s, x, y)     per-cell rows of this rank's cells
  *   bt_xchg_pack(g, l, y, buf)          this rank's replica values, zeros elsewhere
- *   allreduce(buf, sum) over ranks      caller's collective (NCCL / gloo)
+ *   allreduce(buf, sum) over ranks      the ranks' collective (NCCL / gloo)
  *   bt_xchg_finish(g, l, mode, y, x, buf)  local groups + member-order sums
  * mode: 0 sync_additive, 1 sync with Dirichlet identity rows (src = x),
  * 2 sync_broadcast, 3 impose_dirichlet, 4 zero_dirichlet. Replica sums run
  * in ascending cell order, so results are bitwise independent of nranks.
- * Entry points that need a full sync (bt_apply_stencil, bt_sync_*, bt_dot,
- * elementwise, transfers, hierarchies, N1E1) return BT_LOGIC_ERROR on a
- * partitioned grid. */
+ *
+ * With an allreduce hook (bt_grid_set_allreduce) the library runs that
+ * protocol itself, and every P1 entry point works on a partitioned grid as a
+ * collective (all ranks call it in the same order): bt_apply_stencil,
+ * bt_apply_elementwise, bt_extract_diagonal, bt_sync_*, bt_dot, transfers,
+ * hierarchies, smoothers, CG and the V-cycle. Without a hook they return
+ * BT_LOGIC_ERROR on a partitioned grid. bt_random_fill never calls the hook:
+ * on a partitioned grid it fills the block (its part of the single-GPU
+ * stream) and broadcasts the rank-local groups; finish with
+ * bt_exchange(mode 2). N1E1 refuses a partitioned grid.
+ *
+ * The hook sums n doubles at buf (device memory) over the ranks in place
+ * and returns 0 on success. The library synchronizes `stream` before the
+ * call and expects the result in buf when the hook returns. Every entry a
+ * rank contributes is either its own value or 0, so the sum is exact in any
+ * order. */
+typedef int (*bt_allreduce_fn)(double* buf, int64_t n, void* stream, void* user);
+bt_status bt_grid_set_allreduce(bt_grid* g, bt_allreduce_fn fn, void* user);
+/* pack + hook + finish in one call (mode as bt_xchg_finish) */
+bt_status bt_exchange(const bt_grid* g, int level, int mode, double* x, const double* src, void* stream);
 bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks);
 bt_status bt_grid_partition(const bt_grid* g, int* rank, int* nranks, int* cell_begin, int* cell_end);
 int64_t bt_xchg_size(const bt_grid* g, int level); /* -1 on error */

@@ -101,6 +101,8 @@ SIGNATURES = {
     "bt_xchg_pack": (I, [P, I, P, P, P]),
     "bt_xchg_finish": (I, [P, I, I, P, P, P, P]),
     "bt_dot_cells": (I, [P, I, I, P, P, PD, P]),
+    "bt_grid_set_allreduce": (I, [P, P, P]),
+    "bt_exchange": (I, [P, I, I, P, P, P]),
     "bt_xchg_plan_host": (I64, [C.c_char_p, I, I, I, PI64, PI64, PI32, PI32, PI32, PU8]),
 }
 

@@ -19,6 +19,8 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import math
+import traceback
+import weakref
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional
 
@@ -27,6 +29,17 @@ import torch
 
 from . import _lib
 from ._lib import bt_form, bt_multigrid_config, bt_smoother_config
+
+# bt_allreduce_fn: int (*)(double* buf, int64_t n, void* stream, void* user)
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of n fp64 values at a device pointer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
 
 _L = _lib.lib
 
@@ -208,10 +221,29 @@ class Grid:
         `nranks` (bt_grid_set_partition). `allreduce(tensor)` sums a device
         tensor over the ranks in place; default torch.distributed.all_reduce.
         Call before allocating vectors and before compute_stencil: vectors of
-        a partitioned grid hold the rank's cells only (space_size is local)."""
+        a partitioned grid hold the rank's cells only (space_size is local).
+        The library calls `allreduce` itself (bt_grid_set_allreduce) inside
+        syncs, dots, applies and solvers, which become collectives: every
+        rank calls them in the same order."""
         _check(_L.bt_grid_set_partition(self._h, rank, nranks))
         self._allreduce = allreduce
         self._xbufs = {}
+        ref = weakref.ref(self)
+        dev = self.device
+
+        def hook(ptr, n, stream, user):
+            try:
+                g = ref()
+                t = torch.as_tensor(_DeviceArray(ptr, n), device=f"cuda:{dev}")
+                g.allreduce(t)
+                torch.cuda.synchronize(dev)
+                return 0
+            except Exception:  # reported as BT_RUNTIME_ERROR by the library
+                traceback.print_exc()
+                return 1
+
+        self._hook = _ALLREDUCE_FN(hook)
+        _check(_L.bt_grid_set_allreduce(self._h, C.cast(self._hook, C.c_void_p), None))
 
     def partition(self):
         """(rank, nranks, cell_begin, cell_end)"""
@@ -428,12 +460,10 @@ def xchg_finish(fn: FEFunction, l, mode: int, buf: Optional[torch.Tensor], src: 
 
 
 def _exchange(fn: FEFunction, l, mode: int, src: Optional[FEFunction] = None):
-    g = fn.grid
-    buf = g.xchg_buffer(l)
-    if buf is not None and mode in (0, 1, 2):
-        xchg_pack(fn, l, buf)
-        g.allreduce(buf)
-    xchg_finish(fn, l, mode, buf, src)
+    """pack -> the grid's allreduce -> finish (bt_exchange)"""
+    fn.check_level(l)
+    _check(_L.bt_exchange(fn.grid.handle, l, int(mode), _ptr(fn.values[l]),
+                          _ptr(src.values[l]) if src is not None else None, _stream()))
 
 
 def dot_cells(x: FEFunction, y: FEFunction, l) -> np.ndarray:
@@ -447,13 +477,6 @@ def dot_cells(x: FEFunction, y: FEFunction, l) -> np.ndarray:
 
 def dot(x: FEFunction, y: FEFunction, l) -> float:
     _compatible(x, y, l)
-    if x.grid.partitioned():
-        per = torch.from_numpy(dot_cells(x, y, l)).to(f"cuda:{x.grid.device}")
-        x.grid.allreduce(per)
-        s = 0.0
-        for v in per.cpu().tolist():  # cells in order, as on one GPU
-            s += v
-        return s
     out = C.c_double()
     _check(_L.bt_dot(x.grid.handle, x.descriptor.space, l, _ptr(x.values[l]), _ptr(y.values[l]), C.byref(out),
                      _stream()))
@@ -466,9 +489,6 @@ def norm2(x: FEFunction, l) -> float:
 
 def sync_additive(fn: FEFunction, l):
     fn.check_level(l)
-    if fn.grid.partitioned() and fn.descriptor.space == 0:
-        _exchange(fn, l, 0)
-        return
     if fn.descriptor.space == 2:
         _check(_L.bt_n1e1_sync(fn.grid.handle, l, _ptr(fn.values[l]), _stream()))
         return
@@ -477,9 +497,6 @@ def sync_additive(fn: FEFunction, l):
 
 def sync_broadcast(fn: FEFunction, l):
     fn.check_level(l)
-    if fn.grid.partitioned() and fn.descriptor.space == 0:
-        _exchange(fn, l, 2)
-        return
     _check(_L.bt_sync_broadcast(fn.grid.handle, fn.descriptor.space, l, _ptr(fn.values[l]), _stream()))
 
 
@@ -643,10 +660,6 @@ def apply_stencil(table: StencilTable, src: FEFunction, dst: FEFunction, l, bc=B
     _require_pair(src, dst, l)
     if table.level != l or table.grid is not src.grid:
         raise InvalidArgument("apply_stencil: table/grid mismatch")
-    if src.grid.partitioned():  # this rank's cells, then the interface exchange
-        _check(_L.bt_apply_stencil_cells(table.handle, _ptr(src.values[l]), _ptr(dst.values[l]), _stream()))
-        _exchange(dst, l, 1 if int(bc) else 0, src)
-        return
     _check(_L.bt_apply_stencil(table.handle, _ptr(src.values[l]), _ptr(dst.values[l]), int(bc), _stream()))
 
 

@@ -17,7 +17,7 @@ namespace bt {
 
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }
-uint64_t g_launches = 0;
+std::atomic<uint64_t> g_launches{0};
 
 void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -921,10 +921,7 @@ bt_status bt_random_fill(const bt_grid* g, int space, int level, uint64_t seed, 
   // replicas: every group on one handle; on a partitioned grid the groups
   // local to the rank (the caller completes rank-spanning ones with
   // bt_xchg_pack / allreduce / bt_xchg_finish(mode 2))
-  if (g->part_nranks > 1)
-    launch_interface(*g, level, IF_BCAST, shifted(x, *g, BT_SPACE_P1, level), nullptr, s);
-  else
-    launch_interface(*g, level, IF_BCAST, x, nullptr, s, /*full=*/true);
+  launch_interface(*g, level, IF_BCAST, x, nullptr, s);
   BT_CUDA(cudaStreamSynchronize(s));
   BT_CATCH
 }
@@ -944,23 +941,39 @@ bt_status bt_stencil_create(const bt_grid* g, const bt_form* form, int level, bt
   build_stencil_cells(*g, *form, level, cells, st->rows);
   st->d_cells.upload(cells);
   init_stencil_tasks(*st);
-  // assembled diagonal: zero-set-typed partial diagonals, then additive sync
-  const int nc = g->mesh.n_cells();
-  std::vector<double> tbl(16 * (size_t)nc);
-  for (int c = 0; c < nc; ++c) {
-    double cls[6][16];
-    class_matrices(*g, form->kind, level, c, cls);
-    typed_diag(cls, &tbl[16 * (size_t)c]);
-  }
-  DevBuf<double> d_tbl;
-  d_tbl.upload(tbl);
-  st->d_diag.alloc((size_t)(level_slots(BT_SPACE_P1, level) * g->mesh.n_cells()));  // every cell (internal)
-  launch_fill_by_z(*g, level, d_tbl.p, st->d_diag.p, 0);
-  launch_interface(*g, level, IF_SYNC, st->d_diag.p, nullptr, 0, /*full=*/true);
   BT_CUDA(cudaStreamSynchronize(0));
   *out = st.release();
   BT_CATCH
 }
+
+}  // extern "C"
+
+// assembled diagonal (operators.hpp:277-316 for stencil tables): zero-set-typed
+// partial diagonals, then additive sync. Built on first use, because on a
+// partitioned grid the sync is a collective.
+const double* bt::stencil_diag(const bt_stencil& st, cudaStream_t s) {
+  if (st.d_diag.p) return st.d_diag.p;
+  const bt_grid& g = *st.grid;
+  const int nc = g.mesh.n_cells();
+  std::vector<double> tbl(16 * (size_t)nc);
+  for (int c = 0; c < nc; ++c) {
+    double cls[6][16];
+    class_matrices(g, st.form.kind, st.level, c, cls);
+    typed_diag(cls, &tbl[16 * (size_t)c]);
+  }
+  DevBuf<double> d_tbl;
+  d_tbl.upload(tbl);
+  DevBuf<double> diag;
+  diag.alloc((size_t)bt_space_size(&g, BT_SPACE_P1, st.level));
+  launch_fill_by_z(g, st.level, d_tbl.p, diag.p, s);
+  sync(g, st.level, IF_SYNC, diag.p, nullptr, s);
+  BT_CUDA(cudaStreamSynchronize(s));
+  std::swap(st.d_diag.p, diag.p);
+  std::swap(st.d_diag.n, diag.n);
+  return st.d_diag.p;
+}
+
+extern "C" {
 
 void bt_stencil_destroy(bt_stencil* s) { delete s; }
 
@@ -973,8 +986,8 @@ bt_status bt_stencil_rows(const bt_stencil* s, double* rows) {
 
 bt_status bt_stencil_diagonal(const bt_stencil* s, double* diag, void* stream) {
   BT_TRY
-  BT_CUDA(cudaMemcpyAsync(diag, s->d_diag.p, sizeof(double) * s->d_diag.n, cudaMemcpyDeviceToDevice,
-                          (cudaStream_t)stream));
+  const double* d = stencil_diag(*s, (cudaStream_t)stream);
+  BT_CUDA(cudaMemcpyAsync(diag, d, sizeof(double) * s->d_diag.n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   BT_CATCH
 }
 

@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(kT) k_interface(double* __restrict__ v, const 
 }
 
 template <int MODE>
-void launch_mode(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s, bool full) {
-  const IfaceLists& L = full ? g.full : g.loc;
+void launch_mode(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s) {
+  const IfaceLists& L = g.loc;
   const int n = 1 << level;
   const int64_t cs = n_tet(n + 1);
   const int fp = tri32(n - 2);
@@ -155,15 +155,16 @@ void launch_mode(const bt_grid& g, int level, double* v, const double* src, cuda
 
 }  // namespace
 
-void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s,
-                      bool full) {
+void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
+  v = shifted(v, g, BT_SPACE_P1, level);  // local -> global-cell indexing
+  src = shifted(src, g, BT_SPACE_P1, level);
   switch (mode) {
-    case IF_SYNC: launch_mode<IF_SYNC>(g, level, v, src, s, full); break;
-    case IF_SYNC_DIR: launch_mode<IF_SYNC_DIR>(g, level, v, src, s, full); break;
-    case IF_BCAST: launch_mode<IF_BCAST>(g, level, v, src, s, full); break;
-    case IF_IMPOSE: launch_mode<IF_IMPOSE>(g, level, v, src, s, full); break;
-    case IF_ZERO_DIR: launch_mode<IF_ZERO_DIR>(g, level, v, src, s, full); break;
-    case IF_ZERO_NONOWNED: launch_mode<IF_ZERO_NONOWNED>(g, level, v, src, s, full); break;
+    case IF_SYNC: launch_mode<IF_SYNC>(g, level, v, src, s); break;
+    case IF_SYNC_DIR: launch_mode<IF_SYNC_DIR>(g, level, v, src, s); break;
+    case IF_BCAST: launch_mode<IF_BCAST>(g, level, v, src, s); break;
+    case IF_IMPOSE: launch_mode<IF_IMPOSE>(g, level, v, src, s); break;
+    case IF_ZERO_DIR: launch_mode<IF_ZERO_DIR>(g, level, v, src, s); break;
+    case IF_ZERO_NONOWNED: launch_mode<IF_ZERO_NONOWNED>(g, level, v, src, s); break;
   }
 }
 

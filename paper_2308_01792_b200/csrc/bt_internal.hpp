@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <new>
@@ -50,8 +51,8 @@ void set_error(const std::string& m);
   }                                                  \
   return BT_OK;
 
-extern uint64_t g_launches;
-inline void count_launch(int n = 1) { g_launches += (uint64_t)n; }
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 void check_launch(const char* what);
 
 // Device buffer owned by the library.
@@ -217,6 +218,12 @@ struct bt_grid {
   // [part_begin, part_end) of rank part_rank out of part_nranks
   int part_rank = 0, part_nranks = 1, part_begin = 0, part_end = 0;
   mutable std::array<bt::XPlan, 11> xplan;  // per level, built on first use
+  // the ranks' sum-allreduce (bt_grid_set_allreduce): lets the library run
+  // the exchange itself inside syncs, dots and solvers
+  bt_allreduce_fn allreduce = nullptr;
+  void* allreduce_user = nullptr;
+  mutable bt::DevBuf<double> xbuf;       // exchange buffer of the library's own syncs
+  mutable bt::DevBuf<double> dot_cells;  // per-cell dot partials of every cell (partitioned dots)
   // elementwise-kernel tables per (form, level), built on first use
   mutable std::vector<std::unique_ptr<bt::EwTables>> ew_cache;
   mutable bt::DevBuf<double> ew_scratch;  // ApplyMode::Add without a caller scratch
@@ -260,7 +267,7 @@ struct bt_stencil {
   bt_form form{};
   std::vector<std::array<double, 15>> rows;  // host copy of StencilTable::rows
   bt::DevBuf<bt::StencilCell> d_cells;
-  bt::DevBuf<double> d_diag;                 // assembled diagonal
+  mutable bt::DevBuf<double> d_diag;         // assembled diagonal (this handle's cells), built on first use
   bt::FastTasks fast4, fast2;                // fast-kernel marches: 4-layer groups, the 2-layer group
   int part_begin = 0, part_end = 0;          // the grid's cell partition when the tasks were built
   bt::DevBuf<int4> d_gtasks;                 // general rows (layer 0, row 0, corner rows)
@@ -281,8 +288,9 @@ void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<E
                     std::vector<EwAngles>& angles);
 int64_t level_slots(int space, int level);  // per cell
 // Vectors of a partitioned grid hold the rank's cells [part_begin, part_end)
-// only. Kernels index by global cell, so they get the caller's pointer
-// shifted back by part_begin cells (only local cells are ever touched).
+// only; every pointer inside the library is such a local pointer. Kernels
+// index by global cell, so the launchers shift the pointer back by
+// part_begin cells (only local cells are ever touched).
 int64_t part_shift(const bt_grid& g, int space, int level);
 template <class T>
 T* shifted(T* p, const bt_grid& g, int space, int level) {
@@ -296,10 +304,18 @@ void check_level(const bt_grid* g, int level);
 
 // kernel launchers (bt_kernels.cu)
 enum IfaceMode { IF_SYNC = 0, IF_SYNC_DIR = 1, IF_BCAST = 2, IF_IMPOSE = 3, IF_ZERO_DIR = 4, IF_ZERO_NONOWNED = 5 };
-// full = false: the groups local to this handle's partition (g.loc);
-// full = true: every group (setup on full-size vectors, e.g. random_fill)
+// The groups local to this handle's partition (g.loc; every group when
+// unpartitioned). Local pointers.
 void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src,
-                      cudaStream_t s, bool full = false);
+                      cudaStream_t s);
+// Every interface group of a P1 vector, whatever the partition: the local
+// pass plus, on a partitioned grid, pack -> allreduce hook -> member-order
+// combine for rank-spanning groups (collective: every rank calls it).
+void sync(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s);
+// the grid's allreduce hook on n doubles (raises if none is set)
+void allreduce(const bt_grid& g, double* buf, int64_t n, cudaStream_t s);
+// assembled diagonal of a stencil table (collective on a partitioned grid)
+const double* stencil_diag(const bt_stencil& st, cudaStream_t s);
 // exchange for rank-spanning groups (bt_xchg.cu)
 const XPlan& xchg_plan(const bt_grid& g, int level);
 void build_xplan(const Mesh& m, const Topology& t, int level, int rank, int nranks, XPlan& out);

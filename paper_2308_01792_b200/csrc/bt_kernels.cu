@@ -53,10 +53,10 @@ template <int CK, bool DIAG>
 __global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restrict__ x, double* __restrict__ y,
                                                           const EwCell* __restrict__ cells,
                                                           const EwAngles* __restrict__ angles, double c0, double c1,
-                                                          int w, int64_t cell_slots) {
+                                                          int w, int64_t cell_slots, int cell0) {
   __shared__ EwCell sc;
   __shared__ EwAngles sa;
-  const int cell = blockIdx.y;
+  const int cell = cell0 + blockIdx.y;
   {
     const double* src = reinterpret_cast<const double*>(cells + cell);
     double* dst = reinterpret_cast<double*>(&sc);
@@ -143,10 +143,15 @@ __global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restri
 void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells,
                         const EwAngles* d_angles, const double* x, double* y, bool diag_only, cudaStream_t s) {
   const int w = (1 << level) + 1;
-  dim3 grid(ceil_div(tri32(w), kRowsPerCta), g.mesh.n_cells());
+  const int nc = g.part_end - g.part_begin;  // this handle's cells
+  if (!nc) return;
+  dim3 grid(ceil_div(tri32(w), kRowsPerCta), nc);
   const int64_t cs = n_tet(w);
-  const double c0 = ck == 0 ? c[0] : c[0], c1 = c[1];
-#define BT_EW(CK_, D_) k_elementwise<CK_, D_><<<grid, kThreads, 0, s>>>(x, y, d_cells, d_angles, c0, c1, w, cs)
+  const double c0 = c[0], c1 = c[1];
+  x = shifted(x, g, BT_SPACE_P1, level);
+  y = shifted(y, g, BT_SPACE_P1, level);
+#define BT_EW(CK_, D_) \
+  k_elementwise<CK_, D_><<<grid, kThreads, 0, s>>>(x, y, d_cells, d_angles, c0, c1, w, cs, g.part_begin)
   if (ck == 0) { if (diag_only) BT_EW(0, true); else BT_EW(0, false); }
   else if (ck == 1) { if (diag_only) BT_EW(1, true); else BT_EW(1, false); }
   else { if (diag_only) BT_EW(2, true); else BT_EW(2, false); }
@@ -159,8 +164,8 @@ void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, co
 // Row-walk helpers: fill-by-zero-set, owned dot products, transfers
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_fill_by_z(const double* __restrict__ tbl, double* __restrict__ out,
-                                                        int w, int64_t cell_slots) {
-  const int cell = blockIdx.y;
+                                                        int w, int64_t cell_slots, int cell0) {
+  const int cell = cell0 + blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = w - 1, nrows = tri32(w);
   const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
@@ -174,8 +179,10 @@ __global__ void __launch_bounds__(kThreads) k_fill_by_z(const double* __restrict
 
 void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s) {
   const int w = (1 << level) + 1;
-  dim3 grid(ceil_div(tri32(w), kRowsPerCta), g.mesh.n_cells());
-  k_fill_by_z<<<grid, kThreads, 0, s>>>(tbl, out, w, n_tet(w));
+  const int nc = g.part_end - g.part_begin;
+  if (!nc) return;
+  dim3 grid(ceil_div(tri32(w), kRowsPerCta), nc);
+  k_fill_by_z<<<grid, kThreads, 0, s>>>(tbl, shifted(out, g, BT_SPACE_P1, level), w, n_tet(w), g.part_begin);
   count_launch();
   check_launch("k_fill_by_z");
 }
@@ -247,40 +254,61 @@ __global__ void k_ordered_sum(const double* __restrict__ v, int n, double* out) 
   *out = s;
 }
 
-// owned dot over this handle's cells: per-cell sums into host[cell_begin..cell_end)
-// (total != nullptr: also their ordered sum)
+// owned dot over this handle's cells: per-cell sums into host[cell_begin..
+// cell_end) and/or into dev_cells[0 .. cells of the handle) (device); total !=
+// nullptr: also their ordered sum
 static void dot_p1_cells(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s,
-                         double* host_cells, double* total) {
+                         double* host_cells, double* total, double* dev_cells = nullptr) {
   const int w = (1 << level) + 1;
   const int bx = ceil_div(tri32(w), kRowsPerCta);
   const int nc = g.mesh.n_cells(), c0 = g.part_begin, nl = g.part_end - g.part_begin;
   const int64_t np = (int64_t)bx * nc;
   if (g.d_partials.n < (size_t)(np + nc + 1)) g.d_partials.alloc((size_t)(np + nc + 1));
-  double* cells = g.d_partials.p + np;
-  k_dot_partial<<<dim3(bx, nl), kThreads, 0, s>>>(x, y, g.d_info.p, w, n_tet(w), c0, g.d_partials.p);
-  k_cell_sums<<<ceil_div(nl, 128), 128, 0, s>>>(g.d_partials.p, bx, c0, nl, cells);
-  count_launch(2);
+  double* cells = dev_cells ? dev_cells : g.d_partials.p + np;
+  x = shifted(x, g, BT_SPACE_P1, level);
+  y = shifted(y, g, BT_SPACE_P1, level);
+  if (nl) {
+    k_dot_partial<<<dim3(bx, nl), kThreads, 0, s>>>(x, y, g.d_info.p, w, n_tet(w), c0, g.d_partials.p);
+    k_cell_sums<<<ceil_div(nl, 128), 128, 0, s>>>(g.d_partials.p, bx, c0, nl, cells);
+    count_launch(2);
+  }
   if (total) {
-    k_ordered_sum<<<1, 1, 0, s>>>(cells, nl, cells + nc);
+    k_ordered_sum<<<1, 1, 0, s>>>(cells, nl, g.d_partials.p + np + nc);
     count_launch();
   }
   check_launch("k_dot");
-  if (host_cells) BT_CUDA(cudaMemcpyAsync(host_cells + c0, cells, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
-  if (total) BT_CUDA(cudaMemcpyAsync(g.h_pinned, cells + nc, sizeof(double), cudaMemcpyDeviceToHost, s));
-  BT_CUDA(cudaStreamSynchronize(s));
+  if (host_cells && nl)
+    BT_CUDA(cudaMemcpyAsync(host_cells + c0, cells, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
+  if (total) BT_CUDA(cudaMemcpyAsync(g.h_pinned, g.d_partials.p + np + nc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (host_cells || total) BT_CUDA(cudaStreamSynchronize(s));
   if (total) *total = g.h_pinned[0];
 }
 
 double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s) {
   double t = 0.0;
-  dot_p1_cells(g, level, x, y, s, nullptr, &t);
-  return t;
+  if (g.part_nranks == 1) {
+    dot_p1_cells(g, level, x, y, s, nullptr, &t);
+    return t;
+  }
+  // partitioned: this rank's per-cell partials into an every-cell array
+  // (zeros elsewhere), allreduce, then the cells in order as on one GPU
+  const int nc = g.mesh.n_cells();
+  if (g.dot_cells.n < (size_t)nc + 1) g.dot_cells.alloc((size_t)nc + 1);
+  BT_CUDA(cudaMemsetAsync(g.dot_cells.p, 0, sizeof(double) * (size_t)nc, s));
+  dot_p1_cells(g, level, x, y, s, nullptr, nullptr, g.dot_cells.p + g.part_begin);
+  allreduce(g, g.dot_cells.p, nc, s);
+  k_ordered_sum<<<1, 1, 0, s>>>(g.dot_cells.p, nc, g.dot_cells.p + nc);
+  count_launch();
+  check_launch("k_ordered_sum");
+  BT_CUDA(cudaMemcpyAsync(g.h_pinned, g.dot_cells.p + nc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  BT_CUDA(cudaStreamSynchronize(s));
+  return g.h_pinned[0];
 }
 
 // prolongate_p1 (solvers.hpp:227-253), optionally fused with axpy(x, 1, ef)
 __global__ void __launch_bounds__(kThreads) k_prolongate(const double* __restrict__ coarse, double* __restrict__ fine,
-                                                         int wf, int add) {
-  const int cell = blockIdx.y;
+                                                         int wf, int add, int cell0) {
+  const int cell = cell0 + blockIdx.y;
   const int wc = (wf - 1) / 2 + 1;
   const double* cc = coarse + (int64_t)cell * tet32(wc);
   double* fc = fine + (int64_t)cell * tet32(wf);
@@ -320,8 +348,11 @@ __global__ void __launch_bounds__(kThreads) k_prolongate(const double* __restric
 
 void launch_prolongate(const bt_grid& g, int fine_level, const double* coarse, double* fine, bool add, cudaStream_t s) {
   const int wf = (1 << fine_level) + 1;
-  dim3 grid(ceil_div(tri32(wf), kRowsPerCta), g.mesh.n_cells());
-  k_prolongate<<<grid, kThreads, 0, s>>>(coarse, fine, wf, add ? 1 : 0);
+  const int nc = g.part_end - g.part_begin;
+  if (!nc) return;
+  dim3 grid(ceil_div(tri32(wf), kRowsPerCta), nc);
+  k_prolongate<<<grid, kThreads, 0, s>>>(shifted(coarse, g, BT_SPACE_P1, fine_level - 1),
+                                         shifted(fine, g, BT_SPACE_P1, fine_level), wf, add ? 1 : 0, g.part_begin);
   count_launch();
   check_launch("k_prolongate");
 }
@@ -331,12 +362,12 @@ void launch_prolongate(const bt_grid& g, int fine_level, const double* coarse, d
 // order, exactly the reference's scatter order; non-owned fine replicas
 // contribute 0.
 __global__ void __launch_bounds__(kThreads) k_restrict(const double* __restrict__ fine, double* __restrict__ coarse,
-                                                       const DevCellInfo* __restrict__ info, int wc) {
+                                                       const DevCellInfo* __restrict__ info, int wc, int cell0) {
   // directions sorted by (dz, dy, dx)
   constexpr int kOrd[15][3] = {{0, 0, -1}, {1, 0, -1}, {-1, 1, -1}, {0, 1, -1}, {0, -1, 0},
                                {1, -1, 0}, {-1, 0, 0}, {0, 0, 0},   {1, 0, 0},  {-1, 1, 0},
                                {0, 1, 0},  {0, -1, 1}, {1, -1, 1},  {-1, 0, 1}, {0, 0, 1}};
-  const int cell = blockIdx.y;
+  const int cell = cell0 + blockIdx.y;
   const int wf = 2 * (wc - 1) + 1, nf = wf - 1;
   const uint16_t own = info[cell].owned_by_z;
   const double* fc = fine + (int64_t)cell * tet32(wf);
@@ -365,11 +396,15 @@ __global__ void __launch_bounds__(kThreads) k_restrict(const double* __restrict_
 
 void launch_restrict(const bt_grid& g, int fine_level, const double* fine, double* coarse, cudaStream_t s) {
   const int wc = (1 << (fine_level - 1)) + 1;
-  dim3 grid(ceil_div(tri32(wc), kRowsPerCta), g.mesh.n_cells());
-  k_restrict<<<grid, kThreads, 0, s>>>(fine, coarse, g.d_info.p, wc);
-  count_launch();
-  check_launch("k_restrict");
-  launch_interface(g, fine_level - 1, IF_SYNC, coarse, nullptr, s);
+  const int nc = g.part_end - g.part_begin;
+  if (nc) {
+    dim3 grid(ceil_div(tri32(wc), kRowsPerCta), nc);
+    k_restrict<<<grid, kThreads, 0, s>>>(shifted(fine, g, BT_SPACE_P1, fine_level),
+                                         shifted(coarse, g, BT_SPACE_P1, fine_level - 1), g.d_info.p, wc, g.part_begin);
+    count_launch();
+    check_launch("k_restrict");
+  }
+  sync(g, fine_level - 1, IF_SYNC, coarse, nullptr, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -458,7 +493,6 @@ bt_status bt_dot(const bt_grid* g, int space, int level, const double* x, const 
     return BT_OK;
   }
   require_p1(space);
-  require_unpartitioned(g, "dot (use bt_dot_cells and sum the cells in order)");
   *out = dot_p1(*g, level, x, y, (cudaStream_t)stream);
   BT_CATCH
 }
@@ -469,55 +503,48 @@ bt_status bt_dot_cells(const bt_grid* g, int space, int level, const double* x, 
   require_p1(space);
   if (!per_cell) raise(BT_INVALID_ARGUMENT, "bt_dot_cells: output required");
   for (int c = 0; c < g->mesh.n_cells(); ++c) per_cell[c] = 0.0;
-  dot_p1_cells(*g, level, shifted(x, *g, space, level), shifted(y, *g, space, level), (cudaStream_t)stream, per_cell,
-               nullptr);
+  dot_p1_cells(*g, level, x, y, (cudaStream_t)stream, per_cell, nullptr);
   BT_CATCH
 }
 bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, void* stream) {
   BT_TRY
-  require_unpartitioned(g, "sync_additive");
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
+    require_unpartitioned(g, "sync_additive (edge space)");
     launch_edge_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
     return BT_OK;
   }
   require_p1(space);
-  launch_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
+  sync(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
   BT_CATCH
 }
 bt_status bt_sync_broadcast(const bt_grid* g, int space, int level, double* x, void* stream) {
   BT_TRY
-  require_unpartitioned(g, "sync_broadcast");
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
+    require_unpartitioned(g, "sync_broadcast (edge space)");
     launch_edge_interface(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
     return BT_OK;
   }
   require_p1(space);
-  launch_interface(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
+  sync(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
   BT_CATCH
 }
 bt_status bt_impose_dirichlet(const bt_grid* g, int level, const double* src, double* dst, void* stream) {
   BT_TRY
   check_level(g, level);
-  src = shifted(src, *g, BT_SPACE_P1, level);
-  dst = shifted(dst, *g, BT_SPACE_P1, level);
-  launch_interface(*g, level, IF_IMPOSE, dst, src, (cudaStream_t)stream);
-  if (g->part_nranks > 1) launch_xchg_combine(*g, level, IF_IMPOSE, dst, src, nullptr, (cudaStream_t)stream);
+  sync(*g, level, IF_IMPOSE, dst, src, (cudaStream_t)stream);  // no exchange: masks are per cell
   BT_CATCH
 }
 bt_status bt_zero_dirichlet(const bt_grid* g, int level, double* x, void* stream) {
   BT_TRY
   check_level(g, level);
-  x = shifted(x, *g, BT_SPACE_P1, level);
-  launch_interface(*g, level, IF_ZERO_DIR, x, nullptr, (cudaStream_t)stream);
-  if (g->part_nranks > 1) launch_xchg_combine(*g, level, IF_ZERO_DIR, x, nullptr, nullptr, (cudaStream_t)stream);
+  sync(*g, level, IF_ZERO_DIR, x, nullptr, (cudaStream_t)stream);  // no exchange: masks are per cell
   BT_CATCH
 }
 
 bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int bc, void* stream) {
   BT_TRY
-  require_unpartitioned(st ? st->grid : nullptr, "apply_stencil");
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   cudaStream_t s = (cudaStream_t)stream;
@@ -526,7 +553,7 @@ bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int
     return BT_OK;
   }
   launch_stencil(*st, x, y, s);
-  launch_interface(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+  sync(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
   BT_CATCH
 }
 
@@ -534,24 +561,20 @@ bt_status bt_apply_stencil_cells(const bt_stencil* st, const double* x, double* 
   BT_TRY
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
-  const bt_grid& g = *st->grid;
-  launch_stencil(*st, shifted(x, g, BT_SPACE_P1, st->level), shifted(y, g, BT_SPACE_P1, st->level),
-                 (cudaStream_t)stream);
+  launch_stencil(*st, x, y, (cudaStream_t)stream);
   BT_CATCH
 }
 
 bt_status bt_apply_stencil_interface(const bt_stencil* st, const double* x, double* y, int bc, void* stream) {
   BT_TRY
-  require_unpartitioned(st ? st->grid : nullptr, "apply_stencil_interface");
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
-  launch_interface(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, (cudaStream_t)stream);
+  sync(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, (cudaStream_t)stream);
   BT_CATCH
 }
 
 bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level, const double* x, double* y,
                                int mode, int bc, double* scratch, void* stream) {
   BT_TRY
-  require_unpartitioned(g, "apply_elementwise");
   check_level(g, level);
   validate_form(form);
   if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
@@ -570,14 +593,13 @@ bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level,
     out = scratch;
   }
   launch_elementwise(*g, level, ck, c, t.cells.p, t.angles.p, x, out, false, s);
-  launch_interface(*g, level, bc ? IF_SYNC_DIR : IF_SYNC, out, x, s);
+  sync(*g, level, bc ? IF_SYNC_DIR : IF_SYNC, out, x, s);
   if (mode == BT_MODE_ADD) launch_vec(V_AXPY, y, out, 1.0, bt_space_size(g, BT_SPACE_P1, level), s);
   BT_CATCH
 }
 
 bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, double* diag, void* stream) {
   BT_TRY
-  require_unpartitioned(g, "extract_diagonal");
   check_level(g, level);
   validate_form(form);
   cudaStream_t s = (cudaStream_t)stream;
@@ -586,14 +608,13 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
   const double one[4] = {1.0, 0.0, 0.0, 0.0};
   launch_elementwise(*g, level, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, t.cells.p, t.angles.p,
                      nullptr, diag, true, s);
-  launch_interface(*g, level, IF_SYNC, diag, nullptr, s);
+  sync(*g, level, IF_SYNC, diag, nullptr, s);
   BT_CATCH
 }
 
 bt_status bt_prolongate(const bt_grid* g, int fine_level, const double* coarse, double* fine, int add,
                         void* stream) {
   BT_TRY
-  require_unpartitioned(g, "prolongate_p1");
   check_level(g, fine_level);
   check_level(g, fine_level - 1);
   launch_prolongate(*g, fine_level, coarse, fine, add != 0, (cudaStream_t)stream);
@@ -602,7 +623,6 @@ bt_status bt_prolongate(const bt_grid* g, int fine_level, const double* coarse, 
 
 bt_status bt_restrict(const bt_grid* g, int fine_level, const double* fine, double* coarse, void* stream) {
   BT_TRY
-  require_unpartitioned(g, "restrict_p1");
   check_level(g, fine_level);
   check_level(g, fine_level - 1);
   launch_restrict(*g, fine_level, fine, coarse, (cudaStream_t)stream);

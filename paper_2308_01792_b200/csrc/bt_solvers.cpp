@@ -53,7 +53,7 @@ static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int b
     launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, L.ang.p, x, y,
                        false, s);
   }
-  launch_interface(*h.grid, l, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+  sync(*h.grid, l, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
 }
 
 static double dot(bt_hierarchy& h, int l, const double* x, const double* y, cudaStream_t s) {
@@ -70,7 +70,8 @@ static double lambda_max(bt_hierarchy& h, int l, cudaStream_t s) {
   double* z = L.z.p;
   BT_CUDA(cudaStreamSynchronize(s));
   if (bt_random_fill(h.grid, BT_SPACE_P1, l, 0x51cbu, v, s) != BT_OK) raise(BT_CUDA_ERROR, bt_last_error());
-  launch_interface(*h.grid, l, IF_ZERO_DIR, v, nullptr, s);
+  if (h.grid->part_nranks > 1) sync(*h.grid, l, IF_BCAST, v, nullptr, s);  // rank-spanning groups
+  sync(*h.grid, l, IF_ZERO_DIR, v, nullptr, s);
   const double nv = std::sqrt(dot(h, l, v, v, s));
   if (nv == 0) raise(BT_RUNTIME_ERROR, "estimate_lambda_max: empty free space");
   launch_vec(V_SCALE, v, nullptr, 1.0 / nv, n, s);
@@ -113,14 +114,14 @@ static void chebyshev(bt_hierarchy& h, const double* rhs, double* x, int l, int 
   launch_vec(V_COPY, d, r, 0.0, L.n, s);
   launch_vec(V_SCALE, d, nullptr, 1.0 / theta, L.n, s);
   launch_vec(V_AXPY, x, d, 1.0, L.n, s);
-  launch_interface(*h.grid, l, IF_IMPOSE, x, rhs, s);
+  sync(*h.grid, l, IF_IMPOSE, x, rhs, s);
   for (int k = 1; k < order; ++k) {
     scaled_residual(h, l, rhs, x, r, s);
     const double rho_new = 1.0 / (2.0 * sigma - rho);
     launch_vec(V_SCALE, d, nullptr, rho_new * rho, L.n, s);
     launch_vec(V_AXPY, d, r, 2.0 * rho_new / delta, L.n, s);
     launch_vec(V_AXPY, x, d, 1.0, L.n, s);
-    launch_interface(*h.grid, l, IF_IMPOSE, x, rhs, s);
+    sync(*h.grid, l, IF_IMPOSE, x, rhs, s);
     rho = rho_new;
   }
 }
@@ -143,7 +144,7 @@ static void smooth(bt_hierarchy& h, const bt_smoother_config& c, const double* r
     } else if (c.kind == 0) {
       scaled_residual(h, l, rhs, x, L.r.p, s);
       launch_vec(V_AXPY, x, L.r.p, c.omega, L.n, s);
-      launch_interface(*h.grid, l, IF_IMPOSE, x, rhs, s);
+      sync(*h.grid, l, IF_IMPOSE, x, rhs, s);
     } else {
       const double lam = lambda_max(h, l, s);
       chebyshev(h, rhs, x, l, c.order, c.lo * lam, c.hi * lam, s);
@@ -204,7 +205,7 @@ static void v_cycle(bt_hierarchy& h, int l, const double* rhs, double* x, const 
   launch_vec(V_SCALE, r, nullptr, -1.0, L.n, s);
   launch_vec(V_AXPY, r, rhs, 1.0, L.n, s);
   launch_restrict(*h.grid, l, r, C.b.p, s);
-  launch_interface(*h.grid, l - 1, IF_ZERO_DIR, C.b.p, nullptr, s);
+  sync(*h.grid, l - 1, IF_ZERO_DIR, C.b.p, nullptr, s);
   launch_vec(V_ASSIGN, C.x.p, nullptr, 0.0, C.n, s);
   v_cycle(h, l - 1, C.b.p, C.x.p, sm, mg, s);
   launch_prolongate(*h.grid, l, C.x.p, x, true, s);
@@ -220,7 +221,6 @@ extern "C" {
 
 bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel, bt_hierarchy** out) {
   BT_TRY
-  require_unpartitioned(g, "make_hierarchy");
   if (!g) raise(BT_INVALID_ARGUMENT, "make_hierarchy: grid required");
   validate_form(form);
   if (kernel == 1 && form->kind == BT_FORM_DIV_K_GRAD)
@@ -243,7 +243,7 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
       bt_stencil* st = nullptr;
       if (bt_stencil_create(g, form, l, &st) != BT_OK) raise(BT_INVALID_ARGUMENT, bt_last_error());
       L->stencil.reset(st);
-      BT_CUDA(cudaMemcpy(L->diag.p, st->d_diag.p, sizeof(double) * n, cudaMemcpyDeviceToDevice));
+      BT_CUDA(cudaMemcpy(L->diag.p, stencil_diag(*st, 0), sizeof(double) * n, cudaMemcpyDeviceToDevice));
     } else {
       std::vector<EwCell> cells;
       std::vector<EwAngles> angles;
@@ -254,7 +254,7 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
       static const double one[4] = {1.0, 0.0, 0.0, 0.0};
       launch_elementwise(*g, l, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, L->ew.p, L->ang.p, nullptr,
                          L->diag.p, true, 0);
-      launch_interface(*g, l, IF_SYNC, L->diag.p, nullptr, 0);
+      sync(*g, l, IF_SYNC, L->diag.p, nullptr, 0);
     }
     h->levels.push_back(std::move(L));
   }

@@ -756,6 +756,8 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
     raise(BT_LOGIC_ERROR, "apply_stencil: the grid was repartitioned after compute_stencil");
   const int c0 = st.part_begin, nc = st.part_end - st.part_begin;  // this handle's cells
   if (!nc) return;
+  x = shifted(x, *st.grid, BT_SPACE_P1, st.level);  // local -> global-cell indexing
+  y = shifted(y, *st.grid, BT_SPACE_P1, st.level);
   if (!st.symmetric) {
     k_stencil_general<<<dim3((st.natasks + kGW - 1) / kGW, nc), kGT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
                                                                             st.natasks, w, cs, c0);

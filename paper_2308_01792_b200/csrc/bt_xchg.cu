@@ -142,6 +142,7 @@ const XPlan& xchg_plan(const bt_grid& g, int level) {
 
 void launch_xchg_pack(const bt_grid& g, int level, const double* x, double* buf, cudaStream_t s) {
   const XPlan& p = xchg_plan(g, level);
+  x = shifted(x, g, BT_SPACE_P1, level);
   if (!p.buf_size) return;
   BT_CUDA(cudaMemsetAsync(buf, 0, sizeof(double) * (size_t)p.buf_size, s));
   const int n = (int)p.entries.size();
@@ -156,6 +157,8 @@ void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x,
   const XPlan& p = xchg_plan(g, level);
   const int n = (int)p.entries.size();
   if (!n) return;
+  x = shifted(x, g, BT_SPACE_P1, level);
+  src = shifted(src, g, BT_SPACE_P1, level);
   const dim3 grid((n + kT - 1) / kT);
   const XEntry* e = p.d_entries.p;
   switch (mode) {
@@ -168,6 +171,30 @@ void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x,
   }
   count_launch();
   check_launch("k_xcombine");
+}
+
+void allreduce(const bt_grid& g, double* buf, int64_t n, cudaStream_t s) {
+  if (!g.allreduce)
+    raise(BT_LOGIC_ERROR, "partitioned grid: this call needs the ranks' allreduce (bt_grid_set_allreduce)");
+  BT_CUDA(cudaStreamSynchronize(s));
+  if (g.allreduce(buf, n, (void*)s, g.allreduce_user) != 0) raise(BT_RUNTIME_ERROR, "allreduce hook failed");
+}
+
+void sync(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
+  if (g.part_nranks > 1) {
+    const XPlan& p = xchg_plan(g, level);
+    const double* buf = nullptr;
+    if (needs_buffer(mode) && p.buf_size) {
+      if (g.xbuf.n < (size_t)p.buf_size) g.xbuf.alloc((size_t)p.buf_size);
+      launch_xchg_pack(g, level, v, g.xbuf.p, s);
+      allreduce(g, g.xbuf.p, p.buf_size, s);
+      buf = g.xbuf.p;
+    }
+    launch_interface(g, level, mode, v, src, s);
+    launch_xchg_combine(g, level, mode, v, src, buf, s);
+  } else {
+    launch_interface(g, level, mode, v, src, s);
+  }
 }
 
 }  // namespace bt
@@ -203,7 +230,7 @@ int64_t bt_xchg_size(const bt_grid* g, int level) {
 bt_status bt_xchg_pack(const bt_grid* g, int level, const double* x, double* buf, void* stream) {
   BT_TRY
   check_partitioned_level(g, level);
-  launch_xchg_pack(*g, level, shifted(x, *g, BT_SPACE_P1, level), buf, (cudaStream_t)stream);
+  launch_xchg_pack(*g, level, x, buf, (cudaStream_t)stream);
   BT_CATCH
 }
 
@@ -217,10 +244,27 @@ bt_status bt_xchg_finish(const bt_grid* g, int level, int mode, double* x, const
   if (needs_buffer(m) && !buf && xchg_plan(*g, level).buf_size)
     raise(BT_INVALID_ARGUMENT, "bt_xchg_finish: exchange buffer required");
   cudaStream_t s = (cudaStream_t)stream;
-  x = shifted(x, *g, BT_SPACE_P1, level);
-  src = shifted(src, *g, BT_SPACE_P1, level);
   launch_interface(*g, level, m, x, src, s);
   launch_xchg_combine(*g, level, m, x, src, buf, s);
+  BT_CATCH
+}
+
+bt_status bt_grid_set_allreduce(bt_grid* g, bt_allreduce_fn fn, void* user) {
+  BT_TRY
+  if (!g) raise(BT_INVALID_ARGUMENT, "bt_grid_set_allreduce: grid required");
+  g->allreduce = fn;
+  g->allreduce_user = user;
+  BT_CATCH
+}
+
+bt_status bt_exchange(const bt_grid* g, int level, int mode, double* x, const double* src, void* stream) {
+  BT_TRY
+  check_partitioned_level(g, level);
+  if (mode < IF_SYNC || mode > IF_ZERO_NONOWNED) raise(BT_INVALID_ARGUMENT, "bt_exchange: bad mode");
+  const IfaceMode m = (IfaceMode)mode;
+  if ((m == IF_SYNC_DIR || m == IF_IMPOSE) && !src) raise(BT_INVALID_ARGUMENT, "bt_exchange: src required");
+  BT_CUDA(cudaSetDevice(g->device));
+  sync(*g, level, m, x, src, (cudaStream_t)stream);
   BT_CATCH
 }
 

@@ -111,9 +111,8 @@ def test_partitioned_impose_and_zero_dirichlet():
         assert not torch.isnan(yr.values[level]).any()
 
 
-def test_partitioned_grid_refuses_full_sync():
+def test_partitioned_grid_refuses_n1e1():
     g = bt.Grid(bt.cube_kuhn_text(), 2, 3)
     g.set_partition(0, 2)
-    x = bt.allocate(bt.p1_space(), g, 3, 3)
     with pytest.raises(bt.LogicError):
-        bt.apply_elementwise(bt.FormId.mass(), x, bt.allocate(bt.p1_space(), g, 3, 3), 3)
+        bt.N1E1Operator(g, 3)
