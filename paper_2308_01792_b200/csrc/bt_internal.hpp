@@ -331,6 +331,13 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
 bool stencil_fused(const bt_stencil& st);
 void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s);
 void init_stencil_tasks(bt_stencil& st);
+// a second stream (per host thread and device) for kernels that run beside
+// the main launch, with fork / join events
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream();
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c,
                         const EwCell* d_cells, const EwAngles* d_angles, const double* x, double* y,
                         bool diag_only, cudaStream_t s);

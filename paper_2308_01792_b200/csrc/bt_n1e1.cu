@@ -16,10 +16,16 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <string>
 #include <random>
 #include <vector>
 
+#include <type_traits>
+
+#include "bt_async.cuh"
 #include "bt_internal.hpp"
+#include "bt_n1e1_tables.cuh"
 
 namespace bt {
 
@@ -122,6 +128,56 @@ void build_static() {
 }
 
 
+// presence mask of the incident micro-tets of edge (i, j, k) of orientation g
+// (the face kernel's per-row intervals)
+unsigned host_mask(int g, int i, int j, int k, int n) {
+  unsigned mask = 0;
+  for (int q = 0; q < hS.ninc[g]; ++q) {
+    const IncTet& it = hS.inc[g][q];
+    const int ws = it.s == 0 ? n : (it.s == 1 ? n - 2 : n - 1);
+    const int lo = std::max(0, -it.dq[0]);
+    const int hi = (j + it.dq[1] < 0 || k + it.dq[2] < 0) ? -1 : ws - 1 - it.dq[0] - (j + it.dq[1]) - (k + it.dq[2]);
+    if (i >= lo && i <= hi) mask |= 1u << q;
+  }
+  return mask;
+}
+// the 4 mask cases of rows j, k >= 1: full, i == 0, diagonal (i + j + k == n - 1), both
+unsigned case_mask(int g, int wsel, int n) {
+  if (wsel == 0) return (1u << hS.ninc[g]) - 1;  // all incident micro-tets (no such edge at n = 4)
+  static const int rep[4][3] = {{1, 1, 1}, {0, 1, 1}, {-3, 1, 1}, {0, 1, -2}};  // negative: n + value
+  const int i = rep[wsel][0] < 0 ? n + rep[wsel][0] : rep[wsel][0];
+  const int k = rep[wsel][2] < 0 ? n + rep[wsel][2] : rep[wsel][2];
+  return host_mask(g, i, rep[wsel][1], k, n);
+}
+// k_n1e1_fast relies on: for j, k >= 1 an edge's mask depends only on
+// (i == 0, i + j + k == n - 1). Checked exhaustively at width nchk.
+void check_mask_cases(int nchk) {
+  for (int g = 1; g <= 7; ++g) {
+    const int w = g == 7 ? nchk - 1 : nchk;
+    for (int k = 1; k < w; ++k)
+      for (int j = 1; j < w - k; ++j)
+        for (int i = 0; i < w - k - j; ++i) {
+          const int wsel = (i == 0 ? 1 : 0) | (i + j + k == nchk - 1 ? 2 : 0);
+          if (host_mask(g, i, j, k, nchk) != case_mask(g, wsel, nchk))
+            raise(BT_LOGIC_ERROR, "n1e1: mask cases of rows j, k >= 1 do not hold");
+        }
+  }
+}
+// the generated coupling table (bt_n1e1_tables.cuh) must match build_static's
+void check_generated_tables() {
+  for (int g = 1; g <= 7; ++g)
+    for (int m = 0; m < hS.nnb[g]; ++m) {
+      const int s = n1_nb(g, m, 0);
+      const Nb& nb = hS.nb[g][m];
+      const int q = n1_nb(g, m, 3);
+      if (n1_stream(s, 0) != nb.g || n1_stream(s, 1) != nb.d[2] || n1_nb(g, m, 1) != nb.d[1] ||
+          n1_nb(g, m, 2) != nb.d[0] || nb.d[1] > n1_stream(s, 2) || nb.d[1] < n1_stream(s, 3) ||
+          (nb.d[0] == 0) != (q < 0) ||
+          (q >= 0 && (n1_shuf(q, 0) != s || n1_shuf(q, 1) != nb.d[1] || n1_shuf(q, 2) != nb.d[0])))
+        raise(BT_LOGIC_ERROR, "n1e1: generated coupling table differs from build_static");
+    }
+}
+
 // alpha K + beta M on the tet with corners X (same formulas as the oracle)
 void local_n1e1(const double X[4][3], double alpha, double beta, double out[36]) {
   double a[9];
@@ -177,116 +233,349 @@ struct bt_n1e1 {
   // per cell, per orientation g, per presence mask of the incident micro-tets:
   // the merged 19-weight row of the present ones (cS.mask_off / mask_rows)
   bt::DevBuf<double> d_masked;
+  // k_n1e1_fast: per cell, the merged rows of its 4 mask cases (rows j, k >= 1),
+  // and its march tasks {cell, k | block << 16, j0, j1}, longest first
+  bt::DevBuf<double> d_cellw;  // per cell: full rows (7 x kN1Wt), corrections (kN1Corr), padded
+  bt::DevBuf<int4> d_marches;  // one cell's marches {k | block << 16, j0, j1}, spatial order
+  int nmarch = 0;
+  bt::DevBuf<int> d_next;      // per cell: march queue counter
 };
 
 namespace bt {
 namespace {
 
 // ---------------------------------------------------------------------------
-// operator kernel: grid (row block x 7 orientations, cells)
+// Face rows (j = 0 or k = 0 of an orientation's lattice): one warp per row.
+// Every edge applies one merged row — the row of its present incident
+// micro-tets (presence mask from per-row intervals), from the block's shared
+// table — with straight-line loads: a coupled edge that does not exist reads
+// slot 0 with weight 0. Rows with j, k >= 1 are k_n1e1_fast's.
 // ---------------------------------------------------------------------------
-
-// Rows [rb * kRows, ...) of orientation G of one cell. Each warp walks a
-// contiguous run of rows; within a layer the neighbour row starts advance by
-// their row lengths (one add per row). Every edge applies one merged row —
-// the row of its present incident micro-tets (presence mask from per-row
-// intervals), from the block's shared table — with straight-line loads: a
-// coupled edge that does not exist reads slot 0 with weight 0.
 template <int G>
-__device__ __forceinline__ void n1e1_rows(const double* __restrict__ x, double* __restrict__ y,
-                                          const double* sM, int cell, int rb, int n, int64_t cs) {
+__device__ __forceinline__ void n1e1_row(const double* __restrict__ x, double* __restrict__ y, const double* sM,
+                                         int cell, int j, int k, int n, int64_t cs) {
   constexpr int NNB = n1e1_nnb(G), NINC = n1e1_ninc(G);
   const int wg = G == 7 ? n - 1 : n;  // subgroup width: 2^l, xyz 2^l - 1
-  const int nrows = tri32(wg);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rend = min(nrows, (rb + 1) * kRows);
+  const int lane = threadIdx.x & 31;
   const int tn = tet32(n);  // entry offsets: subgroups 1..6 have width n, xyz (7) n - 1
   auto eoff = [&](int q) { return (q - 1) * tn; };
   const double* __restrict__ xc = x + (int64_t)cell * cs;
   double* __restrict__ yc = y + (int64_t)cell * cs + eoff(G);
-  constexpr int kRpw = kRows / kW;
-  int r = rb * kRows + warp * kRpw;
-  const int rlast = min(rend, r + kRpw);
-  if (r >= rlast) return;
-  int j, k;
-  decode_row(wg, r, j, k);
   int base[NNB];
-  auto full_bases = [&]() {
 #pragma unroll
-    for (int m = 0; m < NNB; ++m) {
-      const Nb nb = cS.nb[G][m];
-      const int w2 = nb.g == 7 ? n - 1 : n;
-      base[m] = eoff(nb.g) + row_start(w2, j + nb.d[1], k + nb.d[2]) + nb.d[0];
-    }
-  };
-  full_bases();
-  for (; r < rlast; ++r) {
-    const int L = wg - j - k, t0 = row_start(wg, j, k);
-    // incident micro-tet q exists (anchor in I_tet(w_s)) for i in [lo_q, hi_q]
-    int lo[NINC], hi[NINC];
+  for (int m = 0; m < NNB; ++m) {
+    const Nb nb = cS.nb[G][m];
+    const int w2 = nb.g == 7 ? n - 1 : n;
+    base[m] = eoff(nb.g) + row_start(w2, j + nb.d[1], k + nb.d[2]) + nb.d[0];
+  }
+  const int L = wg - j - k, t0 = row_start(wg, j, k);
+  // incident micro-tet q exists (anchor in I_tet(w_s)) for i in [lo_q, hi_q]
+  int lo[NINC], hi[NINC];
 #pragma unroll
-    for (int q = 0; q < NINC; ++q) {
-      const IncTet& it = cS.inc[G][q];
-      const int ws = it.s == 0 ? n : (it.s == 1 ? n - 2 : n - 1);
-      lo[q] = max(0, -it.dq[0]);
-      hi[q] = (j + it.dq[1] < 0 || k + it.dq[2] < 0) ? -1 : ws - 1 - it.dq[0] - (j + it.dq[1]) - (k + it.dq[2]);
-    }
-    for (int i = lane; i < L; i += 32) {
-      unsigned mask = 0;
+  for (int q = 0; q < NINC; ++q) {
+    const IncTet& it = cS.inc[G][q];
+    const int ws = it.s == 0 ? n : (it.s == 1 ? n - 2 : n - 1);
+    lo[q] = max(0, -it.dq[0]);
+    hi[q] = (j + it.dq[1] < 0 || k + it.dq[2] < 0) ? -1 : ws - 1 - it.dq[0] - (j + it.dq[1]) - (k + it.dq[2]);
+  }
+  for (int i = lane; i < L; i += 32) {
+    unsigned mask = 0;
 #pragma unroll
-      for (int q = 0; q < NINC; ++q)
-        if (i >= lo[q] && i <= hi[q]) mask |= 1u << q;
-      const double* wrow = sM + NNB * mask;
-      double v[NNB];
+    for (int q = 0; q < NINC; ++q)
+      if (i >= lo[q] && i <= hi[q]) mask |= 1u << q;
+    const double* wrow = sM + NNB * mask;
+    double v[NNB];
 #pragma unroll
-      for (int m = 0; m < NNB; ++m) v[m] = __ldg(xc + ((cS.nbmask[G][m] & mask) ? base[m] + i : 0));
-      double acc = 0.0;
+    for (int m = 0; m < NNB; ++m) v[m] = __ldg(xc + ((cS.nbmask[G][m] & mask) ? base[m] + i : 0));
+    double acc = 0.0;
 #pragma unroll
-      for (int m = 0; m < NNB; ++m) acc = fma(wrow[m], v[m], acc);
-      yc[t0 + i] = acc;
-    }
-    // next row: neighbour m's row (j + dj, k + dk) of width w2 has length
-    // w2 - (k + dk) - (j + dj) = L + (w2 - wg) - dk - dj
-    if (++j < wg - k) {
-#pragma unroll
-      for (int m = 0; m < NNB; ++m) {
-        const Nb nb = cS.nb[G][m];
-        base[m] += L + ((nb.g == 7) - (G == 7)) * -1 - nb.d[2] - nb.d[1];
-      }
-    } else {
-      ++k;
-      j = 0;
-      full_bases();
-    }
+    for (int m = 0; m < NNB; ++m) acc = fma(wrow[m], v[m], acc);
+    yc[t0 + i] = acc;
   }
 }
 
-__global__ void __launch_bounds__(kT, 3) k_n1e1(const double* __restrict__ x, double* __restrict__ y,
-                                                const double* __restrict__ masked, int n, int64_t cs) {
-  // this block's (cell, orientation): its masked-row table (<= 64 rows)
+// grid (row chunk x 7 orientations, cells); orientation G's rows here are
+// q < w_G: (j = q, k = 0); q < 2 w_G - 1: (j = 0, k = q - w_G + 1); then, for
+// G != 7, the rows of length 1 with j, k >= 1: k = q - 2 w_G + 2, j = n - 1 - k
+__host__ __device__ inline int n1e1_face_rows(int g, int n) {
+  const int wg = g == 7 ? n - 1 : n;
+  return 2 * wg - 1 + (g == 7 ? 0 : max(0, n - 2));
+}
+__global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, double* __restrict__ y,
+                                                  const double* __restrict__ masked, int n, int64_t cs) {
   __shared__ double sM[64 * 19];
-  const int g = blockIdx.x % 7 + 1;  // the 7 orientations of a row block are consecutive
-  const int rb = blockIdx.x / 7;     // blocks: they gather the same rows, kept in L2
+  const int g = blockIdx.x % 7 + 1;
+  const int chunk = blockIdx.x / 7;
   const int cell = blockIdx.y;
   const int nnb = n1e1_nnb(g);
+  const int wg = g == 7 ? n - 1 : n;
+  const int q = chunk * kW + (threadIdx.x >> 5);
   {
     const double* __restrict__ src = masked + (size_t)cell * cS.mask_rows * 19 + (size_t)cS.mask_off[g] * 19;
     const int nw = (1 << n1e1_ninc(g)) * 19;
-    for (int q = threadIdx.x; q < nw; q += kT) {
-      const int row = q / 19, m = q % 19;  // repack rows to nnb weights
-      if (m < nnb) sM[row * nnb + m] = src[q];
+    for (int e = threadIdx.x; e < nw; e += kT) {
+      const int row = e / 19, m = e % 19;  // repack rows to nnb weights
+      if (m < nnb) sM[row * nnb + m] = src[e];
     }
   }
   __syncthreads();
-  switch (g) {
-    case 1: n1e1_rows<1>(x, y, sM, cell, rb, n, cs); break;
-    case 2: n1e1_rows<2>(x, y, sM, cell, rb, n, cs); break;
-    case 3: n1e1_rows<3>(x, y, sM, cell, rb, n, cs); break;
-    case 4: n1e1_rows<4>(x, y, sM, cell, rb, n, cs); break;
-    case 5: n1e1_rows<5>(x, y, sM, cell, rb, n, cs); break;
-    case 6: n1e1_rows<6>(x, y, sM, cell, rb, n, cs); break;
-    default: n1e1_rows<7>(x, y, sM, cell, rb, n, cs); break;
+  if (q >= n1e1_face_rows(g, n)) return;
+  int j, k;
+  if (q < wg) {
+    j = q;
+    k = 0;
+  } else if (q < 2 * wg - 1) {
+    j = 0;
+    k = q - wg + 1;
+  } else {
+    k = q - 2 * wg + 2;
+    j = n - 1 - k;
   }
+  switch (g) {
+    case 1: n1e1_row<1>(x, y, sM, cell, j, k, n, cs); break;
+    case 2: n1e1_row<2>(x, y, sM, cell, j, k, n, cs); break;
+    case 3: n1e1_row<3>(x, y, sM, cell, j, k, n, cs); break;
+    case 4: n1e1_row<4>(x, y, sM, cell, j, k, n, cs); break;
+    case 5: n1e1_row<5>(x, y, sM, cell, j, k, n, cs); break;
+    case 6: n1e1_row<6>(x, y, sM, cell, j, k, n, cs); break;
+    default: n1e1_row<7>(x, y, sM, cell, j, k, n, cs); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_n1e1_fast: rows j, k >= 1 (of length >= 2) of all 7 orientations, staged
+// like the P1 interior kernel. A warp owns 30 output columns i = 30b ..
+// 30b + 29 of layer k of one cell (lane l: column 30b - 1 + l; lanes 1..30
+// store) and marches rows j0 .. j1 - 1 of all 7 orientations at once. The 19
+// (13) coupled edges of an edge of orientation G lie in 31 x rows (subgroup
+// g, row j + dy, layer k + dz), dy, dz in {-1, 0, 1}, which form 16 streams
+// (g, dz) (bt_n1e1_tables.cuh). Each step stages one new row per stream —
+// row j + max dy — with one 8-byte cp.async per lane into a per-warp ring
+// (zero-filled outside the lattice), so 16 staged rows serve 7 output rows.
+// Each lane keeps its column of the last <= 3 rows of every stream in
+// registers (slot = row mod 3, compile-time per unrolled phase); the 23
+// distinct column i +- 1 values come from the neighbour lanes by shuffle.
+//
+// Block row y works on cell y; its blocks take the cell's marches from a
+// queue. The cell's weights sit in shared memory and every lane reads the
+// same address (broadcast). Rows j, k >= 1 use the full merged row, except
+// at i == 0 and on the diagonal face i + j + k == n - 1, where some incident
+// micro-tets are absent: there a correction (partial - full weight) over the
+// 33 affected couplings is added (rows of length 1, which are both, are the
+// face kernel's). Coupled edges outside the lattice read the zero fill.
+// ---------------------------------------------------------------------------
+constexpr int kN1FT = 128;
+constexpr int kN1FW = kN1FT / 32;
+constexpr int kN1Stages = 3;   // ring stages per warp (prefetch distance 2 steps)
+constexpr int kN1Cols = 30;    // output columns per warp
+constexpr int kN1March = 32;   // rows per march
+constexpr int kN1Wt = 20;      // padded weight row (19 coupled edges)
+constexpr int kN1Corr = kN1Corr0 + kN1Corr1;
+constexpr int kN1RingD = kN1Stages * kN1Streams * 32;  // doubles per warp
+constexpr int kN1CellW = 7 * kN1Wt + kN1Corr;          // per cell: full rows, then corrections (case 0, case 1)
+constexpr int kN1CellWP = (kN1CellW + 1) / 2 * 2;      // padded to 16 bytes
+constexpr int kN1BlocksPerCell = 8;
+
+template <int G, int PH>
+__device__ __forceinline__ double n1_val(const double (&win)[kN1Streams][3], const double (&sh)[kN1Shuf], int m) {
+  const int q = n1_nb(G, m, 3);
+  return q >= 0 ? sh[q] : win[n1_nb(G, m, 0)][(PH + n1_nb(G, m, 1) + 3) % 3];
+}
+
+template <int G, int PH>
+__device__ __forceinline__ double n1_edge(const double (&win)[kN1Streams][3], const double (&sh)[kN1Shuf],
+                                          const double (&w)[kN1Wt]) {
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < n1e1_nnb(G); ++m) acc = fma(w[m], n1_val<G, PH>(win, sh, m), acc);
+  return acc;
+}
+
+template <int C, int PH>
+__device__ __forceinline__ void n1_correct(const double (&win)[kN1Streams][3], const double (&sh)[kN1Shuf],
+                                           const double* __restrict__ cw, double (&e)[8]) {
+  constexpr int NQ = C == 0 ? kN1Corr0 : kN1Corr1;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int G = n1_corr(C, q, 0), m = n1_corr(C, q, 1);
+    double v;
+    switch (G) {  // compile-time after unrolling
+      case 1: v = n1_val<1, PH>(win, sh, m); break;
+      case 2: v = n1_val<2, PH>(win, sh, m); break;
+      case 3: v = n1_val<3, PH>(win, sh, m); break;
+      case 4: v = n1_val<4, PH>(win, sh, m); break;
+      case 5: v = n1_val<5, PH>(win, sh, m); break;
+      case 6: v = n1_val<6, PH>(win, sh, m); break;
+      default: v = n1_val<7, PH>(win, sh, m); break;
+    }
+    e[G] = fma(cw[(C == 0 ? 0 : kN1Corr0) + q], v, e[G]);
+  }
+}
+
+__global__ void __launch_bounds__(kN1FT, 3) k_n1e1_fast(const double* __restrict__ x, double* __restrict__ y,
+                                                        const int4* __restrict__ marches, int nmarch, int n,
+                                                        int64_t cs, const double* __restrict__ cellw,
+                                                        int* __restrict__ next_march) {
+  extern __shared__ __align__(16) double n1_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cl = blockIdx.y;  // this block's cell
+  double* sw = n1_smem;       // the cell's weights (kN1CellWP)
+  for (int q = threadIdx.x; q < kN1CellWP; q += kN1FT) sw[q] = __ldg(cellw + (size_t)cl * kN1CellWP + q);
+  __syncthreads();
+  const int GB = gridDim.x * kN1FW;
+  const int t0 = blockIdx.x * kN1FW + warp;
+  if (t0 >= nmarch) return;
+  double* ring = n1_smem + kN1CellWP + warp * kN1RingD;
+  const uint32_t my_s = smem_u32(ring) + 8u * lane;
+  const int tn = tet32(n);
+  const double* __restrict__ xc = x + (int64_t)cl * cs;
+  double* __restrict__ yc = y + (int64_t)cl * cs;
+  const double (&W)[7][kN1Wt] = *reinterpret_cast<const double(*)[7][kN1Wt]>(sw);
+
+  // ---- producer: lane copies its column of one row per stream per step ----
+  int pt = t0, pnext_t = t0, pleft = 0, pj = 0, pk = 0, pcol = 0;
+  int po[kN1Streams];
+  int4 pnext = marches[t0];
+  auto p_start = [&]() {
+    const int4 tk = pnext;
+    pk = tk.x & 0xffff;
+    pcol = kN1Cols * (tk.x >> 16) - 1 + lane;
+    pj = tk.y - 2;  // two phantom steps fill the register window
+#pragma unroll
+    for (int s = 0; s < kN1Streams; ++s) {
+      const int g = n1_stream(s, 0), w = g == 7 ? n - 1 : n;
+      po[s] = (g - 1) * tn + row_start(w, pj + n1_stream(s, 2), pk + n1_stream(s, 1)) + pcol;
+    }
+    pleft = tk.z - tk.y + 2;
+    // the warp's next march: first come, first served, so the warps of a
+    // cell stay on a compact range of its spatially ordered march list
+    int nt = 0;
+    if (lane == 0) nt = GB + atomicAdd(next_march + cl, 1);
+    pnext_t = __shfl_sync(0xffffffffu, nt, 0);
+    if (pnext_t < nmarch) pnext = marches[pnext_t];
+  };
+  p_start();
+  int ps = 0;
+  auto produce = [&]() {
+    if (pleft > 0) {
+      const uint32_t d = my_s + (uint32_t)(ps * kN1Streams * 32 * 8);
+#pragma unroll
+      for (int s = 0; s < kN1Streams; ++s) {
+        const int g = n1_stream(s, 0), w = g == 7 ? n - 1 : n;
+        const int jr = pj + n1_stream(s, 2);
+        const int len = w - jr - (pk + n1_stream(s, 1));  // staged row's length
+        const bool ok = jr >= 0 && (unsigned)pcol < (unsigned)len;
+        cp8z(d + s * 256, ok ? xc + po[s] : xc, ok);
+        po[s] += len;
+      }
+      ++pj;
+      ps = ps == kN1Stages - 1 ? 0 : ps + 1;
+      if (--pleft == 0) {
+        pt = pnext_t;
+        if (pt < nmarch) p_start();
+      }
+    }
+    cp_commit();
+  };
+#pragma unroll 1
+  for (int q = 0; q < kN1Stages - 1; ++q) produce();
+
+  // ---- consumer ----
+  int cst = 0;
+  auto consume = [&](double (&v)[kN1Streams]) {
+    cp_wait<kN1Stages - 2>();
+    __syncwarp();
+    const double* st = ring + cst * kN1Streams * 32;
+#pragma unroll
+    for (int s = 0; s < kN1Streams; ++s) v[s] = st[s * 32 + lane];
+    cst = cst == kN1Stages - 1 ? 0 : cst + 1;
+    // the stage refilled next is the one read in the previous step, ordered
+    // by the __syncwarp above
+    produce();
+  };
+
+  int t = t0;
+#pragma unroll 1
+  while (t < nmarch) {
+    const int4 tk = marches[t];
+    const int k = tk.x & 0xffff, b = tk.x >> 16, j0 = tk.y, j1 = tk.z;
+    const int i = kN1Cols * b - 1 + lane;
+    const bool out = lane >= 1 && lane <= kN1Cols;
+    int yo[7];  // this lane's output slot in orientation G's row j
+#pragma unroll
+    for (int G = 1; G <= 7; ++G) yo[G - 1] = (G - 1) * tn + row_start(G == 7 ? n - 1 : n, j0, k) + i;
+    double win[kN1Streams][3];
+    auto place = [&](auto phc, const double (&v)[kN1Streams]) {
+      constexpr int PH = decltype(phc)::value;
+#pragma unroll
+      for (int s = 0; s < kN1Streams; ++s) win[s][(PH + n1_stream(s, 2) + 3) % 3] = v[s];
+    };
+    {
+      double v[kN1Streams];
+      consume(v);
+      place(std::integral_constant<int, 0>{}, v);  // phantom step j0 - 2
+      consume(v);
+      place(std::integral_constant<int, 1>{}, v);  // phantom step j0 - 1
+    }
+    int j = j0;
+    auto step = [&](auto phc) {
+      constexpr int PH = decltype(phc)::value;
+      double v[kN1Streams];
+      consume(v);
+      place(phc, v);
+      const int L = n - j - k;  // row length of orientations 1..6 (xyz: L - 1)
+      double sh[kN1Shuf];       // column i +- 1 values, each distinct one shuffled once
+#pragma unroll
+      for (int q = 0; q < kN1Shuf; ++q) {
+        const double u = win[n1_shuf(q, 0)][(PH + n1_shuf(q, 1) + 3) % 3];
+        sh[q] = n1_shuf(q, 2) > 0 ? __shfl_down_sync(0xffffffffu, u, 1) : __shfl_up_sync(0xffffffffu, u, 1);
+      }
+      double e[8];
+      e[1] = n1_edge<1, PH>(win, sh, W[0]);
+      e[2] = n1_edge<2, PH>(win, sh, W[1]);
+      e[3] = n1_edge<3, PH>(win, sh, W[2]);
+      e[4] = n1_edge<4, PH>(win, sh, W[3]);
+      e[5] = n1_edge<5, PH>(win, sh, W[4]);
+      e[6] = n1_edge<6, PH>(win, sh, W[5]);
+      e[7] = n1_edge<7, PH>(win, sh, W[6]);
+      if (b == 0) {  // lane 1 holds i == 0
+        double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        n1_correct<0, PH>(win, sh, sw + 7 * kN1Wt, c);
+        if (i == 0)
+#pragma unroll
+          for (int G = 1; G <= 7; ++G) e[G] += c[G];
+      }
+      const int dl = L - kN1Cols * b;  // the lane holding the diagonal edge i == L - 1
+      if (dl >= 1 && dl <= kN1Cols) {
+        double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        n1_correct<1, PH>(win, sh, sw + 7 * kN1Wt, c);
+        if (i == L - 1)
+#pragma unroll
+          for (int G = 1; G <= 7; ++G) e[G] += c[G];
+      }
+      if (out && i < L) {
+#pragma unroll
+        for (int G = 1; G <= 6; ++G) yc[yo[G - 1]] = e[G];
+        if (i < L - 1) yc[yo[6]] = e[7];
+      }
+#pragma unroll
+      for (int G = 0; G < 6; ++G) yo[G] += L;
+      yo[6] += L - 1;
+      ++j;
+    };
+    while (true) {
+      step(std::integral_constant<int, 2>{});
+      if (j >= j1) break;
+      step(std::integral_constant<int, 0>{});
+      if (j >= j1) break;
+      step(std::integral_constant<int, 1>{});
+      if (j >= j1) break;
+    }
+    // the producer, 2 steps ahead and every march >= 3 steps long, is already
+    // on this warp's next march
+    t = pt;
+  }
+  cp_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -514,6 +803,20 @@ double dot_edges(const bt_grid& g, int level, const double* x, const double* y, 
   return g.h_pinned[0];
 }
 
+bool n1e1_fast_available(int level) { return (1 << level) >= 4; }
+
+constexpr size_t kN1Smem = (kN1CellWP + kN1FW * kN1RingD) * sizeof(double);
+// opt-in shared memory of k_n1e1_fast (once per device)
+void n1e1_fast_setup(int device) {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done[device]) {
+    BT_CUDA(cudaFuncSetAttribute(k_n1e1_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kN1Smem));
+    done[device] = true;
+  }
+}
+
 // mt19937_64 over owned edge slots in canonical (cell, orientation, t) order,
 // then a signed broadcast so replicas carry the same oriented field.
 void random_fill_edges(const bt_grid& g, int level, uint64_t seed, double* x, cudaStream_t s) {
@@ -588,6 +891,59 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
       }
   }
   op->d_masked.upload(masked);
+  // k_n1e1_fast: rows j, k >= 1 of every cell (n >= 4)
+  if (n1e1_fast_available(level)) {  // (n >= 4)
+    const int n = 1 << level;
+    check_generated_tables();
+    check_mask_cases(std::min(n, 64));
+    std::vector<double> cw((size_t)nc * kN1CellWP, 0.0);
+    for (int c = 0; c < nc; ++c) {
+      auto mrow = [&](int gg, unsigned mask) {
+        return &masked[((size_t)c * hS.mask_rows + hS.mask_off[gg] + mask) * 19];
+      };
+      for (int gg = 1; gg <= 7; ++gg) {
+        const double* full = mrow(gg, case_mask(gg, 0, n));
+        for (int m = 0; m < hS.nnb[gg]; ++m) cw[(size_t)c * kN1CellWP + (gg - 1) * kN1Wt + m] = full[m];
+        // corrections: every coupling outside the generated lists must keep its full weight
+        for (int cc = 0; cc < 2; ++cc) {
+          if (cc == 1 && gg == 7) continue;
+          const double* part = mrow(gg, case_mask(gg, cc == 0 ? 1 : 2, n));
+          for (int m = 0; m < hS.nnb[gg]; ++m) {
+            int q = -1;
+            const int nq = cc == 0 ? kN1Corr0 : kN1Corr1;
+            for (int e = 0; e < nq; ++e)
+              if (n1_corr(cc, e, 0) == gg && n1_corr(cc, e, 1) == m) q = e;
+            if (q < 0) {
+              if (part[m] != full[m])
+                raise(BT_LOGIC_ERROR, "n1e1: correction table misses coupling " + std::to_string(m) + " of orientation " +
+                                          std::to_string(gg) + ", case " + std::to_string(cc) + " (masks " +
+                                          std::to_string(case_mask(gg, 0, n)) + " / " +
+                                          std::to_string(case_mask(gg, cc == 0 ? 1 : 2, n)) + ")");
+            } else {
+              cw[(size_t)c * kN1CellWP + 7 * kN1Wt + (cc == 0 ? 0 : kN1Corr0) + q] = part[m] - full[m];
+            }
+          }
+        }
+      }
+    }
+    // One cell's marches in spatial order — column block, row block, layer
+    // k innermost — so the warps working on a cell at any time cover a
+    // compact region whose x rows the neighbouring layers re-read from L2.
+    // Rows j, k >= 1 of length >= 2 (orientations 1..6; xyz rows are one
+    // shorter and all covered).
+    std::vector<int4> marches;
+    for (int b = 0; kN1Cols * b <= n - 3; ++b)
+      for (int j0 = 1; j0 <= n - 2 - kN1Cols * b; j0 += kN1March)
+        for (int k = 1; k <= n - 3; ++k) {
+          const int jmax = b == 0 ? n - k - 2 : n - k - 1 - kN1Cols * b;  // last row with an output in block b
+          if (j0 > jmax) continue;
+          marches.push_back(make_int4(k | (b << 16), j0, std::min(j0 + kN1March, jmax + 1), 0));
+        }
+    op->d_cellw.upload(cw);
+    op->d_marches.upload(marches);
+    op->nmarch = (int)marches.size();
+    op->d_next.alloc((size_t)nc);
+  }
   *out = op.release();
   BT_CATCH
 }
@@ -601,9 +957,28 @@ bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, v
   const bt_grid& g = *op->grid;
   const int n = 1 << op->level;
   cudaStream_t s = (cudaStream_t)stream;
-  dim3 grid(7 * ((tri32(n) + kRows - 1) / kRows), g.mesh.n_cells());  // x: row block x 7 orientations
-  k_n1e1<<<grid, kT, 0, s>>>(x, y, op->d_masked.p, n, level_slots(BT_SPACE_EDGES, op->level));
+  const int64_t cs = level_slots(BT_SPACE_EDGES, op->level);
+  const int nc = g.mesh.n_cells();
+  // face rows (j = 0 or k = 0) and rows of length 1 of every orientation, on
+  // the side stream beside the staged kernel
+  SideStream& ss = side_stream();
+  BT_CUDA(cudaEventRecord(ss.fork, s));
+  BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  const dim3 fgrid(7 * ((n1e1_face_rows(1, n) + kW - 1) / kW), nc);
+  k_n1e1_face<<<fgrid, kT, 0, ss.s>>>(x, y, op->d_masked.p, n, cs);
   count_launch();
+  // the other rows: staged marches over all 7 orientations, kN1BlocksPerCell
+  // blocks per cell sharing the cell's march queue
+  if (op->nmarch) {
+    BT_CUDA(cudaMemsetAsync(op->d_next.p, 0, sizeof(int) * (size_t)nc, s));
+    n1e1_fast_setup(g.device);
+    const int per_cell = std::min(kN1BlocksPerCell, (op->nmarch + kN1FW - 1) / kN1FW);
+    k_n1e1_fast<<<dim3(per_cell, nc), kN1FT, kN1Smem, s>>>(x, y, op->d_marches.p, op->nmarch, n, cs,
+                                                          op->d_cellw.p, op->d_next.p);
+    count_launch();
+  }
+  BT_CUDA(cudaEventRecord(ss.join, ss.s));
+  BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
   check_launch("k_n1e1");
   launch_edge_interface(g, op->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
   BT_CATCH

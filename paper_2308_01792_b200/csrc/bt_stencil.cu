@@ -38,6 +38,7 @@
 #include <string>
 #include <vector>
 
+#include "bt_async.cuh"
 #include "bt_internal.hpp"
 
 namespace bt {
@@ -74,15 +75,6 @@ constexpr int ring_doubles() {  // per warp
   return kStages * (N + 2) * kRowD;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cp8(uint32_t dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 struct Row2 {  // one row at a lane's columns c0, c1 = c0 + 1
   double v0, v1;
@@ -676,10 +668,8 @@ void init_stencil_tasks(bt_stencil& st) {
 
 namespace {
 // side stream (per device) and fork/join events for the small kernels
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
+}  // namespace
+
 // per host thread and device, so concurrent host threads never share the
 // fork/join events
 SideStream& side_stream() {
@@ -694,7 +684,6 @@ SideStream& side_stream() {
   }
   return r;
 }
-}  // namespace
 
 // BT_STENCIL_PARTS (profiling only) drops parts of an apply: bit 0 interior
 // kernel, 1 row ends, 2 general rows, 3 fused boundary kernel.
