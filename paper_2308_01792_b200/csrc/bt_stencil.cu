@@ -45,6 +45,11 @@ namespace bt {
 
 namespace {
 constexpr int kMarchRows = 32;
+// small problems (all slots of the handle <= kSmallSlots): one launch for the
+// whole apply (k_stencil_small) and short marches, whose serial step chains
+// set the latency there
+constexpr int64_t kSmallSlots = int64_t(1) << 21;
+constexpr int kSmallMarch = 4;
 constexpr int kGroup = 4;  // layers per fast march (plus one 2-layer group); 6 measured slower (2 blocks/SM)
 constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
@@ -71,7 +76,7 @@ constexpr int kRowD = 64;  // staged columns [base - 2, base + 62)
 constexpr int kFT = 128;   // k_stencil_fast block
 constexpr int kFW = kFT / 32;
 template <int N>
-constexpr int ring_doubles() {  // per warp
+__host__ __device__ constexpr int ring_doubles() {  // per warp
   return kStages * (N + 2) * kRowD;
 }
 
@@ -107,16 +112,18 @@ struct Win {
 // of column block 0) are not staged: they feed only lane 0's outputs and
 // column 0's, which are never stored. So every copy stays inside its row:
 // any march of any cell runs here, whatever the vector's extent.
+// (body shared by k_stencil_fast and the single-launch k_stencil_small: block
+// vblock of a vgrid-block persistent grid)
 template <int N, int kMaxC>
-__global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2)) k_stencil_fast(const double* __restrict__ x, double* __restrict__ y,
-                                                        const int4* __restrict__ tasks, int ntasks, int w,
-                                                        int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
+__device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, double* __restrict__ y,
+                                                  const int4* __restrict__ tasks, int ntasks, int w,
+                                                  int64_t cell_slots, const FastParams<kMaxC>& fp, int vblock,
+                                                  int vgrid, double* ring_all) {
   constexpr int NS = N + 2;  // staged rows per step: C (layer k-1), layers k..k+N-1, Q (layer k+N)
   constexpr int kStageD = NS * kRowD;
-  extern __shared__ __align__(128) double ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = gridDim.x * kFW;
-  const int t0 = blockIdx.x * kFW + warp;
+  const int G = vgrid * kFW;
+  const int t0 = vblock * kFW + warp;
   if (t0 >= ntasks) return;
   const double* ring = ring_all + warp * ring_doubles<N>();
   const uint32_t my_s = smem_u32(ring) + 8u * lane;
@@ -276,6 +283,14 @@ __global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2)) k_stencil_
   cp_wait<0>();
 }
 
+template <int N, int kMaxC>
+__global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2))
+    k_stencil_fast(const double* __restrict__ x, double* __restrict__ y, const int4* __restrict__ tasks, int ntasks,
+                   int w, int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
+  extern __shared__ __align__(128) double ring_all[];
+  stencil_fast_body<N, kMaxC>(x, y, tasks, ntasks, w, cell_slots, fp, blockIdx.x, gridDim.x, ring_all);
+}
+
 // Both ends of every fast row (1 <= k <= n-2, j >= 1, length L >= 3): the
 // i = 0 vertex (zero set {i = 0}) and the diagonal-face vertex i = L - 1
 // (zero set {S = n}), each from its typed partial row over its 11 present
@@ -425,10 +440,11 @@ __device__ __forceinline__ double typed_partial(const double* __restrict__ x, co
 }
 
 template <bool kDir>
-__global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, double* __restrict__ y, BndArgs a) {
+__device__ __forceinline__ void boundary_body(const double* __restrict__ x, double* __restrict__ y, const BndArgs& a,
+                                              int vblock) {
   const int n = a.n, w = n + 1;
   const int fpts = tri32(n - 2);
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t q = (int64_t)vblock * blockDim.x + threadIdx.x;
   // the group: members as (cell, local-vertex map), barycentric weights
   int count, dir, nl;
   int wt[3];
@@ -508,6 +524,30 @@ __global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, 
   }
 }
 
+template <bool kDir>
+__global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, double* __restrict__ y, BndArgs a) {
+  boundary_body<kDir>(x, y, a, blockIdx.x);
+}
+
+// Small problems (one launch is latency, not bandwidth): the whole fused
+// apply in one kernel — blocks [0, b4) run the 4-layer marches, [b4, b4 + b2)
+// the 2-layer group, the rest the boundary points. The three sets of points
+// are disjoint, so the roles need no ordering.
+template <bool kDir>
+__global__ void __launch_bounds__(kFT, 3)
+    k_stencil_small(const double* __restrict__ x, double* __restrict__ y, const int4* __restrict__ t4, int n4,
+                    const int4* __restrict__ t2, int n2, int w, int64_t cell_slots, int b4, int b2, BndArgs a,
+                    const __grid_constant__ FastParams<kMaxCells> fp) {
+  extern __shared__ __align__(128) double ring_all[];
+  const int b = blockIdx.x;
+  if (b < b4)
+    stencil_fast_body<kGroup, kMaxCells>(x, y, t4, n4, w, cell_slots, fp, b, b4, ring_all);
+  else if (b < b4 + b2)
+    stencil_fast_body<2, kMaxCells>(x, y, t2, n2, w, cell_slots, fp, b - b4, b2, ring_all);
+  else
+    boundary_body<kDir>(x, y, a, b - b4 - b2);
+}
+
 // Any rows of the march schedule, every row read from the zero-set-typed
 // table in shared memory (interior vertices use type 0 = the merged row).
 // Block row y works on cell cell0 + y; every cell runs all ntasks.
@@ -560,6 +600,8 @@ __global__ void __launch_bounds__(kGT, 9) k_stencil_general(const double* __rest
 void init_stencil_tasks(bt_stencil& st) {
   const int w = (1 << st.level) + 1;
   const int n = w - 1;
+  const int march =
+      (int64_t)(st.grid->part_end - st.grid->part_begin) * n_tet(w) <= kSmallSlots ? kSmallMarch : kMarchRows;
   std::vector<int4> fast, fast2, gen, all;  // fast: groups of kGroup layers; fast2: the 2-layer group
   // general rows are unprefetched: one row per task keeps them parallel
   auto push1 = [](std::vector<int4>& v, int k, int b, int a, int e) {
@@ -587,8 +629,8 @@ void init_stencil_tasks(bt_stencil& st) {
     for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (60 wide)
       const int jmax = w - k - kFastCols * b;
       const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;  // layer k's fast rows
-      for (int j0 = 1; j0 < fe; j0 += kMarchRows)
-        (start4 ? fast : fast2).push_back(make_int4(k, b, j0, std::min(j0 + kMarchRows, fe)));
+      for (int j0 = 1; j0 < fe; j0 += march)
+        (start4 ? fast : fast2).push_back(make_int4(k, b, j0, std::min(j0 + march, fe)));
     }
   }
   if ((n - 2) % kGroup != 0 && (n - 2) % kGroup != 2)
@@ -781,10 +823,38 @@ bool stencil_fused(const bt_stencil& st) {
   return st.symmetric && st.grid->part_nranks == 1;
 }
 
+static void launch_stencil_small(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s) {
+  const bt_grid& g = *st.grid;
+  const int n = 1 << st.level, w = n + 1;
+  const int64_t cs = n_tet(w);
+  BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
+            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, cs};
+  const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
+  const int n4 = st.fast4.ntasks, n2 = st.fast2.ntasks;
+  const int b4 = (n4 + kFW - 1) / kFW, b2 = (n2 + kFW - 1) / kFW;
+  const int bb = (int)((pts + kFT - 1) / kFT);
+  const size_t smem = sizeof(double) * kFW * ring_doubles<kGroup>();
+  static std::once_flag once[2];
+  auto kern = bc ? k_stencil_small<true> : k_stencil_small<false>;
+  std::call_once(once[bc ? 1 : 0], [&] {
+    BT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
+  FastParams<kMaxCells> fp;
+  for (int c = 0; c < g.mesh.n_cells(); ++c)
+    for (int d = 0; d < 8; ++d) fp.w[c][d] = st.fast[8 * (size_t)c + d];
+  kern<<<b4 + b2 + bb, kFT, smem, s>>>(x, y, st.fast4.d_tasks.p, n4, st.fast2.d_tasks.p, n2, w, cs, b4, b2, a, fp);
+  count_launch();
+  check_launch("k_stencil_small");
+}
+
 void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s) {
   const bt_grid& g = *st.grid;
   const int n = 1 << st.level;
   const int parts = stencil_parts();
+  if (parts == 15 && g.mesh.n_cells() <= kMaxCells && (int64_t)g.mesh.n_cells() * n_tet(n + 1) <= kSmallSlots) {
+    launch_stencil_small(st, x, y, bc, s);
+    return;
+  }
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
   if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);  // first, so its persistent blocks are resident first
