@@ -175,8 +175,15 @@ def run_ours(args):
     ws, rank, local = dist_env()
     if ws > 1:
         import torch.distributed as dist
+        # one rank per GPU over NCCL; BT_BENCH_BACKEND=gloo runs the same
+        # protocol through host-staged collectives (code-path checks on one GPU)
+        backend = os.environ.get("BT_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     import paper_2308_01792_b200 as bt

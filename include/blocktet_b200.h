@@ -231,9 +231,11 @@ bt_status bt_v_cycle(bt_hierarchy* h, int level, const double* rhs, double* x,
  * bt_exchange(mode 2). N1E1 refuses a partitioned grid.
  *
  * The hook sums n doubles at buf (device memory) over the ranks in place
- * and returns 0 on success. The library synchronizes `stream` before the
- * call and expects the result in buf when the hook returns. Every entry a
- * rank contributes is either its own value or 0, so the sum is exact in any
+ * and returns 0 on success. It is stream-ordered: buf is complete once the
+ * work queued on `stream` before the call has run, and the sum must be in
+ * buf for the work queued on `stream` after it (e.g. ncclAllReduce on
+ * `stream`; a hook may also synchronize and block). Every entry a rank
+ * contributes is either its own value or 0, so the sum is exact in any
  * order. */
 typedef int (*bt_allreduce_fn)(double* buf, int64_t n, void* stream, void* user);
 bt_status bt_grid_set_allreduce(bt_grid* g, bt_allreduce_fn fn, void* user);

@@ -219,7 +219,8 @@ class Grid:
     def set_partition(self, rank: int, nranks: int, allreduce=None):
         """Restrict this handle's compute to the cell block of `rank` out of
         `nranks` (bt_grid_set_partition). `allreduce(tensor)` sums a device
-        tensor over the ranks in place; default torch.distributed.all_reduce.
+        tensor over the ranks in place, stream-ordered on the current stream
+        (or blocking); default torch.distributed.all_reduce.
         Call before allocating vectors and before compute_stencil: vectors of
         a partitioned grid hold the rank's cells only (space_size is local).
         The library calls `allreduce` itself (bt_grid_set_allreduce) inside
@@ -235,8 +236,10 @@ class Grid:
             try:
                 g = ref()
                 t = torch.as_tensor(_DeviceArray(ptr, n), device=f"cuda:{dev}")
-                g.allreduce(t)
-                torch.cuda.synchronize(dev)
+                # stream-ordered: the collective is queued on the library's stream
+                s = torch.cuda.ExternalStream(stream, device=dev) if stream else torch.cuda.default_stream(dev)
+                with torch.cuda.stream(s):
+                    g.allreduce(t)
                 return 0
             except Exception:  # reported as BT_RUNTIME_ERROR by the library
                 traceback.print_exc()

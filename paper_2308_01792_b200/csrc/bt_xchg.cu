@@ -176,7 +176,7 @@ void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x,
 void allreduce(const bt_grid& g, double* buf, int64_t n, cudaStream_t s) {
   if (!g.allreduce)
     raise(BT_LOGIC_ERROR, "partitioned grid: this call needs the ranks' allreduce (bt_grid_set_allreduce)");
-  BT_CUDA(cudaStreamSynchronize(s));
+  // stream-ordered: the hook enqueues the collective on s (or blocks until done)
   if (g.allreduce(buf, n, (void*)s, g.allreduce_user) != 0) raise(BT_RUNTIME_ERROR, "allreduce hook failed");
 }
 
