@@ -204,6 +204,35 @@ bt_status bt_v_cycle(bt_hierarchy* h, int level, const double* rhs, double* x,
                      const bt_smoother_config* sm, const bt_multigrid_config* mg,
                      void* stream);                                     /* :509 */
 
+/* ---- model-problem tools: interpolation, L2 error, full multigrid ---------
+ * A device-evaluable scalar field replaces the reference's std::function
+ * (same kinds as the div_k_grad coefficient): 0 c0; 1 c0 + c1 sin(c2 x)
+ * sin(c2 y) sin(c2 z); 2 c0 + c1 x + c2 y + c3 z. */
+typedef struct {
+  int kind;
+  double c[4];
+} bt_field;
+/* interpolate (fe_function.hpp:454-477), P1: x = f at every vertex, then
+ * sync_broadcast (collective on a partitioned grid) */
+bt_status bt_interpolate(const bt_grid* g, int level, const bt_field* f, double* x, void* stream);
+/* l2_error (solvers.hpp:613-648): || u_h - exact ||_L2 by the 4-point rule per
+ * micro-cell */
+bt_status bt_l2_error(const bt_grid* g, int level, const double* x, const bt_field* exact, double* out,
+                      void* stream);
+typedef struct {      /* IterationRow (solvers.hpp:21) */
+  int level, cycle;
+  double residual;    /* relative to the level's rhs norm */
+  double error;       /* l2_error against `exact`, 0 without one */
+} bt_fmg_row;
+/* fmg (solvers.hpp:547-604): CG on the coarse level, then per finer level
+ * prolongate, impose the level's Dirichlet values and run mg->cycles
+ * V-cycles. rhs_levels[i] belongs to level coarse_level + i; x (level
+ * finest) receives the solution. rows: 1 + cycles * (finest - coarse_level)
+ * entries (max_rows checked). exact may be NULL. */
+bt_status bt_fmg(bt_hierarchy* h, int finest, const double* const* rhs_levels, double* x,
+                 const bt_smoother_config* sm, const bt_multigrid_config* mg, const bt_field* exact,
+                 bt_fmg_row* rows, int max_rows, int* nrows, void* stream);
+
 /* ---- multi-GPU: cell partition --------------------------
  * One process per GPU, each with its own bt_grid. bt_grid_set_partition
  * gives a handle the contiguous cell block [rank*nc/nranks,

@@ -403,6 +403,46 @@ inline void v_cycle(GridHierarchy& h, Level l, const FEFunction& rhs, FEFunction
   check(bt_v_cycle(h.handle.get(), l, rhs.device(l), x.device(l), &s, &m, nullptr));
 }
 
+// ---- model-problem tools: interpolate, l2_error, fmg ------------------------
+// The std::function arguments become device-evaluable Coefficient fields.
+namespace detail {
+inline bt_field c_field(const Coefficient& f) { return bt_field{f.kind, {f.c[0], f.c[1], f.c[2], f.c[3]}}; }
+}  // namespace detail
+inline void interpolate(FEFunction& fn, Level l, const Coefficient& f) {  // fe_function.hpp:454 (P1)
+  const bt_field c = detail::c_field(f);
+  check(bt_interpolate(fn.grid->handle(), l, &c, fn.device(l), nullptr));
+}
+inline double l2_error(const FEFunction& fn, Level l, const Coefficient& exact) {  // solvers.hpp:613
+  const bt_field c = detail::c_field(exact);
+  double out = 0;
+  check(bt_l2_error(fn.grid->handle(), l, fn.device(l), &c, &out, nullptr));
+  return out;
+}
+// fmg (solvers.hpp:547); `exact` replaces the error callback (nullptr: no errors)
+inline IterationReport fmg(GridHierarchy& h, Level finest, const std::vector<FEFunction>& rhs_levels, FEFunction& x,
+                           const SmootherConfig& sm, const MultigridConfig& mg,
+                           const Coefficient* exact = nullptr) {
+  if (finest < mg.coarse_level) throw std::invalid_argument("fmg: finest below coarse level");
+  if ((int)rhs_levels.size() != finest - mg.coarse_level + 1)
+    throw std::invalid_argument("fmg: one rhs per level expected");
+  std::vector<const double*> ptrs;
+  for (size_t i = 0; i < rhs_levels.size(); ++i) ptrs.push_back(rhs_levels[i].device(mg.coarse_level + (int)i));
+  std::vector<bt_fmg_row> rows((size_t)(1 + mg.cycles * (finest - mg.coarse_level)));
+  int n = 0;
+  const bt_smoother_config s = sm.c_config();
+  const bt_multigrid_config m = mg.c_config();
+  bt_field ex{};
+  if (exact) ex = detail::c_field(*exact);
+  check(bt_fmg(h.handle.get(), finest, ptrs.data(), x.device(finest), &s, &m, exact ? &ex : nullptr, rows.data(),
+               (int)rows.size(), &n, nullptr));
+  IterationReport rep;
+  for (int i = 0; i < n; ++i) rep.rows.push_back({rows[i].level, rows[i].cycle, rows[i].residual, rows[i].error, 0.0});
+  rep.iterations = mg.cycles * (finest - mg.coarse_level);
+  rep.residual = n ? rows[n - 1].residual : 0.0;
+  rep.converged = true;
+  return rep;
+}
+
 // ---- N1E1 curl-curl + mass (no reference implementation) -------------------
 struct N1E1Operator {
   std::shared_ptr<const Grid> grid;

@@ -154,6 +154,10 @@ def load_reference():
     lib.ref_cg.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int, _P, _P, _P, C.POINTER(C.c_int)]
     lib.ref_vcycles.argtypes = [C.c_void_p, C.c_int, _P, C.c_int, C.c_double, C.c_int, C.c_int, _P, _P, _P, _P]
     lib.ref_zero_dirichlet.argtypes = [C.c_void_p, C.c_int, _P]
+    lib.ref_interpolate.argtypes = [C.c_void_p, C.c_int, _P, _P]
+    lib.ref_l2_error.argtypes = [C.c_void_p, C.c_int, _P, _P, _P]
+    lib.ref_fmg.argtypes = [C.c_void_p, C.c_int, _P, C.c_int, C.c_double, C.c_int, C.c_int, _P, _P, _P, _P,
+                            C.POINTER(C.c_int)]
     lib.ref_time_apply.restype = C.c_double
     lib.ref_time_apply.argtypes = [C.c_void_p, C.c_int, C.c_int, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P]
     lib.ref_subgroup_offsets.argtypes = [C.c_int, _PI32]
@@ -526,6 +530,29 @@ class Reference(_Base):
         if seconds is not None:
             seconds[:] = secs
         return x, hist
+
+    def interpolate(self, level, fp):
+        """fp = (kind, c0, c1, c2, c3) as kparams"""
+        out = self.zeros(level)
+        self._chk(self.lib.ref_interpolate(self.h, level, _dp(np.asarray(fp, np.float64)), _dp(out)))
+        return out
+
+    def l2_error(self, level, x, fp):
+        out = np.zeros(1)
+        self._chk(self.lib.ref_l2_error(self.h, level, _dp(np.ascontiguousarray(x)),
+                                        _dp(np.asarray(fp, np.float64)), _dp(out)))
+        return float(out[0])
+
+    def fmg(self, finest, sm, rhs_levels, coarse_level, cycles, coarse_tol=1e-12, coarse_maxit=4000, fp=None):
+        """rows (level, cycle, residual, error) and the finest solution"""
+        rhs = np.ascontiguousarray(np.concatenate(rhs_levels))
+        x = self.zeros(finest)
+        rows = np.zeros(4 * (1 + cycles * (finest - coarse_level)))
+        n = C.c_int()
+        fpa = _dp(np.asarray(fp, np.float64)) if fp is not None else None
+        self._chk(self.lib.ref_fmg(self.h, finest, _dp(_sm(sm)), coarse_level, coarse_tol, coarse_maxit, cycles,
+                                   _dp(rhs), _dp(x), fpa, _dp(rows), C.byref(n)))
+        return rows[: 4 * n.value].reshape(-1, 4), x
 
     def time_apply(self, level, x, kind=0, form=0, kp=None, bc=0, reps=3, threads=1):
         kp = kparams() if kp is None else np.asarray(kp, np.float64)

@@ -9,6 +9,7 @@
 // Flat array convention (matches FEFunction::values[level][cell][entry],
 // fe_function.hpp:237-238): one level, cells outer, entries next, slots inner.
 #include <cstdint>
+#include <functional>
 #include <cstring>
 #include <chrono>
 #include <cmath>
@@ -396,6 +397,71 @@ int ref_vcycles(void* h, int l, const double* sm, int coarse_level, double coars
       hist[cyc] = resid();
     }
     store(u, l, x);
+  });
+}
+
+// Model-problem fields, same kinds as make_form's coefficient: p = {kind, c0, c1, c2, c3}.
+std::function<double(Vec3)> make_field(const double* p) {
+  const int kind = static_cast<int>(p[0]);
+  const double c0 = p[1], c1 = p[2], c2 = p[3], c3 = p[4];
+  if (kind == 0) return [c0](Vec3) { return c0; };
+  if (kind == 1)
+    return [c0, c1, c2](Vec3 x) { return c0 + c1 * std::sin(c2 * x.x) * std::sin(c2 * x.y) * std::sin(c2 * x.z); };
+  return [c0, c1, c2, c3](Vec3 x) { return c0 + c1 * x.x + c2 * x.y + c3 * x.z; };
+}
+
+int ref_interpolate(void* h, int l, const double* fp, double* out) {
+  Ctx& c = *static_cast<Ctx*>(h);
+  return guarded([&] {
+    FEFunction u = allocate(p1_space(), c.grid, l, l);
+    interpolate(u, l, make_field(fp));
+    store(u, l, out);
+  });
+}
+
+int ref_l2_error(void* h, int l, const double* x, const double* fp, double* out) {
+  Ctx& c = *static_cast<Ctx*>(h);
+  return guarded([&] {
+    FEFunction u = allocate(p1_space(), c.grid, l, l);
+    load(u, l, x);
+    *out = l2_error(u, l, make_field(fp));
+  });
+}
+
+// Full multigrid from the given per-level right-hand sides (rhs_all: levels
+// coarse_level..finest concatenated); x receives the finest solution; rows:
+// 4 doubles (level, cycle, residual, error) each, error against fp (NULL: none).
+int ref_fmg(void* h, int finest, const double* sm, int coarse_level, double coarse_tol, int coarse_maxit,
+            int cycles, const double* rhs_all, double* x, const double* fp, double* rows, int* nrows) {
+  Ctx& c = *static_cast<Ctx*>(h);
+  return guarded([&] {
+    MultigridConfig mg;
+    mg.coarse_level = coarse_level;
+    mg.coarse_tol = coarse_tol;
+    mg.coarse_maxit = coarse_maxit;
+    mg.cycles = cycles;
+    std::vector<FEFunction> rhs;
+    std::int64_t off = 0;
+    for (int l = coarse_level; l <= finest; ++l) {
+      rhs.push_back(allocate(p1_space(), c.grid, l, l));
+      load(rhs.back(), l, rhs_all + off);
+      off += level_size(rhs.back(), l);
+    }
+    FEFunction u = allocate(p1_space(), c.grid, finest, finest);
+    std::function<double(const FEFunction&, Level)> err;
+    if (fp) {
+      const auto f = make_field(fp);
+      err = [f](const FEFunction& v, Level l) { return l2_error(v, l, f); };
+    }
+    const IterationReport rep = fmg(*c.hier, finest, rhs, u, make_smoother(sm), mg, err);
+    for (std::size_t i = 0; i < rep.rows.size(); ++i) {
+      rows[4 * i] = rep.rows[i].level;
+      rows[4 * i + 1] = rep.rows[i].cycle;
+      rows[4 * i + 2] = rep.rows[i].residual;
+      rows[4 * i + 3] = rep.rows[i].error;
+    }
+    *nrows = static_cast<int>(rep.rows.size());
+    store(u, finest, x);
   });
 }
 

@@ -32,6 +32,14 @@ class bt_smoother_config(C.Structure):
                 ("hi", C.c_double), ("nu1", C.c_int), ("nu2", C.c_int)]
 
 
+class bt_field(C.Structure):
+    _fields_ = [("kind", C.c_int), ("c", C.c_double * 4)]
+
+
+class bt_fmg_row(C.Structure):
+    _fields_ = [("level", C.c_int), ("cycle", C.c_int), ("residual", C.c_double), ("error", C.c_double)]
+
+
 class bt_multigrid_config(C.Structure):
     _fields_ = [("coarse_level", C.c_int), ("cycles", C.c_int), ("coarse_tol", C.c_double),
                 ("coarse_maxit", C.c_int)]
@@ -91,6 +99,10 @@ SIGNATURES = {
     "bt_smooth": (I, [P, C.POINTER(bt_smoother_config), P, P, I, I, I, P]),
     "bt_cg": (I, [P, I, D, I, P, P, PD, PI, P]),
     "bt_v_cycle": (I, [P, I, P, P, C.POINTER(bt_smoother_config), C.POINTER(bt_multigrid_config), P]),
+    "bt_interpolate": (I, [P, I, C.POINTER(bt_field), P, P]),
+    "bt_l2_error": (I, [P, I, P, C.POINTER(bt_field), PD, P]),
+    "bt_fmg": (I, [P, I, C.POINTER(P), P, C.POINTER(bt_smoother_config), C.POINTER(bt_multigrid_config),
+                   C.POINTER(bt_field), C.POINTER(bt_fmg_row), I, PI, P]),
     "bt_n1e1_create": (I, [P, I, D, D, C.POINTER(P)]),
     "bt_n1e1_destroy": (None, [P]),
     "bt_apply_n1e1": (I, [P, P, P, I, P]),

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import bt_form, bt_multigrid_config, bt_smoother_config
+from ._lib import bt_field, bt_fmg_row, bt_form, bt_multigrid_config, bt_smoother_config
 
 # bt_allreduce_fn: int (*)(double* buf, int64_t n, void* stream, void* user)
 _ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
@@ -815,11 +815,21 @@ def smooth(h: GridHierarchy, cfg: SmootherConfig, rhs: FEFunction, x: FEFunction
 
 
 @dataclass
+class IterationRow:
+    """IterationRow (solvers.hpp:21); `seconds` is not reported."""
+    level: int
+    cycle: int
+    residual: float
+    error: float
+
+
+@dataclass
 class IterationReport:
     residuals: List[float]
     iterations: int
     residual: float
     converged: bool
+    rows: List[IterationRow] = field(default_factory=list)
 
 
 def cg(h: GridHierarchy, rhs: FEFunction, x: FEFunction, l, tol, maxit) -> IterationReport:
@@ -833,6 +843,61 @@ def cg(h: GridHierarchy, rhs: FEFunction, x: FEFunction, l, tol, maxit) -> Itera
     res = list(hist[: it.value])
     r = res[-1] if res else 0.0
     return IterationReport(res, it.value, r, bool(res) and r <= tol)
+
+
+def _field(f: Coefficient):
+    s = bt_field()
+    s.kind = int(f.kind)
+    for i, v in enumerate(f.c):
+        s.c[i] = v
+    return s
+
+
+def interpolate(fn: FEFunction, l, f: Coefficient):
+    """interpolate (fe_function.hpp:454-477) for P1 functions; the function
+    is a device-evaluable field (Coefficient kinds) instead of a callable."""
+    fn.check_level(l)
+    if fn.descriptor.space != 0:
+        raise InvalidArgument("interpolate: P1 functions only")
+    s = _field(f)
+    _check(_L.bt_interpolate(fn.grid.handle, l, C.byref(s), _ptr(fn.values[l]), _stream()))
+
+
+def l2_error(fn: FEFunction, l, exact: Coefficient) -> float:
+    """l2_error (solvers.hpp:613-648)."""
+    fn.check_level(l)
+    if fn.descriptor.space != 0:
+        raise InvalidArgument("l2_error: P1 functions only")
+    s = _field(exact)
+    out = C.c_double()
+    _check(_L.bt_l2_error(fn.grid.handle, l, _ptr(fn.values[l]), C.byref(s), C.byref(out), _stream()))
+    return out.value
+
+
+def fmg(h: GridHierarchy, finest, rhs_levels: List[FEFunction], x: FEFunction, sm: SmootherConfig,
+        mg: MultigridConfig, exact: Optional[Coefficient] = None) -> IterationReport:
+    """fmg (solvers.hpp:547-604). rhs_levels[i] belongs to level
+    mg.coarse_level + i; `exact` (a field) replaces the error callback with
+    l2_error against it."""
+    if finest < mg.coarse_level:
+        raise InvalidArgument("fmg: finest below coarse level")
+    if len(rhs_levels) != finest - mg.coarse_level + 1:
+        raise InvalidArgument("fmg: one rhs per level expected")
+    x.check_level(finest)
+    ptrs = (C.c_void_p * len(rhs_levels))()
+    for i, r in enumerate(rhs_levels):
+        r.check_level(mg.coarse_level + i)
+        ptrs[i] = _ptr(r.values[mg.coarse_level + i])
+    nmax = 1 + mg.cycles * (finest - mg.coarse_level)
+    rows = (bt_fmg_row * nmax)()
+    n = C.c_int()
+    s, m = sm.c_struct(), mg.c_struct()
+    ex = _field(exact) if exact is not None else None
+    _check(_L.bt_fmg(h.handle, finest, ptrs, _ptr(x.values[finest]), C.byref(s), C.byref(m),
+                     C.byref(ex) if ex is not None else None, rows, nmax, C.byref(n), _stream()))
+    out = [IterationRow(rows[i].level, rows[i].cycle, rows[i].residual, rows[i].error) for i in range(n.value)]
+    return IterationReport([r.residual for r in out], mg.cycles * (finest - mg.coarse_level),
+                           out[-1].residual if out else 0.0, True, out)
 
 
 def v_cycle(h: GridHierarchy, l, rhs: FEFunction, x: FEFunction, sm: SmootherConfig, mg: MultigridConfig):

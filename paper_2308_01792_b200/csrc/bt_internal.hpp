@@ -229,6 +229,7 @@ struct bt_grid {
   mutable bt::DevBuf<double> ew_scratch;  // ApplyMode::Add without a caller scratch
   // reduction scratch for dot products
   mutable bt::DevBuf<double> d_partials;
+  mutable bt::DevBuf<double> d_maps;  // per cell: the affine map (a row-major, b), built on first use
   mutable double* h_pinned = nullptr;
   ~bt_grid();
 };
@@ -344,6 +345,8 @@ void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const doubl
 void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStream_t s);
 void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s);
 double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s);
+// l2_error (solvers.hpp:613-648) of a P1 function against a field (collective when partitioned)
+double l2_error_p1(const bt_grid& g, int level, const double* x, const bt_field& f, cudaStream_t s);
 // edge space (N1E1, bt_n1e1.cu): signed replica sync / broadcast, Dirichlet rows
 void launch_edge_interface(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src,
                            cudaStream_t s);

@@ -408,6 +408,181 @@ void launch_restrict(const bt_grid& g, int fine_level, const double* fine, doubl
 }
 
 // ---------------------------------------------------------------------------
+// interpolate (fe_function.hpp:454-477, P1) and l2_error (solvers.hpp:613-648).
+// Coordinates follow micro_vertex_coord (micro_index.hpp:266-271) and
+// MacroCellMap::map (coarse_mesh.hpp:87) in the reference's operation order,
+// unfused (_rn intrinsics).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double eval_field(const bt_field& f, double x, double y, double z) {
+  if (f.kind == 0) return f.c[0];
+  if (f.kind == 1) {
+    const double s = __dmul_rn(__dmul_rn(__dmul_rn(f.c[1], sin(__dmul_rn(f.c[2], x))), sin(__dmul_rn(f.c[2], y))),
+                               sin(__dmul_rn(f.c[2], z)));
+    return __dadd_rn(f.c[0], s);
+  }
+  return __dadd_rn(__dadd_rn(__dadd_rn(f.c[0], __dmul_rn(f.c[1], x)), __dmul_rn(f.c[2], y)), __dmul_rn(f.c[3], z));
+}
+__device__ __forceinline__ void map_vertex(const double* __restrict__ m, double h, int i, int j, int k,
+                                           double out[3]) {
+  const double r0 = __dmul_rn(h, (double)i), r1 = __dmul_rn(h, (double)j), r2 = __dmul_rn(h, (double)k);
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    out[d] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[3 * d], r0), __dmul_rn(m[3 * d + 1], r1)),
+                                 __dmul_rn(m[3 * d + 2], r2)),
+                       m[9 + d]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_interpolate(double* __restrict__ out, const double* __restrict__ maps,
+                                                          bt_field f, int w, int64_t cell_slots, int cell0) {
+  const int cell = cell0 + blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrows = tri32(w);
+  const double h = 1.0 / (double)(w - 1);
+  const double* m = maps + 12 * (size_t)cell;
+  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int j, k;
+    decode_row(w, r, j, k);
+    const int L = w - j - k, t0 = row_start(w, j, k);
+    for (int i = lane; i < L; i += 32) {
+      double p[3];
+      map_vertex(m, h, i, j, k, p);
+      out[(int64_t)cell * cell_slots + t0 + i] = eval_field(f, p[0], p[1], p[2]);
+    }
+  }
+}
+
+// one block per (row chunk, cell, class s): sum over the class's micro-cells
+// anchored in the chunk's rows; partial[(cell * 6 + s) * gridDim.x + chunk]
+__global__ void __launch_bounds__(kThreads) k_l2_error(const double* __restrict__ x, const double* __restrict__ maps,
+                                                       bt_field f, int n, int64_t cell_slots, int cell0,
+                                                       double* __restrict__ partial) {
+  __shared__ double red[kWarps];
+  constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
+  const int cell = cell0 + blockIdx.y, s = blockIdx.z;
+  const int ws = s == 0 ? n : (s == 1 ? n - 2 : n - 1);  // class widths (micro_index.hpp:97-121)
+  const int wv = n + 1;
+  const double h = 1.0 / (double)n;
+  const double* m = maps + 12 * (size_t)cell;
+  const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
+  const double qa = (5.0 + 3.0 * sqrt(5.0)) / 20.0, qb = (5.0 - sqrt(5.0)) / 20.0;  // forms.hpp:56-66
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc = 0.0;
+  if (ws > 0) {
+    const int nrows = tri32(ws);
+    const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
+    for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+      int j, k;
+      decode_row(ws, r, j, k);
+      const int L = ws - j - k;
+      for (int i = lane; i < L; i += 32) {
+        double c[4][3], v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int a = i + kOff[s][q][0], b = j + kOff[s][q][1], e = k + kOff[s][q][2];
+          map_vertex(m, h, a, b, e, c[q]);
+          v[q] = __ldg(xc + row_start(wv, b, e) + a);
+        }
+        double u[3], w2[3], z[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          u[d] = __dsub_rn(c[1][d], c[0][d]);
+          w2[d] = __dsub_rn(c[2][d], c[0][d]);
+          z[d] = __dsub_rn(c[3][d], c[0][d]);
+        }
+        const double cx = __dsub_rn(__dmul_rn(w2[1], z[2]), __dmul_rn(w2[2], z[1]));
+        const double cy = __dsub_rn(__dmul_rn(w2[2], z[0]), __dmul_rn(w2[0], z[2]));
+        const double cz = __dsub_rn(__dmul_rn(w2[0], z[1]), __dmul_rn(w2[1], z[0]));
+        const double vol =
+            fabs(__dadd_rn(__dadd_rn(__dmul_rn(u[0], cx), __dmul_rn(u[1], cy)), __dmul_rn(u[2], cz))) / 6.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double xq[3] = {0.0, 0.0, 0.0}, uh = 0.0;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const double bw = t == q ? qa : qb;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) xq[d] = __dadd_rn(xq[d], __dmul_rn(c[t][d], bw));
+            uh = __dadd_rn(uh, __dmul_rn(v[t], bw));
+          }
+          const double diff = __dsub_rn(uh, eval_field(f, xq[0], xq[1], xq[2]));
+          acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(vol, 0.25), diff), diff));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < kWarps; ++q) t += red[q];
+    partial[((int64_t)blockIdx.y * 6 + s) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+static const double* cell_maps(const bt_grid& g) {
+  if (!g.d_maps.p) {
+    std::vector<double> m(12 * (size_t)g.mesh.n_cells());
+    for (int c = 0; c < g.mesh.n_cells(); ++c) {
+      for (int q = 0; q < 9; ++q) m[12 * (size_t)c + q] = g.topo.maps[c].a[q];
+      for (int d = 0; d < 3; ++d) m[12 * (size_t)c + 9 + d] = g.topo.maps[c].b[d];
+    }
+    g.d_maps.upload(m);
+  }
+  return g.d_maps.p;
+}
+
+static void launch_interpolate(const bt_grid& g, int level, const bt_field& f, double* x, cudaStream_t s) {
+  const int w = (1 << level) + 1, nc = g.part_end - g.part_begin;
+  if (nc) {
+    dim3 grid(ceil_div(tri32(w), kRowsPerCta), nc);
+    k_interpolate<<<grid, kThreads, 0, s>>>(shifted(x, g, BT_SPACE_P1, level), cell_maps(g), f, w, n_tet(w),
+                                            g.part_begin);
+    count_launch();
+    check_launch("k_interpolate");
+  }
+  sync(g, level, IF_BCAST, x, nullptr, s);  // replicas bitwise identical (fe_function.hpp:476)
+}
+
+double l2_error_p1(const bt_grid& g, int level, const double* x, const bt_field& f, cudaStream_t s) {
+  const int n = 1 << level, nc = g.mesh.n_cells(), nl = g.part_end - g.part_begin;
+  const int bx = std::max(1, ceil_div(tri32(n), kRowsPerCta));
+  std::vector<double> per_cell(nc, 0.0);
+  if (nl) {
+    DevBuf<double> part((size_t)nl * 6 * bx);
+    k_l2_error<<<dim3(bx, nl, 6), kThreads, 0, s>>>(shifted(x, g, BT_SPACE_P1, level), cell_maps(g), f, n,
+                                                    n_tet(n + 1), g.part_begin, part.p);
+    count_launch();
+    check_launch("k_l2_error");
+    std::vector<double> h(part.n);
+    BT_CUDA(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * part.n, cudaMemcpyDeviceToHost, s));
+    BT_CUDA(cudaStreamSynchronize(s));
+    for (int c = 0; c < nl; ++c) {
+      double t = 0.0;
+      for (size_t q = 0; q < (size_t)6 * bx; ++q) t += h[(size_t)c * 6 * bx + q];
+      per_cell[g.part_begin + c] = t;
+    }
+  }
+  if (g.part_nranks > 1) {  // every cell's sum, then the cells in order as on one GPU
+    if (g.dot_cells.n < (size_t)nc + 1) g.dot_cells.alloc((size_t)nc + 1);
+    BT_CUDA(cudaMemcpyAsync(g.dot_cells.p, per_cell.data(), sizeof(double) * nc, cudaMemcpyHostToDevice, s));
+    allreduce(g, g.dot_cells.p, nc, s);
+    BT_CUDA(cudaMemcpyAsync(per_cell.data(), g.dot_cells.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    BT_CUDA(cudaStreamSynchronize(s));
+  }
+  double acc = 0.0;
+  for (int c = 0; c < nc; ++c) acc += per_cell[c];
+  return std::sqrt(acc);
+}
+
+static void validate_field(const bt_field* f) {
+  if (!f) raise(BT_INVALID_ARGUMENT, "a field is required");
+  if (f->kind < 0 || f->kind > 2) raise(BT_INVALID_ARGUMENT, "field kind must be 0, 1 or 2");
+}
+
+// ---------------------------------------------------------------------------
 // Streaming vector kernels (fe_function.hpp:324-371, solvers.hpp:53-64).
 // Explicit _rn intrinsics keep the reference's unfused rounding.
 // ---------------------------------------------------------------------------
@@ -609,6 +784,24 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
   launch_elementwise(*g, level, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, t.cells.p, t.angles.p,
                      nullptr, diag, true, s);
   sync(*g, level, IF_SYNC, diag, nullptr, s);
+  BT_CATCH
+}
+
+bt_status bt_interpolate(const bt_grid* g, int level, const bt_field* f, double* x, void* stream) {
+  BT_TRY
+  check_level(g, level);
+  validate_field(f);
+  launch_interpolate(*g, level, *f, x, (cudaStream_t)stream);
+  BT_CATCH
+}
+
+bt_status bt_l2_error(const bt_grid* g, int level, const double* x, const bt_field* exact, double* out,
+                      void* stream) {
+  BT_TRY
+  check_level(g, level);
+  validate_field(exact);
+  if (!out) raise(BT_INVALID_ARGUMENT, "l2_error: output required");
+  *out = l2_error_p1(*g, level, x, *exact, (cudaStream_t)stream);
   BT_CATCH
 }
 

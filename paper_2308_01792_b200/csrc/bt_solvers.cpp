@@ -212,6 +212,57 @@ static void v_cycle(bt_hierarchy& h, int l, const double* rhs, double* x, const 
   smooth(h, sm, rhs, x, l, sm.nu2, 1, s);
 }
 
+// relative residual ||b - A v|| / ||b|| with Dirichlet identity rows (fmg's
+// relative_residual, solvers.hpp:558-566)
+static double relative_residual(bt_hierarchy& h, int l, const double* b, const double* v, double* r,
+                                cudaStream_t s) {
+  const int64_t n = h.at(l).n;
+  hier_apply(h, l, v, r, 1, s);
+  launch_vec(V_SCALE, r, nullptr, -1.0, n, s);
+  launch_vec(V_AXPY, r, b, 1.0, n, s);
+  const double nb = std::sqrt(dot(h, l, b, b, s));
+  return std::sqrt(dot(h, l, r, r, s)) / (nb > 0 ? nb : 1.0);
+}
+
+// fmg (solvers.hpp:547-604)
+static int fmg(bt_hierarchy& h, int finest, const double* const* rhs, double* x, const bt_smoother_config& sm,
+               const bt_multigrid_config& mg, const bt_field* exact, bt_fmg_row* rows, int max_rows,
+               cudaStream_t s) {
+  const int cl = mg.coarse_level;
+  if (finest < cl) raise(BT_INVALID_ARGUMENT, "fmg: finest below coarse level");
+  if (cl < h.grid->lo || finest > h.grid->hi) raise(BT_OUT_OF_RANGE, "fmg: levels outside the hierarchy");
+  if (!rhs) raise(BT_INVALID_ARGUMENT, "fmg: one rhs per level expected");
+  for (int l = cl; l <= finest; ++l)
+    if (!rhs[l - cl]) raise(BT_INVALID_ARGUMENT, "fmg: one rhs per level expected");
+  const int need = 1 + mg.cycles * (finest - cl);
+  if (!rows || max_rows < need) raise(BT_INVALID_ARGUMENT, "fmg: row buffer too small");
+  int nrows = 0;
+  auto row = [&](int l, int cyc, const double* b, const double* v, double* r) {
+    const double res = relative_residual(h, l, b, v, r, s);
+    rows[nrows++] = bt_fmg_row{l, cyc, res, exact ? l2_error_p1(*h.grid, l, v, *exact, s) : 0.0};
+  };
+  DevBuf<double> cur(h.at(cl).n), tmp(h.at(cl).n);
+  BT_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(double) * cur.n, s));
+  sync(*h.grid, cl, IF_IMPOSE, cur.p, rhs[0], s);
+  cg(h, cl, mg.coarse_tol, mg.coarse_maxit, rhs[0], cur.p, nullptr, s);
+  row(cl, 0, rhs[0], cur.p, tmp.p);
+  for (int l = cl + 1; l <= finest; ++l) {
+    const double* b = rhs[l - cl];
+    DevBuf<double> next(h.at(l).n), r(h.at(l).n);
+    launch_prolongate(*h.grid, l, cur.p, next.p, false, s);
+    sync(*h.grid, l, IF_IMPOSE, next.p, b, s);
+    for (int cyc = 1; cyc <= mg.cycles; ++cyc) {
+      v_cycle(h, l, b, next.p, sm, mg, s);
+      row(l, cyc, b, next.p, r.p);
+    }
+    std::swap(cur.p, next.p);
+    std::swap(cur.n, next.n);
+  }
+  BT_CUDA(cudaMemcpyAsync(x, cur.p, sizeof(double) * cur.n, cudaMemcpyDeviceToDevice, s));
+  BT_CUDA(cudaStreamSynchronize(s));
+  return nrows;
+}
+
 }  // namespace bt
 
 using namespace bt;
@@ -296,6 +347,17 @@ bt_status bt_cg(bt_hierarchy* h, int level, double tol, int maxit, const double*
   BT_TRY
   const int it = cg(*h, level, tol, maxit, rhs, x, hist, (cudaStream_t)stream);
   if (iterations) *iterations = it;
+  BT_CATCH
+}
+
+bt_status bt_fmg(bt_hierarchy* h, int finest, const double* const* rhs_levels, double* x,
+                 const bt_smoother_config* sm, const bt_multigrid_config* mg, const bt_field* exact,
+                 bt_fmg_row* rows, int max_rows, int* nrows, void* stream) {
+  BT_TRY
+  if (!h || !sm || !mg || !x) raise(BT_INVALID_ARGUMENT, "fmg: hierarchy, configs and x required");
+  if (exact && (exact->kind < 0 || exact->kind > 2)) raise(BT_INVALID_ARGUMENT, "field kind must be 0, 1 or 2");
+  const int nr = fmg(*h, finest, rhs_levels, x, *sm, *mg, exact, rows, max_rows, (cudaStream_t)stream);
+  if (nrows) *nrows = nr;
   BT_CATCH
 }
 

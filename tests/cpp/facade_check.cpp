@@ -93,6 +93,25 @@ int main(int argc, char** argv) {
     for (int c = 0; c < 3; ++c) v_cycle(h, l, rhs, u, sm, mg);
     dump(dir + "/rhs.bin", rhs.values(l));
     dump(dir + "/u.bin", u.values(l));
+    // full multigrid of the model problem (solvers.hpp:547): second-order errors
+    const Coefficient uex = Coefficient::sin_product(0.0, 1.0, M_PI);
+    const Coefficient f = Coefficient::sin_product(0.0, 3.0 * M_PI * M_PI, M_PI);
+    std::vector<FEFunction> rhs_levels;
+    for (int q = 2; q <= l; ++q) {
+      auto fi = allocate(p1_space(), g, q, q), b = allocate(p1_space(), g, q, q);
+      interpolate(fi, q, f);
+      apply_elementwise(FormId::mass(), fi, b, q);
+      zero_dirichlet(b, q);
+      rhs_levels.push_back(std::move(b));
+    }
+    auto xf = allocate(p1_space(), g, l, l);
+    MultigridConfig fm = mg;
+    fm.cycles = 3;
+    fm.coarse_maxit = 200;
+    const IterationReport rep = fmg(h, l, rhs_levels, xf, sm, fm, &uex);
+    EXPECT((int)rep.rows.size() == 1 + 3 * (l - 2));
+    EXPECT(rep.rows.back().error > 0 && rep.rows.back().error < rep.rows.front().error);
+    std::printf("fmg error %.6e\n", rep.rows.back().error);
     std::printf("owned %lld dot %.17g\n", (long long)owned_dof_count(x, l), dot(x, y, l));
     return 0;
   }

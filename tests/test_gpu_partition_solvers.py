@@ -175,3 +175,42 @@ def test_partitioned_without_hook_raises():
         bt.sync_additive(x, 3)
     with pytest.raises(bt.LogicError):
         bt.dot(x, x, 3)
+
+
+def fmg_body(text, lo, hi):
+    U = bt.Coefficient.sin_product(0.0, 1.0, math.pi)
+    F = bt.Coefficient.sin_product(0.0, 3.0 * math.pi ** 2, math.pi)
+
+    def body(setup):
+        g = bt.Grid(text, lo, hi)
+        setup(g)
+        h = bt.make_hierarchy(g, bt.FormId.diffusion(), bt.KernelKind.Elementwise)
+        rhs = []
+        for l in range(lo, hi + 1):
+            f = bt.allocate(bt.p1_space(), g, l, l)
+            bt.interpolate(f, l, F)
+            b = bt.allocate(bt.p1_space(), g, l, l)
+            bt.apply_elementwise(bt.FormId.mass(), f, b, l)
+            bt.zero_dirichlet(b, l)
+            rhs.append(b)
+        x = bt.allocate(bt.p1_space(), g, hi, hi)
+        sm = bt.SmootherConfig.chebyshev(2)
+        sm.nu1 = sm.nu2 = 2
+        mg = bt.MultigridConfig(coarse_level=lo, cycles=2, coarse_tol=0.0, coarse_maxit=30)
+        rep = bt.fmg(h, hi, rhs, x, sm, mg, exact=U)
+        torch.cuda.synchronize()
+        return {"part": g.partition(), "x": x.values[hi].clone(),
+                "rows": [(r.level, r.cycle, r.residual, r.error) for r in rep.rows]}
+    return body
+
+
+def test_partitioned_fmg():
+    text, lo, hi = bt.cubes_mesh_text(2, 0.1, 0), 2, 4
+    body = fmg_body(text, lo, hi)
+    full = body(lambda g: None)
+    ranks = run_ranks(3, body)
+    cs = bt.n_tet((1 << hi) + 1)
+    for out in ranks:
+        _, _, b, e = out["part"]
+        assert torch.equal(out["x"], full["x"][b * cs:e * cs])
+        assert out["rows"] == full["rows"]  # residuals and L2 errors bitwise
