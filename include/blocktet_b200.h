@@ -204,6 +204,14 @@ bt_status bt_v_cycle(bt_hierarchy* h, int level, const double* rhs, double* x,
                      const bt_smoother_config* sm, const bt_multigrid_config* mg,
                      void* stream);                                     /* :509 */
 
+/* gauss_seidel_sweep (operators.hpp:327-387): in-place lexicographic
+ * Gauss-Seidel on every cell's interior (bitwise the sequential order, by
+ * hyperplane wavefronts), then Jacobi with the assembled diagonal on the
+ * synced residual at the other vertices; Dirichlet rows pinned to rhs.
+ * scratch: a P1 vector of the table's level (NULL: allocated per call). */
+bt_status bt_gauss_seidel_sweep(const bt_stencil* table, const double* rhs, double* x, int backward,
+                                double* scratch, void* stream);
+
 /* ---- model-problem tools: interpolation, L2 error, full multigrid ---------
  * A device-evaluable scalar field replaces the reference's std::function
  * (same kinds as the div_k_grad coefficient): 0 c0; 1 c0 + c1 sin(c2 x)

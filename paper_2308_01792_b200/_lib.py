@@ -99,6 +99,7 @@ SIGNATURES = {
     "bt_smooth": (I, [P, C.POINTER(bt_smoother_config), P, P, I, I, I, P]),
     "bt_cg": (I, [P, I, D, I, P, P, PD, PI, P]),
     "bt_v_cycle": (I, [P, I, P, P, C.POINTER(bt_smoother_config), C.POINTER(bt_multigrid_config), P]),
+    "bt_gauss_seidel_sweep": (I, [P, P, P, I, P, P]),
     "bt_interpolate": (I, [P, I, C.POINTER(bt_field), P, P]),
     "bt_l2_error": (I, [P, I, P, C.POINTER(bt_field), PD, P]),
     "bt_fmg": (I, [P, I, C.POINTER(P), P, C.POINTER(bt_smoother_config), C.POINTER(bt_multigrid_config),

@@ -845,6 +845,18 @@ def cg(h: GridHierarchy, rhs: FEFunction, x: FEFunction, l, tol, maxit) -> Itera
     return IterationReport(res, it.value, r, bool(res) and r <= tol)
 
 
+def gauss_seidel_sweep(table: StencilTable, rhs: FEFunction, x: FEFunction, l, direction=None, threads=1):
+    """gauss_seidel_sweep (operators.hpp:327-387): lexicographic Gauss-Seidel on
+    each cell's interior (hyperplane wavefronts, bitwise the sequential
+    order), then Jacobi on the other vertices with the assembled diagonal."""
+    _require_pair(rhs, x, l)
+    if table.level != l or table.grid is not x.grid:
+        raise InvalidArgument("gauss_seidel_sweep: table/grid mismatch")
+    backward = direction is not None and int(direction) == int(SweepDirection.Backward)
+    _check(_L.bt_gauss_seidel_sweep(table.handle, _ptr(rhs.values[l]), _ptr(x.values[l]), int(backward), None,
+                                    _stream()))
+
+
 def _field(f: Coefficient):
     s = bt_field()
     s.kind = int(f.kind)

@@ -332,6 +332,9 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
 bool stencil_fused(const bt_stencil& st);
 void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s);
 void init_stencil_tasks(bt_stencil& st);
+// one hybrid Gauss-Seidel sweep (operators.hpp:327-387); scratch: a P1 vector
+void launch_gs_sweep(const bt_stencil& st, const double* rhs, double* x, double* scratch, bool backward,
+                     cudaStream_t s);
 // a second stream (per host thread and device) for kernels that run beside
 // the main launch, with fork / join events
 struct SideStream {

@@ -787,6 +787,22 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
   BT_CATCH
 }
 
+bt_status bt_gauss_seidel_sweep(const bt_stencil* table, const double* rhs, double* x, int backward,
+                                double* scratch, void* stream) {
+  BT_TRY
+  if (!table) raise(BT_INVALID_ARGUMENT, "gauss_seidel_sweep: table required");
+  if (!rhs || !x || rhs == x) raise(BT_INVALID_ARGUMENT, "gauss_seidel_sweep: distinct rhs and x required");
+  DevBuf<double> own;
+  if (!scratch) {
+    own.alloc((size_t)bt_space_size(table->grid, BT_SPACE_P1, table->level));
+    scratch = own.p;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_gs_sweep(*table, rhs, x, scratch, backward != 0, s);
+  if (own.p) BT_CUDA(cudaStreamSynchronize(s));  // before the scratch is freed
+  BT_CATCH
+}
+
 bt_status bt_interpolate(const bt_grid* g, int level, const bt_field* f, double* x, void* stream) {
   BT_TRY
   check_level(g, level);

@@ -137,10 +137,10 @@ static void smooth(bt_hierarchy& h, const bt_smoother_config& c, const double* r
                    int backward, cudaStream_t s) {
   validate(c);
   LevelData& L = h.at(l);
-  (void)backward;
   for (int q = 0; q < sweeps; ++q) {
     if (c.kind == 1) {
-      raise(BT_INVALID_ARGUMENT, "gauss-seidel smoothing is not available on the device path (use chebyshev/jacobi)");
+      if (h.kernel != 1 || !L.stencil) raise(BT_INVALID_ARGUMENT, "gauss-seidel smoothing requires a stencil table");
+      launch_gs_sweep(*L.stencil, rhs, x, L.r.p, backward != 0, s);
     } else if (c.kind == 0) {
       scaled_residual(h, l, rhs, x, L.r.p, s);
       launch_vec(V_AXPY, x, L.r.p, c.omega, L.n, s);

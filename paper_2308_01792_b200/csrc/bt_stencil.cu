@@ -30,6 +30,7 @@
 // column 0) go through k_stencil_general, which reads the typed rows from
 // shared memory; it is also the fallback for tables that fail the fast-path
 // checks.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -877,6 +878,135 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
   BT_CUDA(cudaEventRecord(ss.join, ss.s));
   BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
   check_launch("k_stencil_fused");
+}
+
+// ---------------------------------------------------------------------------
+// Hybrid Gauss-Seidel sweep (gauss_seidel_sweep, operators.hpp:327-387).
+//
+// Interior: in-place lexicographic Gauss-Seidel per cell. With f(d) =
+// dx + 2 dy + 3 dz, every stencil direction that is lexicographically earlier
+// (k, then j, then i) has f(d) < 0 and every later one f(d) > 0, so the
+// points of one hyperplane i + 2j + 3k = f are independent and hyperplanes in
+// increasing f (forward; decreasing for backward) reproduce the sequential
+// order exactly: every update sees the same neighbour values and evaluates
+// acc = rhs - sum_d row[d] x[p + d] (d = 1..14, unfused), x = acc / row[0]
+// bit for bit. One cooperative launch per sweep, a grid barrier between
+// hyperplanes. Then the Jacobi step on the non-interior points: scratch =
+// apply_stencil(x) (partial rows + replica sums), x = rhs on Dirichlet
+// points, else x + (rhs - scratch) / assembled diagonal.
+// ---------------------------------------------------------------------------
+constexpr int kGsT = 256;
+
+__global__ void __launch_bounds__(kGsT) k_gs_interior(double* __restrict__ x, const double* __restrict__ rhs,
+                                                       const StencilCell* __restrict__ cells, int n, int64_t cs,
+                                                       int cell0, int ncells, int backward) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int w = n + 1;
+  const int npairs = tri32(n - 3);  // rows (j, k) with j, k >= 1, j + k <= n - 2
+  const int64_t items = (int64_t)ncells * npairs;
+  const int fmin = 6, fmax = 3 * n - 6;  // i + 2j + 3k over the interior
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int q = 0; q <= fmax - fmin; ++q) {
+    const int f = backward ? fmax - q : fmin + q;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += stride) {
+      const int cl = (int)(it / npairs);
+      int a, b;
+      decode_tri(n - 3, (int)(it % npairs), a, b);
+      const int j = a + 1, k = b + 1, i = f - 2 * j - 3 * k;
+      if (i < 1 || i > n - 1 - j - k) continue;
+      const int cell = cell0 + cl;
+      const double* __restrict__ row = cells[cell].w[0];
+      int off[15];
+      row_offsets(w, j, k, off);
+      const int64_t t = (int64_t)cell * cs + row_start(w, j, k) + i;
+      double acc = rhs[t];
+#pragma unroll
+      for (int d = 1; d < 15; ++d) acc = __dsub_rn(acc, __dmul_rn(row[d], x[t + off[d]]));
+      x[t] = __ddiv_rn(acc, row[0]);
+    }
+    grid.sync();
+  }
+}
+
+// grid (row chunks of 64 rows, cells): warps over rows, lanes over i
+__global__ void __launch_bounds__(256) k_gs_boundary(double* __restrict__ x, const double* __restrict__ rhs,
+                                                     const double* __restrict__ scratch,
+                                                     const double* __restrict__ diag,
+                                                     const DevCellInfo* __restrict__ info, int n, int64_t cs,
+                                                     int cell0) {
+  const int cell = cell0 + blockIdx.y, w = n + 1;
+  const uint16_t dir = info[cell].dir_by_z;
+  const int64_t base = (int64_t)cell * cs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rend = min(tri32(w), (int)(blockIdx.x + 1) * 64);
+  for (int r = blockIdx.x * 64 + warp; r < rend; r += 8) {
+    int j, k;
+    decode_row(w, r, j, k);
+    const int L = w - j - k;
+    const int64_t t0 = base + row_start(w, j, k);
+    const bool edge_row = j == 0 || k == 0;  // whole row on the lattice boundary
+    for (int i = lane; i < L; i += 32) {
+      if (!edge_row && i != 0 && i != L - 1) continue;  // interior: done by the sweep
+      const int z = zero_set(n, i, j, k);
+      const int64_t u = t0 + i;
+      x[u] = (dir >> z & 1) ? rhs[u] : __dadd_rn(x[u], __ddiv_rn(__dsub_rn(rhs[u], scratch[u]), diag[u]));
+    }
+  }
+}
+
+void launch_gs_sweep(const bt_stencil& st, const double* rhs, double* x, double* scratch, bool backward,
+                     cudaStream_t s) {
+  const bt_grid& g = *st.grid;
+  for (int c = 0; c < g.mesh.n_cells(); ++c)
+    if (st.rows[c][0] == 0.0) raise(BT_INVALID_ARGUMENT, "gauss_seidel_sweep: zero center weight");
+  const int n = 1 << st.level;
+  const int64_t cs = n_tet(n + 1);
+  const int nc = g.part_end - g.part_begin;
+  if (nc && n >= 4) {
+    static std::mutex mu;
+    static int slots[64] = {0};
+    int dev = 0;
+    BT_CUDA(cudaGetDevice(&dev));
+    int grid;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!slots[dev & 63]) {
+        int per_sm = 0, sms = 0;
+        BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_interior, kGsT, 0));
+        BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        slots[dev & 63] = std::max(1, per_sm) * sms;
+      }
+      grid = slots[dev & 63];
+    }
+    const int64_t items = (int64_t)nc * tri32(n - 3);
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (items + kGsT - 1) / kGsT));
+    double* xs = shifted(x, g, BT_SPACE_P1, st.level);
+    const double* rs = shifted(rhs, g, BT_SPACE_P1, st.level);
+    const StencilCell* cells = st.d_cells.p;
+    int cell0 = g.part_begin, bw = backward ? 1 : 0, nn = n;
+    int64_t css = cs;
+    void* args[] = {&xs, &rs, &cells, &nn, &css, &cell0, (void*)&nc, &bw};
+    BT_CUDA(cudaLaunchCooperativeKernel((const void*)k_gs_interior, dim3(grid), dim3(kGsT), args, 0, s));
+    count_launch();
+    check_launch("k_gs_interior");
+  }
+  // non-interior points: Jacobi with the assembled diagonal on the synced residual
+  if (stencil_fused(st)) {
+    launch_stencil_fused(st, x, scratch, 0, s);
+  } else {
+    launch_stencil(st, x, scratch, s);
+    sync(g, st.level, IF_SYNC, scratch, nullptr, s);
+  }
+  const double* diag = stencil_diag(st, s);
+  if (nc) {
+    const dim3 grid((unsigned)((tri32(n + 1) + 63) / 64), nc);
+    k_gs_boundary<<<grid, 256, 0, s>>>(shifted(x, g, BT_SPACE_P1, st.level), shifted(rhs, g, BT_SPACE_P1, st.level),
+                                       shifted(scratch, g, BT_SPACE_P1, st.level),
+                                       shifted(diag, g, BT_SPACE_P1, st.level), g.d_info.p, n, cs, g.part_begin);
+    count_launch();
+    check_launch("k_gs_boundary");
+  }
 }
 
 }  // namespace bt
