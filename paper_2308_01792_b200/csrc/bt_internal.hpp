@@ -258,7 +258,13 @@ struct EwTables {  // device tables of one (form, level) for the elementwise ker
   int level = 0;
   DevBuf<EwCell> cells;
   DevBuf<EwAngles> angles;
+  mutable DevBuf<double> kbar;  // per micro-cell kbar (sin-product coefficient), built on first use
+  mutable bool kbar_tried = false;
 };
+// k_kbar's per-micro-cell kbar of this handle's cells (8 B per micro-cell), or
+// left empty when it would take more than a quarter of the free memory
+void build_kbar_cache(const bt_grid& g, int level, const double* c, const EwCell* d_cells,
+                      const EwAngles* d_angles, DevBuf<double>& out);
 const EwTables& ew_tables(const bt_grid& g, const bt_form& f, int level);
 }  // namespace bt
 
@@ -344,7 +350,7 @@ struct SideStream {
 SideStream& side_stream();
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c,
                         const EwCell* d_cells, const EwAngles* d_angles, const double* x, double* y,
-                        bool diag_only, cudaStream_t s);
+                        bool diag_only, cudaStream_t s, const double* kcache = nullptr);
 void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStream_t s);
 void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s);
 double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s);

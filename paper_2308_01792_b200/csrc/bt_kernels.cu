@@ -48,12 +48,25 @@ static inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b)
 // sin-product coefficient each quadrature phase is C + beta . v, so sin/cos
 // of beta . v (3 sincos per vertex) and the angle-addition formula replace
 // the 12 sin evaluations per micro-cell.
+//
+// CK == 3 (sin product, cached): kbar of every micro-cell was computed once
+// per (form, level) by k_kbar (k_kbar_cache) — k does not depend on x — so an
+// apply gathers it instead of evaluating 4 x 3 phases per (vertex, micro-cell):
+// each micro-cell's kbar was otherwise recomputed by all 4 of its vertices.
 // ---------------------------------------------------------------------------
+// micro-cell classes: widths n, n - 2, n - 1 x 4 (micro_index.hpp:97-121) and
+// their offsets in a cell's kbar block of n^3 values
+__host__ __device__ inline int class_width(int s, int n) { return s == 0 ? n : (s == 1 ? n - 2 : n - 1); }
+__host__ __device__ inline int64_t class_offset(int s, int n) {
+  return s == 0 ? 0 : (s == 1 ? tet32(n) : (int64_t)tet32(n) + tet32(n - 2) + (int64_t)(s - 2) * tet32(n - 1));
+}
+
 template <int CK, bool DIAG>
 __global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restrict__ x, double* __restrict__ y,
                                                           const EwCell* __restrict__ cells,
                                                           const EwAngles* __restrict__ angles, double c0, double c1,
-                                                          int w, int64_t cell_slots, int cell0) {
+                                                          int w, int64_t cell_slots, int cell0,
+                                                          const double* __restrict__ kcache) {
   __shared__ EwCell sc;
   __shared__ EwAngles sa;
   const int cell = cell0 + blockIdx.y;
@@ -73,6 +86,7 @@ __global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restri
   double* __restrict__ yc = y + (int64_t)cell * cell_slots;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = w - 1;
+  const double* __restrict__ kc = CK == 3 ? kcache + (int64_t)blockIdx.y * n * n * n : nullptr;  // this cell's kbar
   const int nrows = tri32(w);
   const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
   for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
@@ -82,6 +96,18 @@ __global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restri
     const int t0 = row_start(w, j, k);
     int off[15];
     row_offsets(w, j, k, off);
+    // CK == 3: kbar index of the (s, slot) micro-cell of vertex (i, j, k) is
+    // kbb[s][slot] + i (row-constant part computed once per row)
+    int kbb[6][4];
+    if (CK == 3) {
+      constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
+#pragma unroll
+      for (int s = 0; s < 6; ++s)
+#pragma unroll
+        for (int slot = 0; slot < 4; ++slot)
+          kbb[s][slot] = (int)class_offset(s, n) +
+                         row_start(class_width(s, n), j - kOff[s][slot][1], k - kOff[s][slot][2]) - kOff[s][slot][0];
+    }
     for (int i = lane; i < L; i += 32) {
       const int t = t0 + i;
       const int z = zero_set(n, i, j, k);
@@ -112,6 +138,8 @@ __global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restri
           double kbar;
           if (CK == 0) {
             kbar = c0;
+          } else if (CK == 3) {
+            kbar = __ldg(kc + kbb[s][slot] + i);
           } else if (CK == 1) {
             kbar = 0.0;
 #pragma unroll
@@ -140,8 +168,66 @@ __global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restri
   }
 }
 
+// kbar of every micro-cell (class s, anchor p) of this handle's cells, as the
+// on-the-fly path evaluates it at the micro-cell's vertex 0 (slot 0):
+// cache[(cell - cell0) * n^3 + class_offset(s) + linearize(w_s, p)]
+__global__ void __launch_bounds__(kThreads) k_kbar(const EwCell* __restrict__ cells,
+                                                   const EwAngles* __restrict__ angles, double c0, double c1,
+                                                   int n, int cell0, double* __restrict__ cache) {
+  constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
+  const int cell = cell0 + blockIdx.y, s = blockIdx.z;
+  const EwCell& e = cells[cell];
+  const EwAngles& an = angles[cell];
+  const int ws = class_width(s, n);
+  if (ws <= 0) return;
+  double* __restrict__ kc = cache + (int64_t)blockIdx.y * n * n * n + class_offset(s, n);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rend = min(tri32(ws), (int)(blockIdx.x + 1) * kRowsPerCta);
+  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
+    int pj, pk;
+    decode_row(ws, r, pj, pk);
+    const int L = ws - pj - pk, t0 = row_start(ws, pj, pk);
+    for (int pi = lane; pi < L; pi += 32) {
+      const int i = pi + kOff[s][0][0], j = pj + kOff[s][0][1], k = pk + kOff[s][0][2];  // vertex 0
+      double sB[3], cB[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double ph = e.beta[d][0] * i + e.beta[d][1] * j + e.beta[d][2] * k;
+        sincos(ph, &sB[d], &cB[d]);
+      }
+      double kbar = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double prod = 1.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) prod *= fma(an.s[s][0][q][d], cB[d], an.c[s][0][q][d] * sB[d]);
+        kbar = fma(0.25, fma(c1, prod, c0), kbar);
+      }
+      kc[t0 + pi] = kbar;
+    }
+  }
+}
+
+// k_kbar's cache for (tables, level) on this handle's cells, or nullptr when
+// it would take more than a quarter of the free device memory
+void build_kbar_cache(const bt_grid& g, int level, const double* c, const EwCell* d_cells,
+                      const EwAngles* d_angles, DevBuf<double>& out) {
+  const int n = 1 << level, nc = g.part_end - g.part_begin;
+  const size_t count = (size_t)nc * n * n * n;
+  size_t free_b = 0, total_b = 0;
+  BT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (!count || count * sizeof(double) > free_b / 4) return;
+  out.alloc(count);
+  dim3 grid(ceil_div(tri32(n), kRowsPerCta), nc, 6);
+  k_kbar<<<grid, kThreads>>>(d_cells, d_angles, c[0], c[1], n, g.part_begin, out.p);
+  count_launch();
+  check_launch("k_kbar");
+  BT_CUDA(cudaDeviceSynchronize());
+}
+
 void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells,
-                        const EwAngles* d_angles, const double* x, double* y, bool diag_only, cudaStream_t s) {
+                        const EwAngles* d_angles, const double* x, double* y, bool diag_only, cudaStream_t s,
+                        const double* kcache) {
   const int w = (1 << level) + 1;
   const int nc = g.part_end - g.part_begin;  // this handle's cells
   if (!nc) return;
@@ -150,10 +236,12 @@ void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, co
   const double c0 = c[0], c1 = c[1];
   x = shifted(x, g, BT_SPACE_P1, level);
   y = shifted(y, g, BT_SPACE_P1, level);
+  if (ck == 1 && kcache) ck = 3;
 #define BT_EW(CK_, D_) \
-  k_elementwise<CK_, D_><<<grid, kThreads, 0, s>>>(x, y, d_cells, d_angles, c0, c1, w, cs, g.part_begin)
+  k_elementwise<CK_, D_><<<grid, kThreads, 0, s>>>(x, y, d_cells, d_angles, c0, c1, w, cs, g.part_begin, kcache)
   if (ck == 0) { if (diag_only) BT_EW(0, true); else BT_EW(0, false); }
   else if (ck == 1) { if (diag_only) BT_EW(1, true); else BT_EW(1, false); }
+  else if (ck == 3) { if (diag_only) BT_EW(3, true); else BT_EW(3, false); }
   else { if (diag_only) BT_EW(2, true); else BT_EW(2, false); }
 #undef BT_EW
   count_launch();
@@ -577,6 +665,16 @@ double l2_error_p1(const bt_grid& g, int level, const double* x, const bt_field&
   return std::sqrt(acc);
 }
 
+// the tables' kbar cache (sin-product coefficients), built on first use
+static const double* kbar_of(const bt_grid& g, const EwTables& t, const double* c) {
+  if (t.form.kind != BT_FORM_DIV_K_GRAD || t.form.coeff_kind != 1) return nullptr;
+  if (!t.kbar_tried) {
+    t.kbar_tried = true;
+    build_kbar_cache(g, t.level, c, t.cells.p, t.angles.p, t.kbar);
+  }
+  return t.kbar.p;
+}
+
 static void validate_field(const bt_field* f) {
   if (!f) raise(BT_INVALID_ARGUMENT, "a field is required");
   if (f->kind < 0 || f->kind > 2) raise(BT_INVALID_ARGUMENT, "field kind must be 0, 1 or 2");
@@ -767,7 +865,7 @@ bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level,
     }
     out = scratch;
   }
-  launch_elementwise(*g, level, ck, c, t.cells.p, t.angles.p, x, out, false, s);
+  launch_elementwise(*g, level, ck, c, t.cells.p, t.angles.p, x, out, false, s, kbar_of(*g, t, c));
   sync(*g, level, bc ? IF_SYNC_DIR : IF_SYNC, out, x, s);
   if (mode == BT_MODE_ADD) launch_vec(V_AXPY, y, out, 1.0, bt_space_size(g, BT_SPACE_P1, level), s);
   BT_CATCH
@@ -781,8 +879,8 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
   const EwTables& t = ew_tables(*g, *form, level);
   const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
   const double one[4] = {1.0, 0.0, 0.0, 0.0};
-  launch_elementwise(*g, level, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, t.cells.p, t.angles.p,
-                     nullptr, diag, true, s);
+  const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
+  launch_elementwise(*g, level, ck, c, t.cells.p, t.angles.p, nullptr, diag, true, s, kbar_of(*g, t, c));
   sync(*g, level, IF_SYNC, diag, nullptr, s);
   BT_CATCH
 }

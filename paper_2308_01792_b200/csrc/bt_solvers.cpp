@@ -18,6 +18,7 @@ struct LevelData {
   std::unique_ptr<bt_stencil> stencil;  // stencil kernel
   DevBuf<EwCell> ew;                    // elementwise kernel tables
   DevBuf<EwAngles> ang;
+  DevBuf<double> kbar;                  // per micro-cell kbar (sin-product coefficient), if it fits
   DevBuf<double> diag;
   double lambda = 0.0;
   // work vectors
@@ -51,7 +52,7 @@ static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int b
     const int ck = h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.coeff_kind : 0;
     static const double one[4] = {1.0, 0.0, 0.0, 0.0};
     launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, L.ang.p, x, y,
-                       false, s);
+                       false, s, L.kbar.p);
   }
   sync(*h.grid, l, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
 }
@@ -303,8 +304,9 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
       if (!angles.empty()) L->ang.upload(angles);
       const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
       static const double one[4] = {1.0, 0.0, 0.0, 0.0};
-      launch_elementwise(*g, l, ck, form->kind == BT_FORM_DIV_K_GRAD ? form->c : one, L->ew.p, L->ang.p, nullptr,
-                         L->diag.p, true, 0);
+      const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
+      if (ck == 1) build_kbar_cache(*g, l, c, L->ew.p, L->ang.p, L->kbar);
+      launch_elementwise(*g, l, ck, c, L->ew.p, L->ang.p, nullptr, L->diag.p, true, 0, L->kbar.p);
       sync(*g, l, IF_SYNC, L->diag.p, nullptr, 0);
     }
     h->levels.push_back(std::move(L));
