@@ -265,7 +265,9 @@ bt_status bt_fmg(bt_hierarchy* h, int finest, const double* const* rhs_levels, d
  * BT_LOGIC_ERROR on a partitioned grid. bt_random_fill never calls the hook:
  * on a partitioned grid it fills the block (its part of the single-GPU
  * stream) and broadcasts the rank-local groups; finish with
- * bt_exchange(mode 2). N1E1 refuses a partitioned grid.
+ * bt_exchange(mode 2). The edge space (N1E1 operator, edge syncs, dots,
+ * random_fill) runs partitioned through its own signed exchange, as a
+ * collective (random_fill included).
  *
  * The hook sums n doubles at buf (device memory) over the ranks in place
  * and returns 0 on success. It is stream-ordered: buf is complete once the

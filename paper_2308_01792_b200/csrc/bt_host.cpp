@@ -882,7 +882,6 @@ bt_status bt_random_fill(const bt_grid* g, int space, int level, uint64_t seed, 
   BT_TRY
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
-    require_unpartitioned(g, "random_fill (edge space)");
     random_fill_edges(*g, level, seed, x, (cudaStream_t)stream);
     return BT_OK;
   }

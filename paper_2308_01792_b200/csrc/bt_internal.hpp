@@ -152,6 +152,7 @@ struct XEntry {
   int32_t base;   // first member of the group
   int32_t count;  // members in the group
   int32_t dir;    // group is Dirichlet-constrained
+  int32_t sign = 1;  // replica orientation (N1E1 edges: -1 when the cell's edge runs the other way)
 };
 struct XPlan {
   bool built = false;
@@ -218,6 +219,7 @@ struct bt_grid {
   // [part_begin, part_end) of rank part_rank out of part_nranks
   int part_rank = 0, part_nranks = 1, part_begin = 0, part_end = 0;
   mutable std::array<bt::XPlan, 11> xplan;  // per level, built on first use
+  mutable std::array<bt::XPlan, 11> xplan_edges;  // the same for N1E1 edge replicas
   // the ranks' sum-allreduce (bt_grid_set_allreduce): lets the library run
   // the exchange itself inside syncs, dots and solvers
   bt_allreduce_fn allreduce = nullptr;
@@ -330,6 +332,13 @@ void launch_xchg_pack(const bt_grid& g, int level, const double* x, double* buf,
 void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x, const double* src,
                          const double* buf, cudaStream_t s);
 void partition_range(int nc, int rank, int nranks, int& begin, int& end);
+// edge space (N1E1): the exchange of rank-spanning signed edge replicas (bt_n1e1.cu)
+const XPlan& xchg_plan_edges(const bt_grid& g, int level);
+void launch_xchg_pack_plan(const XPlan& p, int64_t shift, const double* x, double* buf, cudaStream_t s);
+void launch_xchg_combine_plan(const XPlan& p, int64_t shift, IfaceMode mode, double* x, const double* src,
+                              const double* buf, cudaStream_t s);
+// every signed edge-interface group of an edge-space vector (collective when partitioned)
+void sync_edges(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s);
 // per-cell rows only (no replica sums): interior + row ends + general rows
 void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s);
 // the whole apply_stencil (replica sums and, bc != 0, Dirichlet identity rows

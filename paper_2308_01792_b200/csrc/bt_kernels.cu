@@ -783,8 +783,7 @@ bt_status bt_sync_additive(const bt_grid* g, int space, int level, double* x, vo
   BT_TRY
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
-    require_unpartitioned(g, "sync_additive (edge space)");
-    launch_edge_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
+    sync_edges(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
     return BT_OK;
   }
   require_p1(space);
@@ -795,8 +794,7 @@ bt_status bt_sync_broadcast(const bt_grid* g, int space, int level, double* x, v
   BT_TRY
   check_level(g, level);
   if (space == BT_SPACE_EDGES) {
-    require_unpartitioned(g, "sync_broadcast (edge space)");
-    launch_edge_interface(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
+    sync_edges(*g, level, IF_BCAST, x, nullptr, (cudaStream_t)stream);
     return BT_OK;
   }
   require_p1(space);

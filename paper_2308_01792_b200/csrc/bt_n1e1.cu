@@ -695,23 +695,28 @@ __global__ void __launch_bounds__(kT) k_edge_edges(double* __restrict__ v, const
   });
 }
 
+// the groups local to this handle's partition (g.loc; all groups when
+// unpartitioned); local pointers
 template <int MODE>
 void edge_iface(const bt_grid& g, int level, double* v, const double* src, cudaStream_t s) {
   build_static();
   const int n = 1 << level;
-  EdgeIfaceArgs a{g.d_faces.p, nullptr, g.d_ehdr.p, g.d_emem.p, g.full.d_edge_act.p, (int)g.full.edge_act.size(), n,
+  const IfaceLists& Lg = g.loc;
+  v = shifted(v, g, BT_SPACE_EDGES, level);
+  src = shifted(src, g, BT_SPACE_EDGES, level);
+  EdgeIfaceArgs a{g.d_faces.p, nullptr, g.d_ehdr.p, g.d_emem.p, Lg.d_edge_act.p, (int)Lg.edge_act.size(), n,
                   level_slots(BT_SPACE_EDGES, level)};
   const int per = 3 * tri32(n);
   const bool sync_like = MODE == IF_SYNC || MODE == IF_BCAST || MODE == IF_SYNC_DIR;
   const bool dir_like = MODE == IF_SYNC_DIR || MODE == IF_IMPOSE || MODE == IF_ZERO_DIR;
-  if (sync_like && !g.full.face_shared.empty()) {
-    a.flist = g.full.d_face_shared.p;
-    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.full.face_shared.size()), kT, 0, s>>>(v, src, a);
+  if (sync_like && !Lg.face_shared.empty()) {
+    a.flist = Lg.d_face_shared.p;
+    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)Lg.face_shared.size()), kT, 0, s>>>(v, src, a);
     count_launch();
   }
-  if (dir_like && !g.full.face_bdir.empty()) {
-    a.flist = g.full.d_face_bdir.p;
-    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)g.full.face_bdir.size()), kT, 0, s>>>(v, src, a);
+  if (dir_like && !Lg.face_bdir.empty()) {
+    a.flist = Lg.d_face_bdir.p;
+    k_edge_faces<MODE><<<dim3((per + kT - 1) / kT, (unsigned)Lg.face_bdir.size()), kT, 0, s>>>(v, src, a);
     count_launch();
   }
   if (a.ne) {
@@ -788,19 +793,39 @@ void launch_edge_interface(const bt_grid& g, int level, IfaceMode mode, double* 
   }
 }
 
+// owned-DoF dot over the edge space: per-cell sums (orientation, then row
+// block, in order), then the cells in order — the same association on any
+// number of GPUs
 double dot_edges(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s) {
-  const int n = 1 << level;
+  const int n = 1 << level, nc = g.mesh.n_cells(), nl = g.part_end - g.part_begin;
   const int bx = (tri32(n) + kRows - 1) / kRows;
-  const int64_t np = (int64_t)bx * g.mesh.n_cells() * 7;
-  if (g.d_partials.n < (size_t)np + 1) g.d_partials.alloc((size_t)np + 1);
-  k_edge_dot<<<dim3(bx, g.mesh.n_cells(), 7), kT, 0, s>>>(x, y, g.d_info.p, n, level_slots(BT_SPACE_EDGES, level),
-                                                          g.d_partials.p);
-  k_edge_sum<<<1, 1024, 0, s>>>(g.d_partials.p, np, g.d_partials.p + np);
-  count_launch(2);
-  check_launch("k_edge_dot");
-  BT_CUDA(cudaMemcpyAsync(g.h_pinned, g.d_partials.p + np, sizeof(double), cudaMemcpyDeviceToHost, s));
-  BT_CUDA(cudaStreamSynchronize(s));
-  return g.h_pinned[0];
+  std::vector<double> cells(nc, 0.0);
+  if (nl) {
+    DevBuf<double> part((size_t)bx * nl * 7);
+    k_edge_dot<<<dim3(bx, nl, 7), kT, 0, s>>>(x, y, g.d_info.p + g.part_begin, n,
+                                              level_slots(BT_SPACE_EDGES, level), part.p);
+    count_launch();
+    check_launch("k_edge_dot");
+    std::vector<double> h(part.n);
+    BT_CUDA(cudaMemcpyAsync(h.data(), part.p, sizeof(double) * part.n, cudaMemcpyDeviceToHost, s));
+    BT_CUDA(cudaStreamSynchronize(s));
+    for (int c = 0; c < nl; ++c) {  // partials[(g, cell, block)]
+      double t = 0.0;
+      for (int gg = 0; gg < 7; ++gg)
+        for (int b = 0; b < bx; ++b) t += h[((size_t)gg * nl + c) * bx + b];
+      cells[g.part_begin + c] = t;
+    }
+  }
+  if (g.part_nranks > 1) {
+    if (g.dot_cells.n < (size_t)nc + 1) g.dot_cells.alloc((size_t)nc + 1);
+    BT_CUDA(cudaMemcpyAsync(g.dot_cells.p, cells.data(), sizeof(double) * nc, cudaMemcpyHostToDevice, s));
+    allreduce(g, g.dot_cells.p, nc, s);
+    BT_CUDA(cudaMemcpyAsync(cells.data(), g.dot_cells.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    BT_CUDA(cudaStreamSynchronize(s));
+  }
+  double acc = 0.0;
+  for (int c = 0; c < nc; ++c) acc += cells[c];
+  return acc;
 }
 
 bool n1e1_fast_available(int level) { return (1 << level) >= 4; }
@@ -818,31 +843,168 @@ void n1e1_fast_setup(int device) {
 }
 
 // mt19937_64 over owned edge slots in canonical (cell, orientation, t) order,
-// then a signed broadcast so replicas carry the same oriented field.
+// then a signed broadcast so replicas carry the same oriented field. A
+// partitioned grid draws its cells' part of the single-GPU stream (after
+// discarding the draws of the cells before its block) and broadcasts through
+// the exchange (collective).
 void random_fill_edges(const bt_grid& g, int level, uint64_t seed, double* x, cudaStream_t s) {
   const int n = 1 << level;
   const int64_t cs = level_slots(BT_SPACE_EDGES, level);
-  std::vector<double> h((size_t)(cs * g.mesh.n_cells()), 0.0);
+  const int cb = g.part_begin, ce = g.part_end;
+  std::vector<double> h((size_t)(cs * (ce - cb)), 0.0);
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> dist(-1.0, 1.0);
-  for (int c = 0; c < g.mesh.n_cells(); ++c) {
-    const uint16_t own = g.topo.info[c].owned_by_z;
-    int64_t t = cs * c;
+  auto zset = [&](int e, int i, int j, int k) {
+    const int* a = hOffEdge[e - 1][0];
+    const int* b = hOffEdge[e - 1][1];
+    return zero_set(n, i + a[0], j + a[1], k + a[2]) & zero_set(n, i + b[0], j + b[1], k + b[2]);
+  };
+  if (cb > 0) {  // edges per zero set (the same for every cell), then the owned ones of cells < cb
+    std::vector<int64_t> per_z(16, 0);
     for (int e = 1; e <= 7; ++e) {
       const int w = width_formula(e, level);
-      const int* a = hOffEdge[e - 1][0];
-      const int* b = hOffEdge[e - 1][1];
       for (int k = 0; k < w; ++k)
         for (int j = 0; j < w - k; ++j)
-          for (int i = 0; i < w - k - j; ++i, ++t) {
-            const int z = zero_set(n, i + a[0], j + a[1], k + a[2]) & zero_set(n, i + b[0], j + b[1], k + b[2]);
-            if (own >> z & 1) h[t] = dist(rng);
-          }
+          for (int i = 0; i < w - k - j; ++i) ++per_z[zset(e, i, j, k)];
+    }
+    unsigned long long skip = 0;
+    for (int c = 0; c < cb; ++c)
+      for (int z = 0; z < 16; ++z)
+        if (g.topo.info[c].owned_by_z >> z & 1) skip += (unsigned long long)per_z[z];
+    rng.discard(skip);  // one engine call per value
+  }
+  for (int c = cb; c < ce; ++c) {
+    const uint16_t own = g.topo.info[c].owned_by_z;
+    int64_t t = cs * (c - cb);
+    for (int e = 1; e <= 7; ++e) {
+      const int w = width_formula(e, level);
+      for (int k = 0; k < w; ++k)
+        for (int j = 0; j < w - k; ++j)
+          for (int i = 0; i < w - k - j; ++i, ++t)
+            if (own >> zset(e, i, j, k) & 1) h[t] = dist(rng);
     }
   }
   BT_CUDA(cudaMemcpyAsync(x, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
-  launch_edge_interface(g, level, IF_BCAST, x, nullptr, s);
+  sync_edges(g, level, IF_BCAST, x, nullptr, s);
   BT_CUDA(cudaStreamSynchronize(s));
+}
+
+// host twin of edge_slot: element index and sign of the micro-edge P0 -> P1
+static int64_t edge_slot_host(int n, int64_t cs, int cell, int i0, int j0, int k0, int i1, int j1, int k1,
+                              int& sigma) {
+  const int c = (i1 - i0 + 1) * 9 + (j1 - j0 + 1) * 3 + (k1 - k0 + 1);
+  const int g = hS.dir_g[c];
+  sigma = hS.dir_sigma[c];
+  int ai = sigma > 0 ? i0 : i1, aj = sigma > 0 ? j0 : j1, ak = sigma > 0 ? k0 : k1;
+  aj -= (g == 4 || g == 7) ? 1 : 0;
+  ak -= (g == 5 || g == 6) ? 1 : 0;
+  int64_t eoff = 0;
+  for (int q = 1; q < g; ++q) eoff += tet32(q == 7 ? n - 1 : n);
+  return (int64_t)cell * cs + eoff + row_start(g == 7 ? n - 1 : n, aj, ak) + ai;
+}
+
+static void ijk3_host(const int8_t* lv, int w0, int w1, int w2, int& i, int& j, int& k) {
+  i = (lv[0] == 1 ? w0 : 0) + (lv[1] == 1 ? w1 : 0) + (lv[2] == 1 ? w2 : 0);
+  j = (lv[0] == 2 ? w0 : 0) + (lv[1] == 2 ? w1 : 0) + (lv[2] == 2 ? w2 : 0);
+  k = (lv[0] == 3 ? w0 : 0) + (lv[1] == 3 ? w1 : 0) + (lv[2] == 3 ? w2 : 0);
+}
+
+// exchange plan of the rank-spanning signed edge groups: shared faces'
+// interior micro-edges (k_edge_faces' enumeration), then macro edges'
+// micro-edges (k_edge_edges'); members in ascending cell order
+static void build_xplan_edges(const bt_grid& g, int level, XPlan& out) {
+  build_static();
+  const int nc = g.mesh.n_cells(), n = 1 << level;
+  const int64_t cs = level_slots(BT_SPACE_EDGES, level);
+  std::vector<int> owner(nc);
+  for (int r = 0; r < g.part_nranks; ++r) {
+    int b, e;
+    partition_range(nc, r, g.part_nranks, b, e);
+    for (int c = b; c < e; ++c) owner[c] = r;
+  }
+  const Topology& t = g.topo;
+  out.entries.clear();
+  int64_t off = 0;
+  auto add = [&](int count, int dir, auto&& member) {  // member(m, cell&, slot&, sign&)
+    for (int m = 0; m < count; ++m) {
+      int cell, sg;
+      int64_t slot;
+      member(m, cell, slot, sg);
+      if (owner[cell] == g.part_rank) {
+        XEntry e{slot, (int32_t)(off + m), (int32_t)off, count, dir};
+        e.sign = sg;
+        out.entries.push_back(e);
+      }
+    }
+    off += count;
+  };
+  for (const DevFace& F : t.faces) {
+    if (F.ncell != 2 || owner[F.cell[0]] == owner[F.cell[1]]) continue;
+    for (int tau = 0; tau < 3; ++tau)
+      for (int q = 0; q < tri32(n); ++q) {
+        int aa, bb;
+        decode_tri(n, q, aa, bb);
+        if ((tau == 0 && bb == 0) || (tau == 1 && aa == 0) || (tau == 2 && aa + bb + 1 == n)) continue;
+        int a0 = aa, b0 = bb, a1 = aa, b1 = bb;
+        if (tau == 0) a1 = aa + 1;
+        else if (tau == 1) b1 = bb + 1;
+        else { a0 = aa + 1; b1 = bb + 1; }
+        add(2, F.dir, [&](int m, int& cell, int64_t& slot, int& sg) {
+          int i0, j0, k0, i1, j1, k1;
+          ijk3_host(F.lv[m], n - a0 - b0, a0, b0, i0, j0, k0);
+          ijk3_host(F.lv[m], n - a1 - b1, a1, b1, i1, j1, k1);
+          cell = F.cell[m];
+          slot = edge_slot_host(n, cs, cell, i0, j0, k0, i1, j1, k1, sg);
+        });
+      }
+  }
+  for (const DevPrimHdr& h : t.ehdr) {
+    if (h.count < 2) continue;
+    bool spans = false;
+    for (int m = 1; m < h.count; ++m) spans = spans || owner[t.emem[h.first + m].cell] != owner[t.emem[h.first].cell];
+    if (!spans) continue;
+    for (int aa = 0; aa < n; ++aa)
+      add(h.count, h.dir, [&](int m, int& cell, int64_t& slot, int& sg) {
+        const DevPrimMem& pm = t.emem[h.first + m];
+        const int8_t lv[3] = {pm.lv[0], pm.lv[1], -1};
+        int i0, j0, k0, i1, j1, k1;
+        ijk3_host(lv, n - aa, aa, 0, i0, j0, k0);
+        ijk3_host(lv, n - aa - 1, aa + 1, 0, i1, j1, k1);
+        cell = pm.cell;
+        slot = edge_slot_host(n, cs, cell, i0, j0, k0, i1, j1, k1, sg);
+      });
+  }
+  if (off > INT32_MAX) raise(BT_OUT_OF_RANGE, "exchange buffer exceeds 2^31 entries");
+  out.buf_size = off;
+  out.built = true;
+}
+
+const XPlan& xchg_plan_edges(const bt_grid& g, int level) {
+  XPlan& p = g.xplan_edges.at(level);
+  if (!p.built) {
+    build_xplan_edges(g, level, p);
+    p.d_entries.upload(p.entries);
+  }
+  return p;
+}
+
+void sync_edges(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
+  if (g.part_nranks > 1) {
+    const XPlan& p = xchg_plan_edges(g, level);
+    const int64_t shift = part_shift(g, BT_SPACE_EDGES, level);
+    const bool needs_buf = mode == IF_SYNC || mode == IF_SYNC_DIR || mode == IF_BCAST;
+    const double* buf = nullptr;
+    if (needs_buf && p.buf_size) {
+      if (g.xbuf.n < (size_t)p.buf_size) g.xbuf.alloc((size_t)p.buf_size);
+      launch_xchg_pack_plan(p, shift, v, g.xbuf.p, s);
+      allreduce(g, g.xbuf.p, p.buf_size, s);
+      buf = g.xbuf.p;
+    }
+    launch_edge_interface(g, level, mode, v, src, s);
+    launch_xchg_combine_plan(p, shift, mode, v, src, buf, s);
+  } else {
+    launch_edge_interface(g, level, mode, v, src, s);
+  }
 }
 
 }  // namespace bt
@@ -854,7 +1016,6 @@ extern "C" {
 
 bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta, bt_n1e1** out) {
   BT_TRY
-  require_unpartitioned(g, "N1E1 operator");
   check_level(g, level);
   BT_CUDA(cudaSetDevice(g->device));
   build_static();
@@ -942,7 +1103,7 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
     op->d_cellw.upload(cw);
     op->d_marches.upload(marches);
     op->nmarch = (int)marches.size();
-    op->d_next.alloc((size_t)nc);
+    op->d_next.alloc((size_t)std::max(1, g->part_end - g->part_begin));
   }
   *out = op.release();
   BT_CATCH
@@ -958,14 +1119,20 @@ bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, v
   const int n = 1 << op->level;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t cs = level_slots(BT_SPACE_EDGES, op->level);
-  const int nc = g.mesh.n_cells();
+  // this handle's cells: x, y hold them (block row y = local cell); the
+  // per-cell tables are indexed from the first of them
+  const int nc = g.part_end - g.part_begin, c0 = g.part_begin;
+  if (!nc) {
+    sync_edges(g, op->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+    return BT_OK;
+  }
   // face rows (j = 0 or k = 0) and rows of length 1 of every orientation, on
   // the side stream beside the staged kernel
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
   BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
   const dim3 fgrid(7 * ((n1e1_face_rows(1, n) + kW - 1) / kW), nc);
-  k_n1e1_face<<<fgrid, kT, 0, ss.s>>>(x, y, op->d_masked.p, n, cs);
+  k_n1e1_face<<<fgrid, kT, 0, ss.s>>>(x, y, op->d_masked.p + (size_t)c0 * hS.mask_rows * 19, n, cs);
   count_launch();
   // the other rows: staged marches over all 7 orientations, kN1BlocksPerCell
   // blocks per cell sharing the cell's march queue
@@ -974,20 +1141,20 @@ bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, v
     n1e1_fast_setup(g.device);
     const int per_cell = std::min(kN1BlocksPerCell, (op->nmarch + kN1FW - 1) / kN1FW);
     k_n1e1_fast<<<dim3(per_cell, nc), kN1FT, kN1Smem, s>>>(x, y, op->d_marches.p, op->nmarch, n, cs,
-                                                          op->d_cellw.p, op->d_next.p);
+                                                          op->d_cellw.p + (size_t)c0 * kN1CellWP, op->d_next.p);
     count_launch();
   }
   BT_CUDA(cudaEventRecord(ss.join, ss.s));
   BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
   check_launch("k_n1e1");
-  launch_edge_interface(g, op->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+  sync_edges(g, op->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
   BT_CATCH
 }
 
 bt_status bt_n1e1_sync(const bt_grid* g, int level, double* x, void* stream) {
   BT_TRY
   check_level(g, level);
-  launch_edge_interface(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
+  sync_edges(*g, level, IF_SYNC, x, nullptr, (cudaStream_t)stream);
   BT_CATCH
 }
 

@@ -34,7 +34,10 @@ int64_t slot_of(int64_t cs, int w, int cell, int l0, int w0, int l1, int w1, int
 __global__ void __launch_bounds__(kT) k_xpack(const XEntry* __restrict__ e, int n, const double* __restrict__ x,
                                               double* __restrict__ buf) {
   const int q = blockIdx.x * kT + threadIdx.x;
-  if (q < n) buf[e[q].buf] = x[e[q].slot];
+  if (q < n) {
+    const double v = x[e[q].slot];
+    buf[e[q].buf] = e[q].sign > 0 ? v : -v;  // signed replica (N1E1 edges); P1: sign 1
+  }
 }
 
 template <int MODE>
@@ -46,13 +49,14 @@ __global__ void __launch_bounds__(kT) k_xcombine(const XEntry* __restrict__ e, i
   if (MODE == IF_SYNC || (MODE == IF_SYNC_DIR && !E.dir)) {
     double sum = 0.0;
     for (int m = 0; m < E.count; ++m) sum += buf[E.base + m];
-    x[E.slot] = sum;
+    x[E.slot] = E.sign > 0 ? sum : -sum;
   } else if (MODE == IF_SYNC_DIR || MODE == IF_IMPOSE) {
     if (E.dir) x[E.slot] = src[E.slot];
   } else if (MODE == IF_ZERO_DIR) {
     if (E.dir) x[E.slot] = 0.0;
   } else if (MODE == IF_BCAST) {
-    x[E.slot] = buf[E.base];
+    const double u = buf[E.base];
+    x[E.slot] = E.sign > 0 ? u : -u;
   } else if (MODE == IF_ZERO_NONOWNED) {
     if (E.buf != E.base) x[E.slot] = 0.0;
   }
@@ -141,8 +145,11 @@ const XPlan& xchg_plan(const bt_grid& g, int level) {
 }
 
 void launch_xchg_pack(const bt_grid& g, int level, const double* x, double* buf, cudaStream_t s) {
-  const XPlan& p = xchg_plan(g, level);
-  x = shifted(x, g, BT_SPACE_P1, level);
+  launch_xchg_pack_plan(xchg_plan(g, level), part_shift(g, BT_SPACE_P1, level), x, buf, s);
+}
+
+void launch_xchg_pack_plan(const XPlan& p, int64_t shift, const double* x, double* buf, cudaStream_t s) {
+  if (x) x -= shift;
   if (!p.buf_size) return;
   BT_CUDA(cudaMemsetAsync(buf, 0, sizeof(double) * (size_t)p.buf_size, s));
   const int n = (int)p.entries.size();
@@ -154,11 +161,15 @@ void launch_xchg_pack(const bt_grid& g, int level, const double* x, double* buf,
 
 void launch_xchg_combine(const bt_grid& g, int level, IfaceMode mode, double* x, const double* src,
                          const double* buf, cudaStream_t s) {
-  const XPlan& p = xchg_plan(g, level);
+  launch_xchg_combine_plan(xchg_plan(g, level), part_shift(g, BT_SPACE_P1, level), mode, x, src, buf, s);
+}
+
+void launch_xchg_combine_plan(const XPlan& p, int64_t shift, IfaceMode mode, double* x, const double* src,
+                              const double* buf, cudaStream_t s) {
   const int n = (int)p.entries.size();
   if (!n) return;
-  x = shifted(x, g, BT_SPACE_P1, level);
-  src = shifted(src, g, BT_SPACE_P1, level);
+  if (x) x -= shift;
+  if (src) src -= shift;
   const dim3 grid((n + kT - 1) / kT);
   const XEntry* e = p.d_entries.p;
   switch (mode) {

@@ -111,8 +111,10 @@ def test_partitioned_impose_and_zero_dirichlet():
         assert not torch.isnan(yr.values[level]).any()
 
 
-def test_partitioned_grid_refuses_n1e1():
+def test_partitioned_n1e1_needs_the_allreduce_hook():
     g = bt.Grid(bt.cube_kuhn_text(), 2, 3)
-    g.set_partition(0, 2)
+    bt.api._check(bt.api._L.bt_grid_set_partition(g.handle, 0, 2))  # no allreduce hook
+    op = bt.N1E1Operator(g, 3)
+    x, y = bt.allocate(bt.edge_space(), g, 3, 3), bt.allocate(bt.edge_space(), g, 3, 3)
     with pytest.raises(bt.LogicError):
-        bt.N1E1Operator(g, 3)
+        bt.apply_n1e1(op, x, y, 3)

@@ -214,3 +214,37 @@ def test_partitioned_fmg():
         _, _, b, e = out["part"]
         assert torch.equal(out["x"], full["x"][b * cs:e * cs])
         assert out["rows"] == full["rows"]  # residuals and L2 errors bitwise
+
+
+def n1e1_body(text, L):
+    def body(setup):
+        g = bt.Grid(text, 2, L)
+        setup(g)
+        op = bt.N1E1Operator(g, L)
+        x = bt.allocate(bt.edge_space(), g, L, L)
+        y = bt.allocate(bt.edge_space(), g, L, L)
+        bt.random_fill(x, L, 5)
+        out = {"part": g.partition(), "x": x.values[L].clone()}
+        for bc in (bt.BC.None_, bt.BC.DirichletIdentity):
+            bt.apply_n1e1(op, x, y, L, bc)
+            out[f"y{int(bc)}"] = y.values[L].clone()
+        out["dot"] = bt.dot(x, y, L)
+        bt.sync_additive(x, L)
+        out["sync"] = x.values[L].clone()
+        torch.cuda.synchronize()
+        return out
+    return body
+
+
+@pytest.mark.parametrize("text,L,nranks", [(bt.cube_kuhn_text(), 4, 2), (bt.cubes_mesh_text(2, 0.1, 0), 3, 3)])
+def test_partitioned_n1e1(text, L, nranks):
+    body = n1e1_body(text, L)
+    full = body(lambda g: None)
+    ranks = run_ranks(nranks, body)
+    g = bt.Grid(text, 2, L)
+    cs = g.space_size(2, L) // g.n_cells()
+    for out in ranks:
+        _, _, b, e = out["part"]
+        for k in ("x", "y0", "y1", "sync"):
+            assert torch.equal(out[k], full[k][b * cs:e * cs]), k
+        assert out["dot"] == full["dot"]
