@@ -174,7 +174,7 @@ def cfg5(res, skip_cpu):
     sm.nu1 = sm.nu2 = 2
     form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
     runs = []
-    for n, lo, hi, cpu_ok in [(2, 2, 5, True), (8, 2, 6, False)]:
+    for n, lo, hi, cpu_ok in [(2, 2, 5, True), (8, 2, 6, False), (8, 2, 7, False)]:
         text = bt.cubes_mesh_text(n, 0.1, 0)
         g = bt.Grid(text, lo, hi)
         h = bt.make_hierarchy(g, form, bt.KernelKind.Elementwise)
