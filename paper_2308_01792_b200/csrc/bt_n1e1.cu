@@ -412,7 +412,7 @@ __device__ __forceinline__ void n1_correct(const double (&win)[kN1Streams][3], c
   }
 }
 
-__global__ void __launch_bounds__(kN1FT, 3) k_n1e1_fast(const double* __restrict__ x, double* __restrict__ y,
+__global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict__ x, double* __restrict__ y,
                                                         const int4* __restrict__ marches, int nmarch, int n,
                                                         int64_t cs, const double* __restrict__ cellw,
                                                         int* __restrict__ next_march) {
