@@ -251,12 +251,13 @@ namespace {
 // table — with straight-line loads: a coupled edge that does not exist reads
 // slot 0 with weight 0. Rows with j, k >= 1 are k_n1e1_fast's.
 // ---------------------------------------------------------------------------
+// edges i = ifirst, ifirst + istep, ... of row (j, k): a warp per row
+// (lane, 32), or a thread per row of length 1 (0, 1)
 template <int G>
 __device__ __forceinline__ void n1e1_row(const double* __restrict__ x, double* __restrict__ y, const double* sM,
-                                         int cell, int j, int k, int n, int64_t cs) {
+                                         int cell, int j, int k, int n, int64_t cs, int ifirst, int istep) {
   constexpr int NNB = n1e1_nnb(G), NINC = n1e1_ninc(G);
   const int wg = G == 7 ? n - 1 : n;  // subgroup width: 2^l, xyz 2^l - 1
-  const int lane = threadIdx.x & 31;
   const int tn = tet32(n);  // entry offsets: subgroups 1..6 have width n, xyz (7) n - 1
   auto eoff = [&](int q) { return (q - 1) * tn; };
   const double* __restrict__ xc = x + (int64_t)cell * cs;
@@ -278,7 +279,7 @@ __device__ __forceinline__ void n1e1_row(const double* __restrict__ x, double* _
     lo[q] = max(0, -it.dq[0]);
     hi[q] = (j + it.dq[1] < 0 || k + it.dq[2] < 0) ? -1 : ws - 1 - it.dq[0] - (j + it.dq[1]) - (k + it.dq[2]);
   }
-  for (int i = lane; i < L; i += 32) {
+  for (int i = ifirst; i < L; i += istep) {
     unsigned mask = 0;
 #pragma unroll
     for (int q = 0; q < NINC; ++q)
@@ -297,19 +298,19 @@ __device__ __forceinline__ void n1e1_row(const double* __restrict__ x, double* _
 // grid (row chunk x 7 orientations, cells); orientation G's rows here are
 // q < w_G: (j = q, k = 0); q < 2 w_G - 1: (j = 0, k = q - w_G + 1); then, for
 // G != 7, the rows of length 1 with j, k >= 1: k = q - 2 w_G + 2, j = n - 1 - k
-__host__ __device__ inline int n1e1_face_rows(int g, int n) {
-  const int wg = g == 7 ? n - 1 : n;
-  return 2 * wg - 1 + (g == 7 ? 0 : max(0, n - 2));
-}
+__host__ __device__ inline int n1e1_long_rows(int g, int n) { return 2 * (g == 7 ? n - 1 : n) - 1; }
+__host__ __device__ inline int n1e1_short_rows(int g, int n) { return g == 7 ? 0 : max(0, n - 2); }
+// block x = chunk * 7 + (g - 1): chunks [0, kLong) hold kW long rows each (a
+// warp per row), the rest kT rows of length 1 each (a thread per row)
 __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, double* __restrict__ y,
-                                                  const double* __restrict__ masked, int n, int64_t cs) {
+                                                  const double* __restrict__ masked, int n, int64_t cs,
+                                                  int long_chunks) {
   __shared__ double sM[64 * 19];
   const int g = blockIdx.x % 7 + 1;
   const int chunk = blockIdx.x / 7;
   const int cell = blockIdx.y;
   const int nnb = n1e1_nnb(g);
   const int wg = g == 7 ? n - 1 : n;
-  const int q = chunk * kW + (threadIdx.x >> 5);
   {
     const double* __restrict__ src = masked + (size_t)cell * cS.mask_rows * 19 + (size_t)cS.mask_off[g] * 19;
     const int nw = (1 << n1e1_ninc(g)) * 19;
@@ -319,26 +320,30 @@ __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, 
     }
   }
   __syncthreads();
-  if (q >= n1e1_face_rows(g, n)) return;
-  int j, k;
-  if (q < wg) {
-    j = q;
-    k = 0;
-  } else if (q < 2 * wg - 1) {
-    j = 0;
-    k = q - wg + 1;
-  } else {
-    k = q - 2 * wg + 2;
+  int j, k, ifirst, istep;
+  if (chunk < long_chunks) {  // (j = q, k = 0), then (j = 0, k = q - w_G + 1)
+    const int q = chunk * kW + (threadIdx.x >> 5);
+    if (q >= n1e1_long_rows(g, n)) return;
+    j = q < wg ? q : 0;
+    k = q < wg ? 0 : q - wg + 1;
+    ifirst = threadIdx.x & 31;
+    istep = 32;
+  } else {  // rows of length 1 with j, k >= 1 (orientations 1..6): k = q + 1, j = n - 1 - k
+    const int q = (chunk - long_chunks) * kT + threadIdx.x;
+    if (q >= n1e1_short_rows(g, n)) return;
+    k = q + 1;
     j = n - 1 - k;
+    ifirst = 0;
+    istep = 1;
   }
   switch (g) {
-    case 1: n1e1_row<1>(x, y, sM, cell, j, k, n, cs); break;
-    case 2: n1e1_row<2>(x, y, sM, cell, j, k, n, cs); break;
-    case 3: n1e1_row<3>(x, y, sM, cell, j, k, n, cs); break;
-    case 4: n1e1_row<4>(x, y, sM, cell, j, k, n, cs); break;
-    case 5: n1e1_row<5>(x, y, sM, cell, j, k, n, cs); break;
-    case 6: n1e1_row<6>(x, y, sM, cell, j, k, n, cs); break;
-    default: n1e1_row<7>(x, y, sM, cell, j, k, n, cs); break;
+    case 1: n1e1_row<1>(x, y, sM, cell, j, k, n, cs, ifirst, istep); break;
+    case 2: n1e1_row<2>(x, y, sM, cell, j, k, n, cs, ifirst, istep); break;
+    case 3: n1e1_row<3>(x, y, sM, cell, j, k, n, cs, ifirst, istep); break;
+    case 4: n1e1_row<4>(x, y, sM, cell, j, k, n, cs, ifirst, istep); break;
+    case 5: n1e1_row<5>(x, y, sM, cell, j, k, n, cs, ifirst, istep); break;
+    case 6: n1e1_row<6>(x, y, sM, cell, j, k, n, cs, ifirst, istep); break;
+    default: n1e1_row<7>(x, y, sM, cell, j, k, n, cs, ifirst, istep); break;
   }
 }
 
@@ -1131,8 +1136,10 @@ bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, v
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
   BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-  const dim3 fgrid(7 * ((n1e1_face_rows(1, n) + kW - 1) / kW), nc);
-  k_n1e1_face<<<fgrid, kT, 0, ss.s>>>(x, y, op->d_masked.p + (size_t)c0 * hS.mask_rows * 19, n, cs);
+  const int long_chunks = (n1e1_long_rows(1, n) + kW - 1) / kW;
+  const int short_chunks = (n1e1_short_rows(1, n) + kT - 1) / kT;
+  const dim3 fgrid(7 * (long_chunks + short_chunks), nc);
+  k_n1e1_face<<<fgrid, kT, 0, ss.s>>>(x, y, op->d_masked.p + (size_t)c0 * hS.mask_rows * 19, n, cs, long_chunks);
   count_launch();
   // the other rows: staged marches over all 7 orientations, kN1BlocksPerCell
   // blocks per cell sharing the cell's march queue
