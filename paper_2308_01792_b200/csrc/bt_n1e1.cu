@@ -379,7 +379,7 @@ constexpr int kN1Corr = kN1Corr0 + kN1Corr1;
 constexpr int kN1RingD = kN1Stages * kN1Streams * 32;  // doubles per warp
 constexpr int kN1CellW = 7 * kN1Wt + kN1Corr;          // per cell: full rows, then corrections (case 0, case 1)
 constexpr int kN1CellWP = (kN1CellW + 1) / 2 * 2;      // padded to 16 bytes
-constexpr int kN1BlocksPerCell = 8;
+constexpr int kN1BlocksPerCell = 16;
 
 template <int G, int PH>
 __device__ __forceinline__ double n1_val(const double (&win)[kN1Streams][3], const double (&sh)[kN1Shuf], int m) {
