@@ -363,6 +363,17 @@ void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const doubl
 void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStream_t s);
 void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s);
 double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s);
+// the owned dot left on the device at *dst (stream-ordered; collective when partitioned)
+void dot_p1_device(const bt_grid& g, int level, const double* x, const double* y, double* dst, cudaStream_t s);
+// device-resident CG scalars (bt_solvers.cpp cg)
+struct CgState {
+  double nb2, rs, pap, rs_new, denom, alpha, malpha, beta, one;
+  int it, done, breakdown;
+};
+void launch_cg_init(CgState* st, double tol, cudaStream_t s);
+void launch_cg_alpha(CgState* st, cudaStream_t s);
+void launch_cg_update(CgState* st, double tol, double* hist, cudaStream_t s);
+void launch_vec_dev(int op, double* y, const double* x, const double* a, const int* done, int64_t n, cudaStream_t s);
 // l2_error (solvers.hpp:613-648) of a P1 function against a field (collective when partitioned)
 double l2_error_p1(const bt_grid& g, int level, const double* x, const bt_field& f, cudaStream_t s);
 // edge space (N1E1, bt_n1e1.cu): signed replica sync / broadcast, Dirichlet rows

@@ -393,6 +393,95 @@ double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cud
   return g.h_pinned[0];
 }
 
+// the same owned dot, left on the device at *dst (stream-ordered, no host sync)
+void dot_p1_device(const bt_grid& g, int level, const double* x, const double* y, double* dst, cudaStream_t s) {
+  const int nc = g.mesh.n_cells();
+  if (g.part_nranks == 1) {
+    const int w = (1 << level) + 1;
+    const int bx = ceil_div(tri32(w), kRowsPerCta);
+    const int64_t np = (int64_t)bx * nc;
+    if (g.d_partials.n < (size_t)(np + nc + 1)) g.d_partials.alloc((size_t)(np + nc + 1));
+    dot_p1_cells(g, level, x, y, s, nullptr, nullptr, g.d_partials.p + np);
+    k_ordered_sum<<<1, 1, 0, s>>>(g.d_partials.p + np, nc, dst);
+  } else {
+    if (g.dot_cells.n < (size_t)nc + 1) g.dot_cells.alloc((size_t)nc + 1);
+    BT_CUDA(cudaMemsetAsync(g.dot_cells.p, 0, sizeof(double) * (size_t)nc, s));
+    dot_p1_cells(g, level, x, y, s, nullptr, nullptr, g.dot_cells.p + g.part_begin);
+    allreduce(g, g.dot_cells.p, nc, s);
+    k_ordered_sum<<<1, 1, 0, s>>>(g.dot_cells.p, nc, dst);
+  }
+  count_launch();
+  check_launch("k_ordered_sum");
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident CG scalars (cg, solvers.hpp:84-131): the scalar recurrences
+// run in one-thread kernels in the reference's operation order, so no host
+// round trip per iteration; `done` stops every later update (convergence or
+// breakdown), exactly where the reference returns or throws.
+// ---------------------------------------------------------------------------
+__global__ void k_cg_init(CgState* st, double tol) {
+  const double nb = sqrt(st->nb2);
+  st->denom = nb > 0 ? nb : 1.0;
+  st->one = 1.0;
+  st->it = 0;
+  st->breakdown = 0;
+  st->done = sqrt(st->rs) / st->denom <= tol ? 1 : 0;
+}
+__global__ void k_cg_alpha(CgState* st) {
+  if (st->done) return;
+  if (!(st->pap > 0)) {
+    st->breakdown = 1;
+    st->done = 1;
+    return;
+  }
+  st->alpha = st->rs / st->pap;
+  st->malpha = -st->alpha;
+}
+__global__ void k_cg_update(CgState* st, double tol, double* hist) {
+  if (st->done) return;
+  st->it += 1;
+  const double r = sqrt(st->rs_new) / st->denom;
+  if (hist) hist[st->it - 1] = r;
+  if (r <= tol) {
+    st->done = 1;
+    return;
+  }
+  st->beta = st->rs_new / st->rs;
+  st->rs = st->rs_new;
+}
+// y = y + a x / y = a y with a read from the device, skipped once done
+template <int OP>
+__global__ void __launch_bounds__(kThreads) k_vec_dev(double* __restrict__ y, const double* __restrict__ x,
+                                                      const double* __restrict__ a, const int* __restrict__ done,
+                                                      int64_t n) {
+  if (*done) return;
+  const double av = *a;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    if (OP == V_SCALE) y[q] = __dmul_rn(y[q], av);
+    else y[q] = __dadd_rn(y[q], __dmul_rn(av, x[q]));
+  }
+}
+void launch_cg_init(CgState* st, double tol, cudaStream_t s) {
+  k_cg_init<<<1, 1, 0, s>>>(st, tol);
+  count_launch();
+}
+void launch_cg_alpha(CgState* st, cudaStream_t s) {
+  k_cg_alpha<<<1, 1, 0, s>>>(st);
+  count_launch();
+}
+void launch_cg_update(CgState* st, double tol, double* hist, cudaStream_t s) {
+  k_cg_update<<<1, 1, 0, s>>>(st, tol, hist);
+  count_launch();
+}
+void launch_vec_dev(int op, double* y, const double* x, const double* a, const int* done, int64_t n, cudaStream_t s) {
+  const int blocks = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 8);
+  if (op == V_SCALE) k_vec_dev<V_SCALE><<<blocks, kThreads, 0, s>>>(y, x, a, done, n);
+  else k_vec_dev<V_AXPY><<<blocks, kThreads, 0, s>>>(y, x, a, done, n);
+  count_launch();
+  check_launch("k_vec_dev");
+}
+
 // prolongate_p1 (solvers.hpp:227-253), optionally fused with axpy(x, 1, ef)
 __global__ void __launch_bounds__(kThreads) k_prolongate(const double* __restrict__ coarse, double* __restrict__ fine,
                                                          int wf, int add, int cell0) {

@@ -153,39 +153,54 @@ static void smooth(bt_hierarchy& h, const bt_smoother_config& c, const double* r
   }
 }
 
-// cg (solvers.hpp:84-131)
+// cg (solvers.hpp:84-131) with the scalar recurrences on the device (no host
+// round trip per iteration; the host polls the done flag every kPoll
+// iterations). Operation order as the reference: r = -(A x) + rhs, p = r,
+// alpha = rs / pap, x += alpha p, r += (-alpha) ap, p = (rs_new / rs) p + r.
 static int cg(bt_hierarchy& h, int l, double tol, int maxit, const double* rhs, double* x, double* hist,
               cudaStream_t s) {
+  constexpr int kPoll = 8;
   LevelData& L = h.at(l);
   const int64_t n = L.n;
   double* r = L.r.p;
   double* p = L.p.p;
   double* ap = L.ap.p;
+  DevBuf<CgState> st(1);
+  DevBuf<double> dh((size_t)std::max(maxit, 1));
+  CgState* S = st.p;
   hier_apply(h, l, x, r, 1, s);
   launch_vec(V_SCALE, r, nullptr, -1.0, n, s);
   launch_vec(V_AXPY, r, rhs, 1.0, n, s);
   launch_vec(V_COPY, p, r, 0.0, n, s);
-  const double nb = std::sqrt(dot(h, l, rhs, rhs, s));
-  const double denom = nb > 0 ? nb : 1.0;
-  double rs = dot(h, l, r, r, s);
-  int iters = 0;
-  if (std::sqrt(rs) / denom <= tol) return 0;
+  dot_p1_device(*h.grid, l, rhs, rhs, &S->nb2, s);
+  dot_p1_device(*h.grid, l, r, r, &S->rs, s);
+  launch_cg_init(S, tol, s);
+  CgState hs{};
+  auto poll = [&] {
+    BT_CUDA(cudaMemcpyAsync(&hs, S, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    BT_CUDA(cudaStreamSynchronize(s));
+  };
+  poll();
+  if (hs.done) return 0;
   for (int it = 1; it <= maxit; ++it) {
     hier_apply(h, l, p, ap, 1, s);
-    const double pap = dot(h, l, p, ap, s);
-    if (!(pap > 0)) raise(BT_RUNTIME_ERROR, "cg breakdown: operator is not positive definite");
-    const double alpha = rs / pap;
-    launch_vec(V_AXPY, x, p, alpha, n, s);
-    launch_vec(V_AXPY, r, ap, -alpha, n, s);
-    const double rs_new = dot(h, l, r, r, s);
-    iters = it;
-    if (hist) hist[it - 1] = std::sqrt(rs_new) / denom;
-    if (std::sqrt(rs_new) / denom <= tol) break;
-    launch_vec(V_SCALE, p, nullptr, rs_new / rs, n, s);
-    launch_vec(V_AXPY, p, r, 1.0, n, s);
-    rs = rs_new;
+    dot_p1_device(*h.grid, l, p, ap, &S->pap, s);
+    launch_cg_alpha(S, s);
+    launch_vec_dev(V_AXPY, x, p, &S->alpha, &S->done, n, s);
+    launch_vec_dev(V_AXPY, r, ap, &S->malpha, &S->done, n, s);
+    dot_p1_device(*h.grid, l, r, r, &S->rs_new, s);
+    launch_cg_update(S, tol, dh.p, s);
+    launch_vec_dev(V_SCALE, p, nullptr, &S->beta, &S->done, n, s);
+    launch_vec_dev(V_AXPY, p, r, &S->one, &S->done, n, s);  // p += 1.0 r
+    if (it % kPoll == 0 || it == maxit) {
+      poll();
+      if (hs.done) break;
+    }
   }
-  return iters;
+  if (hs.breakdown) raise(BT_RUNTIME_ERROR, "cg breakdown: operator is not positive definite");
+  if (hist && hs.it)
+    BT_CUDA(cudaMemcpy(hist, dh.p, sizeof(double) * (size_t)hs.it, cudaMemcpyDeviceToHost));
+  return hs.it;
 }
 
 // v_cycle (solvers.hpp:509-541). Level-l temporaries: r (residual), and the
