@@ -475,6 +475,7 @@ void launch_cg_update(CgState* st, double tol, double* hist, cudaStream_t s) {
   count_launch();
 }
 void launch_vec_dev(int op, double* y, const double* x, const double* a, const int* done, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
   const int blocks = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 8);
   if (op == V_SCALE) k_vec_dev<V_SCALE><<<blocks, kThreads, 0, s>>>(y, x, a, done, n);
   else k_vec_dev<V_AXPY><<<blocks, kThreads, 0, s>>>(y, x, a, done, n);
@@ -906,7 +907,8 @@ bt_status bt_zero_dirichlet(const bt_grid* g, int level, double* x, void* stream
 bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int bc, void* stream) {
   BT_TRY
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
-  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  if (x == y && bt_space_size(st->grid, BT_SPACE_P1, st->level) > 0)  // (empty cell blocks pass nulls)
+    raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   cudaStream_t s = (cudaStream_t)stream;
   if (stencil_fused(*st)) {
     launch_stencil_fused(*st, x, y, bc, s);
@@ -920,7 +922,8 @@ bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int
 bt_status bt_apply_stencil_cells(const bt_stencil* st, const double* x, double* y, void* stream) {
   BT_TRY
   if (!st) raise(BT_INVALID_ARGUMENT, "apply_stencil: table required");
-  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  if (x == y && bt_space_size(st->grid, BT_SPACE_P1, st->level) > 0)  // (empty cell blocks pass nulls)
+    raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   launch_stencil(*st, x, y, (cudaStream_t)stream);
   BT_CATCH
 }
@@ -937,7 +940,8 @@ bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level,
   BT_TRY
   check_level(g, level);
   validate_form(form);
-  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  if (x == y && bt_space_size(g, BT_SPACE_P1, level) > 0)  // (empty cell blocks pass nulls)
+    raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   cudaStream_t s = (cudaStream_t)stream;
   const EwTables& t = ew_tables(*g, *form, level);
   const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
@@ -976,7 +980,8 @@ bt_status bt_gauss_seidel_sweep(const bt_stencil* table, const double* rhs, doub
                                 double* scratch, void* stream) {
   BT_TRY
   if (!table) raise(BT_INVALID_ARGUMENT, "gauss_seidel_sweep: table required");
-  if (!rhs || !x || rhs == x) raise(BT_INVALID_ARGUMENT, "gauss_seidel_sweep: distinct rhs and x required");
+  if (rhs == x && bt_space_size(table->grid, BT_SPACE_P1, table->level) > 0)
+    raise(BT_INVALID_ARGUMENT, "gauss_seidel_sweep: distinct rhs and x required");
   DevBuf<double> own;
   if (!scratch) {
     own.alloc((size_t)bt_space_size(table->grid, BT_SPACE_P1, table->level));

@@ -1119,7 +1119,8 @@ void bt_n1e1_destroy(bt_n1e1* op) { delete op; }
 bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, void* stream) {
   BT_TRY
   if (!op) raise(BT_INVALID_ARGUMENT, "apply_n1e1: operator required");
-  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  if (x == y && bt_space_size(op->grid, BT_SPACE_EDGES, op->level) > 0)
+    raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   const bt_grid& g = *op->grid;
   const int n = 1 << op->level;
   cudaStream_t s = (cudaStream_t)stream;

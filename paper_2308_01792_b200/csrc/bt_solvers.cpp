@@ -248,8 +248,8 @@ static int fmg(bt_hierarchy& h, int finest, const double* const* rhs, double* x,
   if (finest < cl) raise(BT_INVALID_ARGUMENT, "fmg: finest below coarse level");
   if (cl < h.grid->lo || finest > h.grid->hi) raise(BT_OUT_OF_RANGE, "fmg: levels outside the hierarchy");
   if (!rhs) raise(BT_INVALID_ARGUMENT, "fmg: one rhs per level expected");
-  for (int l = cl; l <= finest; ++l)
-    if (!rhs[l - cl]) raise(BT_INVALID_ARGUMENT, "fmg: one rhs per level expected");
+  for (int l = cl; l <= finest; ++l)  // (an empty cell block passes nulls)
+    if (!rhs[l - cl] && h.at(l).n > 0) raise(BT_INVALID_ARGUMENT, "fmg: one rhs per level expected");
   const int need = 1 + mg.cycles * (finest - cl);
   if (!rows || max_rows < need) raise(BT_INVALID_ARGUMENT, "fmg: row buffer too small");
   int nrows = 0;
@@ -258,7 +258,7 @@ static int fmg(bt_hierarchy& h, int finest, const double* const* rhs, double* x,
     rows[nrows++] = bt_fmg_row{l, cyc, res, exact ? l2_error_p1(*h.grid, l, v, *exact, s) : 0.0};
   };
   DevBuf<double> cur(h.at(cl).n), tmp(h.at(cl).n);
-  BT_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(double) * cur.n, s));
+  if (cur.n) BT_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(double) * cur.n, s));
   sync(*h.grid, cl, IF_IMPOSE, cur.p, rhs[0], s);
   cg(h, cl, mg.coarse_tol, mg.coarse_maxit, rhs[0], cur.p, nullptr, s);
   row(cl, 0, rhs[0], cur.p, tmp.p);
@@ -274,7 +274,7 @@ static int fmg(bt_hierarchy& h, int finest, const double* const* rhs, double* x,
     std::swap(cur.p, next.p);
     std::swap(cur.n, next.n);
   }
-  BT_CUDA(cudaMemcpyAsync(x, cur.p, sizeof(double) * cur.n, cudaMemcpyDeviceToDevice, s));
+  if (cur.n) BT_CUDA(cudaMemcpyAsync(x, cur.p, sizeof(double) * cur.n, cudaMemcpyDeviceToDevice, s));
   BT_CUDA(cudaStreamSynchronize(s));
   return nrows;
 }
@@ -335,7 +335,8 @@ void bt_hierarchy_destroy(bt_hierarchy* h) { delete h; }
 
 bt_status bt_hierarchy_apply(bt_hierarchy* h, int level, const double* x, double* y, int bc, void* stream) {
   BT_TRY
-  if (x == y) raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
+  if (x == y && h && bt_space_size(h->grid, BT_SPACE_P1, level) > 0)
+    raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   hier_apply(*h, level, x, y, bc, (cudaStream_t)stream);
   BT_CATCH
 }
@@ -371,7 +372,8 @@ bt_status bt_fmg(bt_hierarchy* h, int finest, const double* const* rhs_levels, d
                  const bt_smoother_config* sm, const bt_multigrid_config* mg, const bt_field* exact,
                  bt_fmg_row* rows, int max_rows, int* nrows, void* stream) {
   BT_TRY
-  if (!h || !sm || !mg || !x) raise(BT_INVALID_ARGUMENT, "fmg: hierarchy, configs and x required");
+  if (!h || !sm || !mg) raise(BT_INVALID_ARGUMENT, "fmg: hierarchy and configs required");
+  if (!x && bt_space_size(h->grid, BT_SPACE_P1, finest) > 0) raise(BT_INVALID_ARGUMENT, "fmg: x required");
   if (exact && (exact->kind < 0 || exact->kind > 2)) raise(BT_INVALID_ARGUMENT, "field kind must be 0, 1 or 2");
   const int nr = fmg(*h, finest, rhs_levels, x, *sm, *mg, exact, rows, max_rows, (cudaStream_t)stream);
   if (nrows) *nrows = nr;

@@ -248,3 +248,43 @@ def test_partitioned_n1e1(text, L, nranks):
         for k in ("x", "y0", "y1", "sync"):
             assert torch.equal(out[k], full[k][b * cs:e * cs]), k
         assert out["dot"] == full["dot"]
+
+
+def test_more_ranks_than_cells():
+    """8 ranks on 6 cells: two ranks hold no cell and still take part in every collective."""
+    text, L = bt.cube_kuhn_text(), 4
+    body = operators_body(text, L)
+    full = body(lambda g: None)
+    ranks = run_ranks(8, body)
+    assert any(out["part"][2] == out["part"][3] for out in ranks)  # an empty block
+    check_slices(full, ranks, L, ["x", "stencil0", "stencil1", "elementwise", "diag_ew", "diag_stencil",
+                                  "prolongate", "sync"], ["restrict"])
+    for out in ranks:
+        assert out["dot"] == full["dot"]
+    vb = vcycle_body(text, 2, 4, bt.KernelKind.Stencil)
+    vfull = vb(lambda g: None)
+    cs = bt.n_tet((1 << 4) + 1)
+    for out in run_ranks(8, vb):
+        _, _, b, e = out["part"]
+        assert torch.equal(out["x"], vfull["x"][b * cs:e * cs])
+        assert out["hist"] == vfull["hist"] and out["cg"] == vfull["cg"]
+
+
+def test_more_ranks_than_cells_n1e1_and_fmg():
+    text = bt.cube_kuhn_text()
+    nb = n1e1_body(text, 3)
+    full = nb(lambda g: None)
+    g = bt.Grid(text, 2, 3)
+    cs = g.space_size(2, 3) // g.n_cells()
+    for out in run_ranks(8, nb):
+        _, _, b, e = out["part"]
+        for k in ("x", "y0", "y1", "sync"):
+            assert torch.equal(out[k], full[k][b * cs:e * cs]), k
+        assert out["dot"] == full["dot"]
+    fb = fmg_body(text, 2, 4)
+    ffull = fb(lambda g: None)
+    cs = bt.n_tet((1 << 4) + 1)
+    for out in run_ranks(8, fb):
+        _, _, b, e = out["part"]
+        assert torch.equal(out["x"], ffull["x"][b * cs:e * cs])
+        assert out["rows"] == ffull["rows"]
