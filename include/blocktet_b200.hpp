@@ -85,6 +85,13 @@ class Grid {
   Level max_level() const { return bt_grid_max_level(g_); }
   bool has_level(Level l) const { return l >= min_level() && l <= max_level(); }
   const bt_grid* handle() const { return g_; }
+  // multi-GPU (one process per GPU): this handle computes and stores the cell
+  // block of `rank`; `allreduce` sums device doubles over the ranks in stream
+  // order (e.g. ncclAllReduce on the stream). Call before allocating.
+  void set_partition(int rank, int nranks, bt_allreduce_fn allreduce, void* user) {
+    check(bt_grid_set_partition(g_, rank, nranks));
+    check(bt_grid_set_allreduce(g_, allreduce, user));
+  }
 
  private:
   bt_grid* g_ = nullptr;
@@ -92,6 +99,14 @@ class Grid {
 inline std::shared_ptr<const Grid> make_grid(const std::string& mesh_text, Level min_level, Level max_level,
                                              int device = 0) {
   return std::make_shared<const Grid>(mesh_text, min_level, max_level, device);
+}
+// make_grid for one rank of a partitioned run
+inline std::shared_ptr<const Grid> make_partitioned_grid(const std::string& mesh_text, Level min_level,
+                                                         Level max_level, int device, int rank, int nranks,
+                                                         bt_allreduce_fn allreduce, void* user) {
+  auto g = std::make_shared<Grid>(mesh_text, min_level, max_level, device);
+  g->set_partition(rank, nranks, allreduce, user);
+  return g;
 }
 inline std::string cubes_mesh_text(int n, double perturb = 0.1, std::uint64_t seed = 0) {
   std::string s((size_t)bt_cubes_mesh_text(n, perturb, seed, nullptr, 0), '\0');
