@@ -23,6 +23,8 @@ struct LevelData {
   double lambda = 0.0;
   // work vectors
   DevBuf<double> r, d, p, ap, z, b, x, tmp;
+  DevBuf<CgState> cg;                   // CG scalars (device-resident)
+  DevBuf<double> cg_hist;               // CG residual history (grown on demand)
 };
 
 }  // namespace bt
@@ -165,9 +167,22 @@ static int cg(bt_hierarchy& h, int l, double tol, int maxit, const double* rhs, 
   double* r = L.r.p;
   double* p = L.p.p;
   double* ap = L.ap.p;
-  DevBuf<CgState> st(1);
-  DevBuf<double> dh((size_t)std::max(maxit, 1));
-  CgState* S = st.p;
+  // Inside a CUDA-graph capture the host cannot poll: every iteration is
+  // recorded and the done flag turns the ones after convergence into no-ops
+  // (a breakdown then stops the updates instead of raising).
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  BT_CUDA(cudaStreamIsCapturing(s, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (!L.cg.p) {
+    if (capturing) raise(BT_LOGIC_ERROR, "cg: run once before capturing a graph (buffers)");
+    L.cg.alloc(1);
+  }
+  if (hist && L.cg_hist.n < (size_t)std::max(maxit, 1)) {
+    if (capturing) raise(BT_LOGIC_ERROR, "cg: no residual history inside a graph capture");
+    L.cg_hist.alloc((size_t)std::max(maxit, 1));
+  }
+  double* dh = hist ? L.cg_hist.p : nullptr;
+  CgState* S = L.cg.p;
   hier_apply(h, l, x, r, 1, s);
   launch_vec(V_SCALE, r, nullptr, -1.0, n, s);
   launch_vec(V_AXPY, r, rhs, 1.0, n, s);
@@ -177,6 +192,7 @@ static int cg(bt_hierarchy& h, int l, double tol, int maxit, const double* rhs, 
   launch_cg_init(S, tol, s);
   CgState hs{};
   auto poll = [&] {
+    if (capturing) return;
     BT_CUDA(cudaMemcpyAsync(&hs, S, sizeof(CgState), cudaMemcpyDeviceToHost, s));
     BT_CUDA(cudaStreamSynchronize(s));
   };
@@ -189,7 +205,7 @@ static int cg(bt_hierarchy& h, int l, double tol, int maxit, const double* rhs, 
     launch_vec_dev(V_AXPY, x, p, &S->alpha, &S->done, n, s);
     launch_vec_dev(V_AXPY, r, ap, &S->malpha, &S->done, n, s);
     dot_p1_device(*h.grid, l, r, r, &S->rs_new, s);
-    launch_cg_update(S, tol, dh.p, s);
+    launch_cg_update(S, tol, dh, s);
     launch_vec_dev(V_SCALE, p, nullptr, &S->beta, &S->done, n, s);
     launch_vec_dev(V_AXPY, p, r, &S->one, &S->done, n, s);  // p += 1.0 r
     if (it % kPoll == 0 || it == maxit) {
@@ -197,9 +213,9 @@ static int cg(bt_hierarchy& h, int l, double tol, int maxit, const double* rhs, 
       if (hs.done) break;
     }
   }
+  if (capturing) return 0;
   if (hs.breakdown) raise(BT_RUNTIME_ERROR, "cg breakdown: operator is not positive definite");
-  if (hist && hs.it)
-    BT_CUDA(cudaMemcpy(hist, dh.p, sizeof(double) * (size_t)hs.it, cudaMemcpyDeviceToHost));
+  if (hist && hs.it) BT_CUDA(cudaMemcpy(hist, dh, sizeof(double) * (size_t)hs.it, cudaMemcpyDeviceToHost));
   return hs.it;
 }
 

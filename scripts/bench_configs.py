@@ -202,6 +202,15 @@ def cfg5(res, skip_cpu):
         slots = g.space_size(0, hi)
         run = {"mesh": f"{n}x{n}x{n} cubes x 6 perturbed Kuhn tets ({6 * n ** 3} cells)", "levels": f"{lo}->{hi}",
                "fine_slots": slots, "gpu_sec_per_cycle": float(np.median(ts)), "residual_history": hist}
+        if slots < 50_000_000:  # latency-bound sizes: the same cycle replayed from a CUDA graph
+            graph = torch.cuda.CUDAGraph()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                with torch.cuda.graph(graph, stream=st):
+                    bt.v_cycle(h, hi, rhs, xx, sm, mg)
+            run["gpu_sec_per_cycle_graph"] = timed(graph.replay, 5)
+            del graph
         if cpu_ok and not skip_cpu:
             rr = pyoracle.Reference(text, lo, hi)
             rr.make_hierarchy(form=2, kp=pyoracle.kparams(), kernel=0, threads=nproc())
