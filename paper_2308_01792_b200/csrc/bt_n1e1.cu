@@ -141,25 +141,27 @@ unsigned host_mask(int g, int i, int j, int k, int n) {
   }
   return mask;
 }
-// the 4 mask cases of rows j, k >= 1: full, i == 0, diagonal (i + j + k == n - 1), both
-unsigned case_mask(int g, int wsel, int n) {
-  if (wsel == 0) return (1u << hS.ninc[g]) - 1;  // all incident micro-tets (no such edge at n = 4)
-  static const int rep[4][3] = {{1, 1, 1}, {0, 1, 1}, {-3, 1, 1}, {0, 1, -2}};  // negative: n + value
-  const int i = rep[wsel][0] < 0 ? n + rep[wsel][0] : rep[wsel][0];
-  const int k = rep[wsel][2] < 0 ? n + rep[wsel][2] : rep[wsel][2];
-  return host_mask(g, i, rep[wsel][1], k, n);
+// the mask cases of rows j >= 1: row case k0 (layer k == 0, or k >= 1) x lane
+// case wsel (0 full, 1 i == 0, 2 diagonal i + j + k == n - 1, 3 both)
+unsigned case_mask(int g, int wsel, int n, int k0) {
+  if (wsel == 0 && !k0) return (1u << hS.ninc[g]) - 1;  // all incident micro-tets (no such edge at n = 4)
+  static const int rep[2][4][3] = {{{1, 1, 1}, {0, 1, 1}, {-3, 1, 1}, {0, 1, -2}},   // k >= 1 (negative: n + value)
+                                   {{1, 1, 0}, {0, 1, 0}, {-2, 1, 0}, {0, -1, 0}}};  // k == 0
+  const int* r = rep[k0][wsel];
+  auto v = [&](int a) { return a < 0 ? n + a : a; };
+  return host_mask(g, v(r[0]), v(r[1]), v(r[2]), n);
 }
-// k_n1e1_fast relies on: for j, k >= 1 an edge's mask depends only on
-// (i == 0, i + j + k == n - 1). Checked exhaustively at width nchk.
+// k_n1e1_fast relies on: for rows j >= 1 an edge's mask depends only on
+// (k == 0, i == 0, i + j + k == n - 1). Checked exhaustively at width nchk.
 void check_mask_cases(int nchk) {
   for (int g = 1; g <= 7; ++g) {
     const int w = g == 7 ? nchk - 1 : nchk;
-    for (int k = 1; k < w; ++k)
+    for (int k = 0; k < w; ++k)
       for (int j = 1; j < w - k; ++j)
         for (int i = 0; i < w - k - j; ++i) {
           const int wsel = (i == 0 ? 1 : 0) | (i + j + k == nchk - 1 ? 2 : 0);
-          if (host_mask(g, i, j, k, nchk) != case_mask(g, wsel, nchk))
-            raise(BT_LOGIC_ERROR, "n1e1: mask cases of rows j, k >= 1 do not hold");
+          if (host_mask(g, i, j, k, nchk) != case_mask(g, wsel, nchk, k == 0 ? 1 : 0))
+            raise(BT_LOGIC_ERROR, "n1e1: mask cases of rows j >= 1 do not hold");
         }
   }
 }
@@ -298,8 +300,8 @@ __device__ __forceinline__ void n1e1_row(const double* __restrict__ x, double* _
 // grid (row chunk x 7 orientations, cells); orientation G's rows here are
 // q < w_G: (j = q, k = 0); q < 2 w_G - 1: (j = 0, k = q - w_G + 1); then, for
 // G != 7, the rows of length 1 with j, k >= 1: k = q - 2 w_G + 2, j = n - 1 - k
-__host__ __device__ inline int n1e1_long_rows(int g, int n) { return 2 * (g == 7 ? n - 1 : n) - 1; }
-__host__ __device__ inline int n1e1_short_rows(int g, int n) { return g == 7 ? 0 : max(0, n - 2); }
+__host__ __device__ inline int n1e1_long_rows(int g, int n) { return g == 7 ? n - 1 : n; }
+__host__ __device__ inline int n1e1_short_rows(int g, int n) { return g == 7 ? 0 : max(0, n - 1); }
 // block x = chunk * 7 + (g - 1): chunks [0, kLong) hold kW long rows each (a
 // warp per row), the rest kT rows of length 1 each (a thread per row)
 __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, double* __restrict__ y,
@@ -321,17 +323,17 @@ __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, 
   }
   __syncthreads();
   int j, k, ifirst, istep;
-  if (chunk < long_chunks) {  // (j = q, k = 0), then (j = 0, k = q - w_G + 1)
+  if (chunk < long_chunks) {  // rows j = 0 of every layer: (0, k = q)
     const int q = chunk * kW + (threadIdx.x >> 5);
     if (q >= n1e1_long_rows(g, n)) return;
-    j = q < wg ? q : 0;
-    k = q < wg ? 0 : q - wg + 1;
+    j = 0;
+    k = q;
     ifirst = threadIdx.x & 31;
     istep = 32;
-  } else {  // rows of length 1 with j, k >= 1 (orientations 1..6): k = q + 1, j = n - 1 - k
+  } else {  // rows of length 1 with j >= 1 (orientations 1..6): k = q, j = n - 1 - k
     const int q = (chunk - long_chunks) * kT + threadIdx.x;
     if (q >= n1e1_short_rows(g, n)) return;
-    k = q + 1;
+    k = q;
     j = n - 1 - k;
     ifirst = 0;
     istep = 1;
@@ -377,8 +379,11 @@ constexpr int kN1March = 32;   // rows per march
 constexpr int kN1Wt = 20;      // padded weight row (19 coupled edges)
 constexpr int kN1Corr = kN1Corr0 + kN1Corr1;
 constexpr int kN1RingD = kN1Stages * kN1Streams * 32;  // doubles per warp
-constexpr int kN1CellW = 7 * kN1Wt + kN1Corr;          // per cell: full rows, then corrections (case 0, case 1)
-constexpr int kN1CellWP = (kN1CellW + 1) / 2 * 2;      // padded to 16 bytes
+// per cell and row case (layer k >= 1, layer 0): the base rows, then the
+// corrections of lane cases 0 (i == 0) and 1 (diagonal)
+constexpr int kN1CaseW = 7 * kN1Wt + kN1Corr;
+constexpr int kN1CaseWP = (kN1CaseW + 1) / 2 * 2;      // padded to 16 bytes
+constexpr int kN1CellWP = 2 * kN1CaseWP;
 constexpr int kN1BlocksPerCell = 16;
 
 template <int G, int PH>
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
   const int tn = tet32(n);
   const double* __restrict__ xc = x + (int64_t)cl * cs;
   double* __restrict__ yc = y + (int64_t)cl * cs;
-  const double (&W)[7][kN1Wt] = *reinterpret_cast<const double(*)[7][kN1Wt]>(sw);
+
 
   // ---- producer: lane copies its column of one row per stream per step ----
   int pt = t0, pnext_t = t0, pleft = 0, pj = 0, pk = 0, pcol = 0;
@@ -468,8 +473,9 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
       for (int s = 0; s < kN1Streams; ++s) {
         const int g = n1_stream(s, 0), w = g == 7 ? n - 1 : n;
         const int jr = pj + n1_stream(s, 2);
-        const int len = w - jr - (pk + n1_stream(s, 1));  // staged row's length
-        const bool ok = jr >= 0 && (unsigned)pcol < (unsigned)len;
+        const int kr = pk + n1_stream(s, 1);
+        const int len = w - jr - kr;  // staged row's length
+        const bool ok = jr >= 0 && kr >= 0 && (unsigned)pcol < (unsigned)len;
         cp8z(d + s * 256, ok ? xc + po[s] : xc, ok);
         po[s] += len;
       }
@@ -504,6 +510,8 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
   while (t < nmarch) {
     const int4 tk = marches[t];
     const int k = tk.x & 0xffff, b = tk.x >> 16, j0 = tk.y, j1 = tk.z;
+    const double* wcase = sw + (k == 0 ? kN1CaseWP : 0);  // layer 0: its own base rows and corrections
+    const double (&W)[7][kN1Wt] = *reinterpret_cast<const double(*)[7][kN1Wt]>(wcase);
     const int i = kN1Cols * b - 1 + lane;
     const bool out = lane >= 1 && lane <= kN1Cols;
     int yo[7];  // this lane's output slot in orientation G's row j
@@ -545,7 +553,7 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
       e[7] = n1_edge<7, PH>(win, sh, W[6]);
       if (b == 0) {  // lane 1 holds i == 0
         double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        n1_correct<0, PH>(win, sh, sw + 7 * kN1Wt, c);
+        n1_correct<0, PH>(win, sh, wcase + 7 * kN1Wt, c);
         if (i == 0)
 #pragma unroll
           for (int G = 1; G <= 7; ++G) e[G] += c[G];
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
       const int dl = L - kN1Cols * b;  // the lane holding the diagonal edge i == L - 1
       if (dl >= 1 && dl <= kN1Cols) {
         double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        n1_correct<1, PH>(win, sh, sw + 7 * kN1Wt, c);
+        n1_correct<1, PH>(win, sh, wcase + 7 * kN1Wt, c);
         if (i == L - 1)
 #pragma unroll
           for (int G = 1; G <= 7; ++G) e[G] += c[G];
@@ -1067,26 +1075,27 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
       auto mrow = [&](int gg, unsigned mask) {
         return &masked[((size_t)c * hS.mask_rows + hS.mask_off[gg] + mask) * 19];
       };
-      for (int gg = 1; gg <= 7; ++gg) {
-        const double* full = mrow(gg, case_mask(gg, 0, n));
-        for (int m = 0; m < hS.nnb[gg]; ++m) cw[(size_t)c * kN1CellWP + (gg - 1) * kN1Wt + m] = full[m];
-        // corrections: every coupling outside the generated lists must keep its full weight
-        for (int cc = 0; cc < 2; ++cc) {
-          if (cc == 1 && gg == 7) continue;
-          const double* part = mrow(gg, case_mask(gg, cc == 0 ? 1 : 2, n));
-          for (int m = 0; m < hS.nnb[gg]; ++m) {
-            int q = -1;
-            const int nq = cc == 0 ? kN1Corr0 : kN1Corr1;
-            for (int e = 0; e < nq; ++e)
-              if (n1_corr(cc, e, 0) == gg && n1_corr(cc, e, 1) == m) q = e;
-            if (q < 0) {
-              if (part[m] != full[m])
-                raise(BT_LOGIC_ERROR, "n1e1: correction table misses coupling " + std::to_string(m) + " of orientation " +
-                                          std::to_string(gg) + ", case " + std::to_string(cc) + " (masks " +
-                                          std::to_string(case_mask(gg, 0, n)) + " / " +
-                                          std::to_string(case_mask(gg, cc == 0 ? 1 : 2, n)) + ")");
-            } else {
-              cw[(size_t)c * kN1CellWP + 7 * kN1Wt + (cc == 0 ? 0 : kN1Corr0) + q] = part[m] - full[m];
+      for (int k0 = 0; k0 < 2; ++k0) {
+        double* cc_w = &cw[(size_t)c * kN1CellWP + (size_t)k0 * kN1CaseWP];
+        for (int gg = 1; gg <= 7; ++gg) {
+          const double* base = mrow(gg, case_mask(gg, 0, n, k0));
+          for (int m = 0; m < hS.nnb[gg]; ++m) cc_w[(gg - 1) * kN1Wt + m] = base[m];
+          // corrections: every coupling outside the generated lists must keep its base weight
+          for (int cc = 0; cc < 2; ++cc) {
+            if (cc == 1 && gg == 7) continue;
+            const double* part = mrow(gg, case_mask(gg, cc == 0 ? 1 : 2, n, k0));
+            for (int m = 0; m < hS.nnb[gg]; ++m) {
+              int q = -1;
+              const int nq = cc == 0 ? kN1Corr0 : kN1Corr1;
+              for (int e = 0; e < nq; ++e)
+                if (n1_corr(cc, e, 0) == gg && n1_corr(cc, e, 1) == m) q = e;
+              if (q < 0) {
+                if (part[m] != base[m])
+                  raise(BT_LOGIC_ERROR, "n1e1: correction table misses coupling " + std::to_string(m) +
+                                            " of orientation " + std::to_string(gg) + ", case " + std::to_string(cc));
+              } else {
+                cc_w[7 * kN1Wt + (cc == 0 ? 0 : kN1Corr0) + q] = part[m] - base[m];
+              }
             }
           }
         }
@@ -1095,12 +1104,12 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
     // One cell's marches in spatial order — column block, row block, layer
     // k innermost — so the warps working on a cell at any time cover a
     // compact region whose x rows the neighbouring layers re-read from L2.
-    // Rows j, k >= 1 of length >= 2 (orientations 1..6; xyz rows are one
-    // shorter and all covered).
+    // Rows j >= 1 of length >= 2 (orientations 1..6; xyz rows are one
+    // shorter and all covered), layer 0 included.
     std::vector<int4> marches;
-    for (int b = 0; kN1Cols * b <= n - 3; ++b)
-      for (int j0 = 1; j0 <= n - 2 - kN1Cols * b; j0 += kN1March)
-        for (int k = 1; k <= n - 3; ++k) {
+    for (int b = 0; kN1Cols * b <= n - 2; ++b)
+      for (int j0 = 1; j0 <= n - 1 - kN1Cols * b; j0 += kN1March)
+        for (int k = 0; k <= n - 3; ++k) {
           const int jmax = b == 0 ? n - k - 2 : n - k - 1 - kN1Cols * b;  // last row with an output in block b
           if (j0 > jmax) continue;
           marches.push_back(make_int4(k | (b << 16), j0, std::min(j0 + kN1March, jmax + 1), 0));

@@ -45,6 +45,23 @@ def test_n1e1_parity(mesh, l):
             assert rel(host(y, l), o.n1e1_apply(l, xh, alpha, beta, int(bc))) <= REL
 
 
+@pytest.mark.parametrize("l", [5, 6])
+def test_n1e1_parity_several_column_blocks(l):
+    """Levels 5 and 6: the staged kernel's rows span 2 or 3 column blocks of 30 (and layer 0 and the diagonal end
+    fall into blocks b >= 1)."""
+    text = cube_kuhn_text()
+    g = bt.Grid(text, l, l)
+    o = Oracle(text, l, l)
+    x = bt.allocate(bt.edge_space(), g)
+    y = bt.allocate(bt.edge_space(), g)
+    bt.random_fill(x, l, 5)
+    xh = host(x, l)
+    op = bt.N1E1Operator(g, l, 1.0, 1.0)
+    for bc in (bt.BC.None_, bt.BC.DirichletIdentity):
+        bt.apply_n1e1(op, x, y, l, bc)
+        assert rel(host(y, l), o.n1e1_apply(l, xh, 1.0, 1.0, int(bc))) <= REL
+
+
 def test_n1e1_config4_family_properties():
     """Config 4 family (perturbed Kuhn cubes, tangential Dirichlet): curl grad
     = 0 and symmetry at level 5 on 48 macro-tets, oracle parity at level 3."""
