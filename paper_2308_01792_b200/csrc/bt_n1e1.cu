@@ -141,27 +141,32 @@ unsigned host_mask(int g, int i, int j, int k, int n) {
   }
   return mask;
 }
-// the mask cases of rows j >= 1: row case k0 (layer k == 0, or k >= 1) x lane
-// case wsel (0 full, 1 i == 0, 2 diagonal i + j + k == n - 1, 3 both)
-unsigned case_mask(int g, int wsel, int n, int k0) {
-  if (wsel == 0 && !k0) return (1u << hS.ninc[g]) - 1;  // all incident micro-tets (no such edge at n = 4)
-  static const int rep[2][4][3] = {{{1, 1, 1}, {0, 1, 1}, {-3, 1, 1}, {0, 1, -2}},   // k >= 1 (negative: n + value)
-                                   {{1, 1, 0}, {0, 1, 0}, {-2, 1, 0}, {0, -1, 0}}};  // k == 0
-  const int* r = rep[k0][wsel];
+// the mask cases of an edge: row case rc (bit 0: k == 0, bit 1: j == 0) x
+// lane case wsel (0 full, 1 i == 0, 2 diagonal i + j + k == n - 1, 3 both)
+unsigned case_mask(int g, int wsel, int n, int rc) {
+  if (wsel == 0 && rc == 0) return (1u << hS.ninc[g]) - 1;  // all incident micro-tets (no such edge at n = 4)
+  static const int rep[4][4][3] = {  // representative (i, j, k); negative: n + value
+      {{1, 1, 1}, {0, 1, 1}, {-3, 1, 1}, {0, 1, -2}},    // j, k >= 1
+      {{1, 1, 0}, {0, 1, 0}, {-2, 1, 0}, {0, -1, 0}},    // k == 0, j >= 1
+      {{1, 0, 1}, {0, 0, 1}, {-2, 0, 1}, {0, 0, -1}},    // j == 0, k >= 1
+      {{1, 0, 0}, {0, 0, 0}, {-1, 0, 0}, {0, 0, 0}}};    // j == k == 0 (no "both" edge for n > 1)
+  const int* r = rep[rc][wsel];
   auto v = [&](int a) { return a < 0 ? n + a : a; };
   return host_mask(g, v(r[0]), v(r[1]), v(r[2]), n);
 }
-// k_n1e1_fast relies on: for rows j >= 1 an edge's mask depends only on
-// (k == 0, i == 0, i + j + k == n - 1). Checked exhaustively at width nchk.
+// k_n1e1_fast relies on: an edge's mask depends only on (j == 0, k == 0,
+// i == 0, i + j + k == n - 1). Checked exhaustively at width nchk.
 void check_mask_cases(int nchk) {
   for (int g = 1; g <= 7; ++g) {
     const int w = g == 7 ? nchk - 1 : nchk;
     for (int k = 0; k < w; ++k)
-      for (int j = 1; j < w - k; ++j)
+      for (int j = 0; j < w - k; ++j)
         for (int i = 0; i < w - k - j; ++i) {
           const int wsel = (i == 0 ? 1 : 0) | (i + j + k == nchk - 1 ? 2 : 0);
-          if (host_mask(g, i, j, k, nchk) != case_mask(g, wsel, nchk, k == 0 ? 1 : 0))
-            raise(BT_LOGIC_ERROR, "n1e1: mask cases of rows j >= 1 do not hold");
+          if (wsel == 3) continue;  // rows of length 1: the face kernel's
+          const int rc = (k == 0 ? 1 : 0) | (j == 0 ? 2 : 0);
+          if (host_mask(g, i, j, k, nchk) != case_mask(g, wsel, nchk, rc))
+            raise(BT_LOGIC_ERROR, "n1e1: mask cases do not hold");
         }
   }
 }
@@ -300,8 +305,8 @@ __device__ __forceinline__ void n1e1_row(const double* __restrict__ x, double* _
 // grid (row chunk x 7 orientations, cells); orientation G's rows here are
 // q < w_G: (j = q, k = 0); q < 2 w_G - 1: (j = 0, k = q - w_G + 1); then, for
 // G != 7, the rows of length 1 with j, k >= 1: k = q - 2 w_G + 2, j = n - 1 - k
-__host__ __device__ inline int n1e1_long_rows(int g, int n) { return g == 7 ? n - 1 : n; }
-__host__ __device__ inline int n1e1_short_rows(int g, int n) { return g == 7 ? 0 : max(0, n - 1); }
+__host__ __device__ inline int n1e1_long_rows(int g, int n) { return 0; }
+__host__ __device__ inline int n1e1_short_rows(int g, int n) { return g == 7 ? 0 : n; }
 // block x = chunk * 7 + (g - 1): chunks [0, kLong) hold kW long rows each (a
 // warp per row), the rest kT rows of length 1 each (a thread per row)
 __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, double* __restrict__ y,
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, 
     k = q;
     ifirst = threadIdx.x & 31;
     istep = 32;
-  } else {  // rows of length 1 with j >= 1 (orientations 1..6): k = q, j = n - 1 - k
+  } else {  // rows of length 1 (orientations 1..6): k = q, j = n - 1 - k
     const int q = (chunk - long_chunks) * kT + threadIdx.x;
     if (q >= n1e1_short_rows(g, n)) return;
     k = q;
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, 
 }
 
 // ---------------------------------------------------------------------------
-// k_n1e1_fast: rows j, k >= 1 (of length >= 2) of all 7 orientations, staged
+// k_n1e1_fast: every row of length >= 2 of all 7 orientations, staged
 // like the P1 interior kernel. A warp owns 30 output columns i = 30b ..
 // 30b + 29 of layer k of one cell (lane l: column 30b - 1 + l; lanes 1..30
 // store) and marches rows j0 .. j1 - 1 of all 7 orientations at once. The 19
@@ -379,11 +384,11 @@ constexpr int kN1March = 32;   // rows per march
 constexpr int kN1Wt = 20;      // padded weight row (19 coupled edges)
 constexpr int kN1Corr = kN1Corr0 + kN1Corr1;
 constexpr int kN1RingD = kN1Stages * kN1Streams * 32;  // doubles per warp
-// per cell and row case (layer k >= 1, layer 0): the base rows, then the
-// corrections of lane cases 0 (i == 0) and 1 (diagonal)
+// per cell and row case (bit 0: layer k == 0, bit 1: row j == 0): the base
+// rows, then the corrections of lane cases 0 (i == 0) and 1 (diagonal)
 constexpr int kN1CaseW = 7 * kN1Wt + kN1Corr;
 constexpr int kN1CaseWP = (kN1CaseW + 1) / 2 * 2;      // padded to 16 bytes
-constexpr int kN1CellWP = 2 * kN1CaseWP;
+constexpr int kN1CellWP = 4 * kN1CaseWP;
 constexpr int kN1BlocksPerCell = 16;
 
 template <int G, int PH>
@@ -510,8 +515,6 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
   while (t < nmarch) {
     const int4 tk = marches[t];
     const int k = tk.x & 0xffff, b = tk.x >> 16, j0 = tk.y, j1 = tk.z;
-    const double* wcase = sw + (k == 0 ? kN1CaseWP : 0);  // layer 0: its own base rows and corrections
-    const double (&W)[7][kN1Wt] = *reinterpret_cast<const double(*)[7][kN1Wt]>(wcase);
     const int i = kN1Cols * b - 1 + lane;
     const bool out = lane >= 1 && lane <= kN1Cols;
     int yo[7];  // this lane's output slot in orientation G's row j
@@ -537,6 +540,9 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
       consume(v);
       place(phc, v);
       const int L = n - j - k;  // row length of orientations 1..6 (xyz: L - 1)
+      // this row's case: layer 0 and row 0 have their own base rows and corrections
+      const double* wcase = sw + ((k == 0 ? 1 : 0) | (j == 0 ? 2 : 0)) * kN1CaseWP;
+      const double (&W)[7][kN1Wt] = *reinterpret_cast<const double(*)[7][kN1Wt]>(wcase);
       double sh[kN1Shuf];       // column i +- 1 values, each distinct one shuffled once
 #pragma unroll
       for (int q = 0; q < kN1Shuf; ++q) {
@@ -1075,7 +1081,7 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
       auto mrow = [&](int gg, unsigned mask) {
         return &masked[((size_t)c * hS.mask_rows + hS.mask_off[gg] + mask) * 19];
       };
-      for (int k0 = 0; k0 < 2; ++k0) {
+      for (int k0 = 0; k0 < 4; ++k0) {  // row case
         double* cc_w = &cw[(size_t)c * kN1CellWP + (size_t)k0 * kN1CaseWP];
         for (int gg = 1; gg <= 7; ++gg) {
           const double* base = mrow(gg, case_mask(gg, 0, n, k0));
@@ -1104,12 +1110,12 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
     // One cell's marches in spatial order — column block, row block, layer
     // k innermost — so the warps working on a cell at any time cover a
     // compact region whose x rows the neighbouring layers re-read from L2.
-    // Rows j >= 1 of length >= 2 (orientations 1..6; xyz rows are one
-    // shorter and all covered), layer 0 included.
+    // Every row of length >= 2 (orientations 1..6; xyz rows are one shorter
+    // and all covered).
     std::vector<int4> marches;
     for (int b = 0; kN1Cols * b <= n - 2; ++b)
-      for (int j0 = 1; j0 <= n - 1 - kN1Cols * b; j0 += kN1March)
-        for (int k = 0; k <= n - 3; ++k) {
+      for (int j0 = 0; j0 <= n - 1 - kN1Cols * b; j0 += kN1March)
+        for (int k = 0; k <= n - 2; ++k) {
           const int jmax = b == 0 ? n - k - 2 : n - k - 1 - kN1Cols * b;  // last row with an output in block b
           if (j0 > jmax) continue;
           marches.push_back(make_int4(k | (b << 16), j0, std::min(j0 + kN1March, jmax + 1), 0));
