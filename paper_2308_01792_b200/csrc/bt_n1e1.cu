@@ -240,9 +240,9 @@ struct bt_n1e1 {
   // per cell, per orientation g, per presence mask of the incident micro-tets:
   // the merged 19-weight row of the present ones (cS.mask_off / mask_rows)
   bt::DevBuf<double> d_masked;
-  // k_n1e1_fast: per cell, the merged rows of its 4 mask cases (rows j, k >= 1),
-  // and its march tasks {cell, k | block << 16, j0, j1}, longest first
-  bt::DevBuf<double> d_cellw;  // per cell: full rows (7 x kN1Wt), corrections (kN1Corr), padded
+  // k_n1e1_fast: per cell and row case (j == 0, k == 0), the base merged rows
+  // and the lane-case corrections; one cell's march list
+  bt::DevBuf<double> d_cellw;  // per cell: 4 x (base rows 7 x kN1Wt, corrections kN1Corr), padded
   bt::DevBuf<int4> d_marches;  // one cell's marches {k | block << 16, j0, j1}, spatial order
   int nmarch = 0;
   bt::DevBuf<int> d_next;      // per cell: march queue counter
@@ -252,11 +252,12 @@ namespace bt {
 namespace {
 
 // ---------------------------------------------------------------------------
-// Face rows (j = 0 or k = 0 of an orientation's lattice): one warp per row.
-// Every edge applies one merged row — the row of its present incident
-// micro-tets (presence mask from per-row intervals), from the block's shared
-// table — with straight-line loads: a coupled edge that does not exist reads
-// slot 0 with weight 0. Rows with j, k >= 1 are k_n1e1_fast's.
+// Per-edge path (k_n1e1_face): rows of length 1, whose single edge is both
+// at i == 0 and on the diagonal face. Every edge applies one merged row — the
+// row of its present incident micro-tets (presence mask from per-row
+// intervals), from the block's shared table — with straight-line loads: a
+// coupled edge that does not exist reads slot 0 with weight 0. Every longer
+// row is k_n1e1_fast's.
 // ---------------------------------------------------------------------------
 // edges i = ifirst, ifirst + istep, ... of row (j, k): a warp per row
 // (lane, 32), or a thread per row of length 1 (0, 1)
@@ -302,9 +303,9 @@ __device__ __forceinline__ void n1e1_row(const double* __restrict__ x, double* _
   }
 }
 
-// grid (row chunk x 7 orientations, cells); orientation G's rows here are
-// q < w_G: (j = q, k = 0); q < 2 w_G - 1: (j = 0, k = q - w_G + 1); then, for
-// G != 7, the rows of length 1 with j, k >= 1: k = q - 2 w_G + 2, j = n - 1 - k
+// grid (row chunk x 7 orientations, cells): orientation G's rows of length 1
+// (G != 7: k = q, j = n - 1 - k). The warp-per-row mode (long rows) is kept for
+// any other row set but unused: k_n1e1_fast takes every longer row.
 __host__ __device__ inline int n1e1_long_rows(int g, int n) { return 0; }
 __host__ __device__ inline int n1e1_short_rows(int g, int n) { return g == 7 ? 0 : n; }
 // block x = chunk * 7 + (g - 1): chunks [0, kLong) hold kW long rows each (a
@@ -370,11 +371,12 @@ __global__ void __launch_bounds__(kT) k_n1e1_face(const double* __restrict__ x, 
 //
 // Block row y works on cell y; its blocks take the cell's marches from a
 // queue. The cell's weights sit in shared memory and every lane reads the
-// same address (broadcast). Rows j, k >= 1 use the full merged row, except
-// at i == 0 and on the diagonal face i + j + k == n - 1, where some incident
-// micro-tets are absent: there a correction (partial - full weight) over the
-// 33 affected couplings is added (rows of length 1, which are both, are the
-// face kernel's). Coupled edges outside the lattice read the zero fill.
+// same address (broadcast). The presence mask of an edge's incident
+// micro-tets depends on a row case (j == 0, k == 0: uniform over a step, each
+// with its own merged rows) and a lane case (i == 0, diagonal face i + j + k ==
+// n - 1), for which a correction (partial - base weight) over the 33 affected
+// couplings is added (rows of length 1, which are both, are the face
+// kernel's). Coupled edges outside the lattice read the zero fill.
 // ---------------------------------------------------------------------------
 constexpr int kN1FT = 128;
 constexpr int kN1FW = kN1FT / 32;
@@ -1071,7 +1073,7 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
       }
   }
   op->d_masked.upload(masked);
-  // k_n1e1_fast: rows j, k >= 1 of every cell (n >= 4)
+  // k_n1e1_fast: every row of length >= 2 of every cell (n >= 4)
   if (n1e1_fast_available(level)) {  // (n >= 4)
     const int n = 1 << level;
     check_generated_tables();
