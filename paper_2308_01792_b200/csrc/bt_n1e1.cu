@@ -625,8 +625,7 @@ __device__ __forceinline__ int64_t edge_slot(int n, int64_t cs, int cell, int i0
   const int o2 = g == 5 || g == 6 ? 1 : 0;  // z-offset for xz, yz
   aj -= o0;
   ak -= o2;
-  int eoff = 0;
-  for (int q = 1; q < g; ++q) eoff += tet32(q == 7 ? n - 1 : n);
+  const int eoff = (g - 1) * tet32(n);  // subgroups 1..6 have width n; xyz (7) comes last
   const int wg = g == 7 ? n - 1 : n;
   return (int64_t)cell * cs + eoff + row_start(wg, aj, ak) + ai;
 }
@@ -635,6 +634,37 @@ __device__ __forceinline__ void ijk3(const int8_t* lv, int w0, int w1, int w2, i
   i = (lv[0] == 1 ? w0 : 0) + (lv[1] == 1 ? w1 : 0) + (lv[2] == 1 ? w2 : 0);
   j = (lv[0] == 2 ? w0 : 0) + (lv[1] == 2 ? w1 : 0) + (lv[2] == 2 ? w2 : 0);
   k = (lv[0] == 3 ? w0 : 0) + (lv[1] == 3 ? w1 : 0) + (lv[2] == 3 ? w2 : 0);
+}
+
+// faces (at most 2 members): slots and signs computed once, then the same
+// member-order operations as signed_group
+template <int MODE, class S>
+__device__ __forceinline__ void signed_group2(double* __restrict__ v, const double* __restrict__ src, int count,
+                                              bool dir, S slot) {
+  int sg[2] = {1, 1};
+  int64_t t[2] = {0, 0};
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+    if (m < count) t[m] = slot(m, sg[m]);
+  if (MODE == IF_SYNC || (MODE == IF_SYNC_DIR && !dir)) {
+    if (count < 2) return;
+    const double a = v[t[0]], b = v[t[1]];
+    double sum = 0;
+    sum += sg[0] > 0 ? a : -a;
+    sum += sg[1] > 0 ? b : -b;
+    v[t[0]] = sg[0] > 0 ? sum : -sum;
+    v[t[1]] = sg[1] > 0 ? sum : -sum;
+  } else if (MODE == IF_SYNC_DIR || MODE == IF_IMPOSE) {
+    if (!dir) return;
+    for (int m = 0; m < count; ++m) v[t[m]] = src[t[m]];
+  } else if (MODE == IF_ZERO_DIR) {
+    if (!dir) return;
+    for (int m = 0; m < count; ++m) v[t[m]] = 0.0;
+  } else if (MODE == IF_BCAST) {
+    if (count < 2) return;
+    const double u = sg[0] > 0 ? v[t[0]] : -v[t[0]];
+    v[t[1]] = sg[1] > 0 ? u : -u;
+  }
 }
 
 template <int MODE, class S>
@@ -689,7 +719,7 @@ __global__ void __launch_bounds__(kT) k_edge_faces(double* __restrict__ v, const
   else if (tau == 1) b1 = bb + 1;
   else { a0 = aa + 1; b1 = bb + 1; }
   const DevFace f = a.faces[a.flist[blockIdx.y]];
-  signed_group<MODE>(v, src, f.ncell, f.dir != 0, [&](int m, int& sg) {
+  signed_group2<MODE>(v, src, f.ncell, f.dir != 0, [&](int m, int& sg) {
     int i0, j0, k0, i1, j1, k1;
     ijk3(f.lv[m], n - a0 - b0, a0, b0, i0, j0, k0);
     ijk3(f.lv[m], n - a1 - b1, a1, b1, i1, j1, k1);
