@@ -382,7 +382,7 @@ constexpr int kN1FT = 128;
 constexpr int kN1FW = kN1FT / 32;
 constexpr int kN1Stages = 3;   // ring stages per warp (prefetch distance 2 steps)
 constexpr int kN1Cols = 30;    // output columns per warp
-constexpr int kN1March = 32;   // rows per march
+constexpr int kN1March = 64;   // rows per march
 constexpr int kN1Wt = 20;      // padded weight row (19 coupled edges)
 constexpr int kN1Corr = kN1Corr0 + kN1Corr1;
 constexpr int kN1RingD = kN1Stages * kN1Streams * 32;  // doubles per warp
