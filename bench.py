@@ -215,18 +215,13 @@ def run_ours(args):
     def step(ev=None):
         # events bracket the device work of one apply: on 1 GPU the whole
         # apply_stencil (interior kernel || fused boundary kernel incl. the
-        # replica sums); on N GPUs the per-cell rows (the exchange follows)
+        # replica sums); on N GPUs the whole partitioned apply, exchange included
         if ev is not None:
             ev[0].record(stream)
-        if ws > 1:
-            bt.api._check(L.bt_apply_stencil_cells(table.handle, xp, yp, sp))
-            if ev is not None:
-                ev[1].record(stream)
-            bt.api._exchange(y, LEVEL, 0)
-        else:
-            bt.api._check(L.bt_apply_stencil(table.handle, xp, yp, 0, sp))
-            if ev is not None:
-                ev[1].record(stream)
+        # N > 1: per-cell rows with the NCCL interface exchange overlapped with the interior marches
+        bt.api._check(L.bt_apply_stencil(table.handle, xp, yp, 0, sp))
+        if ev is not None:
+            ev[1].record(stream)
 
     for _ in range(args.warmup):
         step()

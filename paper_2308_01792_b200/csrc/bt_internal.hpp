@@ -339,8 +339,10 @@ void launch_xchg_combine_plan(const XPlan& p, int64_t shift, IfaceMode mode, dou
                               const double* buf, cudaStream_t s);
 // every signed edge-interface group of an edge-space vector (collective when partitioned)
 void sync_edges(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s);
-// per-cell rows only (no replica sums): interior + row ends + general rows
-void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s);
+// per-cell rows (interior + row ends + general rows); xmode >= 0 also runs
+// the interface pass in that mode (IfaceMode, src = x) — with the rank
+// exchange on a partitioned grid — overlapped with the interior marches
+void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s, int xmode = -1);
 // the whole apply_stencil (replica sums and, bc != 0, Dirichlet identity rows
 // included): interior kernel and fused boundary kernel run concurrently.
 // Available when stencil_fused(st): symmetric tables on an unpartitioned grid.

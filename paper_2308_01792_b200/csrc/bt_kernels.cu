@@ -914,8 +914,7 @@ bt_status bt_apply_stencil(const bt_stencil* st, const double* x, double* y, int
     launch_stencil_fused(*st, x, y, bc, s);
     return BT_OK;
   }
-  launch_stencil(*st, x, y, s);
-  sync(*st->grid, st->level, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
+  launch_stencil(*st, x, y, s, bc ? IF_SYNC_DIR : IF_SYNC);  // interface pass overlapped with the interior
   BT_CATCH
 }
 

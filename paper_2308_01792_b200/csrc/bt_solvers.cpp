@@ -49,7 +49,8 @@ static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int b
       launch_stencil_fused(*L.stencil, x, y, bc, s);  // interior and boundary (incl. sync, Dirichlet rows)
       return;
     }
-    launch_stencil(*L.stencil, x, y, s);
+    launch_stencil(*L.stencil, x, y, s, bc ? IF_SYNC_DIR : IF_SYNC);
+    return;
   } else {
     const int ck = h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.coeff_kind : 0;
     static const double one[4] = {1.0, 0.0, 0.0, 0.0};

@@ -781,30 +781,35 @@ static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double*
   }
 }
 
-void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s) {
+void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream_t s, int xmode) {
   const int w = (1 << st.level) + 1;
   const int64_t cs = n_tet(w);
   if (st.part_begin != st.grid->part_begin || st.part_end != st.grid->part_end)
     raise(BT_LOGIC_ERROR, "apply_stencil: the grid was repartitioned after compute_stencil");
   const int c0 = st.part_begin, nc = st.part_end - st.part_begin;  // this handle's cells
-  if (!nc) return;
+  const double* xl = x;  // local pointers (for the interface pass)
+  double* yl = y;
   x = shifted(x, *st.grid, BT_SPACE_P1, st.level);  // local -> global-cell indexing
   y = shifted(y, *st.grid, BT_SPACE_P1, st.level);
-  if (!st.symmetric) {
-    k_stencil_general<<<dim3((st.natasks + kGW - 1) / kGW, nc), kGT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
-                                                                            st.natasks, w, cs, c0);
-    count_launch();
-    check_launch("k_stencil_general");
+  if (!st.symmetric || !nc) {
+    if (nc) {
+      k_stencil_general<<<dim3((st.natasks + kGW - 1) / kGW, nc), kGT, 0, s>>>(x, y, st.d_cells.p, st.d_atasks.p,
+                                                                              st.natasks, w, cs, c0);
+      count_launch();
+      check_launch("k_stencil_general");
+    }
+    if (xmode >= 0) sync(*st.grid, st.level, (IfaceMode)xmode, yl, xl, s);
     return;
   }
-  // fast rows on s; row ends and general rows on the side stream, overlapping
-  // the (latency-bound, persistent) fast kernel on the SMs' spare slots
+  // The rows that hold the lattice-boundary (interface) points — row ends and
+  // general rows — go first, on the side stream, followed there by the
+  // interface pass (xmode >= 0: including the rank exchange), so the
+  // exchange overlaps the interior marches on s. The two sets of points are
+  // disjoint: the interior kernels write interior points only.
   const int parts = stencil_parts();
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
-  if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);
   BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-  if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s);  // the 2-layer group
   if ((parts & 2) && w - 1 >= 4) {
     const int n = w - 1;
     k_stencil_ends<<<dim3((n - 3 + 127) / 128, n - 3, nc), 128, 0, ss.s>>>(x, y, st.d_ends.p, w, cs, c0);
@@ -815,6 +820,9 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
                                                                                st.ngtasks, w, cs, c0);
     count_launch();
   }
+  if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);
+  if (parts & 1) launch_fast<2>(st, st.fast2, x, y, s);  // the 2-layer group
+  if (xmode >= 0) sync(*st.grid, st.level, (IfaceMode)xmode, yl, xl, ss.s);
   BT_CUDA(cudaEventRecord(ss.join, ss.s));
   BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
   check_launch("k_stencil");
