@@ -54,18 +54,30 @@ def _run(cmd, log):
 def build(force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     deps = _deps()
-    objs = []
+    objs, jobs = [], []
+    for src in CU_SOURCES:
+        o = os.path.join(OBJ, src + ".o")
+        if force or _stale(o, deps):
+            jobs.append([NVCC, *ARCH, *CU_FLAGS, "-c", os.path.join(CSRC, src), "-o", o])
+        objs.append(o)
+    for src in CXX_SOURCES:
+        o = os.path.join(OBJ, src + ".o")
+        if force or _stale(o, deps):
+            jobs.append([CXX, *CXX_FLAGS, "-c", os.path.join(CSRC, src), "-o", o])
+        objs.append(o)
     with open(os.path.join(OBJ, "build.log"), "w") as log:
-        for src in CU_SOURCES:
-            o = os.path.join(OBJ, src + ".o")
-            if force or _stale(o, deps):
-                _run([NVCC, *ARCH, *CU_FLAGS, "-c", os.path.join(CSRC, src), "-o", o], log)
-            objs.append(o)
-        for src in CXX_SOURCES:
-            o = os.path.join(OBJ, src + ".o")
-            if force or _stale(o, deps):
-                _run([CXX, *CXX_FLAGS, "-c", os.path.join(CSRC, src), "-o", o], log)
-            objs.append(o)
+        # translation units compile in parallel (the logs are written in order)
+        import concurrent.futures as cf
+        import io
+        logs = [io.StringIO() for _ in jobs]
+        with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+            futs = [ex.submit(_run, cmd, lg) for cmd, lg in zip(jobs, logs)]
+            errors = [f.exception() for f in futs]
+        for lg in logs:
+            log.write(lg.getvalue())
+        for e in errors:
+            if e is not None:
+                raise e
         if force or _stale(OUT, objs):
             _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart_static", "-lrt", "-lpthread", "-ldl"], log)
     return OUT
