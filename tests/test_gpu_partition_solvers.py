@@ -288,3 +288,34 @@ def test_more_ranks_than_cells_n1e1_and_fmg():
         _, _, b, e = out["part"]
         assert torch.equal(out["x"], ffull["x"][b * cs:e * cs])
         assert out["rows"] == ffull["rows"]
+
+
+def gs_body(text, lo, hi):
+    def body(setup):
+        g = bt.Grid(text, lo, hi)
+        setup(g)
+        h = bt.make_hierarchy(g, bt.FormId.diffusion(), bt.KernelKind.Stencil)
+        rhs = bt.allocate(bt.p1_space(), g)
+        x = bt.allocate(bt.p1_space(), g)
+        bt.random_fill(rhs, hi, 0)
+        bt.zero_dirichlet(rhs, hi)
+        gs = bt.SmootherConfig.gauss_seidel()
+        bt.smooth(h, gs, rhs, x, hi, 2)
+        bt.smooth(h, gs, rhs, x, hi, 1, bt.SweepDirection.Backward)
+        mg = bt.MultigridConfig(coarse_level=lo, coarse_tol=0.0, coarse_maxit=20)
+        for _ in range(2):
+            bt.v_cycle(h, hi, rhs, x, gs, mg)  # the reference's default smoother
+        torch.cuda.synchronize()
+        return {"part": g.partition(), "x": x.values[hi].clone()}
+    return body
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_partitioned_gauss_seidel(nranks):
+    text, lo, hi = bt.cubes_mesh_text(2, 0.1, 0), 2, 4
+    body = gs_body(text, lo, hi)
+    full = body(lambda g: None)
+    cs = bt.n_tet((1 << hi) + 1)
+    for out in run_ranks(nranks, body):
+        _, _, b, e = out["part"]
+        assert torch.equal(out["x"], full["x"][b * cs:e * cs])
