@@ -798,6 +798,7 @@ def make_hierarchy(grid: Grid, form: FormId, kernel=KernelKind.Stencil, threads=
 
 
 def hierarchy_apply(h: GridHierarchy, x: FEFunction, y: FEFunction, l, bc=BC.DirichletIdentity):
+    _require_pair(x, y, l)
     _check(_L.bt_hierarchy_apply(h.handle, l, _ptr(x.values[l]), _ptr(y.values[l]), int(bc), _stream()))
 
 
@@ -809,6 +810,7 @@ def spectral_estimate(h: GridHierarchy, l) -> float:
 
 def smooth(h: GridHierarchy, cfg: SmootherConfig, rhs: FEFunction, x: FEFunction, l, sweeps,
            direction=SweepDirection.Forward):
+    _require_pair(rhs, x, l)
     c = cfg.c_struct()
     _check(_L.bt_smooth(h.handle, C.byref(c), _ptr(rhs.values[l]), _ptr(x.values[l]), l, sweeps, int(direction),
                         _stream()))
@@ -836,6 +838,7 @@ def cg(h: GridHierarchy, rhs: FEFunction, x: FEFunction, l, tol, maxit) -> Itera
     """cg (solvers.hpp:84) with hierarchy_apply(.., DirichletIdentity) as the
     operator (the reference's std::function operator argument cannot cross
     the C ABI; every reference caller passes this operator)."""
+    _require_pair(rhs, x, l)
     hist = np.zeros(max(maxit, 1))
     it = C.c_int()
     _check(_L.bt_cg(h.handle, l, tol, maxit, _ptr(rhs.values[l]), _ptr(x.values[l]),
@@ -913,6 +916,9 @@ def fmg(h: GridHierarchy, finest, rhs_levels: List[FEFunction], x: FEFunction, s
 
 
 def v_cycle(h: GridHierarchy, l, rhs: FEFunction, x: FEFunction, sm: SmootherConfig, mg: MultigridConfig):
+    if mg.coarse_level < h.grid.min_level() or l < mg.coarse_level:  # solvers.hpp:512-513
+        raise InvalidArgument("v_cycle: level range invalid")
+    _require_pair(rhs, x, l)
     s = sm.c_struct()
     m = mg.c_struct()
     _check(_L.bt_v_cycle(h.handle, l, _ptr(rhs.values[l]), _ptr(x.values[l]), C.byref(s), C.byref(m), _stream()))

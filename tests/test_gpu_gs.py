@@ -138,3 +138,18 @@ def test_gauss_seidel_needs_a_stencil_table():
     x, rhs = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
     with pytest.raises(bt.InvalidArgument):
         bt.smooth(h, GS, rhs, x, 3, 1)
+
+
+def test_vcycle_level_guards():
+    """test_solvers.cpp 'level guards': a coarse level below the grid's, or a V-cycle below the coarse level."""
+    g = bt.Grid(bt.cube_kuhn_text(), 2, 4)
+    h = bt.make_hierarchy(g, bt.FormId.diffusion())
+    x, rhs = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
+    low = bt.MultigridConfig(coarse_level=1)
+    with pytest.raises(bt.InvalidArgument):
+        bt.v_cycle(h, 3, rhs, x, GS, low)
+    with pytest.raises((bt.InvalidArgument, bt.OutOfRange)):
+        bt.v_cycle(h, 1, rhs, x, GS, bt.MultigridConfig())
+    bad = bt.SmootherConfig.jacobi(1.5)  # omega outside (0, 1]
+    with pytest.raises(bt.InvalidArgument):
+        bt.smooth(h, bad, rhs, x, 4, 1)
