@@ -515,15 +515,19 @@ def random_fill(fn: FEFunction, l, seed):
 
 def zero_dirichlet(fn: FEFunction, l):
     """detail::zero_dirichlet (solvers.hpp:66)."""
+    fn.check_level(l)
     _check(_L.bt_zero_dirichlet(fn.grid.handle, l, _ptr(fn.values[l]), _stream()))
 
 
 def impose_dirichlet(src: FEFunction, dst: FEFunction, l):
     """detail::impose_dirichlet (operators.hpp:98)."""
+    _compatible(src, dst, l)
     _check(_L.bt_impose_dirichlet(dst.grid.handle, l, _ptr(src.values[l]), _ptr(dst.values[l]), _stream()))
 
 
 def hadamard(fn: FEFunction, diag: FEFunction, l, divide: bool):
+    """detail::hadamard (solvers.hpp:53-64)."""
+    _compatible(fn, diag, l)
     _check(_L.bt_hadamard(fn.grid.handle, l, _ptr(fn.values[l]), _ptr(diag.values[l]), int(divide), _stream()))
 
 
