@@ -290,3 +290,27 @@ def test_config3_small_and_properties():
     bt.apply_elementwise(bt.FormId.div_k_grad(bt.Coefficient.constant(2.0)), u, au, 6)
     bt.apply_elementwise(bt.FormId.diffusion(), u, av, 6)
     assert rel(host(au, 6), 2.0 * host(av, 6)) <= REL
+
+
+def test_config3_full_size_against_reference():
+    """Config 3 at full size (384 perturbed tets, L6, div(k grad) with the sin
+    product coefficient; 18.4 M slots): the cached-kbar elementwise apply against
+    the compiled reference, plus symmetry in the owned inner product."""
+    from pyoracle import Reference
+    text, l = cubes_mesh_text(4, 0.1, 0), 6
+    g = bt.Grid(text, l, l)
+    form = bt.FormId.div_k_grad(SIN)
+    x = bt.allocate(bt.p1_space(), g)
+    y = bt.allocate(bt.p1_space(), g)
+    bt.random_fill(x, l, 0)
+    bt.apply_elementwise(form, x, y, l)
+    r = Reference(text, l, l)
+    ref = r.apply_elementwise(l, host(x, l), form=2, kp=kparams(), threads=os.cpu_count() or 1)
+    assert rel(host(y, l), ref) <= REL
+    u, v, au, av = (bt.allocate(bt.p1_space(), g) for _ in range(4))
+    bt.random_fill(u, l, 1)
+    bt.random_fill(v, l, 2)
+    bt.apply_elementwise(form, u, au, l)
+    bt.apply_elementwise(form, v, av, l)
+    a, b = bt.dot(u, av, l), bt.dot(v, au, l)
+    assert abs(a - b) <= 1e-12 * max(abs(a), 1.0)
