@@ -84,3 +84,23 @@ def test_n1e1_config4_family_properties():
     s1, s2 = bt.dot(a, ab, l), bt.dot(b, aa, l)
     assert abs(s1 - s2) <= 1e-12 * abs(s1)
     assert rel(host(aa, l), o.n1e1_apply(l, host(a, l), 1.0, 1.0, 0)) <= REL
+
+
+def test_n1e1_config4_full_size_properties():
+    """Config 4 at full size (384 perturbed tets, L7, 958 M edge slots; no
+    reference N1E1 exists and the CPU oracle is too slow at this size):
+    symmetry of alpha K + beta M in the owned inner product, and bitwise
+    repeatability of the apply."""
+    text, l = cubes_mesh_text(4, 0.1, 0), 7
+    g = bt.Grid(text, l, l)
+    op = bt.N1E1Operator(g, l)
+    u, v, au, av = (bt.allocate(bt.edge_space(), g, l, l) for _ in range(4))
+    bt.random_fill(u, l, 1)
+    bt.random_fill(v, l, 2)
+    bt.apply_n1e1(op, u, au, l, bt.BC.None_)
+    bt.apply_n1e1(op, v, av, l, bt.BC.None_)
+    a, b = bt.dot(u, av, l), bt.dot(v, au, l)
+    assert abs(a - b) <= 1e-11 * max(abs(a), 1.0)
+    first = au.values[l].clone()
+    bt.apply_n1e1(op, u, au, l, bt.BC.None_)
+    assert torch.equal(au.values[l], first)
