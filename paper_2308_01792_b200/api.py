@@ -359,18 +359,51 @@ class FEFunction:
         self.check_level(l)
         return self.values[l]
 
-    def slots_of(self, l):
-        return self.grid.space_size(self.descriptor.space, l) // self.grid.n_cells()
+    def entries(self):
+        """Subgroups of the space's entries, in storage order (SpaceDescriptor::entries)."""
+        return [0] if self.descriptor.space == 0 else ([0] if self.descriptor.space == 1 else []) + list(range(1, 8))
 
-    def array(self, l, cell):
+    def slots_of(self, l, entry=None):
+        """Slots of one entry (FEFunction::slots_of, fe_function.hpp:245-248),
+        or of a whole cell when entry is None."""
+        ents = self.entries()
+        if entry is None:
+            return sum(n_tet(width_formula(g, l)) for g in ents)
+        if not 0 <= entry < len(ents):
+            raise OutOfRange("entry out of range")
+        return n_tet(width_formula(ents[entry], l))
+
+    def offset(self, l, entry, t, d=0):
+        """Layout-aware slot offset of (t, d) (FEFunction::offset,
+        fe_function.hpp:257-261); every space here has m = 1."""
+        if d != 0:
+            raise OutOfRange("linearize: bad DoF index")
+        return int(t)
+
+    def array(self, l, cell, entry=None):
+        """This rank's values of `cell` (and one entry of it): a view into
+        values[l]. Cells outside the rank's block raise OutOfRange."""
+        self.check_level(l)
+        _, _, b, e = self.grid.partition()
+        if not b <= cell < e:
+            raise OutOfRange("cell not held by this rank")
         n = self.slots_of(l)
-        return self.values[l][cell * n:(cell + 1) * n]
+        base = (cell - b) * n
+        if entry is None:
+            return self.values[l][base:base + n]
+        ents = self.entries()
+        first = sum(n_tet(width_formula(g, l)) for g in ents[:entry]) if 0 <= entry < len(ents) else 0
+        return self.values[l][base + first:base + first + self.slots_of(l, entry)]
 
     def host(self, l) -> np.ndarray:
         return self.values[l].cpu().numpy()
 
     def at(self, l, cell, entry, t, d=0):
-        return float(self.array(l, cell)[t].item())
+        a = self.array(l, cell, entry)
+        o = self.offset(l, entry, t, d)
+        if not 0 <= o < a.numel():
+            raise OutOfRange("slot out of range")
+        return float(a[o].item())
 
 
 def allocate(descriptor: SpaceDescriptor, grid: Grid, min_level: int = -1, max_level: int = -1) -> FEFunction:

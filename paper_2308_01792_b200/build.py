@@ -27,13 +27,15 @@ CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-fno-fast-math", "-ffp-contract=off",
              f"-I{CUDA_HOME}/include"]
 
-CU_SOURCES = ["bt_kernels.cu", "bt_stencil.cu", "bt_interface.cu", "bt_n1e1.cu", "bt_xchg.cu"]
+CU_SOURCES = ["bt_kernels.cu", "bt_stencil.cu", "bt_prism.cu", "bt_interface.cu", "bt_n1e1.cu", "bt_xchg.cu"]
 CXX_SOURCES = ["bt_host.cpp", "bt_solvers.cpp"]
 
 
-def _deps():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
-        os.path.join(ROOT, "include", "blocktet_b200.h")]
+def _deps(src=None):
+    """A translation unit depends on itself and on every header."""
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
+    return hdrs + [os.path.join(ROOT, "include", "blocktet_b200.h")] + (
+        [os.path.join(CSRC, src)] if src else [])
 
 
 def _stale(target, sources):
@@ -53,16 +55,15 @@ def _run(cmd, log):
 
 def build(force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    deps = _deps()
     objs, jobs = [], []
     for src in CU_SOURCES:
         o = os.path.join(OBJ, src + ".o")
-        if force or _stale(o, deps):
+        if force or _stale(o, _deps(src)):
             jobs.append([NVCC, *ARCH, *CU_FLAGS, "-c", os.path.join(CSRC, src), "-o", o])
         objs.append(o)
     for src in CXX_SOURCES:
         o = os.path.join(OBJ, src + ".o")
-        if force or _stale(o, deps):
+        if force or _stale(o, _deps(src)):
             jobs.append([CXX, *CXX_FLAGS, "-c", os.path.join(CSRC, src), "-o", o])
         objs.append(o)
     with open(os.path.join(OBJ, "build.log"), "w") as log:

@@ -741,7 +741,18 @@ bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks) {
   g->part_nranks = nranks;
   partition_range(g->mesh.n_cells(), rank, nranks, g->part_begin, g->part_end);
   interface_lists(*g, g->part_begin, g->part_end, g->loc);
+  // everything derived from the previous partition: exchange plans (P1 and
+  // N1E1 edges), elementwise tables (their kbar blocks are indexed relative to
+  // part_begin), reduction and exchange scratch
+  BT_CUDA(cudaDeviceSynchronize());
   for (auto& p : g->xplan) p.reset();
+  for (auto& p : g->xplan_edges) p.reset();
+  g->ew_cache.clear();
+  g->ew_scratch.release();
+  g->d_partials.release();
+  g->dot_cells.release();
+  g->xbuf.release();
+  ++g->part_epoch;
   BT_CATCH
 }
 int bt_num_cells(const bt_grid* g) { return g ? g->mesh.n_cells() : 0; }

@@ -218,6 +218,9 @@ struct bt_grid {
   // cell partition (bt_grid_set_partition): this handle computes cells
   // [part_begin, part_end) of rank part_rank out of part_nranks
   int part_rank = 0, part_nranks = 1, part_begin = 0, part_end = 0;
+  // bumped by every bt_grid_set_partition: objects built for one partition
+  // (stencil tables, hierarchies, N1E1 operators) refuse to run on another
+  int part_epoch = 0;
   mutable std::array<bt::XPlan, 11> xplan;  // per level, built on first use
   mutable std::array<bt::XPlan, 11> xplan_edges;  // the same for N1E1 edge replicas
   // the ranks' sum-allreduce (bt_grid_set_allreduce): lets the library run
@@ -286,6 +289,10 @@ struct bt_stencil {
   bool symmetric = false;                    // fast-path preconditions hold (see bt_stencil.cu)
   std::vector<double> fast;                  // per cell: the 8 symmetric interior weights
   bt::DevBuf<double> d_ends;                 // per cell: typed rows of the two row ends (11 + 11)
+  bt::DevBuf<int4> d_prism;                  // k_stencil_prism units (bt_prism.cu), longest first
+  int nprism = 0;
+  bt::DevBuf<double> d_w8;                   // per cell (global index): the 8 symmetric weights
+  bt::DevBuf<int> d_prism_ctr;               // unit queue + finished-CTA counter (self-resetting)
 };
 
 namespace bt {
@@ -349,6 +356,10 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
 bool stencil_fused(const bt_stencil& st);
 void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s);
 void init_stencil_tasks(bt_stencil& st);
+// interior points of a symmetric table as prism k-marches (bt_prism.cu)
+void init_prism_tasks(bt_stencil& st);
+bool prism_ok(const bt_stencil& st, const double* x);
+void launch_prism(const bt_stencil& st, const double* x, double* y, cudaStream_t s);
 // one hybrid Gauss-Seidel sweep (operators.hpp:327-387); scratch: a P1 vector
 void launch_gs_sweep(const bt_stencil& st, const double* rhs, double* x, double* scratch, bool backward,
                      cudaStream_t s);

@@ -246,6 +246,7 @@ struct bt_n1e1 {
   bt::DevBuf<int4> d_marches;  // one cell's marches {k | block << 16, j0, j1}, spatial order
   int nmarch = 0;
   bt::DevBuf<int> d_next;      // per cell: march queue counter
+  int part_epoch = 0;          // the grid's partition at creation
 };
 
 namespace bt {
@@ -1072,6 +1073,7 @@ bt_status bt_n1e1_create(const bt_grid* g, int level, double alpha, double beta,
   build_static();
   auto op = std::make_unique<bt_n1e1>();
   op->grid = g;
+  op->part_epoch = g->part_epoch;
   op->level = level;
   op->alpha = alpha;
   op->beta = beta;
@@ -1166,6 +1168,8 @@ void bt_n1e1_destroy(bt_n1e1* op) { delete op; }
 bt_status bt_apply_n1e1(const bt_n1e1* op, const double* x, double* y, int bc, void* stream) {
   BT_TRY
   if (!op) raise(BT_INVALID_ARGUMENT, "apply_n1e1: operator required");
+  if (op->part_epoch != op->grid->part_epoch)
+    raise(BT_LOGIC_ERROR, "apply_n1e1: the grid was repartitioned after the operator was built");
   if (x == y && bt_space_size(op->grid, BT_SPACE_EDGES, op->level) > 0)
     raise(BT_INVALID_ARGUMENT, "source and destination must be distinct");
   const bt_grid& g = *op->grid;

@@ -34,7 +34,10 @@ struct bt_hierarchy {
   bt_form form{};
   int kernel = 1;
   std::vector<std::unique_ptr<bt::LevelData>> levels;
+  int part_epoch = 0;  // the grid's partition when the levels were built
   bt::LevelData& at(int l) {
+    if (part_epoch != grid->part_epoch)
+      bt::raise(BT_LOGIC_ERROR, "hierarchy: the grid was repartitioned after the hierarchy was built");
     if (l < grid->lo || l > grid->hi) bt::raise(BT_OUT_OF_RANGE, "level not in hierarchy");
     return *levels[l - grid->lo];
   }
@@ -312,6 +315,7 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
   BT_CUDA(cudaSetDevice(g->device));
   auto h = std::make_unique<bt_hierarchy>();
   h->grid = g;
+  h->part_epoch = g->part_epoch;
   h->form = *form;
   h->kernel = kernel;
   for (int l = g->lo; l <= g->hi; ++l) {

@@ -237,15 +237,18 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     // cross lanes. Within the 1e-12 parity tolerance of the reference order.
     auto layer = [&](const Row2& a, const Row2& b, const Row2& c, const Row2& am1, const Row2& A1, const Row2& B0,
                      const Row2& C1, int LY, double* py_, bool ok) {
-      const double upv = W[1] * a.v1 + W[4] * A1.v1 + W[5] * B0.v1 + W[7] * C1.v1;  // to column c1 + 1
-      const double dnv = W[1] * a.v0 + W[4] * am1.v0 + W[5] * c.v0 + W[7] * b.v0;   // to column c0 - 1
+      // explicit fma chains: k_stencil_prism (bt_prism.cu) evaluates the same
+      // expressions per column, so the two kernels agree bit for bit
+      const double upv = fma(W[7], C1.v1, fma(W[5], B0.v1, fma(W[4], A1.v1, W[1] * a.v1)));  // to column c1 + 1
+      const double dnv = fma(W[7], b.v0, fma(W[5], c.v0, fma(W[4], am1.v0, W[1] * a.v0)));   // to column c0 - 1
       const double lft = __shfl_up_sync(0xffffffffu, upv, 1);    // column c0 - 1's, for c0
       const double rgt = __shfl_down_sync(0xffffffffu, dnv, 1);  // column c1 + 1's, for c1
-      double s0 = W[0] * a.v0 + W[2] * (A1.v0 + am1.v0) + W[3] * (B0.v0 + c.v0) + W[6] * (C1.v0 + b.v0);
-      double s1 = W[0] * a.v1 + W[2] * (A1.v1 + am1.v1) + W[3] * (B0.v1 + c.v1) + W[6] * (C1.v1 + b.v1);
-      s0 += W[1] * a.v1 + W[4] * am1.v1 + W[5] * c.v1 + W[7] * b.v1;  // i+1 of c0 = own c1
-      s1 += W[1] * a.v0 + W[4] * A1.v0 + W[5] * B0.v0 + W[7] * C1.v0;  // i-1 of c1 = own c0
+      double s0 = fma(W[6], C1.v0 + b.v0, fma(W[3], B0.v0 + c.v0, fma(W[2], A1.v0 + am1.v0, W[0] * a.v0)));
+      double s1 = fma(W[6], C1.v1 + b.v1, fma(W[3], B0.v1 + c.v1, fma(W[2], A1.v1 + am1.v1, W[0] * a.v1)));
+      // every column: (centre + its i-1 partial) + its i+1 partial
       s0 += lft;
+      s0 += fma(W[7], b.v1, fma(W[5], c.v1, fma(W[4], am1.v1, W[1] * a.v1)));  // i+1 of c0 = own c1
+      s1 += fma(W[7], C1.v0, fma(W[5], B0.v0, fma(W[4], A1.v0, W[1] * a.v0)));  // i-1 of c1 = own c0
       s1 += rgt;
       // row ends (i = 0, i = LY - 1) are the boundary kernel's
       if (ok && out && c0 < LY - 1 && c0 > 0) py_[c0] = s0;
@@ -707,6 +710,7 @@ void init_stencil_tasks(bt_stencil& st) {
     }
   }
   st.d_ends.upload(ends);
+  init_prism_tasks(st);
 }
 
 namespace {
@@ -729,7 +733,9 @@ SideStream& side_stream() {
 }
 
 // BT_STENCIL_PARTS (profiling only) drops parts of an apply: bit 0 interior
-// kernel, 1 row ends, 2 general rows, 3 fused boundary kernel.
+// kernel, 1 row ends, 2 general rows, 3 fused boundary kernel; bit 4 set
+// selects k_stencil_prism (bt_prism.cu) for the interior instead of the
+// k_stencil_fast marches.
 static int stencil_parts() {
   static const int parts = [] {
     const char* e = std::getenv("BT_STENCIL_PARTS");
@@ -866,9 +872,15 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
   }
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
-  if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);  // first, so its persistent blocks are resident first
-  BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-  if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s);  // the 2-layer group, beside the main launch
+  const bool prism = prism_ok(st, x) && (parts & 16);
+  if (prism) {
+    if (parts & 1) launch_prism(st, x, y, s);  // every interior point (bt_prism.cu)
+    BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  } else {
+    if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);  // first, so its persistent blocks are resident first
+    BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+    if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s);  // the 2-layer group, beside the main launch
+  }
   if (!(parts & 8)) {
     BT_CUDA(cudaEventRecord(ss.join, ss.s));
     BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
