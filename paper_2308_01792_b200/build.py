@@ -23,6 +23,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
             "-Xptxas", "-v"]
+PER_FILE = {}  # per translation unit extra flags
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-fno-fast-math", "-ffp-contract=off",
              f"-I{CUDA_HOME}/include"]
@@ -59,7 +60,7 @@ def build(force: bool = False) -> str:
     for src in CU_SOURCES:
         o = os.path.join(OBJ, src + ".o")
         if force or _stale(o, _deps(src)):
-            jobs.append([NVCC, *ARCH, *CU_FLAGS, "-c", os.path.join(CSRC, src), "-o", o])
+            jobs.append([NVCC, *ARCH, *CU_FLAGS, *PER_FILE.get(src, []), "-c", os.path.join(CSRC, src), "-o", o])
         objs.append(o)
     for src in CXX_SOURCES:
         o = os.path.join(OBJ, src + ".o")

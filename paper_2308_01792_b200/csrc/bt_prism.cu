@@ -46,6 +46,7 @@ constexpr int kPCols = 62;               // output columns per item (lanes hold 
 constexpr int kPNR = 4;                  // output rows per item
 constexpr int kPCons = 15;               // consumer warps (+ the producer: 4 warps per SM sub-partition)
 constexpr int kPThreads = (kPCons + 1) * 32;
+constexpr int kPMaxReg = 96;             // leaves registers for a k_boundary block beside each CTA
 constexpr int kPK = 12;                  // output layers per unit (k-chunk)
 
 struct StageMeta {
@@ -101,7 +102,7 @@ struct Rows6 {
   double A[6], B[6];
 };
 
-__global__ void __launch_bounds__(kPThreads, 1)
+__global__ void __maxnreg__(kPMaxReg)
     k_stencil_prism(const double* __restrict__ x, double* __restrict__ y, const int4* __restrict__ units, int nunits,
                     const double* __restrict__ wts, int w, int64_t cs, int* __restrict__ ctr, int mode) {
   extern __shared__ __align__(128) double psm[];
