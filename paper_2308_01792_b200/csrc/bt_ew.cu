@@ -1,0 +1,383 @@
+// Elementwise P1 apply with an on-the-fly coefficient (apply_elementwise
+// operators.hpp:115-164, local_matrix forms.hpp:75-120), and the assembled
+// diagonal (extract_diagonal operators.hpp:277-316).
+//
+// y_v = sum over the micro-cells T of v (class s, v = vertex `slot` of T):
+// kbar_T * (G_s row slot) . x_T, with G_s the cell's class matrix
+// (class_matrices operators.hpp:54-69; diffusion for div_k_grad, since the
+// affine map makes grad phi constant per class) and kbar_T = 1/4 sum_q k(x_q)
+// the reference's 4-point rule (forms.hpp:107-116). kbar depends on the
+// micro-cell only, so each one is evaluated ONCE, into shared memory, and the
+// vertices then pull it (the sum over (s, slot) in the fixed order of the
+// reference's per-vertex contributions; no atomics, no cache in HBM).
+//
+// Work unit: a tile of one macro-cell — rows j0 .. j0+7, columns i0 .. i0+63
+// — marched bottom-up over the layers k. Step k first evaluates kbar for every
+// micro-cell anchored in layer k at rows j0-1 .. j0+7 and columns i0-1 ..
+// i0+63 (all 6 classes; a vertex's micro-cells are anchored at v - o with o
+// in {0,1}^3) into a two-layer ring, then computes the tile's vertices of
+// layer k (warp = row, lanes = columns i0 + lane and i0 + lane + 32).
+//
+// kbar of the sin-product coefficient k = c0 + c1 sin(f x) sin(f y) sin(f z):
+// the phase of quadrature point q of class s at anchor p is beta_d . p +
+// gamma_{s,q,d} (affine map), so with S_d, C_d = sin, cos(beta_d . p) and the
+// 8 monomials M_m = prod_d (bit d of m ? C_d : S_d),
+//   kbar = c0 + sum_m coefh[s][m] M_m,
+//   coefh[s][m] = c1/4 sum_q prod_d (bit d ? sin gamma_{s,q,d} : cos gamma_{s,q,d})
+// (host tables): 3 sincos per anchor (by angle addition of a column table and
+// a row table), 12 products and 8 FMAs per micro-cell instead of 12 sin.
+// Affine k: kbar = k(centroid) = lin0[s] + lin . p exactly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "bt_internal.hpp"
+
+namespace bt {
+
+namespace {
+constexpr int kER = 8;          // rows per tile
+constexpr int kEC = 64;         // columns per tile (two per lane)
+constexpr int kEA = kEC + 1;    // anchor columns i0-1 .. i0+63
+constexpr int kERA = kER + 1;   // anchor rows j0-1 .. j0+kER-1
+constexpr int kET = 256;        // threads
+
+// present micro-cells (bit 4 s + slot) and needed stencil directions per zero
+// set (as bt_kernels.cu); stencil direction of (o_j - o_slot) for class s
+__constant__ uint32_t kEwPresent[16] = {0xffffff, 0xe8cc8e, 0x962b4d, 0x80080c, 0x4d962b, 0x48840a,
+                                        0x40209,  0x8,      0x337117, 0x204006, 0x122105, 0x4,
+                                        0x11003,  0x2,      0x1,      0x0};
+__constant__ uint32_t kEwDirMask[16] = {0x7fff, 0x7f71, 0x26ff, 0x2671, 0x5d6f, 0x5d61, 0x46f, 0x461,
+                                        0x3b9f, 0x3b11, 0x229f, 0x2211, 0x190f, 0x1901, 0xf,   0x0};
+
+__host__ __device__ inline int ew_class_width(int s, int n) { return s == 0 ? n : (s == 1 ? n - 2 : n - 1); }
+
+struct EwShared {
+  double kb[2][6][kERA][kEA];  // kbar ring: [layer & 1][class][anchor row][anchor column]
+  double colT[3][2][kEA];      // sin, cos of beta_d[0] * p_i
+  double rowT[2][3][2][kERA];  // [layer & 1]: sin, cos of beta_d[1] * p_j + beta_d[2] * p_k
+  EwCell cell;
+};
+
+template <int CK, bool DIAG>
+__global__ void __launch_bounds__(kET) k_ew(const double* __restrict__ x, double* __restrict__ y,
+                                            const EwCell* __restrict__ cells, const int4* __restrict__ units, double c0,
+                                            int n, int64_t cs) {
+  extern __shared__ __align__(16) double ew_smem[];
+  EwShared& S = *reinterpret_cast<EwShared*>(ew_smem);
+  const int4 U = units[blockIdx.x];
+  const int cell = U.x, j0 = U.y, i0 = U.z, kmax = U.w;
+  const int w = n + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const double* src = reinterpret_cast<const double*>(cells + cell);
+    double* dst = reinterpret_cast<double*>(&S.cell);
+    for (int q = tid; q < (int)(sizeof(EwCell) / 8); q += kET) dst[q] = src[q];
+  }
+  __syncthreads();
+  const EwCell& E = S.cell;
+  // row table of layer k (sincos of the row phase per anchor row), into buffer b
+  auto row_table = [&](int k, int b) {
+    if (CK == 1 && tid < 3 * kERA) {
+      const int d = tid / kERA, r = tid % kERA;
+      double sv, cv;
+      sincos(E.beta[d][1] * (j0 - 1 + r) + E.beta[d][2] * k, &sv, &cv);
+      S.rowT[b][d][0][r] = sv;
+      S.rowT[b][d][1][r] = cv;
+    }
+  };
+  if (CK == 1) {
+    for (int q = tid; q < 3 * kEA; q += kET) {
+      const int d = q / kEA, c = q % kEA;
+      double sv, cv;
+      sincos(E.beta[d][0] * (i0 - 1 + c), &sv, &cv);
+      S.colT[d][0][c] = sv;
+      S.colT[d][1][c] = cv;
+    }
+    row_table(0, 0);
+  }
+  __syncthreads();
+  constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
+  constexpr int kTetDir[6][4][4] = {{{0, 1, 2, 3}, {8, 0, 11, 12}, {9, 4, 0, 13}, {10, 5, 6, 0}},
+                                    {{0, 13, 12, 3}, {6, 0, 11, 2}, {5, 4, 0, 1}, {10, 9, 8, 0}},
+                                    {{0, 13, 7, 3}, {6, 0, 1, 2}, {14, 8, 0, 11}, {10, 9, 4, 0}},
+                                    {{0, 11, 2, 3}, {4, 0, 1, 7}, {9, 8, 0, 13}, {10, 14, 6, 0}},
+                                    {{0, 11, 12, 3}, {4, 0, 13, 7}, {5, 6, 0, 1}, {10, 14, 8, 0}},
+                                    {{0, 1, 7, 3}, {8, 0, 13, 12}, {14, 6, 0, 11}, {10, 5, 4, 0}}};
+  const double* __restrict__ xc = x + (int64_t)cell * cs;
+  double* __restrict__ yc = y + (int64_t)cell * cs;
+
+  for (int k = 0; k <= kmax; ++k) {
+    const int b = k & 1;
+    // ---- kbar of the micro-cells anchored in layer k (rows j0-1 .. j0+7,
+    // columns i0-1 .. i0+63 with pi + pj + k <= n - 1), enumerated densely ----
+    {
+      int acount[kERA + 1];
+      acount[0] = 0;
+      const int ca = max(i0 - 1, 0);
+#pragma unroll
+      for (int r = 0; r < kERA; ++r) {
+        const int pj = j0 - 1 + r;
+        const int hi = min(i0 + kEC, n - k - pj);  // exclusive column bound
+        acount[r + 1] = acount[r] + (pj >= 0 && hi > ca ? hi - ca : 0);
+      }
+      for (int q = tid; q < acount[kERA]; q += kET) {
+        int r = 0, base = 0;  // (no dynamic indexing: acount stays in registers)
+#pragma unroll
+        for (int t = 1; t < kERA; ++t)
+          if (q >= acount[t]) {
+            r = t;
+            base = acount[t];
+          }
+        const int pi = ca + q - base, pj = j0 - 1 + r;
+        const int c = pi - (i0 - 1);
+        if (CK == 0) {
+#pragma unroll
+          for (int s = 0; s < 6; ++s) S.kb[b][s][r][c] = c0;
+        } else if (CK == 2) {
+          const double lp = E.lin[0] * pi + E.lin[1] * pj + E.lin[2] * k;
+#pragma unroll
+          for (int s = 0; s < 6; ++s) S.kb[b][s][r][c] = E.lin0[s] + lp;
+        } else {
+          double Sd[3], Cd[3];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {  // sin, cos of (column phase + row phase)
+            const double sa = S.colT[d][0][c], ca_ = S.colT[d][1][c];
+            const double sb = S.rowT[b][d][0][r], cb = S.rowT[b][d][1][r];
+            Sd[d] = fma(sa, cb, ca_ * sb);
+            Cd[d] = fma(ca_, cb, -(sa * sb));
+          }
+          const double m2[4] = {Sd[0] * Sd[1], Cd[0] * Sd[1], Sd[0] * Cd[1], Cd[0] * Cd[1]};
+          double M[8];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            M[m] = m2[m] * Sd[2];
+            M[m + 4] = m2[m] * Cd[2];
+          }
+#pragma unroll
+          for (int s = 0; s < 6; ++s) {
+            double kb = c0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) kb = fma(E.coefh[s][m], M[m], kb);
+            S.kb[b][s][r][c] = kb;
+          }
+        }
+      }
+    }
+    if (CK == 1 && k < kmax) row_table(k + 1, b ^ 1);
+    __syncthreads();
+    // ---- vertices of layer k (rows j0 .. j0+7, columns i0 .. i0+63 inside
+    // the layer), enumerated densely; a thread takes two at a time so each
+    // class row G_s[slot] is loaded once for both.
+    // Branch-free over the 24 (class, slot) pairs: an absent micro-cell gets
+    // kbar 0 (selected, so stale ring values never enter) and absent
+    // directions read 0, which adds +0.0 to the sum: the present terms are
+    // summed in the reference's order, bit for bit as a skip would.
+    int vcount[kER + 1];
+    vcount[0] = 0;
+#pragma unroll
+    for (int r = 0; r < kER; ++r) {
+      const int hi = min(i0 + kEC, w - k - (j0 + r));  // row length L = w - k - j
+      vcount[r + 1] = vcount[r] + (hi > i0 ? hi - i0 : 0);
+    }
+    for (int q0 = tid; q0 < vcount[kER]; q0 += 2 * kET) {
+      uint32_t present[2];
+      double xv[2][15];
+      int tt[2], rr[2], cc[2];
+      bool live[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = q0 + h * kET;
+        live[h] = q < vcount[kER];
+        int r = 0, base = 0;
+#pragma unroll
+        for (int t = 1; t < kER; ++t)
+          if (q >= vcount[t]) {
+            r = t;
+            base = vcount[t];
+          }
+        const int j = j0 + r, i = i0 + (live[h] ? q - base : 0);
+        rr[h] = r;
+        cc[h] = i - i0;
+        const int z = live[h] ? zero_set(n, i, j, k) : 15;
+        present[h] = kEwPresent[z];
+        tt[h] = row_start(w, j, k) + i;
+        if (!DIAG) {
+          int off[15];
+          row_offsets(w, j, k, off);
+          const uint32_t dm = kEwDirMask[z];
+#pragma unroll
+          for (int d = 0; d < 15; ++d) xv[h][d] = (dm >> d & 1) ? __ldg(xc + tt[h] + off[d]) : 0.0;
+        }
+      }
+      double acc[2] = {0.0, 0.0};
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+#pragma unroll
+        for (int slot = 0; slot < 4; ++slot) {
+          double g[4];
+          if (DIAG) {
+            g[0] = E.G[s][5 * slot];
+          } else {
+            const double2 g01 = *reinterpret_cast<const double2*>(&E.G[s][4 * slot]);
+            const double2 g23 = *reinterpret_cast<const double2*>(&E.G[s][4 * slot + 2]);
+            g[0] = g01.x;
+            g[1] = g01.y;
+            g[2] = g23.x;
+            g[3] = g23.y;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            // anchor v - o: ring layer k - o_k, row j - o_j, column i - o_i
+            const double kr = S.kb[(k - kOff[s][slot][2]) & 1][s][rr[h] + 1 - kOff[s][slot][1]]
+                                  [cc[h] + 1 - kOff[s][slot][0]];
+            const double kb = (present[h] >> (4 * s + slot) & 1) ? kr : 0.0;
+            if (DIAG) {
+              acc[h] = fma(kb, g[0], acc[h]);
+            } else {
+              double row = 0.0;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) row = fma(g[jj], xv[h][kTetDir[s][slot][jj]], row);
+              acc[h] = fma(kb, row, acc[h]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (live[h]) yc[tt[h]] = acc[h];
+    }
+    __syncthreads();  // the ring slot of layer k - 1 is rewritten next step
+  }
+}
+
+// Exact positivity check of k at every quadrature point of every micro-cell
+// (local_matrix's "div_k_grad coefficient must be positive", forms.hpp:114),
+// for coefficients whose sign is not settled on the host. Sets *bad.
+__global__ void __launch_bounds__(256) k_kpos(const double* __restrict__ maps, bt_form f, int n, int cell0,
+                                              int* __restrict__ bad) {
+  constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
+  const int cell = cell0 + blockIdx.y, s = blockIdx.z;
+  const int ws = ew_class_width(s, n);
+  const double* A = maps + 12 * cell;  // row-major 3x3, then b
+  const double h = 1.0 / n;
+  const double qa = (5.0 + 3.0 * sqrt(5.0)) / 20.0, qb = (5.0 - sqrt(5.0)) / 20.0;
+  const int64_t cnt = (int64_t)ws * (ws + 1) * (ws + 2) / 6;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cnt; p += (int64_t)gridDim.x * blockDim.x) {
+    // delinearize p in I_tet(ws)
+    int64_t t = p;
+    int kk = 0;
+    while (t >= (int64_t)(ws - kk) * (ws - kk + 1) / 2) t -= (int64_t)(ws - kk) * (ws - kk + 1) / 2, ++kk;
+    int jj = 0;
+    while (t >= ws - kk - jj) t -= ws - kk - jj, ++jj;
+    const int ii = (int)t;
+    for (int q = 0; q < 4; ++q) {
+      double r[3];
+      for (int a = 0; a < 3; ++a) {
+        double dl = 0;
+        for (int v = 0; v < 4; ++v) dl += (v == q ? qa : qb) * kOff[s][v][a];
+        r[a] = h * ((a == 0 ? ii : (a == 1 ? jj : kk)) + dl);
+      }
+      double xq[3];
+      for (int d = 0; d < 3; ++d) xq[d] = A[3 * d] * r[0] + A[3 * d + 1] * r[1] + A[3 * d + 2] * r[2] + A[9 + d];
+      const double kv = f.coeff_kind == 1
+                            ? f.c[0] + f.c[1] * sin(f.c[2] * xq[0]) * sin(f.c[2] * xq[1]) * sin(f.c[2] * xq[2])
+                            : f.c[0] + f.c[1] * xq[0] + f.c[2] * xq[1] + f.c[3] * xq[2];
+      if (!(kv > 0.0)) atomicExch(bad, 1);
+    }
+  }
+}
+}  // namespace
+
+// tiles of this handle's cells: (cell, j0, i0, top layer)
+static const DevBuf<int4>& ew_units(const bt_grid& g, int level, int& count) {
+  static thread_local struct {
+    const bt_grid* g = nullptr;
+    int level = -1, begin = -1, end = -1, epoch = -1;
+    DevBuf<int4> d;
+    int count = 0;
+  } cache[4];
+  for (auto& c : cache)
+    if (c.g == &g && c.level == level && c.begin == g.part_begin && c.end == g.part_end && c.epoch == g.part_epoch) {
+      count = c.count;
+      return c.d;
+    }
+  auto& c = cache[level & 3];
+  const int n = 1 << level;
+  std::vector<int4> u;
+  for (int cell = g.part_begin; cell < g.part_end; ++cell)
+    for (int j0 = 0; j0 <= n; j0 += kER)
+      for (int i0 = 0; i0 + j0 <= n; i0 += kEC) u.push_back(make_int4(cell, j0, i0, n - j0 - i0));
+  c.d.upload(u);
+  c.g = &g;
+  c.level = level;
+  c.begin = g.part_begin;
+  c.end = g.part_end;
+  c.epoch = g.part_epoch;
+  c.count = (int)u.size();
+  count = c.count;
+  return c.d;
+}
+
+void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells, const double* x,
+                        double* y, bool diag_only, cudaStream_t s) {
+  const int n = 1 << level, w = n + 1;
+  if (g.part_end == g.part_begin) return;
+  int nu = 0;
+  const DevBuf<int4>& units = ew_units(g, level, nu);
+  x = shifted(x, g, BT_SPACE_P1, level);  // global-cell indexing
+  y = shifted(y, g, BT_SPACE_P1, level);
+  const size_t smem = sizeof(EwShared);
+  const double c0 = c[0];
+#define BT_EW(CK_, D_)                                                                                   \
+  {                                                                                                      \
+    static bool attr = false;                                                                            \
+    if (!attr) {                                                                                         \
+      BT_CUDA(cudaFuncSetAttribute(k_ew<CK_, D_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      attr = true;                                                                                       \
+    }                                                                                                    \
+    k_ew<CK_, D_><<<nu, kET, smem, s>>>(x, y, d_cells, units.p, c0, n, n_tet(w));                        \
+  }
+  if (ck == 0) { if (diag_only) BT_EW(0, true) else BT_EW(0, false) }
+  else if (ck == 1) { if (diag_only) BT_EW(1, true) else BT_EW(1, false) }
+  else { if (diag_only) BT_EW(2, true) else BT_EW(2, false) }
+#undef BT_EW
+  count_launch();
+  check_launch("k_ew");
+}
+
+// local_matrix's positivity check of a div_k_grad coefficient (forms.hpp:114):
+// settled on the host when the coefficient's range is (sin product: c0 > |c1|;
+// affine: positive at every macro-cell vertex, hence on the cells), else
+// evaluated at every quadrature point on the device
+void check_coefficient(const bt_grid& g, const bt_form& f, int level, const double* d_maps, cudaStream_t s) {
+  if (f.kind != BT_FORM_DIV_K_GRAD) return;
+  if (f.coeff_kind == 0) {
+    if (!(f.c[0] > 0)) raise(BT_INVALID_ARGUMENT, "div_k_grad coefficient must be positive");
+    return;
+  }
+  if (f.coeff_kind == 1 && f.c[0] > std::fabs(f.c[1])) return;
+  if (f.coeff_kind == 2) {
+    bool ok = true;
+    for (int c = g.part_begin; c < g.part_end && ok; ++c)
+      for (int v = 0; v < 4 && ok; ++v) {
+        const auto& p = g.mesh.coords[g.mesh.cells[c][v]];
+        ok = f.c[0] + f.c[1] * p[0] + f.c[2] * p[1] + f.c[3] * p[2] > 0;
+      }
+    if (ok) return;
+  }
+  const int n = 1 << level, nl = g.part_end - g.part_begin;
+  if (!nl) return;
+  DevBuf<int> bad(1);
+  BT_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+  k_kpos<<<dim3(64, nl, 6), 256, 0, s>>>(d_maps, f, n, g.part_begin, bad.p);
+  count_launch();
+  check_launch("k_kpos");
+  int h = 0;
+  BT_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BT_CUDA(cudaStreamSynchronize(s));
+  if (h) raise(BT_INVALID_ARGUMENT, "div_k_grad coefficient must be positive");
+}
+
+}  // namespace bt

@@ -398,13 +398,11 @@ static void typed_diag(const double cls[6][16], double out[16]) {
   }
 }
 
-void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<EwCell>& cells,
-                    std::vector<EwAngles>& angles) {
+void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<EwCell>& cells) {
   const int nc = g.mesh.n_cells();
   cells.assign(nc, EwCell{});
   const bool var = f.kind == BT_FORM_DIV_K_GRAD;
   const int ck = var ? f.coeff_kind : 0;
-  angles.assign(ck == 1 ? nc : 0, EwAngles{});
   const double h = 1.0 / (double)(1 << level);
   const double qa = (5.0 + 3.0 * std::sqrt(5.0)) / 20.0;  // forms.hpp:56-61
   const double qb = (5.0 - std::sqrt(5.0)) / 20.0;
@@ -415,49 +413,58 @@ void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<E
     for (int d = 0; d < 3; ++d)
       for (int q = 0; q < 3; ++q) e.beta[d][q] = (ck == 1 ? f.c[2] : 0.0) * mp.a[3 * d + q] * h;
     if (ck == 2) {
+      // k affine: kbar = k(centroid) = c0 + c . (A h (p + centroid_s) + b)
       for (int q = 0; q < 3; ++q) {
         e.lin[q] = 0;
         for (int d = 0; d < 3; ++d) e.lin[q] += f.c[1 + d] * mp.a[3 * d + q] * h;
       }
-      for (int s = 0; s < 6; ++s)
-        for (int slot = 0; slot < 4; ++slot) {
-          double r[3];
-          for (int q = 0; q < 3; ++q) {
-            double mean = 0;
-            for (int i = 0; i < 4; ++i) mean += kOffCell[s][i][q];
-            r[q] = 0.25 * mean - kOffCell[s][slot][q];
-          }
-          double v = f.c[0];
-          for (int d = 0; d < 3; ++d) {
-            double x = mp.b[d];
-            for (int q = 0; q < 3; ++q) x += mp.a[3 * d + q] * h * r[q];
-            v += f.c[1 + d] * x;
-          }
-          e.lin0[s][slot] = v;
+      for (int s = 0; s < 6; ++s) {
+        double r[3];
+        for (int q = 0; q < 3; ++q) {
+          double mean = 0;
+          for (int i = 0; i < 4; ++i) mean += kOffCell[s][i][q];
+          r[q] = 0.25 * mean;
         }
+        double v = f.c[0];
+        for (int d = 0; d < 3; ++d) {
+          double x = mp.b[d];
+          for (int q = 0; q < 3; ++q) x += mp.a[3 * d + q] * h * r[q];
+          v += f.c[1 + d] * x;
+        }
+        e.lin0[s] = v;
+      }
     }
     if (ck == 1) {
-      // phase of quadrature point q of the (s, slot) micro-cell relative to the
-      // vertex it is pulled into: f * (A h (delta_sq - o_slot) + b)
-      EwAngles& an = angles[c];
+      // phase of quadrature point q of class s relative to its anchor p:
+      // gamma_{s,q,d} = f (A h delta_{s,q} + b)_d; the monomial coefficients
+      // coefh[s][m] = c1/4 sum_q prod_d (bit d of m ? sin : cos)(gamma_{s,q,d})
       const double fr = f.c[2];
-      for (int s = 0; s < 6; ++s)
-        for (int slot = 0; slot < 4; ++slot)
-          for (int q = 0; q < 4; ++q) {
-            double r[3];
-            for (int a = 0; a < 3; ++a) {
-              double dl = 0;
-              for (int i = 0; i < 4; ++i) dl += (i == q ? qa : qb) * kOffCell[s][i][a];
-              r[a] = dl - kOffCell[s][slot][a];
-            }
-            for (int d = 0; d < 3; ++d) {
-              double x = mp.b[d];
-              for (int a = 0; a < 3; ++a) x += mp.a[3 * d + a] * h * r[a];
-              const double ph = fr * x;
-              an.s[s][slot][q][d] = std::sin(ph);
-              an.c[s][slot][q][d] = std::cos(ph);
-            }
+      for (int s = 0; s < 6; ++s) {
+        double sg[4][3], cg[4][3];
+        for (int q = 0; q < 4; ++q) {
+          double r[3];
+          for (int a = 0; a < 3; ++a) {
+            double dl = 0;
+            for (int i = 0; i < 4; ++i) dl += (i == q ? qa : qb) * kOffCell[s][i][a];
+            r[a] = dl;
           }
+          for (int d = 0; d < 3; ++d) {
+            double x = mp.b[d];
+            for (int a = 0; a < 3; ++a) x += mp.a[3 * d + a] * h * r[a];
+            sg[q][d] = std::sin(fr * x);
+            cg[q][d] = std::cos(fr * x);
+          }
+        }
+        for (int m = 0; m < 8; ++m) {
+          double acc = 0;
+          for (int q = 0; q < 4; ++q) {
+            double p = 1;
+            for (int d = 0; d < 3; ++d) p *= (m >> d & 1) ? sg[q][d] : cg[q][d];
+            acc += p;
+          }
+          e.coefh[s][m] = 0.25 * f.c[1] * acc;
+        }
+      }
     }
   }
 }
@@ -555,11 +562,10 @@ const EwTables& ew_tables(const bt_grid& g, const bt_form& f, int level) {
   auto t = std::make_unique<EwTables>();
   t->form = f;
   t->level = level;
+  check_coefficient(g, f, level, cell_maps(g), 0);
   std::vector<EwCell> cells;
-  std::vector<EwAngles> angles;
-  build_ew_cells(g, f, level, cells, angles);
+  build_ew_cells(g, f, level, cells);
   t->cells.upload(cells);
-  if (!angles.empty()) t->angles.upload(angles);
   if (g.ew_cache.size() >= 16) g.ew_cache.erase(g.ew_cache.begin());
   g.ew_cache.push_back(std::move(t));
   return *g.ew_cache.back();
@@ -742,8 +748,7 @@ bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks) {
   partition_range(g->mesh.n_cells(), rank, nranks, g->part_begin, g->part_end);
   interface_lists(*g, g->part_begin, g->part_end, g->loc);
   // everything derived from the previous partition: exchange plans (P1 and
-  // N1E1 edges), elementwise tables (their kbar blocks are indexed relative to
-  // part_begin), reduction and exchange scratch
+  // N1E1 edges), elementwise tables, reduction and exchange scratch
   BT_CUDA(cudaDeviceSynchronize());
   for (auto& p : g->xplan) p.reset();
   for (auto& p : g->xplan_edges) p.reset();

@@ -174,7 +174,6 @@ struct FastTasks {
   std::vector<int> chunk_first;  // first task of each kMaxCells-cell chunk (+ end)
 };
 struct EwCell;
-struct EwAngles;
 struct EwTables;
 
 struct Topology {
@@ -247,29 +246,19 @@ struct StencilCell {
   double w[16][15];
   uint32_t mask[16];
 };
-// Per-cell data for the elementwise (on-the-fly) kernel.
+// Per-cell data for the elementwise kernel (bt_ew.cu).
 struct EwCell {
-  double G[6][16];        // class matrices (diffusion for div_k_grad; else the form)
-  double beta[3][3];      // angle slope: f * A[d][e] * h   (coeff kind 1)
-  double lin[3];          // c . (A h) for coeff kind 2
-  double lin0[6][4];      // kind 2: c0 + c.(A h (ō_s - o_slot) + b)
-};
-struct EwAngles {         // kind 1: sin/cos of the (class, slot, q, d) phase
-  double s[6][4][4][3];
-  double c[6][4][4][3];
+  double G[6][16];      // class matrices (diffusion for div_k_grad; else the form)
+  double beta[3][3];    // coeff kind 1: phase slope f * A[d][e] * h per lattice direction e
+  double coefh[6][8];   // coeff kind 1: c1/4 sum_q prod_d (bit d of m ? sin : cos)(gamma_{s,q,d})
+  double lin[3];        // coeff kind 2: c . (A h) per lattice direction
+  double lin0[6];       // coeff kind 2: c0 + c . (A h centroid_s + b)
 };
 struct EwTables {  // device tables of one (form, level) for the elementwise kernel
   bt_form form{};
   int level = 0;
   DevBuf<EwCell> cells;
-  DevBuf<EwAngles> angles;
-  mutable DevBuf<double> kbar;  // per micro-cell kbar (sin-product coefficient), built on first use
-  mutable bool kbar_tried = false;
 };
-// k_kbar's per-micro-cell kbar of this handle's cells (8 B per micro-cell), or
-// left empty when it would take more than a quarter of the free memory
-void build_kbar_cache(const bt_grid& g, int level, const double* c, const EwCell* d_cells,
-                      const EwAngles* d_angles, DevBuf<double>& out);
 const EwTables& ew_tables(const bt_grid& g, const bt_form& f, int level);
 }  // namespace bt
 
@@ -300,8 +289,7 @@ namespace bt {
 void class_matrices(const bt_grid& g, int form_kind, int level, int cell, double out[6][16]);
 void build_stencil_cells(const bt_grid& g, const bt_form& f, int level,
                          std::vector<StencilCell>& cells, std::vector<std::array<double, 15>>& rows);
-void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<EwCell>& cells,
-                    std::vector<EwAngles>& angles);
+void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<EwCell>& cells);
 int64_t level_slots(int space, int level);  // per cell
 // Vectors of a partitioned grid hold the rank's cells [part_begin, part_end)
 // only; every pointer inside the library is such a local pointer. Kernels
@@ -370,9 +358,12 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream& side_stream();
-void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c,
-                        const EwCell* d_cells, const EwAngles* d_angles, const double* x, double* y,
-                        bool diag_only, cudaStream_t s, const double* kcache = nullptr);
+void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c, const EwCell* d_cells,
+                        const double* x, double* y, bool diag_only, cudaStream_t s);
+// local_matrix's positivity check of a div_k_grad coefficient (bt_ew.cu)
+void check_coefficient(const bt_grid& g, const bt_form& f, int level, const double* d_maps, cudaStream_t s);
+// per cell: the affine map (a row-major, b), built on first use (bt_kernels.cu)
+const double* cell_maps(const bt_grid& g);
 void launch_vec(int op, double* y, const double* x, double a, int64_t n, cudaStream_t s);
 void launch_fill_by_z(const bt_grid& g, int level, const double* tbl, double* out, cudaStream_t s);
 double dot_p1(const bt_grid& g, int level, const double* x, const double* y, cudaStream_t s);

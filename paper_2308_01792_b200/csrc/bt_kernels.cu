@@ -17,236 +17,11 @@
 
 namespace bt {
 
-// Present micro-cells (bit 4*s + slot) and needed stencil directions per zero
-// set; derived from in_i_tet(w_s, p - o_slot) (verified exhaustively in
-// tests/test_index.py against the reference rule).
-__constant__ uint32_t kPresent[16] = {0xffffff, 0xe8cc8e, 0x962b4d, 0x80080c, 0x4d962b, 0x48840a,
-                                      0x40209,  0x8,      0x337117, 0x204006, 0x122105, 0x4,
-                                      0x11003,  0x2,      0x1,      0x0};
-__constant__ uint32_t kDirMask[16] = {0x7fff, 0x7f71, 0x26ff, 0x2671, 0x5d6f, 0x5d61, 0x46f, 0x461,
-                                      0x3b9f, 0x3b11, 0x229f, 0x2211, 0x190f, 0x1901, 0xf,   0x0};
-// stencil direction of (o_j - o_slot) for class s (operators.hpp:219)
-#define BT_TET_DIR                                                                      \
-  {{{0, 1, 2, 3}, {8, 0, 11, 12}, {9, 4, 0, 13}, {10, 5, 6, 0}},                        \
-   {{0, 13, 12, 3}, {6, 0, 11, 2}, {5, 4, 0, 1}, {10, 9, 8, 0}},                        \
-   {{0, 13, 7, 3}, {6, 0, 1, 2}, {14, 8, 0, 11}, {10, 9, 4, 0}},                        \
-   {{0, 11, 2, 3}, {4, 0, 1, 7}, {9, 8, 0, 13}, {10, 14, 6, 0}},                        \
-   {{0, 11, 12, 3}, {4, 0, 13, 7}, {5, 6, 0, 1}, {10, 14, 8, 0}},                       \
-   {{0, 1, 7, 3}, {8, 0, 13, 12}, {14, 6, 0, 11}, {10, 5, 4, 0}}}
-
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerCta = 64;
 
 static inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
-
-// ---------------------------------------------------------------------------
-// Elementwise P1 apply with on-the-fly coefficient (apply_elementwise
-// operators.hpp:115-164, local_matrix forms.hpp:75-120), pull form:
-// y_v = sum over present micro-cells T of v: kbar_T * (G_s row) . x_T, with
-// kbar_T = 1/4 sum_q k(x_q) by the reference's 4-point rule. For the
-// sin-product coefficient each quadrature phase is C + beta . v, so sin/cos
-// of beta . v (3 sincos per vertex) and the angle-addition formula replace
-// the 12 sin evaluations per micro-cell.
-//
-// CK == 3 (sin product, cached): kbar of every micro-cell was computed once
-// per (form, level) by k_kbar (k_kbar_cache) — k does not depend on x — so an
-// apply gathers it instead of evaluating 4 x 3 phases per (vertex, micro-cell):
-// each micro-cell's kbar was otherwise recomputed by all 4 of its vertices.
-// ---------------------------------------------------------------------------
-// micro-cell classes: widths n, n - 2, n - 1 x 4 (micro_index.hpp:97-121) and
-// their offsets in a cell's kbar block of n^3 values
-__host__ __device__ inline int class_width(int s, int n) { return s == 0 ? n : (s == 1 ? n - 2 : n - 1); }
-__host__ __device__ inline int64_t class_offset(int s, int n) {
-  return s == 0 ? 0 : (s == 1 ? tet32(n) : (int64_t)tet32(n) + tet32(n - 2) + (int64_t)(s - 2) * tet32(n - 1));
-}
-
-template <int CK, bool DIAG>
-__global__ void __launch_bounds__(kThreads) k_elementwise(const double* __restrict__ x, double* __restrict__ y,
-                                                          const EwCell* __restrict__ cells,
-                                                          const EwAngles* __restrict__ angles, double c0, double c1,
-                                                          int w, int64_t cell_slots, int cell0,
-                                                          const double* __restrict__ kcache) {
-  __shared__ EwCell sc;
-  __shared__ EwAngles sa;
-  const int cell = cell0 + blockIdx.y;
-  {
-    const double* src = reinterpret_cast<const double*>(cells + cell);
-    double* dst = reinterpret_cast<double*>(&sc);
-    for (int q = threadIdx.x; q < (int)(sizeof(EwCell) / 8); q += blockDim.x) dst[q] = src[q];
-    if (CK == 1) {
-      const double* sa_src = reinterpret_cast<const double*>(angles + cell);
-      double* sa_dst = reinterpret_cast<double*>(&sa);
-      for (int q = threadIdx.x; q < (int)(sizeof(EwAngles) / 8); q += blockDim.x) sa_dst[q] = sa_src[q];
-    }
-  }
-  __syncthreads();
-  constexpr int kTetDir[6][4][4] = BT_TET_DIR;
-  const double* __restrict__ xc = x + (int64_t)cell * cell_slots;
-  double* __restrict__ yc = y + (int64_t)cell * cell_slots;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n = w - 1;
-  const double* __restrict__ kc = CK == 3 ? kcache + (int64_t)blockIdx.y * n * n * n : nullptr;  // this cell's kbar
-  const int nrows = tri32(w);
-  const int rend = min(nrows, (int)(blockIdx.x + 1) * kRowsPerCta);
-  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
-    int j, k;
-    decode_row(w, r, j, k);
-    const int L = w - j - k;
-    const int t0 = row_start(w, j, k);
-    int off[15];
-    row_offsets(w, j, k, off);
-    // CK == 3: kbar index of the (s, slot) micro-cell of vertex (i, j, k) is
-    // kbb[s][slot] + i (row-constant part computed once per row)
-    int kbb[6][4];
-    if (CK == 3) {
-      constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
-#pragma unroll
-      for (int s = 0; s < 6; ++s)
-#pragma unroll
-        for (int slot = 0; slot < 4; ++slot)
-          kbb[s][slot] = (int)class_offset(s, n) +
-                         row_start(class_width(s, n), j - kOff[s][slot][1], k - kOff[s][slot][2]) - kOff[s][slot][0];
-    }
-    for (int i = lane; i < L; i += 32) {
-      const int t = t0 + i;
-      const int z = zero_set(n, i, j, k);
-      const uint32_t present = kPresent[z];
-      double xv[15];
-      if (!DIAG) {
-        const uint32_t dm = kDirMask[z];
-#pragma unroll
-        for (int d = 0; d < 15; ++d) xv[d] = (dm >> d & 1) ? __ldg(xc + t + off[d]) : 0.0;
-      }
-      double sB[3], cB[3];
-      double lin = 0.0;
-      if (CK == 1) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const double ph = sc.beta[d][0] * i + sc.beta[d][1] * j + sc.beta[d][2] * k;
-          sincos(ph, &sB[d], &cB[d]);
-        }
-      } else if (CK == 2) {
-        lin = sc.lin[0] * i + sc.lin[1] * j + sc.lin[2] * k;
-      }
-      double acc = 0.0;
-#pragma unroll
-      for (int s = 0; s < 6; ++s) {
-#pragma unroll
-        for (int slot = 0; slot < 4; ++slot) {
-          if (!(present >> (4 * s + slot) & 1)) continue;
-          double kbar;
-          if (CK == 0) {
-            kbar = c0;
-          } else if (CK == 3) {
-            kbar = __ldg(kc + kbb[s][slot] + i);
-          } else if (CK == 1) {
-            kbar = 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              double prod = 1.0;
-#pragma unroll
-              for (int d = 0; d < 3; ++d)
-                prod *= fma(sa.s[s][slot][q][d], cB[d], sa.c[s][slot][q][d] * sB[d]);
-              kbar = fma(0.25, fma(c1, prod, c0), kbar);
-            }
-          } else {
-            kbar = sc.lin0[s][slot] + lin;
-          }
-          if (DIAG) {
-            acc = fma(kbar, sc.G[s][5 * slot], acc);
-          } else {
-            double row = 0.0;
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) row = fma(sc.G[s][4 * slot + jj], xv[kTetDir[s][slot][jj]], row);
-            acc = fma(kbar, row, acc);
-          }
-        }
-      }
-      yc[t] = acc;
-    }
-  }
-}
-
-// kbar of every micro-cell (class s, anchor p) of this handle's cells, as the
-// on-the-fly path evaluates it at the micro-cell's vertex 0 (slot 0):
-// cache[(cell - cell0) * n^3 + class_offset(s) + linearize(w_s, p)]
-__global__ void __launch_bounds__(kThreads) k_kbar(const EwCell* __restrict__ cells,
-                                                   const EwAngles* __restrict__ angles, double c0, double c1,
-                                                   int n, int cell0, double* __restrict__ cache) {
-  constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
-  const int cell = cell0 + blockIdx.y, s = blockIdx.z;
-  const EwCell& e = cells[cell];
-  const EwAngles& an = angles[cell];
-  const int ws = class_width(s, n);
-  if (ws <= 0) return;
-  double* __restrict__ kc = cache + (int64_t)blockIdx.y * n * n * n + class_offset(s, n);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rend = min(tri32(ws), (int)(blockIdx.x + 1) * kRowsPerCta);
-  for (int r = blockIdx.x * kRowsPerCta + warp; r < rend; r += kWarps) {
-    int pj, pk;
-    decode_row(ws, r, pj, pk);
-    const int L = ws - pj - pk, t0 = row_start(ws, pj, pk);
-    for (int pi = lane; pi < L; pi += 32) {
-      const int i = pi + kOff[s][0][0], j = pj + kOff[s][0][1], k = pk + kOff[s][0][2];  // vertex 0
-      double sB[3], cB[3];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double ph = e.beta[d][0] * i + e.beta[d][1] * j + e.beta[d][2] * k;
-        sincos(ph, &sB[d], &cB[d]);
-      }
-      double kbar = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double prod = 1.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) prod *= fma(an.s[s][0][q][d], cB[d], an.c[s][0][q][d] * sB[d]);
-        kbar = fma(0.25, fma(c1, prod, c0), kbar);
-      }
-      kc[t0 + pi] = kbar;
-    }
-  }
-}
-
-// k_kbar's cache for (tables, level) on this handle's cells, or nullptr when
-// it would take more than a quarter of the free device memory
-void build_kbar_cache(const bt_grid& g, int level, const double* c, const EwCell* d_cells,
-                      const EwAngles* d_angles, DevBuf<double>& out) {
-  const int n = 1 << level, nc = g.part_end - g.part_begin;
-  const size_t count = (size_t)nc * n * n * n;
-  size_t free_b = 0, total_b = 0;
-  BT_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  if (!count || count * sizeof(double) > free_b / 4) return;
-  out.alloc(count);
-  dim3 grid(ceil_div(tri32(n), kRowsPerCta), nc, 6);
-  k_kbar<<<grid, kThreads>>>(d_cells, d_angles, c[0], c[1], n, g.part_begin, out.p);
-  count_launch();
-  check_launch("k_kbar");
-  BT_CUDA(cudaDeviceSynchronize());
-}
-
-void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells,
-                        const EwAngles* d_angles, const double* x, double* y, bool diag_only, cudaStream_t s,
-                        const double* kcache) {
-  const int w = (1 << level) + 1;
-  const int nc = g.part_end - g.part_begin;  // this handle's cells
-  if (!nc) return;
-  dim3 grid(ceil_div(tri32(w), kRowsPerCta), nc);
-  const int64_t cs = n_tet(w);
-  const double c0 = c[0], c1 = c[1];
-  x = shifted(x, g, BT_SPACE_P1, level);
-  y = shifted(y, g, BT_SPACE_P1, level);
-  if (ck == 1 && kcache) ck = 3;
-#define BT_EW(CK_, D_) \
-  k_elementwise<CK_, D_><<<grid, kThreads, 0, s>>>(x, y, d_cells, d_angles, c0, c1, w, cs, g.part_begin, kcache)
-  if (ck == 0) { if (diag_only) BT_EW(0, true); else BT_EW(0, false); }
-  else if (ck == 1) { if (diag_only) BT_EW(1, true); else BT_EW(1, false); }
-  else if (ck == 3) { if (diag_only) BT_EW(3, true); else BT_EW(3, false); }
-  else { if (diag_only) BT_EW(2, true); else BT_EW(2, false); }
-#undef BT_EW
-  count_launch();
-  check_launch("k_elementwise");
-}
 
 // ---------------------------------------------------------------------------
 // Row-walk helpers: fill-by-zero-set, owned dot products, transfers
@@ -700,7 +475,7 @@ __global__ void __launch_bounds__(kThreads) k_l2_error(const double* __restrict_
   }
 }
 
-static const double* cell_maps(const bt_grid& g) {
+const double* cell_maps(const bt_grid& g) {
   if (!g.d_maps.p) {
     std::vector<double> m(12 * (size_t)g.mesh.n_cells());
     for (int c = 0; c < g.mesh.n_cells(); ++c) {
@@ -753,16 +528,6 @@ double l2_error_p1(const bt_grid& g, int level, const double* x, const bt_field&
   double acc = 0.0;
   for (int c = 0; c < nc; ++c) acc += per_cell[c];
   return std::sqrt(acc);
-}
-
-// the tables' kbar cache (sin-product coefficients), built on first use
-static const double* kbar_of(const bt_grid& g, const EwTables& t, const double* c) {
-  if (t.form.kind != BT_FORM_DIV_K_GRAD || t.form.coeff_kind != 1) return nullptr;
-  if (!t.kbar_tried) {
-    t.kbar_tried = true;
-    build_kbar_cache(g, t.level, c, t.cells.p, t.angles.p, t.kbar);
-  }
-  return t.kbar.p;
 }
 
 static void validate_field(const bt_field* f) {
@@ -955,7 +720,7 @@ bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level,
     }
     out = scratch;
   }
-  launch_elementwise(*g, level, ck, c, t.cells.p, t.angles.p, x, out, false, s, kbar_of(*g, t, c));
+  launch_elementwise(*g, level, ck, c, t.cells.p, x, out, false, s);
   sync(*g, level, bc ? IF_SYNC_DIR : IF_SYNC, out, x, s);
   if (mode == BT_MODE_ADD) launch_vec(V_AXPY, y, out, 1.0, bt_space_size(g, BT_SPACE_P1, level), s);
   BT_CATCH
@@ -970,7 +735,7 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
   const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
   const double one[4] = {1.0, 0.0, 0.0, 0.0};
   const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
-  launch_elementwise(*g, level, ck, c, t.cells.p, t.angles.p, nullptr, diag, true, s, kbar_of(*g, t, c));
+  launch_elementwise(*g, level, ck, c, t.cells.p, nullptr, diag, true, s);
   sync(*g, level, IF_SYNC, diag, nullptr, s);
   BT_CATCH
 }

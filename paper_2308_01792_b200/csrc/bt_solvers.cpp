@@ -17,8 +17,6 @@ struct LevelData {
   int64_t n = 0;
   std::unique_ptr<bt_stencil> stencil;  // stencil kernel
   DevBuf<EwCell> ew;                    // elementwise kernel tables
-  DevBuf<EwAngles> ang;
-  DevBuf<double> kbar;                  // per micro-cell kbar (sin-product coefficient), if it fits
   DevBuf<double> diag;
   double lambda = 0.0;
   // work vectors
@@ -57,8 +55,7 @@ static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int b
   } else {
     const int ck = h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.coeff_kind : 0;
     static const double one[4] = {1.0, 0.0, 0.0, 0.0};
-    launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, L.ang.p, x, y,
-                       false, s, L.kbar.p);
+    launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, x, y, false, s);
   }
   sync(*h.grid, l, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
 }
@@ -333,16 +330,14 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
       L->stencil.reset(st);
       BT_CUDA(cudaMemcpy(L->diag.p, stencil_diag(*st, 0), sizeof(double) * n, cudaMemcpyDeviceToDevice));
     } else {
+      check_coefficient(*g, *form, l, cell_maps(*g), 0);
       std::vector<EwCell> cells;
-      std::vector<EwAngles> angles;
-      build_ew_cells(*g, *form, l, cells, angles);
+      build_ew_cells(*g, *form, l, cells);
       L->ew.upload(cells);
-      if (!angles.empty()) L->ang.upload(angles);
       const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
       static const double one[4] = {1.0, 0.0, 0.0, 0.0};
       const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
-      if (ck == 1) build_kbar_cache(*g, l, c, L->ew.p, L->ang.p, L->kbar);
-      launch_elementwise(*g, l, ck, c, L->ew.p, L->ang.p, nullptr, L->diag.p, true, 0, L->kbar.p);
+      launch_elementwise(*g, l, ck, c, L->ew.p, nullptr, L->diag.p, true, 0);
       sync(*g, l, IF_SYNC, L->diag.p, nullptr, 0);
     }
     h->levels.push_back(std::move(L));
