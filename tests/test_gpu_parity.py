@@ -6,6 +6,7 @@ Bars (BASELINE.json north_star): index maps, DoF layouts, masks, groups,
 random inputs and transfers are bit-exact; fp64 operator applies, diagonals
 and V-cycle residual histories within relative L2 1e-12 (REL below).
 """
+import math
 import os
 
 import numpy as np
@@ -294,7 +295,8 @@ def test_config3_small_and_properties():
 
 def test_config3_full_size_against_reference():
     """Config 3 at full size (384 perturbed tets, L6, div(k grad) with the sin
-    product coefficient; 18.4 M slots): the cached-kbar elementwise apply against
+    product coefficient; 18.4 M slots): the elementwise apply (kbar once per
+    micro-cell, on the fly) against
     the compiled reference, plus symmetry in the owned inner product."""
     from pyoracle import Reference
     text, l = cubes_mesh_text(4, 0.1, 0), 6
@@ -314,3 +316,43 @@ def test_config3_full_size_against_reference():
     bt.apply_elementwise(form, v, av, l)
     a, b = bt.dot(u, av, l), bt.dot(v, au, l)
     assert abs(a - b) <= 1e-12 * max(abs(a), 1.0)
+
+
+@pytest.mark.parametrize("l", [7])
+def test_elementwise_column_tiles_against_reference(l):
+    """Config-5 family (2x2x2 perturbed Kuhn cubes) at level 7, where rows are
+    longer than one 64-column tile of the elementwise kernel: the apply (both
+    BCs) and the assembled diagonal against the compiled reference, for the
+    sin-product and an affine coefficient."""
+    from pyoracle import Reference
+    text = cubes_mesh_text(2, 0.1, 0)
+    g = bt.Grid(text, l, l)
+    r = Reference(text, l, l)
+    x = bt.allocate(bt.p1_space(), g)
+    y = bt.allocate(bt.p1_space(), g)
+    d = bt.allocate(bt.p1_space(), g)
+    bt.random_fill(x, l, 3)
+    xh = host(x, l)
+    aff = bt.Coefficient.affine(2.0, 0.3, -0.2, 0.1)
+    for coeff, kp in ((SIN, kparams()), (aff, kparams(2, 2.0, 0.3, -0.2, 0.1))):
+        form = bt.FormId.div_k_grad(coeff)
+        for bc in (bt.BC.None_, bt.BC.DirichletIdentity):
+            bt.apply_elementwise(form, x, y, l, bc=bc)
+            ref = r.apply_elementwise(l, xh, form=2, kp=kp, bc=int(bc), threads=os.cpu_count() or 1)
+            assert rel(host(y, l), ref) <= REL
+        bt.extract_diagonal(form, d, l)
+        assert rel(host(d, l), r.extract_diagonal(l, form=2, kp=kp)) <= REL
+
+
+def test_div_k_grad_coefficient_must_be_positive():
+    """local_matrix raises invalid_argument when k <= 0 at a quadrature point
+    (forms.hpp:114); sin product with c0 <= |c1| is checked point by point."""
+    g = bt.Grid(cube_kuhn_text(), 3, 3)
+    x = bt.allocate(bt.p1_space(), g)
+    y = bt.allocate(bt.p1_space(), g)
+    with pytest.raises(bt.InvalidArgument):
+        bt.apply_elementwise(bt.FormId.div_k_grad(bt.Coefficient.sin_product(0.2, 1.0, 2 * math.pi)), x, y, 3)
+    with pytest.raises(bt.InvalidArgument):
+        bt.apply_elementwise(bt.FormId.div_k_grad(bt.Coefficient.affine(0.5, -1.0, 0.0, 0.0)), x, y, 3)
+    # positive on the mesh although c0 <= |c1|: accepted (k = 1.5 + 2 sin(pi x/8) ... > 0 on [0,1]^3)
+    bt.apply_elementwise(bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.5, 2.0, math.pi / 8)), x, y, 3)
