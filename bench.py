@@ -4,24 +4,36 @@
 Headline (BASELINE.json metric, config 2 = configs[1]): constant-coefficient
 P1 15-point stencil apply with the full ghost-layer (interface replica) update
 on the unit cube split into 6 Kuhn macro-tets at level 8 (17,173,254 slots,
-16,974,593 owned DoFs), fp64, x = random_fill(seed 0). One step = one
-apply (per-cell rows kernel + interface pass). Inputs (x + y = 275 MB) exceed
-the 126 MB L2, so no explicit flush is needed between steps.
+16,974,593 owned DoFs), fp64, x = random_fill(seed 0). One step = one apply
+(interior kernel || fused boundary kernel, replica sums included). Inputs
+(x + y = 275 MB) exceed the 126 MB L2, so no explicit flush is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 1|2|3|4|5] [--no-cpu] [--no-extra]
 
-Under torchrun (N > 1) the macro-cells are partitioned over the ranks
-(weak scaling: an N x 1 x 1 box of unit cubes, 6 Kuhn macro-tets = one
-config-2-sized block per GPU, level 8). Each step is the per-cell rows
-kernel on the rank's cells plus the interface exchange of the groups that
-span ranks (pack, NCCL allreduce, member-order finish); times are max over
-ranks. `--impl reference` times the reference CPU implementation
-(oracle/_ref, the unmodified blocktet headers) on the host cores instead.
+--config selects the workload of the printed line (default 2, the headline).
+At N = 1 the line also carries `configs`: the other BASELINE configs measured
+in the same run, each with its own roofline (the slower of HBM bytes at the
+measured copy peak and fp64 flops at the fp64 peak measured here by a DFMA
+microbenchmark), e2e and CPU baseline (bounded samples, stated):
+  1  ref-tet L6 stencil, Dirichlet rows, 1 + 10 applies per step (CUDA graph)
+  3  384 perturbed Kuhn tets L6, div(k grad) elementwise (k = 1 + .5 sin sin sin)
+  4  384 perturbed Kuhn tets L7, N1E1 curl-curl + mass, tangential Dirichlet
+  5  V(2,2) Chebyshev(2) multigrid, var-coeff elementwise, 50 coarse CG its:
+     3,072 tets L2 -> 7 on one GPU (L2 -> 8 holds 70 GB per vector: multi-GPU)
+
+Under torchrun (N > 1) config 2 runs weak-scaled (an N x 1 x 1 box of unit
+cubes, 6 Kuhn macro-tets = one config-2-sized block per GPU, level 8), cells
+partitioned over the ranks with the interface exchange inside each step;
+times are max over ranks. `--impl reference` times the reference CPU
+implementation (oracle/_ref, the unmodified blocktet headers) on the host
+cores for the same config, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -34,9 +46,24 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-LEVEL = 8
-WORKLOAD = "cube-kuhn (6 macro-tets) L8, P1 const-coeff 15-point stencil apply + interface sync"
 METRIC = "GDoF/s of matrix-free operator apply (fp64)"
+WORKLOADS = {
+    1: "ref-tet (1 macro-tet) L6, P1 const-coeff 15-point stencil, zero Dirichlet (identity rows), "
+       "1 + 10 applies per step",
+    2: "cube-kuhn (6 macro-tets) L8, P1 const-coeff 15-point stencil apply + interface sync",
+    3: "4x4x4 cubes x 6 perturbed Kuhn tets (384 cells) L6, div(k grad) elementwise on the fly, "
+       "k = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z), + interface sync",
+    4: "4x4x4 cubes x 6 perturbed Kuhn tets (384 cells) L7, N1E1 curl-curl + mass (alpha = beta = 1), "
+       "tangential zero Dirichlet (identity rows) + signed interface sync",
+    5: "8x8x8 cubes x 6 perturbed Kuhn tets (3,072 cells) L2->7, V(2,2)-cycle, Chebyshev(2)-Jacobi, "
+       "var-coeff elementwise div(k grad), linear transfers, 50 coarse CG its (one step = one V-cycle)",
+}
+# algorithmic fp64 flops of the elementwise apply (bt_ew.cu): per micro-cell the
+# class-matrix row times x_T for its 4 vertices (16 FMA) and the kbar-weighted
+# accumulation (4 FMA), kbar by the monomial expansion (8 FMA); per anchor the
+# 3 sincos by angle addition (12 flops) and the 8 monomials (12 flops)
+EW_FLOPS_PER_MICROCELL = 2 * (16 + 4 + 8)
+EW_FLOPS_PER_ANCHOR = 24
 
 
 def dist_env():
@@ -44,6 +71,17 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -94,80 +132,467 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def measured_peaks():
+def measured_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
-        return float(pk["hbm_gbs"]), "measured"
+        return float(pk["hbm_gbs"]), "measured MEASURED_PEAKS.json hbm_gbs (copy)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback B200_PROFILING.md 6.65 TB/s"
 
 
-def cpu_baseline_sample(threads=None):
-    """Reference CPU apply (oracle/_ref = blocktet headers, -O3, no -march),
-    config 2 at full size, threads = min(#cells, nproc). Bounded sample:
-    median of 5 applies (~2-10 s)."""
+def measure_fp64(bt, torch):
+    """FP64 FMA peak of this GPU (TFLOP/s): bt_dfma_probe, 16 independent
+    DFMA chains per thread, 8 blocks of 256 threads per SM, CUDA events, best
+    of 5 after a warm-up."""
+    from paper_2308_01792_b200 import _lib
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    blocks, iters = 8 * sms, 4096
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sp = bt.api._stream()
+    for _ in range(2):
+        bt.api._check(_lib.lib.bt_dfma_probe(blocks, iters, bt.api._ptr(sink), sp))
+    best = 0.0
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        bt.api._check(_lib.lib.bt_dfma_probe(blocks, iters, bt.api._ptr(sink), sp))
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, 2.0 * blocks * 256 * 16 * iters / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
+def roofline(bytes_, flops, sec, hbm_gbs, fp64_tflops, kernel, kernel_ms, share, extra=None):
+    """The slower of bytes at the HBM peak and flops at the fp64 peak."""
+    t_hbm = bytes_ / (hbm_gbs * 1e9)
+    t_fp = flops / (fp64_tflops * 1e12) if flops else 0.0
+    if t_fp > t_hbm:
+        r = {"bound": "fp64", "achieved": flops / sec / 1e12, "peak": fp64_tflops, "unit": "TFLOP/s",
+             "frac": t_fp / sec, "peak_source": "measured in this run (bt_dfma_probe DFMA microbenchmark)",
+             "algorithmic_flops_per_launch": flops, "hbm_frac": t_hbm / sec}
+    else:
+        r = {"bound": "hbm", "achieved": bytes_ / sec / 1e9, "peak": hbm_gbs, "unit": "GB/s", "frac": t_hbm / sec,
+             "peak_source": measured_hbm()[1], "algorithmic_bytes_per_launch": bytes_}
+        if flops:
+            r["fp64_frac"] = t_fp / sec
+    r.update({"kernel": kernel, "kernel_ms": kernel_ms, "kernel_share": share, "traffic": None,
+              "algorithmic_bytes_per_launch": bytes_})
+    if extra:
+        r.update(extra)
+    return r
+
+
+def timed_steps(torch, step, K, W, stream, dist_max=False):
+    """W untimed steps, then K steps between events (barrier + sync both
+    sides); per-step events for the kernel share. Returns (total_ms, per-step
+    ms list)."""
+    for _ in range(W):
+        step(None)
+    torch.cuda.synchronize()
+    if dist_max:
+        torch.distributed.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for q in range(K):
+        step(evs[q])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    total = t0.elapsed_time(t1)
+    if dist_max:
+        t = torch.tensor([total], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total = float(t.item())
+    return total, [a.elapsed_time(b) for a, b in evs]
+
+
+def e2e_serve(torch, bt, apply_fn, xdev, ydev, nsteps, ws):
+    """Pipelined serving loop through the public API: every step copies its
+    input pinned host -> device and its result device -> pinned host;
+    consecutive steps overlap on three streams (H2D of step s+1, apply of
+    step s, D2H of step s-1; PCIe is full duplex), double-buffered. Returns
+    (ms, h2d bytes, d2h bytes, last host result)."""
+    n_in, n_out = xdev[0].numel(), ydev[0].numel()
+    hx = torch.empty(n_in, dtype=torch.float64, pin_memory=True)
+    hx.copy_(xdev[0].cpu())
+    hys = [torch.empty(n_out, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+
+    single = xdev[0] is xdev[1]  # one device buffer pair: step q+1's copies wait for step q
+    lag = 1 if single else 2
+
+    def serve(k):
+        for q in range(k):
+            b = q & 1
+            with torch.cuda.stream(s_in):
+                if q >= lag:
+                    s_in.wait_event(ev_cmp[(q - lag) & 1])  # the apply of step q-lag has read its input
+                xdev[b].copy_(hx, non_blocking=True)
+                ev_in[b].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in[b])
+                if q >= lag:
+                    s_cmp.wait_event(ev_out[(q - lag) & 1])  # the D2H of step q-lag has read its result
+                apply_fn(b)
+                ev_cmp[b].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[b])
+                hys[b].copy_(ydev[b], non_blocking=True)
+                ev_out[b].record(s_out)
+
+    serve(2)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_in)
+    serve(nsteps)
+    s_out.wait_event(ev_out[(nsteps - 1) & 1])
+    e1.record(s_out)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, 8 * n_in, 8 * n_out, hys[(nsteps - 1) & 1]
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (rank 0, N = 1; bounded samples)
+# ---------------------------------------------------------------------------
+def _pyoracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
-    nproc = os.cpu_count() or 1
-    threads = threads or min(6, nproc)
-    kind = "reference"
-    try:
-        r = pyoracle.Reference(pyoracle.cube_kuhn_text(), LEVEL, LEVEL)
-        x = r.random_fill(LEVEL, 0)
-        sec = r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=5, threads=threads)
-        owned = r.owned_count(LEVEL)
-    except (FileNotFoundError, OSError):
-        kind = "port"
-        threads = 1
-        o = pyoracle.Oracle(pyoracle.cube_kuhn_text(), LEVEL, LEVEL, with_edges=False)
-        x = o.random_fill(LEVEL, 0)
-        t0 = time.perf_counter()
-        o.apply_stencil(LEVEL, x, 0)
-        sec = time.perf_counter() - t0
-        owned = o.owned_count(LEVEL)
-    return {"value": owned / sec / 1e9, "unit": "GDoF/s", "cores": threads, "kind": kind,
-            "sample": f"median of 5 full config-2 applies (cube-kuhn L8, {owned} owned DoFs), "
-                      f"{threads} threads of {nproc} host cores, {sec * 1e3:.1f} ms/apply"}
+    return pyoracle
 
 
-def run_reference(args):
-    """The reference CPU apply (oracle/_ref, unmodified blocktet headers) on
-    the host cores, same workload/metric; rank 0 only. Each step is one full
-    config-2 apply; K is capped so the run stays within about a minute."""
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
+def cpu_baseline(cfg, xh=None):
+    po = _pyoracle()
     nproc = os.cpu_count() or 1
-    threads = min(6, nproc)  # the reference parallelises over macro-cells only (threading.hpp:14)
+    model = cpu_model()
     try:
-        r = pyoracle.Reference(pyoracle.cube_kuhn_text(), LEVEL, LEVEL)
-        kind = "reference"
+        if cfg == 1:
+            r = po.Reference(po.ref_tet_text(), 6, 6)
+            x = r.random_fill(6, 0)
+            sec = 11 * r.time_apply(6, xh if xh is not None else x, kind=0, form=0, bc=1, reps=101, threads=1)
+            owned = 11 * r.owned_count(6)
+            return {"value": owned / sec / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "reference", "cpu": model,
+                    "sample": f"reference apply_stencil, ref-tet L6, median of 101 applies x 11 per step, 1 thread "
+                              f"(1 cell: no parallelism) of {nproc} host cores, {sec * 1e3:.2f} ms/step"}
+        if cfg == 2:
+            threads = min(6, nproc)
+            r = po.Reference(po.cube_kuhn_text(), 8, 8)
+            x = r.random_fill(8, 0)
+            sec = r.time_apply(8, x, kind=0, form=0, bc=0, reps=5, threads=threads)
+            owned = r.owned_count(8)
+            return {"value": owned / sec / 1e9, "unit": "GDoF/s", "cores": threads, "kind": "reference",
+                    "cpu": model, "sample": f"reference apply_stencil, median of 5 full config-2 applies "
+                                            f"({owned} owned DoFs), {threads} threads (= cells) of {nproc} host "
+                                            f"cores, {sec * 1e3:.1f} ms/apply"}
+        if cfg == 3:
+            text = po.cubes_mesh_text(4, 0.1, 0)
+            r = po.Reference(text, 6, 6)
+            x = r.random_fill(6, 0)
+            sec = r.time_apply(6, x, kind=1, form=2, kp=po.kparams(), bc=0, reps=1, threads=nproc)
+            owned = r.owned_count(6)
+            return {"value": owned / sec / 1e9, "unit": "GDoF/s", "cores": nproc, "kind": "reference", "cpu": model,
+                    "sample": f"reference apply_elementwise(div_k_grad), 1 full config-3 apply, {nproc} threads, "
+                              f"{sec:.2f} s/apply"}
+        if cfg == 4:
+            Ls = 4
+            o = po.Oracle(po.cubes_mesh_text(4, 0.1, 0), Ls, Ls)
+            xs = o.n1e1_random_fill(Ls, 0)
+            t0 = time.perf_counter()
+            o.n1e1_apply(Ls, xs)
+            sec = time.perf_counter() - t0
+            owned = o.owned_count(Ls, space=2)
+            return {"value": owned / sec / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port", "cpu": model,
+                    "sample": f"N1E1 restatement (oracle/bt_oracle_n1e1.c; the reference has no N1E1), config-4 mesh "
+                              f"at L{Ls} ({owned} owned edges), 1 thread, {sec:.3f} s/apply"}
+        if cfg == 5:
+            text = po.cubes_mesh_text(2, 0.1, 0)
+            lo, hi = 2, 5
+            r = po.Reference(text, lo, hi)
+            r.make_hierarchy(form=2, kp=po.kparams(), kernel=0, threads=nproc)
+            rhs = r.random_fill(hi, 0)
+            secs = np.zeros(3)
+            import paper_2308_01792_b200 as bt
+            smc = bt.SmootherConfig.chebyshev(2)
+            smc.nu1 = smc.nu2 = 2
+            sm = smc.as_array()
+            r.vcycles(hi, sm, rhs, np.zeros(len(rhs)), 3, lo, 0.0, 50, seconds=secs)
+            sec = float(np.median(secs))
+            owned = r.owned_count(hi)
+            return {"value": owned / sec / 1e9, "unit": "GDoF/s", "cores": nproc, "kind": "reference", "cpu": model,
+                    "sample": f"reference v_cycle, reduced instance 2x2x2 cubes (48 tets) L2->5 ({owned} fine owned "
+                              f"DoFs), median of 3 cycles, {nproc} threads, {sec:.3f} s/cycle"}
     except (FileNotFoundError, OSError) as e:
-        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
-        return
-    x = r.random_fill(LEVEL, 0)
-    owned = r.owned_count(LEVEL)
-    for _ in range(min(args.warmup, 1)):
-        r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=1, threads=threads)
-    t0 = time.perf_counter()
-    first = r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=1, threads=threads)
-    K = max(1, min(args.steps, int(60.0 / max(first, 1e-3))))
-    t0 = time.perf_counter()
-    for _ in range(K):
-        r.time_apply(LEVEL, x, kind=0, form=0, bc=0, reps=1, threads=threads)
-    sec = (time.perf_counter() - t0) / K
-    value = owned / sec / 1e9
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": args.gpus,
-            "steps": K, "warmup": min(args.warmup, 1), "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_fill seed 0)",
-            "config": {"workload": WORKLOAD, "level": LEVEL, "cells": 6, "threads": threads},
-            "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": kind,
-                             "sample": f"{K} full config-2 applies, {threads} threads of {nproc} host cores"},
-            "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+        return {"value": None, "unavailable": f"oracle/_ref not built: {e}"}
+    return None
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+class Work:
+    """One config on this rank: step(ev) runs one step on device-resident
+    data; serve_fn / buffers for e2e; units for the metric and roofline."""
+
+
+def setup_config(cfg, bt, torch, ws, rank):
+    w = Work()
+    L = bt.api._L
+    sp = bt.api._stream()
+    if cfg in (1, 2):
+        lvl = 6 if cfg == 1 else 8
+        if cfg == 1:
+            text = bt.ref_tet_text()
+        else:
+            text = bt.box_mesh_text(ws, 1, 1) if ws > 1 else bt.cube_kuhn_text()
+        g = bt.Grid(text, lvl, lvl)
+        if ws > 1:
+            g.set_partition(rank, ws)
+        t = bt.compute_stencil(bt.FormId.diffusion(), g, lvl)
+        x, y = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
+        bt.random_fill(x, lvl, 0)
+        bc = 0
+        if cfg == 1:
+            bt.zero_dirichlet(x, lvl)
+            bc = 1
+        slots = x.values[lvl].numel()
+        w.owned = bt.owned_dof_count(x, lvl)
+        xp, yp = bt.api._ptr(x.values[lvl]), bt.api._ptr(y.values[lvl])
+        reps = 11 if cfg == 1 else 1
+        w.bytes = 16.0 * slots * reps
+        w.flops = 2.0 * 15 * slots * reps
+        w.dofs_per_step = w.owned * reps
+        w.kernel = "k_stencil_small (one launch)" if cfg == 1 else (
+            "k_stencil_fast || k_boundary" if ws == 1 else "k_stencil (per-cell rows) + exchange")
+        if cfg == 1:
+            graph = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                bt.apply_stencil(t, x, y, lvl, bt.BC.DirichletIdentity)
+                torch.cuda.synchronize()
+                n0 = L.bt_launch_count()
+                with torch.cuda.graph(graph, stream=s):
+                    for _ in range(reps):
+                        bt.apply_stencil(t, x, y, lvl, bt.BC.DirichletIdentity)
+            torch.cuda.synchronize()
+            w.graph = graph
+            w.graph_launches = int(L.bt_launch_count() - n0)  # the library kernels each replay runs
+
+            def run():
+                graph.replay()
+        else:
+            def run():
+                bt.api._check(L.bt_apply_stencil(t.handle, xp, yp, bc, sp))
+        xs = [bt.allocate(bt.p1_space(), g) for _ in range(2)]
+        ys = [bt.allocate(bt.p1_space(), g) for _ in range(2)]
+        for q in range(2):
+            xs[q].values[lvl].copy_(x.values[lvl])
+
+        def apply_b(b):
+            for _ in range(reps):
+                bt.apply_stencil(t, xs[b], ys[b], lvl, bt.BC(bc))
+        w.e2e = (apply_b, [q.values[lvl] for q in xs], [q.values[lvl] for q in ys])
+        w.check = (y.values[lvl], reps)
+        w.keep = (g, t, x, y, xs, ys)
+        w.config = {"workload": WORKLOADS[cfg] if not (cfg == 2 and ws > 1) else
+                    f"{ws}x1x1 unit cubes x 6 Kuhn macro-tets ({6 * ws} cells, 6 per GPU) L8, P1 const-coeff "
+                    "15-point stencil apply + interface sync (cells partitioned over ranks)",
+                    "level": lvl, "cells": g.n_cells(), "slots_per_gpu": slots, "owned_dofs": w.owned,
+                    "bc": "dirichlet identity rows" if bc else "none",
+                    "l2": ("inputs larger than L2 (x+y = %.0f MB per GPU)" % (16e-6 * slots)) if cfg == 2 else
+                    "0.77 MB: L2-resident by design of the config (latency bound)"}
+    elif cfg == 3:
+        lvl = 6
+        g = bt.Grid(bt.cubes_mesh_text(4, 0.1, 0), lvl, lvl)
+        form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
+        x, y = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
+        bt.random_fill(x, lvl, 0)
+        slots = x.values[lvl].numel()
+        w.owned = bt.owned_dof_count(x, lvl)
+        micro = g.n_cells() * 8 ** lvl
+        w.bytes = 16.0 * slots
+        w.flops = float(EW_FLOPS_PER_MICROCELL * micro + EW_FLOPS_PER_ANCHOR * slots)
+        w.dofs_per_step = w.owned
+        w.kernel = "k_ew<1,0> (+ k_interface sync)"
+        cf = form.c_struct()
+        xp, yp = bt.api._ptr(x.values[lvl]), bt.api._ptr(y.values[lvl])
+
+        def run():
+            bt.api._check(L.bt_apply_elementwise(g.handle, bt.api.C.byref(cf), lvl, xp, yp, 0, 0, None, sp))
+        xs = [bt.allocate(bt.p1_space(), g) for _ in range(2)]
+        ys = [bt.allocate(bt.p1_space(), g) for _ in range(2)]
+        for q in range(2):
+            xs[q].values[lvl].copy_(x.values[lvl])
+        w.e2e = (lambda b: bt.apply_elementwise(form, xs[b], ys[b], lvl), [q.values[lvl] for q in xs],
+                 [q.values[lvl] for q in ys])
+        w.check = (y.values[lvl], 1)
+        w.keep = (g, x, y, xs, ys, cf)
+        w.config = {"workload": WORKLOADS[3], "level": lvl, "cells": g.n_cells(), "slots": slots,
+                    "owned_dofs": w.owned, "micro_cells": micro, "bc": "none",
+                    "l2": "inputs larger than L2 (x+y = %.0f MB)" % (16e-6 * slots),
+                    "flops_model": f"{EW_FLOPS_PER_MICROCELL} per micro-cell + {EW_FLOPS_PER_ANCHOR} per vertex"}
+    elif cfg == 4:
+        lvl = 7
+        g = bt.Grid(bt.cubes_mesh_text(4, 0.1, 0), lvl, lvl)
+        op = bt.N1E1Operator(g, lvl)
+        x, y = bt.allocate(bt.edge_space(), g, lvl, lvl), bt.allocate(bt.edge_space(), g, lvl, lvl)
+        bt.random_fill(x, lvl, 0)
+        slots = x.values[lvl].numel()
+        w.owned = bt.owned_dof_count(x, lvl)
+        w.bytes = 16.0 * slots
+        w.flops = 0.0
+        w.dofs_per_step = w.owned
+        w.kernel = "k_n1e1_fast + k_n1e1_face (+ signed sync)"
+
+        def run():
+            bt.apply_n1e1(op, x, y, lvl, bt.BC.DirichletIdentity)
+        xs = [bt.allocate(bt.edge_space(), g, lvl, lvl)]
+        ys = [bt.allocate(bt.edge_space(), g, lvl, lvl)]
+        xs[0].values[lvl].copy_(x.values[lvl])
+        # e2e: one device buffer pair (7.7 GB each), so consecutive steps serialise on them
+        w.e2e = (lambda b: bt.apply_n1e1(op, xs[0], ys[0], lvl, bt.BC.DirichletIdentity),
+                 [xs[0].values[lvl]] * 2, [ys[0].values[lvl]] * 2)
+        w.check = (y.values[lvl], 1)
+        w.keep = (g, op, x, y, xs, ys)
+        w.config = {"workload": WORKLOADS[4], "level": lvl, "cells": g.n_cells(), "edge_slots": slots,
+                    "owned_dofs": w.owned, "bc": "tangential Dirichlet identity rows",
+                    "l2": "inputs larger than L2 (x+y = %.1f GB)" % (16e-9 * slots)}
+    elif cfg == 5:
+        lo, hi = 2, 7
+        g = bt.Grid(bt.cubes_mesh_text(8, 0.1, 0), lo, hi)
+        form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
+        h = bt.make_hierarchy(g, form, bt.KernelKind.Elementwise)
+        rhs, x = bt.allocate(bt.p1_space(), g, lo, hi), bt.allocate(bt.p1_space(), g, lo, hi)
+        bt.random_fill(rhs, hi, 0)
+        bt.zero_dirichlet(rhs, hi)
+        sm = bt.SmootherConfig.chebyshev(2)
+        sm.nu1 = sm.nu2 = 2
+        mg = bt.MultigridConfig(coarse_level=lo, cycles=1, coarse_tol=0.0, coarse_maxit=50)
+        bt.v_cycle(h, hi, rhs, x, sm, mg)  # warm-up: spectral estimates, CG buffers
+        bt.assign(x, hi, 0.0)
+        w.owned = bt.owned_dof_count(x, hi)
+        # per cycle: 9 elementwise applies per level l > lo (2+2 Chebyshev(2)
+        # sweeps of 2 applies, plus the residual) and 50 + 1 on the coarse level
+        byts = flps = 0.0
+        for l in range(lo, hi + 1):
+            sl = g.space_size(0, l)
+            micro = g.n_cells() * 8 ** l
+            na = 9 if l > lo else 51
+            byts += na * 16.0 * sl
+            flps += na * float(EW_FLOPS_PER_MICROCELL * micro + EW_FLOPS_PER_ANCHOR * sl)
+        w.bytes, w.flops = byts, flps
+        w.dofs_per_step = w.owned
+        w.kernel = "V-cycle (k_ew applies dominate)"
+
+        def run():
+            bt.v_cycle(h, hi, rhs, x, sm, mg)
+        xs = [bt.allocate(bt.p1_space(), g, hi, hi) for _ in range(1)]
+
+        def apply_b(b):
+            bt.assign(x, hi, 0.0)
+            bt.copy(xs[0], rhs, hi)
+            bt.v_cycle(h, hi, rhs, x, sm, mg)
+        xs[0].values[hi].copy_(rhs.values[hi])
+        w.e2e = (apply_b, [xs[0].values[hi]] * 2, [x.values[hi]] * 2)
+        w.check = None
+        w.keep = (g, h, rhs, x, xs)
+        w.hist_fn = (h, rhs, x, hi)
+        w.config = {"workload": WORKLOADS[5], "levels": f"{lo}->{hi}", "cells": g.n_cells(),
+                    "fine_slots": g.space_size(0, hi), "fine_owned_dofs": w.owned, "coarse_maxit": 50,
+                    "coarse_tol": 0.0, "smoother": "Chebyshev(2)-Jacobi V(2,2)",
+                    "note": "full config 5 is L2->8 (70 GB per vector): multi-GPU only; this is the largest "
+                            "single-GPU instance of the family",
+                    "roofline_model": "per cycle 9 applies per level > 2 and 51 on level 2, each max(16 B/slot at "
+                                      "HBM, elementwise flops at fp64); vector passes and transfers not counted"}
+    w.run = run
+    return w
+
+
+def run_config(cfg, args, bt, torch, ws, rank, hbm, fp64, extra=False):
+    stream = torch.cuda.current_stream()
+    w = setup_config(cfg, bt, torch, ws, rank)
+    L = bt.api._L
+
+    def step(ev):
+        if ev is not None:
+            ev[0].record(stream)
+        w.run()
+        if ev is not None:
+            ev[1].record(stream)
+
+    K = args.steps if not extra else (3 if cfg == 5 else (20 if cfg == 4 else 100))
+    W = args.warmup if not extra else 3
+    if cfg == 5:
+        K, W = min(K, 5), min(W, 1) if W else 1
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = L.bt_launch_count()
+    total_ms, kern = timed_steps(torch, step, K, max(W, 1 if cfg == 5 else 3), stream, dist_max=ws > 1)
+    launches = int(L.bt_launch_count() - launches0)
+    if getattr(w, "graph_launches", 0):  # graph replays launch the captured kernels without host calls
+        launches = w.graph_launches * K
+    clk = clocks.stop()
+    ms_step = total_ms / K
+    value = w.dofs_per_step / (ms_step * 1e-3) / 1e9  # owned DoFs of the whole job (all ranks)
+    kmean = float(np.mean(kern))
+    rl = roofline(w.bytes, w.flops, kmean * 1e-3, hbm, fp64, w.kernel, kmean, kmean / ms_step)
+    if cfg == 2 and ws == 1:
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+                rl["traffic"] = float(json.load(f)["apply_total"])
+        except Exception:
+            pass
+    # e2e through the public API with host buffers
+    apply_b, xdev, ydev = w.e2e
+    nsteps = 2 if cfg == 5 else (6 if cfg == 4 else max(4, min(20, K)))
+    e2e_ms, bi, bo, hy = e2e_serve(torch, bt, apply_b, xdev, ydev, nsteps, ws)
+    if w.check is not None:
+        assert np.array_equal(hy.numpy(), w.check[0].cpu().numpy()), "e2e result differs from resident run"
+    e2e_value = w.dofs_per_step * nsteps / (e2e_ms * 1e-3) / 1e9
+    out = {"metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": K, "warmup": W,
+           "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (random_fill seed 0, reference mt19937_64 stream)",
+           "config": dict(w.config, config=cfg, parallelism=(
+               f"cells partitioned over {ws} ranks, memory-sharded vectors (NCCL interface exchange)"
+               if ws > 1 else "1 GPU")),
+           "roofline": rl,
+           "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+                   "steps": nsteps, "mode": "pipelined serving loop: H2D / step / D2H of consecutive steps overlap"
+                   + (" (double-buffered)" if cfg in (1, 2, 3) else " (one device buffer pair: H2D of step s+1 waits for the "
+                                                                  "apply of step s)")},
+           "gpu_launches": launches, "clocks": clk}
+    if cfg == 5:
+        h, rhs, x, hi = w.hist_fn
+        r = bt.allocate(bt.p1_space(), h.grid, hi, hi)
+        bt.assign(x, hi, 0.0)
+        hist = []
+        nb = bt.norm2(rhs, hi)
+        sm = bt.SmootherConfig.chebyshev(2)
+        sm.nu1 = sm.nu2 = 2
+        mg = bt.MultigridConfig(coarse_level=2, cycles=1, coarse_tol=0.0, coarse_maxit=50)
+        for _ in range(5):
+            bt.v_cycle(h, hi, rhs, x, sm, mg)
+            bt.hierarchy_apply(h, x, r, hi)
+            r.values[hi].mul_(-1.0).add_(rhs.values[hi])
+            hist.append(bt.norm2(r, hi) / nb)
+        out["config"]["residual_history"] = hist
+        out["config"]["sec_per_cycle"] = ms_step * 1e-3
+    del w
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args):
@@ -187,173 +612,99 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     import paper_2308_01792_b200 as bt
-    from paper_2308_01792_b200 import _lib
 
-    dev = torch.cuda.current_device()
-    if ws > 1:
-        text = bt.box_mesh_text(ws, 1, 1)
-        workload = (f"{ws}x1x1 unit cubes x 6 Kuhn macro-tets ({6 * ws} cells, 6 per GPU) L8, P1 const-coeff "
-                    "15-point stencil apply + interface sync (cells partitioned over ranks)")
-    else:
-        text, workload = bt.cube_kuhn_text(), WORKLOAD
-    grid = bt.Grid(text, LEVEL, LEVEL, device=dev)
-    if ws > 1:
-        grid.set_partition(rank, ws)
-    table = bt.compute_stencil(bt.FormId.diffusion(), grid, LEVEL)
-    x = bt.allocate(bt.p1_space(), grid)
-    y = bt.allocate(bt.p1_space(), grid)
-    bt.random_fill(x, LEVEL, 0)
-    owned = bt.owned_dof_count(x, LEVEL)  # whole job
-    cs = bt.n_tet((1 << LEVEL) + 1)
-    _, _, c_begin, c_end = grid.partition()
-    slots = (c_end - c_begin) * cs  # this rank's slots
-    L = _lib.lib
-    stream = torch.cuda.current_stream()
-    sp = bt.api._stream()
-    xp, yp = bt.api._ptr(x.values[LEVEL]), bt.api._ptr(y.values[LEVEL])
-
-    def step(ev=None):
-        # events bracket the device work of one apply: on 1 GPU the whole
-        # apply_stencil (interior kernel || fused boundary kernel incl. the
-        # replica sums); on N GPUs the whole partitioned apply, exchange included
-        if ev is not None:
-            ev[0].record(stream)
-        # N > 1: per-cell rows with the NCCL interface exchange overlapped with the interior marches
-        bt.api._check(L.bt_apply_stencil(table.handle, xp, yp, 0, sp))
-        if ev is not None:
-            ev[1].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    K = args.steps
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(dev)
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    time.sleep(0.3)
-    launches0 = L.bt_launch_count()
-    t_start.record(stream)
-    for q in range(K):
-        step(evs[q])
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    launches = L.bt_launch_count() - launches0
-    clk = clocks.stop()
-    total_ms = t_start.elapsed_time(t_end)
-    kern_ms = [a.elapsed_time(b) for a, b in evs]
-    if ws > 1:
-        t = torch.tensor([total_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_step = total_ms / K
-    value = owned * K / (total_ms * 1e-3) / 1e9
-    kmean = float(np.mean(kern_ms))
-    peak, peak_kind = measured_peaks()
-    traffic = None  # DRAM bytes per apply from the committed ncu capture (profiles/r1_traffic.json)
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            traffic = float(json.load(f)["apply_total"]) if ws == 1 else None
-    except Exception:
-        traffic = None
-    alg_bytes = 16.0 * slots  # read x once, write y once
-    achieved = alg_bytes / (kmean * 1e-3) / 1e9
-
-    # e2e through the public API, as a pipelined serving loop: every step
-    # copies its inputs pinned host -> device and its result device -> pinned
-    # host; consecutive steps overlap on three streams (H2D of step s+1, apply
-    # of step s, D2H of step s-1 — PCIe is full duplex), double-buffered.
-    # (per rank: its own cells' vector — a partitioned grid stores only those)
-    lo, hi = 0, slots
-    assert x.values[LEVEL].numel() == slots
-    hx = torch.empty(slots, dtype=torch.float64, pin_memory=True)
-    hx.copy_(x.values[LEVEL][lo:hi].cpu())
-    hys = [torch.empty(slots, dtype=torch.float64, pin_memory=True) for _ in range(2)]
-    xs = [bt.allocate(bt.p1_space(), grid) for _ in range(2)]
-    ys = [bt.allocate(bt.p1_space(), grid) for _ in range(2)]
-    s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_cmp = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
-
-    def serve(nsteps):
-        for q in range(nsteps):
-            b = q & 1
-            with torch.cuda.stream(s_in):
-                if q >= 2:
-                    s_in.wait_event(ev_cmp[b])  # the apply of step q-2 has read xs[b]
-                xs[b].values[LEVEL][lo:hi].copy_(hx, non_blocking=True)
-                ev_in[b].record(s_in)
-            with torch.cuda.stream(s_cmp):
-                s_cmp.wait_event(ev_in[b])
-                if q >= 2:
-                    s_cmp.wait_event(ev_out[b])  # the D2H of step q-2 has read ys[b]
-                bt.apply_stencil(table, xs[b], ys[b], LEVEL)
-                ev_cmp[b].record(s_cmp)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_cmp[b])
-                hys[b].copy_(ys[b].values[LEVEL][lo:hi], non_blocking=True)
-                ev_out[b].record(s_out)
-
-    e2e_steps = max(4, min(20, K))
-    serve(4)  # warm-up
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s_in)
-    serve(e2e_steps)
-    s_out.wait_event(ev_out[(e2e_steps - 1) & 1])
-    e1.record(s_out)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if ws > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    hy = hys[(e2e_steps - 1) & 1]
-    assert np.array_equal(hy.numpy(), y.values[LEVEL][lo:hi].cpu().numpy()), "e2e result differs from resident run"
-    e2e_value = owned * e2e_steps / (e2e_ms * 1e-3) / 1e9
-
+    cfg = args.config
+    if ws > 1 and cfg != 2:
+        raise SystemExit("bench.py: N > 1 runs config 2 (weak-scaled); other configs are single-GPU here")
+    hbm, _ = measured_hbm()
+    fp64 = measure_fp64(bt, torch)
+    line = run_config(cfg, args, bt, torch, ws, rank, hbm, fp64)
     if rank == 0:
-        cpu = cpu_baseline_sample() if ws == 1 and not args.no_cpu else None
-        line = {
-            "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (random_fill seed 0, reference mt19937_64 stream)",
-            "config": {"workload": workload, "level": LEVEL, "cells": grid.n_cells(), "slots_per_gpu": slots,
-                       "owned_dofs": owned, "bc": "none",
-                       "l2": "inputs larger than L2 (x+y = %.0f MB per GPU)" % (alg_bytes / 1e6),
-                       "parallelism": f"cells partitioned over {ws} ranks, memory-sharded vectors (NCCL interface exchange)"
-                       if ws > 1 else "1 GPU"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_stencil_fast || k_boundary" if ws == 1 else "k_stencil (per-cell rows)",
-                         "kernel_ms": kmean, "kernel_share": kmean / ms_step,
-                         "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs (copy)",
-                         "algorithmic_bytes_per_launch": alg_bytes},
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * slots,
-                    "d2h_bytes_per_step": 8 * slots, "steps": e2e_steps,
-                    "mode": "pipelined serving loop: H2D / apply / D2H of consecutive steps overlap (double-buffered)"},
-            "gpu_launches": int(launches),
-            "clocks": clk,
-        }
+        line["fp64_peak_tflops_measured"] = fp64
+        line["cpu_baseline"] = None if (ws > 1 or args.no_cpu) else cpu_baseline(cfg)
+        if ws == 1 and not args.no_extra:
+            others = {}
+            for c in (1, 2, 3, 4, 5):
+                if c == cfg:
+                    continue
+                try:
+                    o = run_config(c, args, bt, torch, 1, 0, hbm, fp64, extra=True)
+                    o["cpu_baseline"] = None if args.no_cpu else cpu_baseline(c)
+                    for k in ("metric", "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "n_gpus"):
+                        o.pop(k, None)
+                    others[str(c)] = o
+                except Exception as e:  # noqa: BLE001 - reported in the line, the headline stands
+                    others[str(c)] = {"error": f"{type(e).__name__}: {e}"}
+                    torch.cuda.empty_cache()
+            line["configs"] = others
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
+def run_reference(args):
+    """The reference CPU path (oracle/_ref, unmodified blocktet headers) on
+    the host cores, same config / metric; rank 0 only. Buffers are allocated
+    and loaded once (ref_time_apply); each step's time is the median of the
+    K applies it times internally, with K bounded so the run stays within
+    about a minute."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = args.config
+    po = _pyoracle()
+    nproc = os.cpu_count() or 1
+    try:
+        if cfg in (1, 2):
+            lvl = 6 if cfg == 1 else 8
+            text = po.ref_tet_text() if cfg == 1 else po.cube_kuhn_text()
+            threads = 1 if cfg == 1 else min(6, nproc)  # the reference parallelises over macro-cells only
+            r = po.Reference(text, lvl, lvl)
+            x = r.random_fill(lvl, 0)
+            owned = r.owned_count(lvl)
+            first = r.time_apply(lvl, x, kind=0, form=0, bc=int(cfg == 1), reps=1, threads=threads)
+            K = max(1, min(args.steps, int(45.0 / max(first, 1e-4))))
+            sec = r.time_apply(lvl, x, kind=0, form=0, bc=int(cfg == 1), reps=K, threads=threads)
+            if cfg == 1:
+                sec, owned = 11 * sec, 11 * owned
+        elif cfg == 3:
+            r = po.Reference(po.cubes_mesh_text(4, 0.1, 0), 6, 6)
+            x = r.random_fill(6, 0)
+            owned = r.owned_count(6)
+            threads = nproc
+            first = r.time_apply(6, x, kind=1, form=2, kp=po.kparams(), bc=0, reps=1, threads=threads)
+            K = max(1, min(args.steps, int(45.0 / max(first, 1e-4))))
+            sec = r.time_apply(6, x, kind=1, form=2, kp=po.kparams(), bc=0, reps=K, threads=threads)
+        else:
+            print(json.dumps({"impl": "reference", "config": cfg,
+                              "unavailable": "config 4 has no reference operator (N1E1 absent upstream); config 5 "
+                                             "at this size exceeds the host (reduced instance in the ours line)"}))
+            return
+    except (FileNotFoundError, OSError) as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
+        return
+    value = owned / sec / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": args.gpus,
+            "steps": K, "warmup": 1, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_fill seed 0)",
+            "config": {"workload": WORKLOADS[cfg], "config": cfg, "threads": threads, "cpu": cpu_model()},
+            "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": "reference",
+                             "cpu": cpu_model(),
+                             "sample": f"median of {K} applies (buffers allocated and loaded once), {threads} "
+                                       f"threads of {nproc} host cores"},
+            "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline samples")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configs' sub-lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -74,6 +74,12 @@ const char* bt_version(void);
 /* Number of kernel launches issued by this process so far (instrumentation
  * for bench.py's gpu_launches claim). */
 uint64_t bt_launch_count(void);
+/* Measurement utility (not a reference interface): `blocks` x 256 threads each
+ * issue 16 independent fp64 FMA chains of `iters` steps (16 * iters DFMA per
+ * thread) on `stream`; *sink receives a data-dependent sum so nothing is
+ * eliminated. bench.py times it with CUDA events to measure the FP64 peak that
+ * the FP64-bound rooflines (configs 3 and 5) are quoted against. */
+bt_status bt_dfma_probe(int blocks, int iters, double* sink, void* stream);
 
 /* ---- index algebra (micro_index.hpp:85-165, host side) ------------------ */
 int64_t bt_n_tri(int64_t w);                                /* :85 */

@@ -51,6 +51,7 @@ SIGNATURES = {
     "bt_last_error": (C.c_char_p, []),
     "bt_version": (C.c_char_p, []),
     "bt_launch_count": (C.c_uint64, []),
+    "bt_dfma_probe": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "bt_n_tri": (I64, [I64]),
     "bt_n_tet": (I64, [I64]),
     "bt_width_formula": (I, [I, I]),

@@ -530,6 +530,22 @@ double l2_error_p1(const bt_grid& g, int level, const double* x, const bt_field&
   return std::sqrt(acc);
 }
 
+// FP64 FMA throughput probe (bt_dfma_probe): 16 independent chains per thread
+__global__ void __launch_bounds__(256) k_dfma_probe(int iters, double* sink) {
+  double a[16];
+  const double m = 1.0 - 1e-9 * (threadIdx.x & 7), c = 1e-12 * (blockIdx.x & 3);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) a[q] = 1.0 + q * 1e-3 + threadIdx.x * 1e-6;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) a[q] = fma(a[q], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) s += a[q];
+  if (s == 12345.678) sink[0] = s;  // never true; keeps the chains alive
+}
+
 static void validate_field(const bt_field* f) {
   if (!f) raise(BT_INVALID_ARGUMENT, "a field is required");
   if (f->kind < 0 || f->kind > 2) raise(BT_INVALID_ARGUMENT, "field kind must be 0, 1 or 2");
@@ -793,3 +809,12 @@ bt_status bt_restrict(const bt_grid* g, int fine_level, const double* fine, doub
 }
 
 }  // extern "C"
+
+extern "C" bt_status bt_dfma_probe(int blocks, int iters, double* sink, void* stream) {
+  BT_TRY
+  if (blocks < 1 || iters < 1 || !sink) bt::raise(BT_INVALID_ARGUMENT, "dfma_probe: blocks, iters >= 1 and a sink");
+  bt::k_dfma_probe<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, sink);
+  bt::count_launch();
+  bt::check_launch("k_dfma_probe");
+  BT_CATCH
+}
