@@ -375,6 +375,15 @@ struct CgState {
   int it, done, breakdown;
 };
 void launch_cg_init(CgState* st, double tol, cudaStream_t s);
+// fused smoother update (kind 0: first Chebyshev step, 1: later steps, 2: Jacobi)
+void launch_smooth_update(int kind, double* x, double* d, const double* ax, const double* rhs, const double* diag,
+                          double c1, double c2, int64_t n, cudaStream_t s);
+// device-resident estimate_lambda_max scalars
+struct LamState {
+  double num, den, nn2, rho, inv;
+  int done, empty;
+};
+void launch_lam_step(LamState* st, bool first, cudaStream_t s);
 void launch_cg_alpha(CgState* st, cudaStream_t s);
 void launch_cg_update(CgState* st, double tol, double* hist, cudaStream_t s);
 void launch_vec_dev(int op, double* y, const double* x, const double* a, const int* done, int64_t n, cudaStream_t s);

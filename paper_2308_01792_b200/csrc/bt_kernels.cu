@@ -237,6 +237,69 @@ __global__ void __launch_bounds__(kThreads) k_vec_dev(double* __restrict__ y, co
     else y[q] = __dadd_rn(y[q], __dmul_rn(av, x[q]));
   }
 }
+// Fused Chebyshev / Jacobi update (chebyshev_apply solvers.hpp:425-456,
+// smooth 460-492): from ax = A x (Dirichlet identity rows, synced),
+//   r = D^-1 (rhs - A x)          (scale(r, -1); axpy(r, 1, rhs); hadamard /)
+//   KIND 0 (Chebyshev, first):  d = r * c1                (copy; scale 1/theta)
+//   KIND 1 (Chebyshev, later):  d = d * c1 + c2 * r       (scale rho' rho; axpy 2 rho'/delta)
+//   KIND 2 (Jacobi):            d = c2 * r (not stored)   (axpy omega)
+//   x = x + d
+// one pass instead of 6 to 7 streaming passes, every step rounded as the
+// reference's separate vector operations round it (bitwise the unfused path)
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) k_smooth_update(double* __restrict__ x, double* __restrict__ d,
+                                                            const double* __restrict__ ax,
+                                                            const double* __restrict__ rhs,
+                                                            const double* __restrict__ diag, double c1, double c2,
+                                                            int64_t n) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const double r = __ddiv_rn(__dadd_rn(__dmul_rn(ax[q], -1.0), __dmul_rn(1.0, rhs[q])), diag[q]);
+    double dn;
+    if (KIND == 0) dn = __dmul_rn(r, c1);
+    else if (KIND == 1) dn = __dadd_rn(__dmul_rn(d[q], c1), __dmul_rn(c2, r));
+    else dn = __dmul_rn(c2, r);
+    if (KIND != 2) d[q] = dn;
+    x[q] = __dadd_rn(x[q], KIND == 2 ? dn : __dmul_rn(1.0, dn));
+  }
+}
+
+void launch_smooth_update(int kind, double* x, double* d, const double* ax, const double* rhs, const double* diag,
+                          double c1, double c2, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  const int blocks = (int)std::min<int64_t>(ceil_div(n, kThreads), (int64_t)148 * 8);
+  if (kind == 0) k_smooth_update<0><<<blocks, kThreads, 0, s>>>(x, d, ax, rhs, diag, c1, c2, n);
+  else if (kind == 1) k_smooth_update<1><<<blocks, kThreads, 0, s>>>(x, d, ax, rhs, diag, c1, c2, n);
+  else k_smooth_update<2><<<blocks, kThreads, 0, s>>>(x, d, ax, rhs, diag, c1, c2, n);
+  count_launch();
+  check_launch("k_smooth_update");
+}
+
+// estimate_lambda_max scalars on the device (solvers.hpp:140-172): after the
+// dots num = v.w, den = v.z, nn2 = v.v: rho = num / den, and the scale 1/||v||
+// (or stop once ||v|| == 0, where the reference breaks out of its loop)
+__global__ void k_lam_step(LamState* st) {
+  if (st->done) return;
+  st->rho = st->num / st->den;
+  const double nn = sqrt(st->nn2);
+  if (nn == 0) {
+    st->done = 1;
+    return;
+  }
+  st->inv = 1.0 / nn;
+}
+__global__ void k_lam_norm(LamState* st) {  // the start vector's normalisation
+  const double nv = sqrt(st->nn2);
+  st->empty = nv == 0 ? 1 : 0;
+  st->inv = nv == 0 ? 0.0 : 1.0 / nv;
+  st->done = 0;
+  st->rho = 0.0;
+}
+void launch_lam_step(LamState* st, bool first, cudaStream_t s) {
+  if (first) k_lam_norm<<<1, 1, 0, s>>>(st);
+  else k_lam_step<<<1, 1, 0, s>>>(st);
+  count_launch();
+}
+
 void launch_cg_init(CgState* st, double tol, cudaStream_t s) {
   k_cg_init<<<1, 1, 0, s>>>(st, tol);
   count_launch();

@@ -19,9 +19,13 @@ struct LevelData {
   DevBuf<EwCell> ew;                    // elementwise kernel tables
   DevBuf<double> diag;
   double lambda = 0.0;
-  // work vectors
+  // work vectors, allocated on first use (need()): the finest level of a
+  // V-cycle holds only r (the smoother's A x), d (the Chebyshev direction)
+  // and tmp (the residual); b, x serve as the coarse problem of the level
+  // above; p, ap, z as CG and spectral-estimate vectors
   DevBuf<double> r, d, p, ap, z, b, x, tmp;
   DevBuf<CgState> cg;                   // CG scalars (device-resident)
+  DevBuf<LamState> lam;                 // estimate_lambda_max scalars (device-resident)
   DevBuf<double> cg_hist;               // CG residual history (grown on demand)
 };
 
@@ -42,6 +46,15 @@ struct bt_hierarchy {
 };
 
 namespace bt {
+
+// a level's work vector, allocated (zeroed) on first use
+static double* need(DevBuf<double>& b, int64_t n) {
+  if (!b.p && n > 0) {
+    b.alloc((size_t)n);  // (inside a graph capture this fails: run once before capturing)
+    BT_CUDA(cudaMemset(b.p, 0, sizeof(double) * (size_t)n));
+  }
+  return b.p;
+}
 
 static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int bc, cudaStream_t s) {
   LevelData& L = h.at(l);
@@ -64,47 +77,49 @@ static double dot(bt_hierarchy& h, int l, const double* x, const double* y, cuda
   return dot_p1(*h.grid, l, x, y, s);
 }
 
-// estimate_lambda_max (solvers.hpp:140-172) through spectral_estimate (:362)
+// estimate_lambda_max (solvers.hpp:140-172) through spectral_estimate (:362).
+// The scalars stay on the device (LamState; one host read at the end), the
+// iterate in the level's p / ap / z vectors.
 static double lambda_max(bt_hierarchy& h, int l, cudaStream_t s) {
   LevelData& L = h.at(l);
   if (L.lambda != 0.0) return L.lambda;
   const int64_t n = L.n;
-  double* v = L.p.p;
-  double* w = L.ap.p;
-  double* z = L.z.p;
+  double* v = need(L.p, n);
+  double* w = need(L.ap, n);
+  double* z = need(L.z, n);
+  if (!L.lam.p) L.lam.alloc(1);
+  LamState* S = L.lam.p;
   BT_CUDA(cudaStreamSynchronize(s));
   if (bt_random_fill(h.grid, BT_SPACE_P1, l, 0x51cbu, v, s) != BT_OK) raise(BT_CUDA_ERROR, bt_last_error());
   if (h.grid->part_nranks > 1) sync(*h.grid, l, IF_BCAST, v, nullptr, s);  // rank-spanning groups
   sync(*h.grid, l, IF_ZERO_DIR, v, nullptr, s);
-  const double nv = std::sqrt(dot(h, l, v, v, s));
-  if (nv == 0) raise(BT_RUNTIME_ERROR, "estimate_lambda_max: empty free space");
-  launch_vec(V_SCALE, v, nullptr, 1.0 / nv, n, s);
-  double rho = 0;
+  dot_p1_device(*h.grid, l, v, v, &S->nn2, s);
+  launch_lam_step(S, true, s);
+  LamState hs{};
+  BT_CUDA(cudaMemcpyAsync(&hs, S, sizeof(LamState), cudaMemcpyDeviceToHost, s));
+  BT_CUDA(cudaStreamSynchronize(s));
+  if (hs.empty) raise(BT_RUNTIME_ERROR, "estimate_lambda_max: empty free space");
+  launch_vec_dev(V_SCALE, v, nullptr, &S->inv, &S->done, n, s);
   for (int k = 0; k < 25; ++k) {
     hier_apply(h, l, v, w, 1, s);
     launch_vec(V_COPY, z, v, 0.0, n, s);
     launch_vec(V_MUL, z, L.diag.p, 0.0, n, s);
-    rho = dot(h, l, v, w, s) / dot(h, l, v, z, s);
+    dot_p1_device(*h.grid, l, v, w, &S->num, s);
+    dot_p1_device(*h.grid, l, v, z, &S->den, s);
     launch_vec(V_COPY, v, w, 0.0, n, s);
     launch_vec(V_DIV, v, L.diag.p, 0.0, n, s);
-    const double nn = std::sqrt(dot(h, l, v, v, s));
-    if (nn == 0) break;
-    launch_vec(V_SCALE, v, nullptr, 1.0 / nn, n, s);
+    dot_p1_device(*h.grid, l, v, v, &S->nn2, s);
+    launch_lam_step(S, false, s);  // rho = num / den; 1 / ||v|| (or stop at ||v|| == 0)
+    launch_vec_dev(V_SCALE, v, nullptr, &S->inv, &S->done, n, s);
   }
-  L.lambda = 1.1 * rho;
+  BT_CUDA(cudaMemcpyAsync(&hs, S, sizeof(LamState), cudaMemcpyDeviceToHost, s));
+  BT_CUDA(cudaStreamSynchronize(s));
+  L.lambda = 1.1 * hs.rho;
   return L.lambda;
 }
 
-// r = D^-1 (rhs - A x)   (scale(r,-1); axpy(r,1,rhs); hadamard(r, diag, /))
-static void scaled_residual(bt_hierarchy& h, int l, const double* rhs, const double* x, double* r, cudaStream_t s) {
-  LevelData& L = h.at(l);
-  hier_apply(h, l, x, r, 1, s);
-  launch_vec(V_SCALE, r, nullptr, -1.0, L.n, s);
-  launch_vec(V_AXPY, r, rhs, 1.0, L.n, s);
-  launch_vec(V_DIV, r, L.diag.p, 0.0, L.n, s);
-}
-
-// chebyshev_apply (solvers.hpp:425-456)
+// chebyshev_apply (solvers.hpp:425-456): per step one apply (A x into r), one
+// fused update pass (residual, D^-1, direction, x += d) and the Dirichlet pin
 static void chebyshev(bt_hierarchy& h, const double* rhs, double* x, int l, int order, double a, double b,
                       cudaStream_t s) {
   LevelData& L = h.at(l);
@@ -112,19 +127,15 @@ static void chebyshev(bt_hierarchy& h, const double* rhs, double* x, int l, int 
   const double delta = 0.5 * (b - a);
   const double sigma = theta / delta;
   double rho = 1.0 / sigma;
-  double* r = L.r.p;
-  double* d = L.d.p;
-  scaled_residual(h, l, rhs, x, r, s);
-  launch_vec(V_COPY, d, r, 0.0, L.n, s);
-  launch_vec(V_SCALE, d, nullptr, 1.0 / theta, L.n, s);
-  launch_vec(V_AXPY, x, d, 1.0, L.n, s);
+  double* r = need(L.r, L.n);
+  double* d = need(L.d, L.n);
+  hier_apply(h, l, x, r, 1, s);
+  launch_smooth_update(0, x, d, r, rhs, L.diag.p, 1.0 / theta, 0.0, L.n, s);
   sync(*h.grid, l, IF_IMPOSE, x, rhs, s);
   for (int k = 1; k < order; ++k) {
-    scaled_residual(h, l, rhs, x, r, s);
+    hier_apply(h, l, x, r, 1, s);
     const double rho_new = 1.0 / (2.0 * sigma - rho);
-    launch_vec(V_SCALE, d, nullptr, rho_new * rho, L.n, s);
-    launch_vec(V_AXPY, d, r, 2.0 * rho_new / delta, L.n, s);
-    launch_vec(V_AXPY, x, d, 1.0, L.n, s);
+    launch_smooth_update(1, x, d, r, rhs, L.diag.p, rho_new * rho, 2.0 * rho_new / delta, L.n, s);
     sync(*h.grid, l, IF_IMPOSE, x, rhs, s);
     rho = rho_new;
   }
@@ -144,10 +155,11 @@ static void smooth(bt_hierarchy& h, const bt_smoother_config& c, const double* r
   for (int q = 0; q < sweeps; ++q) {
     if (c.kind == 1) {
       if (h.kernel != 1 || !L.stencil) raise(BT_INVALID_ARGUMENT, "gauss-seidel smoothing requires a stencil table");
-      launch_gs_sweep(*L.stencil, rhs, x, L.r.p, backward != 0, s);
-    } else if (c.kind == 0) {
-      scaled_residual(h, l, rhs, x, L.r.p, s);
-      launch_vec(V_AXPY, x, L.r.p, c.omega, L.n, s);
+      launch_gs_sweep(*L.stencil, rhs, x, need(L.r, L.n), backward != 0, s);
+    } else if (c.kind == 0) {  // damped Jacobi: x += omega D^-1 (rhs - A x), fused
+      double* r = need(L.r, L.n);
+      hier_apply(h, l, x, r, 1, s);
+      launch_smooth_update(2, x, nullptr, r, rhs, L.diag.p, 0.0, c.omega, L.n, s);
       sync(*h.grid, l, IF_IMPOSE, x, rhs, s);
     } else {
       const double lam = lambda_max(h, l, s);
@@ -165,9 +177,9 @@ static int cg(bt_hierarchy& h, int l, double tol, int maxit, const double* rhs, 
   constexpr int kPoll = 8;
   LevelData& L = h.at(l);
   const int64_t n = L.n;
-  double* r = L.r.p;
-  double* p = L.p.p;
-  double* ap = L.ap.p;
+  double* r = need(L.r, n);
+  double* p = need(L.p, n);
+  double* ap = need(L.ap, n);
   // Inside a CUDA-graph capture the host cannot poll: every iteration is
   // recorded and the done flag turns the ones after convergence into no-ops
   // (a breakdown then stops the updates instead of raising).
@@ -233,15 +245,17 @@ static void v_cycle(bt_hierarchy& h, int l, const double* rhs, double* x, const 
   LevelData& L = h.at(l);
   LevelData& C = h.at(l - 1);
   smooth(h, sm, rhs, x, l, sm.nu1, 0, s);
-  double* r = L.tmp.p;
+  double* r = need(L.tmp, L.n);
+  double* cb = need(C.b, C.n);
+  double* cx = need(C.x, C.n);
   hier_apply(h, l, x, r, 1, s);
   launch_vec(V_SCALE, r, nullptr, -1.0, L.n, s);
   launch_vec(V_AXPY, r, rhs, 1.0, L.n, s);
-  launch_restrict(*h.grid, l, r, C.b.p, s);
-  sync(*h.grid, l - 1, IF_ZERO_DIR, C.b.p, nullptr, s);
-  launch_vec(V_ASSIGN, C.x.p, nullptr, 0.0, C.n, s);
-  v_cycle(h, l - 1, C.b.p, C.x.p, sm, mg, s);
-  launch_prolongate(*h.grid, l, C.x.p, x, true, s);
+  launch_restrict(*h.grid, l, r, cb, s);
+  sync(*h.grid, l - 1, IF_ZERO_DIR, cb, nullptr, s);
+  launch_vec(V_ASSIGN, cx, nullptr, 0.0, C.n, s);
+  v_cycle(h, l - 1, cb, cx, sm, mg, s);
+  launch_prolongate(*h.grid, l, cx, x, true, s);
   smooth(h, sm, rhs, x, l, sm.nu2, 1, s);
 }
 
@@ -320,10 +334,7 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
     L->level = l;
     L->n = bt_space_size(g, BT_SPACE_P1, l);
     const size_t n = (size_t)L->n;
-    for (DevBuf<double>* b : {&L->r, &L->d, &L->p, &L->ap, &L->z, &L->b, &L->x, &L->tmp, &L->diag}) {
-      b->alloc(n);
-      BT_CUDA(cudaMemset(b->p, 0, sizeof(double) * n));
-    }
+    need(L->diag, (int64_t)n);  // the work vectors are allocated on first use
     if (kernel == 1) {
       bt_stencil* st = nullptr;
       if (bt_stencil_create(g, form, l, &st) != BT_OK) raise(BT_INVALID_ARGUMENT, bt_last_error());
