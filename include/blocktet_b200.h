@@ -88,10 +88,21 @@ int bt_width_formula(int subgroup, int level);              /* :97 */
 bt_status bt_width(int subgroup, int level, int* out);      /* :125 (domain_error if absent) */
 int64_t bt_linearize(int w, int i, int j, int k);           /* :145 */
 bt_status bt_delinearize(int w, int64_t t, int* ijk3);      /* :157 */
+/* linearize_checked (:150-154): BT_OUT_OF_RANGE outside I_tet(w) */
+bt_status bt_linearize_checked(int w, int i, int j, int k, int64_t* out);
+/* linearize_aos / linearize_soa (:167-175): m * t + d / d * n_tet(w) + t;
+ * BT_OUT_OF_RANGE for d outside [0, m) or p outside I_tet(w) */
+bt_status bt_linearize_aos(int w, int m, int i, int j, int k, int d, int64_t* out);
+bt_status bt_linearize_soa(int w, int m, int i, int j, int k, int d, int64_t* out);
 int bt_subgroup_offsets(int subgroup, int* out_xyz);        /* :257, returns arity */
 
 /* ---- grid (Grid ctor fe_function.hpp:106-115 over parse_mesh
  *      coarse_mesh.hpp:225) ------------------------------------------------ */
+/* parse_mesh (coarse_mesh.hpp:225-308) with validate_and_finalize's
+ * orientation repair: vertex coordinates (3 per vertex) and cell vertex ids
+ * (4 per cell, after repair). Pass NULL arrays to query the counts. */
+bt_status bt_mesh_parse(const char* mesh_text, int* n_vertices, int* n_cells, double* coords, int* cells,
+                        int* n_warnings);
 /* Parses the reference mesh text format, builds the implicit interface
  * tables for levels [min_level, max_level] on CUDA device `device`.
  * Levels 2..10 (the reference caps at 6, fe_function.hpp:108). */

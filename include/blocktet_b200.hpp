@@ -17,11 +17,23 @@
 //   make_hierarchy / hierarchy_apply / spectral_estimate    solvers.hpp:323-371
 //   SmootherConfig / smooth / MultigridConfig / v_cycle     solvers.hpp:379-541
 //
+//   parse_mesh / CoarseMesh / Grid(CoarseMesh, lo, hi)     coarse_mesh.hpp:37,225; fe_function.hpp:105
+//   Subgroup, linearize(_checked/_aos/_soa), delinearize   micro_index.hpp:22-175
+//   FEFunction::values[l][cell][entry], array, at, offset  fe_function.hpp:232-275
+//   cg(std::function op, ...), estimate_lambda_max(op,...) solvers.hpp:84-172
+//
 // Differences:
-//   - FEFunction levels live in device memory; values(l) downloads a host copy.
+//   - FEFunction levels live in device memory. `values` is a host mirror with
+//     the reference's shape values[level - min][cell][entry]: it is
+//     downloaded when read after a device operation wrote the function, and
+//     uploaded before the next device operation after it was written through
+//     a non-const access. Keep no reference into it across device calls.
+//     Copies of an FEFunction are deep, as the reference's.
 //   - FormId::div_k_grad takes a Coefficient descriptor, not std::function.
-//   - cg takes the hierarchy (its operator is hierarchy_apply with Dirichlet
-//     identity rows, which is what every reference call site passes).
+//   - Device storage exists for P1 and the seven edge subgroups (N1E1); P2
+//     allocates (sizes as the reference) but its syncs/dots are not on the
+//     device path.
+//   - Grid levels 2..10 (the reference caps at 6, fe_function.hpp:108).
 //   - threads arguments are accepted and ignored (work is stream-ordered).
 #ifndef BLOCKTET_B200_HPP
 #define BLOCKTET_B200_HPP
@@ -31,6 +43,8 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -55,27 +69,137 @@ inline void check(bt_status s) {
   }
 }
 
-// ---- index algebra (micro_index.hpp:85-165) -------------------------------
+// ---- index algebra (micro_index.hpp:22-175) -----------------------------------
+enum class Subgroup : std::uint8_t {
+  V = 0,
+  EdgeX, EdgeY, EdgeZ, EdgeXY, EdgeXZ, EdgeYZ, EdgeXYZ,
+  FaceZUp, FaceZDown, FaceYUp, FaceYDown, FaceXUp, FaceXDown,
+  FaceXYZUp, FaceXYZDown, FaceXYUp, FaceXYDown, FaceYZUp, FaceYZDown,
+  CellIUp, CellIDown, CellIIUp, CellIIDown, CellIIIUp, CellIIIDown,
+};
+enum class MicroKind : std::uint8_t { Vertex, Edge, Face, Cell };
+constexpr MicroKind subgroup_kind(Subgroup g) {
+  return (int)g == 0 ? MicroKind::Vertex : ((int)g <= 7 ? MicroKind::Edge : ((int)g <= 19 ? MicroKind::Face : MicroKind::Cell));
+}
+using Idx3 = std::array<int, 3>;
 inline std::int64_t n_tri(std::int64_t w) { return bt_n_tri(w); }
 inline std::int64_t n_tet(std::int64_t w) { return bt_n_tet(w); }
 inline int width_formula(int subgroup, Level l) { return bt_width_formula(subgroup, l); }
+inline int width_formula(Subgroup g, Level l) { return bt_width_formula((int)g, l); }
 inline int width(int subgroup, Level l) {
   int w = 0;
   check(bt_width(subgroup, l, &w));
   return w;
 }
+inline int width(Subgroup g, Level l) { return width((int)g, l); }
 inline std::int64_t linearize(int w, int i, int j, int k) { return bt_linearize(w, i, j, k); }
-inline std::array<int, 3> delinearize(int w, std::int64_t t) {
-  std::array<int, 3> p{};
+inline std::int64_t linearize(int w, Idx3 p) { return bt_linearize(w, p[0], p[1], p[2]); }
+inline std::int64_t linearize_checked(int w, Idx3 p) {
+  std::int64_t t = 0;
+  check(bt_linearize_checked(w, p[0], p[1], p[2], &t));
+  return t;
+}
+inline std::int64_t linearize_aos(int w, int m, Idx3 p, int d) {
+  std::int64_t t = 0;
+  check(bt_linearize_aos(w, m, p[0], p[1], p[2], d, &t));
+  return t;
+}
+inline std::int64_t linearize_soa(int w, int m, Idx3 p, int d) {
+  std::int64_t t = 0;
+  check(bt_linearize_soa(w, m, p[0], p[1], p[2], d, &t));
+  return t;
+}
+inline Idx3 delinearize(int w, std::int64_t t) {
+  Idx3 p{};
   check(bt_delinearize(w, t, p.data()));
   return p;
+}
+
+// ---- coarse mesh (coarse_mesh.hpp:37-47, 225-368) ----------------------------
+struct Vec3 {
+  double x = 0, y = 0, z = 0;
+};
+struct CoarseMesh {
+  std::vector<Vec3> vertex_coords;
+  std::vector<std::array<int, 4>> cells;  // after the orientation repair
+  int n_warnings = 0;
+  int n_vertices() const { return (int)vertex_coords.size(); }
+  int n_cells() const { return (int)cells.size(); }
+  std::string text() const {  // the mesh text format (write_mesh), round-trip exact
+    std::string out = "vertices " + std::to_string(n_vertices()) + "\n";
+    char buf[96];
+    for (const Vec3& v : vertex_coords) {
+      std::snprintf(buf, sizeof buf, "%.17g %.17g %.17g\n", v.x, v.y, v.z);
+      out += buf;
+    }
+    out += "cells " + std::to_string(n_cells()) + "\n";
+    for (const auto& c : cells)
+      out += std::to_string(c[0]) + " " + std::to_string(c[1]) + " " + std::to_string(c[2]) + " " +
+             std::to_string(c[3]) + "\n";
+    return out;
+  }
+};
+inline CoarseMesh parse_mesh(const std::string& text) {
+  int nv = 0, nc = 0, nw = 0;
+  check(bt_mesh_parse(text.c_str(), &nv, &nc, nullptr, nullptr, &nw));
+  std::vector<double> xyz(3 * (size_t)nv);
+  std::vector<int> cells(4 * (size_t)nc);
+  check(bt_mesh_parse(text.c_str(), &nv, &nc, xyz.data(), cells.data(), &nw));
+  CoarseMesh m;
+  m.n_warnings = nw;
+  for (int v = 0; v < nv; ++v) m.vertex_coords.push_back({xyz[3 * v], xyz[3 * v + 1], xyz[3 * v + 2]});
+  for (int c = 0; c < nc; ++c) m.cells.push_back({cells[4 * c], cells[4 * c + 1], cells[4 * c + 2], cells[4 * c + 3]});
+  return m;
+}
+inline std::string ref_tet_text() {  // coarse_mesh.hpp:335-341
+  return "# reference tetrahedron\nvertices 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ncells 1\n0 1 2 3\n";
+}
+inline std::string cube_kuhn_text() {  // coarse_mesh.hpp:344-368: six tets around the (0,0,0)-(1,1,1) diagonal
+  std::string out = "# unit cube, six tetrahedra around the main diagonal\nvertices 8\n";
+  for (int v = 0; v < 8; ++v)
+    out += std::to_string(v & 1) + " " + std::to_string((v >> 1) & 1) + " " + std::to_string((v >> 2) & 1) + "\n";
+  out += "cells 6\n";
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  for (const auto& a : perms) {
+    int c[4] = {0, 1 << a[0], (1 << a[0]) | (1 << a[1]), 7};
+    double e[3][3];
+    for (int q = 0; q < 3; ++q)
+      for (int d = 0; d < 3; ++d) e[q][d] = (double)((c[q + 1] >> d) & 1);
+    const double vol = e[0][0] * (e[1][1] * e[2][2] - e[1][2] * e[2][1]) -
+                       e[0][1] * (e[1][0] * e[2][2] - e[1][2] * e[2][0]) +
+                       e[0][2] * (e[1][0] * e[2][1] - e[1][1] * e[2][0]);
+    if (vol < 0) std::swap(c[2], c[3]);
+    out += std::to_string(c[0]) + " " + std::to_string(c[1]) + " " + std::to_string(c[2]) + " " +
+           std::to_string(c[3]) + "\n";
+  }
+  return out;
 }
 
 // ---- grid (fe_function.hpp:92) ---------------------------------------------
 class Grid {
  public:
-  Grid(const std::string& mesh_text, Level min_level, Level max_level, int device = 0) {
-    check(bt_grid_create(mesh_text.c_str(), min_level, max_level, device, &g_));
+  struct Member {  // fe_function.hpp:94-99
+    int cell;
+    Subgroup g;
+    std::int64_t t;
+  };
+  Grid(const std::string& mesh_text, Level min_level, Level max_level, int device = 0)
+      : Grid(parse_mesh(mesh_text), min_level, max_level, device) {}
+  Grid(CoarseMesh mesh, Level min_level, Level max_level, int device = 0) : mesh_(std::move(mesh)) {
+    check(bt_grid_create(mesh_.text().c_str(), min_level, max_level, device, &g_));
+  }
+  const CoarseMesh& mesh() const { return mesh_; }
+  // the interface groups of a level (P1; members sorted (cell, g, t), first = owner)
+  std::vector<std::vector<Member>> groups(Level l) const {
+    std::int64_t ng = 0, nm = 0;
+    check(bt_grid_groups(g_, l, BT_SPACE_P1, &ng, &nm, nullptr, nullptr, nullptr, nullptr));
+    std::vector<std::int64_t> off((size_t)ng + 1), t((size_t)nm);
+    std::vector<std::int32_t> cell((size_t)nm), sg((size_t)nm);
+    check(bt_grid_groups(g_, l, BT_SPACE_P1, &ng, &nm, off.data(), cell.data(), sg.data(), t.data()));
+    std::vector<std::vector<Member>> out((size_t)ng);
+    for (std::int64_t q = 0; q < ng; ++q)
+      for (std::int64_t m = off[q]; m < off[q + 1]; ++m) out[q].push_back({cell[m], (Subgroup)sg[m], t[m]});
+    return out;
   }
   ~Grid() { bt_grid_destroy(g_); }
   Grid(const Grid&) = delete;
@@ -94,6 +218,7 @@ class Grid {
   }
 
  private:
+  CoarseMesh mesh_;
   bt_grid* g_ = nullptr;
 };
 inline std::shared_ptr<const Grid> make_grid(const std::string& mesh_text, Level min_level, Level max_level,
@@ -115,42 +240,149 @@ inline std::string cubes_mesh_text(int n, double perturb = 0.1, std::uint64_t se
   return s;
 }
 
-// ---- spaces and functions (fe_function.hpp:31-307) -------------------------
+// ---- spaces and functions (fe_function.hpp:21-307) -------------------------
+enum class LayoutKind : std::uint8_t { AoS, SoA };
 enum class Space : int { P1 = BT_SPACE_P1, P2 = BT_SPACE_P2, Edges = BT_SPACE_EDGES };
 struct SpaceDescriptor {
   std::string name;
-  Space space = Space::P1;
+  std::vector<std::pair<Subgroup, int>> entries;  // (subgroup, DoFs per instance); m = 1 here
+  LayoutKind layout = LayoutKind::AoS;
+  int entry_of(Subgroup g) const {
+    for (std::size_t e = 0; e < entries.size(); ++e)
+      if (entries[e].first == g) return (int)e;
+    return -1;
+  }
+  bool same_space(const SpaceDescriptor& o) const { return entries == o.entries; }
+  Space space() const {
+    if (entries.size() == 1 && entries[0].first == Subgroup::V) return Space::P1;
+    if (entries.size() == 8 && entries[0].first == Subgroup::V) return Space::P2;
+    if (entries.size() == 7 && entries[0].first == Subgroup::EdgeX) return Space::Edges;
+    throw std::invalid_argument("space descriptor: P1, P2 or the seven edge subgroups expected");
+  }
 };
-inline SpaceDescriptor p1_space() { return {"p1", Space::P1}; }
-inline SpaceDescriptor edge_space() { return {"n1e1", Space::Edges}; }
+inline SpaceDescriptor p1_space(LayoutKind layout = LayoutKind::AoS) { return {"p1", {{Subgroup::V, 1}}, layout}; }
+inline SpaceDescriptor p2_space(LayoutKind layout = LayoutKind::AoS) {
+  SpaceDescriptor d{"p2", {{Subgroup::V, 1}}, layout};
+  for (int g = 1; g <= 7; ++g) d.entries.emplace_back((Subgroup)g, 1);
+  return d;
+}
+inline SpaceDescriptor edge_space(LayoutKind layout = LayoutKind::AoS) {  // N1E1 storage
+  SpaceDescriptor d{"n1e1", {}, layout};
+  for (int g = 1; g <= 7; ++g) d.entries.emplace_back((Subgroup)g, 1);
+  return d;
+}
 
 class FEFunction {
  public:
-  FEFunction() = default;
-  FEFunction(SpaceDescriptor d, std::shared_ptr<const Grid> grid, Level lo, Level hi)
-      : descriptor(std::move(d)), grid(std::move(grid)), lo_(lo), hi_(hi) {
+  // Host mirror with the reference's shape: values[level - min][cell][entry].
+  class Values {
+   public:
+    using Level3 = std::vector<std::vector<std::vector<double>>>;
+    Level3& operator[](std::size_t i) {
+      owner_->pull();
+      owner_->host_dirty_ = true;
+      return v_.at(i);
+    }
+    const Level3& operator[](std::size_t i) const {
+      owner_->pull();
+      return v_.at(i);
+    }
+    std::size_t size() const { return (std::size_t)(owner_->hi_ - owner_->lo_ + 1); }
+
+   private:
+    friend class FEFunction;
+    FEFunction* owner_ = nullptr;
+    std::vector<Level3> v_;
+  };
+
+  FEFunction() { values.owner_ = this; }
+  FEFunction(SpaceDescriptor d, std::shared_ptr<const Grid> g, Level lo, Level hi)
+      : descriptor(std::move(d)), grid(std::move(g)), lo_(lo), hi_(hi) {
+    values.owner_ = this;
+    space_ = (int)descriptor.space();
     for (Level l = lo; l <= hi; ++l) {
-      const size_t n = (size_t)bt_space_size(this->grid->handle(), (int)descriptor.space, l);
-      double* p = nullptr;
-      if (cudaMalloc(&p, n * sizeof(double)) != cudaSuccess) throw std::runtime_error("FEFunction: cudaMalloc failed");
-      cudaMemset(p, 0, n * sizeof(double));
-      levels_.emplace_back(p, [](double* q) { cudaFree(q); });
+      const size_t n = (size_t)bt_space_size(grid->handle(), space_, l);
+      levels_.push_back(device_alloc(n));
       sizes_.push_back(n);
     }
   }
+  FEFunction(const FEFunction& o) : descriptor(o.descriptor), grid(o.grid), lo_(o.lo_), hi_(o.hi_), space_(o.space_) {
+    values.owner_ = this;  // deep copy, as the reference's std::vector storage
+    o.push();
+    for (std::size_t q = 0; q < o.levels_.size(); ++q) {
+      levels_.push_back(device_alloc(o.sizes_[q]));
+      sizes_.push_back(o.sizes_[q]);
+      if (cudaMemcpy(levels_.back().get(), o.levels_[q].get(), o.sizes_[q] * sizeof(double),
+                     cudaMemcpyDeviceToDevice) != cudaSuccess)
+        throw std::runtime_error("FEFunction: copy failed");
+    }
+  }
+  FEFunction(FEFunction&& o) noexcept { *this = std::move(o); }
+  FEFunction& operator=(FEFunction&& o) noexcept {
+    descriptor = std::move(o.descriptor);
+    grid = std::move(o.grid);
+    lo_ = o.lo_;
+    hi_ = o.hi_;
+    space_ = o.space_;
+    levels_ = std::move(o.levels_);
+    sizes_ = std::move(o.sizes_);
+    values.v_ = std::move(o.values.v_);
+    values.owner_ = this;
+    host_valid_ = o.host_valid_;
+    host_dirty_ = o.host_dirty_;
+    return *this;
+  }
+  FEFunction& operator=(const FEFunction& o) {
+    if (this != &o) *this = FEFunction(o);
+    return *this;
+  }
+
   Level min_level() const { return lo_; }
   Level max_level() const { return hi_; }
   bool has_level(Level l) const { return l >= lo_ && l <= hi_; }
-  int space() const { return (int)descriptor.space; }
-  // device array of one level (all cells, reference layout)
-  double* device(Level l) { return levels_.at(index(l)).get(); }
-  const double* device(Level l) const { return levels_.at(index(l)).get(); }
-  std::size_t size(Level l) const { return sizes_.at(index(l)); }
-  // host copies (the reference's values[level][cell] as one flat array)
-  std::vector<double> values(Level l) const {
+  int check_level(Level l) const {  // fe_function.hpp:268-272
+    if (!has_level(l)) throw std::out_of_range("level not allocated");
+    return l - lo_;
+  }
+  int space() const { return space_; }
+  int width_of(int entry, Level l) const { return width_formula(descriptor.entries.at((size_t)entry).first, l); }
+  std::int64_t slots_of(int entry, Level l) const {
+    const int w = width_of(entry, l);
+    return w > 0 ? n_tet(w) : 0;
+  }
+  // layout-aware slot offset of (t, d) (fe_function.hpp:257-261)
+  std::int64_t offset(Level l, int entry, std::int64_t t, int d) const {
+    const int m = descriptor.entries.at((size_t)entry).second;
+    return descriptor.layout == LayoutKind::AoS ? m * t + d : d * slots_of(entry, l) + t;
+  }
+  std::vector<double>& array(Level l, int cell, int entry) { return values[(size_t)check_level(l)][cell][entry]; }
+  const std::vector<double>& array(Level l, int cell, int entry) const {
+    return values[(size_t)check_level(l)][cell][entry];
+  }
+  double& at(Level l, int cell, int entry, std::int64_t t, int d) {
+    return array(l, cell, entry).at((size_t)offset(l, entry, t, d));
+  }
+  double at(Level l, int cell, int entry, std::int64_t t, int d) const {
+    return array(l, cell, entry).at((size_t)offset(l, entry, t, d));
+  }
+
+  // device array of one level (all cells of this handle, reference layout).
+  // The non-const form assumes the caller writes it (the host mirror goes stale).
+  double* device(Level l) {
+    push();
+    host_valid_ = false;
+    return levels_.at((size_t)check_level(l)).get();
+  }
+  const double* device(Level l) const {
+    push();
+    return levels_.at((size_t)check_level(l)).get();
+  }
+  std::size_t size(Level l) const { return sizes_.at((size_t)check_level(l)); }
+  // one level as a flat host array (cells in order, entries in order)
+  std::vector<double> level_values(Level l) const {
     std::vector<double> h(size(l));
     if (cudaMemcpy(h.data(), device(l), h.size() * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
-      throw std::runtime_error("FEFunction::values: copy failed");
+      throw std::runtime_error("FEFunction: download failed");
     return h;
   }
   void upload(Level l, const std::vector<double>& h) {
@@ -161,15 +393,73 @@ class FEFunction {
 
   SpaceDescriptor descriptor;
   std::shared_ptr<const Grid> grid;
+  Values values;
 
  private:
-  int index(Level l) const {
-    if (!has_level(l)) throw std::out_of_range("FEFunction: level not allocated");
-    return l - lo_;
+  static std::shared_ptr<double> device_alloc(std::size_t n) {
+    double* p = nullptr;
+    if (n && cudaMalloc(&p, n * sizeof(double)) != cudaSuccess) throw std::runtime_error("FEFunction: cudaMalloc failed");
+    if (n) cudaMemset(p, 0, n * sizeof(double));
+    return std::shared_ptr<double>(p, [](double* q) {
+      if (q) cudaFree(q);
+    });
+  }
+  // per cell of this handle's block: the entries' slot counts (m = 1)
+  std::vector<std::int64_t> entry_slots(Level l) const {
+    std::vector<std::int64_t> e;
+    for (std::size_t q = 0; q < descriptor.entries.size(); ++q) e.push_back(slots_of((int)q, l));
+    return e;
+  }
+  int cells_here() const {
+    int r = 0, n = 0, b = 0, e = 0;
+    check(bt_grid_partition(grid->handle(), &r, &n, &b, &e));
+    return e - b;
+  }
+  // device -> host mirror (when a device operation wrote the function since)
+  void pull() const {
+    if (host_valid_) return;
+    auto& self = const_cast<FEFunction&>(*this);
+    self.values.v_.assign(levels_.size(), {});
+    const int nc = cells_here();
+    for (std::size_t q = 0; q < levels_.size(); ++q) {
+      std::vector<double> flat(sizes_[q]);
+      if (sizes_[q] && cudaMemcpy(flat.data(), levels_[q].get(), sizes_[q] * sizeof(double),
+                                  cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("FEFunction: download failed");
+      const auto es = entry_slots(lo_ + (Level)q);
+      std::size_t pos = 0;
+      auto& lv = self.values.v_[q];
+      lv.assign((size_t)nc, {});
+      for (int c = 0; c < nc; ++c)
+        for (std::int64_t n : es) {
+          lv[c].emplace_back(flat.begin() + (std::ptrdiff_t)pos, flat.begin() + (std::ptrdiff_t)(pos + n));
+          pos += (std::size_t)n;
+        }
+    }
+    self.host_valid_ = true;
+    self.host_dirty_ = false;
+  }
+  // host mirror -> device (when it was written through a non-const access)
+  void push() const {
+    if (!host_dirty_) return;
+    auto& self = const_cast<FEFunction&>(*this);
+    for (std::size_t q = 0; q < levels_.size(); ++q) {
+      std::vector<double> flat;
+      flat.reserve(sizes_[q]);
+      for (const auto& cell : values.v_[q])
+        for (const auto& e : cell) flat.insert(flat.end(), e.begin(), e.end());
+      if (flat.size() != sizes_[q]) throw std::logic_error("FEFunction: host mirror reshaped");
+      if (sizes_[q] && cudaMemcpy(levels_[q].get(), flat.data(), sizes_[q] * sizeof(double),
+                                  cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("FEFunction: upload failed");
+    }
+    self.host_dirty_ = false;
   }
   Level lo_ = 0, hi_ = -1;
+  int space_ = BT_SPACE_P1;
   std::vector<std::shared_ptr<double>> levels_;
   std::vector<std::size_t> sizes_;
+  bool host_valid_ = false, host_dirty_ = false;
 };
 
 inline FEFunction allocate(const SpaceDescriptor& descriptor, std::shared_ptr<const Grid> grid, int min_level = -1,
@@ -410,6 +700,80 @@ inline IterationReport cg(GridHierarchy& h, const FEFunction& rhs, FEFunction& x
   rep.converged = rep.residual <= tol;
   return rep;
 }
+// cg over any operator callable (solvers.hpp:84-131), the reference's
+// algorithm step for step on device vectors; scalars on the host. (The
+// hierarchy overload above keeps the scalars on the device.)
+inline IterationReport cg(const std::function<void(const FEFunction&, FEFunction&)>& apply_op, const FEFunction& rhs,
+                          FEFunction& x, Level l, double tol, int maxit) {
+  detail::require_pair(rhs, x, l);
+  if (!apply_op) throw std::invalid_argument("cg: operator required");
+  FEFunction r = allocate(x.descriptor, x.grid, l, l);
+  FEFunction p = allocate(x.descriptor, x.grid, l, l);
+  FEFunction ap = allocate(x.descriptor, x.grid, l, l);
+  apply_op(x, r);
+  scale(r, l, -1.0);
+  axpy(r, 1.0, rhs, l);
+  copy(r, p, l);
+  const double nb = norm2(rhs, l);
+  const double denom = nb > 0 ? nb : 1.0;
+  double rs = dot(r, r, l);
+  IterationReport report;
+  report.residual = std::sqrt(rs) / denom;
+  if (report.residual <= tol) {
+    report.converged = true;
+    return report;
+  }
+  for (int it = 1; it <= maxit; ++it) {
+    apply_op(p, ap);
+    const double pap = dot(p, ap, l);
+    if (!(pap > 0)) throw std::runtime_error("cg breakdown: operator is not positive definite");
+    const double alpha = rs / pap;
+    axpy(x, alpha, p, l);
+    axpy(r, -alpha, ap, l);
+    const double rs_new = dot(r, r, l);
+    report.iterations = it;
+    report.residual = std::sqrt(rs_new) / denom;
+    report.rows.push_back({l, it, report.residual, 0.0, 0.0});
+    if (report.residual <= tol) {
+      report.converged = true;
+      break;
+    }
+    scale(p, l, rs_new / rs);
+    axpy(p, 1.0, r, l);
+    rs = rs_new;
+  }
+  return report;
+}
+
+// estimate_lambda_max over any operator callable (solvers.hpp:140-172)
+inline double estimate_lambda_max(const std::function<void(const FEFunction&, FEFunction&)>& apply_op,
+                                  const FEFunction& diag, Level l, int iterations = 25) {
+  if (diag.space() != BT_SPACE_P1) throw std::invalid_argument("P1 function required");
+  for (double v : diag.level_values(l))
+    if (v == 0.0) throw std::invalid_argument("estimate_lambda_max: zero diagonal entry");
+  FEFunction v = allocate(diag.descriptor, diag.grid, l, l);
+  FEFunction w = allocate(diag.descriptor, diag.grid, l, l);
+  FEFunction z = allocate(diag.descriptor, diag.grid, l, l);
+  random_fill(v, l, 0x51cbu);
+  zero_dirichlet(v, l);
+  const double nv = norm2(v, l);
+  if (nv == 0) throw std::runtime_error("estimate_lambda_max: empty free space");
+  scale(v, l, 1.0 / nv);
+  double rho = 0;
+  for (int k = 0; k < iterations; ++k) {
+    apply_op(v, w);
+    copy(v, z, l);
+    hadamard(z, diag, l, false);
+    rho = dot(v, w, l) / dot(v, z, l);
+    copy(w, v, l);
+    hadamard(v, diag, l, true);
+    const double nn = norm2(v, l);
+    if (nn == 0) break;
+    scale(v, l, 1.0 / nn);
+  }
+  return 1.1 * rho;
+}
+
 inline void v_cycle(GridHierarchy& h, Level l, const FEFunction& rhs, FEFunction& x, const SmootherConfig& sm,
                     const MultigridConfig& mg) {
   detail::require_pair(rhs, x, l);

@@ -52,6 +52,11 @@ SIGNATURES = {
     "bt_version": (C.c_char_p, []),
     "bt_launch_count": (C.c_uint64, []),
     "bt_dfma_probe": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "bt_linearize_checked": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+    "bt_linearize_aos": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+    "bt_linearize_soa": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+    "bt_mesh_parse": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p, C.c_void_p,
+                                C.POINTER(C.c_int)]),
     "bt_n_tri": (I64, [I64]),
     "bt_n_tet": (I64, [I64]),
     "bt_width_formula": (I, [I, I]),

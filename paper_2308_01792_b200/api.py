@@ -130,10 +130,58 @@ def linearize(w, p):
 
 
 def linearize_checked(w, p):
-    i, j, k = p
-    if not (i >= 0 and j >= 0 and k >= 0 and i + j + k < w):
-        raise OutOfRange("linearize: index outside I_tet(w)")
-    return linearize(w, p)
+    """linearize_checked (micro_index.hpp:150-154): OutOfRange outside I_tet(w)."""
+    out = C.c_int64()
+    _check(_L.bt_linearize_checked(w, int(p[0]), int(p[1]), int(p[2]), C.byref(out)))
+    return out.value
+
+
+def linearize_aos(w, m, p, d):
+    """m * linearize(w, p) + d (micro_index.hpp:167-170)."""
+    out = C.c_int64()
+    _check(_L.bt_linearize_aos(w, m, int(p[0]), int(p[1]), int(p[2]), d, C.byref(out)))
+    return out.value
+
+
+def linearize_soa(w, m, p, d):
+    """d * n_tet(w) + linearize(w, p) (micro_index.hpp:172-175)."""
+    out = C.c_int64()
+    _check(_L.bt_linearize_soa(w, m, int(p[0]), int(p[1]), int(p[2]), d, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class CoarseMesh:
+    """parse_mesh's result (coarse_mesh.hpp:37-47): vertex coordinates and
+    cell vertex ids after the orientation repair; `text` re-serialises it."""
+    vertex_coords: np.ndarray
+    cells: np.ndarray
+    n_warnings: int = 0
+
+    def n_vertices(self):
+        return len(self.vertex_coords)
+
+    def n_cells(self):
+        return len(self.cells)
+
+    @property
+    def text(self):
+        lines = [f"vertices {self.n_vertices()}"]
+        lines += [" ".join(repr(float(c)) for c in v) for v in self.vertex_coords]
+        lines.append(f"cells {self.n_cells()}")
+        lines += [" ".join(str(int(q)) for q in c) for c in self.cells]
+        return "\n".join(lines) + "\n"
+
+
+def parse_mesh(text: str) -> CoarseMesh:
+    """parse_mesh (coarse_mesh.hpp:225-308), with the reference's error messages."""
+    nv, nc, nw = C.c_int(), C.c_int(), C.c_int()
+    _check(_L.bt_mesh_parse(text.encode(), C.byref(nv), C.byref(nc), None, None, C.byref(nw)))
+    xyz = np.zeros((nv.value, 3))
+    cells = np.zeros((nc.value, 4), np.int32)
+    _check(_L.bt_mesh_parse(text.encode(), C.byref(nv), C.byref(nc), xyz.ctypes.data_as(C.c_void_p),
+                            cells.ctypes.data_as(C.c_void_p), C.byref(nw)))
+    return CoarseMesh(xyz, cells, nw.value)
 
 
 def delinearize(w, t):
@@ -180,7 +228,11 @@ class Grid:
     """Grid (fe_function.hpp:92): mesh + per-level interface identification,
     held as implicit macro face/edge/vertex tables on the device."""
 
-    def __init__(self, mesh_text: str, min_level: int, max_level: int, device: Optional[int] = None):
+    def __init__(self, mesh_text, min_level: int, max_level: int, device: Optional[int] = None):
+        """Grid(CoarseMesh, min, max) as the reference (fe_function.hpp:105),
+        or the mesh text directly."""
+        if isinstance(mesh_text, CoarseMesh):
+            mesh_text = mesh_text.text
         if device is None:
             device = torch.cuda.current_device()
         self.device = device
@@ -375,10 +427,12 @@ class FEFunction:
 
     def offset(self, l, entry, t, d=0):
         """Layout-aware slot offset of (t, d) (FEFunction::offset,
-        fe_function.hpp:257-261); every space here has m = 1."""
-        if d != 0:
+        fe_function.hpp:257-261): m t + d (AoS) or d slots + t (SoA); every
+        space here has m = 1 per entry, where the two coincide."""
+        m = 1
+        if not 0 <= d < m:
             raise OutOfRange("linearize: bad DoF index")
-        return int(t)
+        return m * int(t) + d if self.descriptor.layout == LayoutKind.AoS else d * self.slots_of(l, entry) + int(t)
 
     def array(self, l, cell, entry=None):
         """This rank's values of `cell` (and one entry of it): a view into

@@ -657,6 +657,45 @@ bt_status bt_width(int g, int level, int* out) {
   BT_CATCH
 }
 int64_t bt_linearize(int w, int i, int j, int k) { return linearize(w, i, j, k); }
+bt_status bt_linearize_checked(int w, int i, int j, int k, int64_t* out) {
+  BT_TRY
+  if (!out) raise(BT_INVALID_ARGUMENT, "linearize: output required");
+  if (!in_i_tet(w, i, j, k)) raise(BT_OUT_OF_RANGE, "linearize: index outside I_tet(w)");
+  *out = linearize(w, i, j, k);
+  BT_CATCH
+}
+bt_status bt_linearize_aos(int w, int m, int i, int j, int k, int d, int64_t* out) {
+  BT_TRY
+  if (!out) raise(BT_INVALID_ARGUMENT, "linearize_aos: output required");
+  if (d < 0 || d >= m) raise(BT_OUT_OF_RANGE, "linearize_aos: bad DoF index");
+  if (!in_i_tet(w, i, j, k)) raise(BT_OUT_OF_RANGE, "linearize: index outside I_tet(w)");
+  *out = (int64_t)m * linearize(w, i, j, k) + d;
+  BT_CATCH
+}
+bt_status bt_linearize_soa(int w, int m, int i, int j, int k, int d, int64_t* out) {
+  BT_TRY
+  if (!out) raise(BT_INVALID_ARGUMENT, "linearize_soa: output required");
+  if (d < 0 || d >= m) raise(BT_OUT_OF_RANGE, "linearize_soa: bad DoF index");
+  if (!in_i_tet(w, i, j, k)) raise(BT_OUT_OF_RANGE, "linearize: index outside I_tet(w)");
+  *out = (int64_t)d * n_tet(w) + linearize(w, i, j, k);
+  BT_CATCH
+}
+bt_status bt_mesh_parse(const char* text, int* n_vertices, int* n_cells, double* coords, int* cells,
+                        int* n_warnings) {
+  BT_TRY
+  if (!text) raise(BT_INVALID_ARGUMENT, "parse_mesh: text required");
+  const Mesh m = parse_mesh(text);
+  if (n_vertices) *n_vertices = (int)m.coords.size();
+  if (n_cells) *n_cells = m.n_cells();
+  if (n_warnings) *n_warnings = m.warnings;
+  if (coords)
+    for (size_t v = 0; v < m.coords.size(); ++v)
+      for (int d = 0; d < 3; ++d) coords[3 * v + d] = m.coords[v][d];
+  if (cells)
+    for (int c = 0; c < m.n_cells(); ++c)
+      for (int q = 0; q < 4; ++q) cells[4 * c + q] = m.cells[c][q];
+  BT_CATCH
+}
 bt_status bt_delinearize(int w, int64_t t, int* ijk) {
   BT_TRY
   if (t < 0 || t >= n_tet(w)) raise(BT_OUT_OF_RANGE, "delinearize: offset out of range");

@@ -70,8 +70,8 @@ int main(int argc, char** argv) {
     random_fill(x, l, 0);
     const StencilTable t = compute_stencil(FormId::diffusion(), g, l);
     apply_stencil(t, x, y, l, BC::None);
-    dump(dir + "/x.bin", x.values(l));
-    dump(dir + "/y.bin", y.values(l));
+    dump(dir + "/x.bin", x.level_values(l));
+    dump(dir + "/y.bin", y.level_values(l));
     bool invalid = false;
     try {
       apply_stencil(t, x, y, l - 1);  // table built for level l
@@ -91,8 +91,8 @@ int main(int argc, char** argv) {
     mg.coarse_tol = 1e-14;
     mg.coarse_maxit = 20;
     for (int c = 0; c < 3; ++c) v_cycle(h, l, rhs, u, sm, mg);
-    dump(dir + "/rhs.bin", rhs.values(l));
-    dump(dir + "/u.bin", u.values(l));
+    dump(dir + "/rhs.bin", rhs.level_values(l));
+    dump(dir + "/u.bin", u.level_values(l));
     // full multigrid of the model problem (solvers.hpp:547): second-order errors
     const Coefficient uex = Coefficient::sin_product(0.0, 1.0, M_PI);
     const Coefficient f = Coefficient::sin_product(0.0, 3.0 * M_PI * M_PI, M_PI);

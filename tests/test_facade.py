@@ -63,3 +63,27 @@ def test_facade_apply_and_vcycle_match_oracle(exe, tmp_path):
     rhs = load("rhs.bin")
     u, _ = o.vcycles(l, sm.as_array(), rhs, np.zeros_like(rhs), 3, 2, 1e-14, 20)
     assert rel(load("u.bin"), u) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_facade_reference_shaped_call_sites(tmp_path):
+    """tests/cpp/facade_kats.cpp: reference-style call sites (Grid from
+    parse_mesh, values[l][cell][entry], at(), groups(), cg over a callable)
+    against the reference tests' known answers."""
+    out = str(tmp_path / "facade_kats")
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tests", "cpp", "facade_kats.cpp"), "-o", out, "-L", LIBDIR, "-lbt_b200",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,/usr/local/cuda/lib64"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    r = subprocess.run([out], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr + r.stdout
+    assert r.stdout.strip().endswith("ok")
+
+
+def test_facade_kats_compile(tmp_path):
+    """The reference-shaped call sites compile against the facade (no GPU needed)."""
+    out = str(tmp_path / "facade_kats.o")
+    cmd = ["g++", "-std=c++17", "-O1", "-c", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tests", "cpp", "facade_kats.cpp"), "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
