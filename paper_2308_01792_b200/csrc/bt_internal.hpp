@@ -159,11 +159,16 @@ struct XPlan {
   int64_t buf_size = 0;
   std::vector<XEntry> entries;
   DevBuf<XEntry> d_entries;
+  // P1 plans: each entry's lattice point (cell, i, j, k), for the fused
+  // stencil apply, which computes this rank's members' partial rows straight
+  // into the exchange buffer (k_xpartials, bt_stencil.cu)
+  DevBuf<int4> d_pts;
   void reset() {
     built = false;
     buf_size = 0;
     entries.clear();
     d_entries.release();
+    d_pts.release();
   }
 };
 
@@ -354,8 +359,8 @@ void launch_gs_sweep(const bt_stencil& st, const double* rhs, double* x, double*
 // a second stream (per host thread and device) for kernels that run beside
 // the main launch, with fork / join events
 struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t s = nullptr, s2 = nullptr;  // s2: a second side stream (partitioned fused apply)
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
 };
 SideStream& side_stream();
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c, const EwCell* d_cells,

@@ -345,6 +345,7 @@ struct BndArgs {
   const StencilCell* cells;
   int nf, ne, nv, n;
   int64_t cs;
+  int cb, ce;  // this handle's cells: groups with a member outside are skipped (exchanged instead)
 };
 
 __device__ __forceinline__ void bary_ijk(const int8_t* lv, int nl, const int* wt, int& i, int& j, int& k) {
@@ -494,6 +495,12 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
       bary_ijk(pm.lv, nl, wt, i, j, k);
     }
   };
+  // partitioned grid: only groups whose members are all this handle's cells
+  // (the rank-spanning ones go through the exchange, k_xpartials)
+  for (int m = 0; m < count; ++m) {
+    const int c = F ? F->cell[m] : mem[m].cell;
+    if (c < a.cb || c >= a.ce) return;
+  }
   double sum = 0.0, single = 0.0;
   if (F) {  // face point: one or two members, all their loads in flight together
     Gather11 g0, g1;
@@ -531,6 +538,30 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
 template <bool kDir>
 __global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, double* __restrict__ y, BndArgs a) {
   boundary_body<kDir>(x, y, a, blockIdx.x);
+}
+
+// Rank-spanning interface groups of a partitioned fused apply: this rank's
+// members' per-cell partial rows (the same typed rows, in the same operation
+// order, as k_boundary forms them) straight into the exchange buffer; after
+// the ranks' allreduce, k_xcombine sums every group in member order from 0.0,
+// which is k_boundary's replica sum bit for bit.
+__global__ void __launch_bounds__(128) k_xpartials(const double* __restrict__ x, double* __restrict__ buf,
+                                                   const XEntry* __restrict__ e, const int4* __restrict__ pts,
+                                                   int nent, BndArgs a) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nent) return;
+  const int4 P = pts[q];
+  const int z = zero_set(a.n, P.y, P.z, P.w);
+  double v;
+  if (__popc(z) == 1) {  // face point: its 11 present directions
+    Gather11 gt;
+    gather11(x, a, P.x, P.y, P.z, P.w, gt);
+    v = face_row(gt);
+  } else {
+    int64_t slot;
+    v = typed_partial(x, a, P.x, P.y, P.z, P.w, slot);
+  }
+  buf[e[q].buf] = v;
 }
 
 // Small problems (one launch is latency, not bandwidth): the whole fused
@@ -726,8 +757,10 @@ SideStream& side_stream() {
   SideStream& r = ss[dev & 15];
   if (!r.s) {
     BT_CUDA(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
+    BT_CUDA(cudaStreamCreateWithFlags(&r.s2, cudaStreamNonBlocking));
     BT_CUDA(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
     BT_CUDA(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
+    BT_CUDA(cudaEventCreateWithFlags(&r.join2, cudaEventDisableTiming));
   }
   return r;
 }
@@ -747,7 +780,8 @@ static int stencil_parts() {
 // fast kernel launches (interior rows of the N-layer marches in ft) for this
 // handle's cells, on stream s
 template <int N>
-static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double* x, double* y, cudaStream_t s) {
+static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double* x, double* y, cudaStream_t s,
+                        int reserve_sms = 0) {
   if (!ft.ntasks) return;
   const int w = (1 << st.level) + 1;
   const int64_t cs = n_tet(w);
@@ -755,21 +789,23 @@ static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double*
   auto kern = k_stencil_fast<N, kMaxCells>;
   // persistent grid: SMs x resident blocks, per device (set up once)
   static std::mutex mu;
-  static int grids[64] = {0};
+  static int grids[64] = {0}, persm[64] = {0};
   int dev = 0;
   BT_CUDA(cudaGetDevice(&dev));
-  int grid;
+  int grid, per_sm;
   {
     std::lock_guard<std::mutex> lock(mu);
     int& gr = grids[dev & 63];
     if (!gr) {
       BT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int sms = 0, per_sm = 0;
+      int sms = 0, ps = 0;
       BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFT, smem));
-      gr = sms * std::max(1, per_sm);
+      BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, kFT, smem));
+      persm[dev & 63] = std::max(1, ps);
+      gr = sms * persm[dev & 63];
     }
     grid = gr;
+    per_sm = persm[dev & 63];
   }
   FastParams<kMaxCells> fp;  // copied into the launch's parameter buffer
   for (int ch = 0; ch + 1 < (int)ft.chunk_first.size(); ++ch) {
@@ -781,7 +817,8 @@ static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double*
       for (int d = 0; d < 8; ++d) fp.w[c][d] = f[d];
     }
     const int64_t e0 = (int64_t)cc0 * cs;
-    const int blocks = std::min(grid, (nt + kFW - 1) / kFW);
+    // reserve_sms: leave SMs free for concurrent kernels (exchange, boundary)
+    const int blocks = std::min(std::max(per_sm, grid - reserve_sms * per_sm), (nt + kFW - 1) / kFW);
     kern<<<blocks, kFT, smem, s>>>(x + e0, y + e0, ft.d_tasks.p + t0, nt, w, cs, fp);
     count_launch();
   }
@@ -835,7 +872,7 @@ void launch_stencil(const bt_stencil& st, const double* x, double* y, cudaStream
 }
 
 bool stencil_fused(const bt_stencil& st) {
-  return st.symmetric && st.grid->part_nranks == 1;
+  return st.symmetric;
 }
 
 static void launch_stencil_small(const bt_stencil& st, const double* x, double* y, int bc, cudaStream_t s) {
@@ -843,7 +880,7 @@ static void launch_stencil_small(const bt_stencil& st, const double* x, double* 
   const int n = 1 << st.level, w = n + 1;
   const int64_t cs = n_tet(w);
   BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
-            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, cs};
+            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, cs, 0, g.mesh.n_cells()};
   const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
   const int n4 = st.fast4.ntasks, n2 = st.fast2.ntasks;
   const int b4 = (n4 + kFW - 1) / kFW, b2 = (n2 + kFW - 1) / kFW;
@@ -866,37 +903,66 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
   const bt_grid& g = *st.grid;
   const int n = 1 << st.level;
   const int parts = stencil_parts();
-  if (parts == 15 && g.mesh.n_cells() <= kMaxCells && (int64_t)g.mesh.n_cells() * n_tet(n + 1) <= kSmallSlots) {
+  const bool part = g.part_nranks > 1;
+  if (st.part_begin != g.part_begin || st.part_end != g.part_end)
+    raise(BT_LOGIC_ERROR, "apply_stencil: the grid was repartitioned after compute_stencil");
+  if (!part && parts == 15 && g.mesh.n_cells() <= kMaxCells &&
+      (int64_t)g.mesh.n_cells() * n_tet(n + 1) <= kSmallSlots) {
     launch_stencil_small(st, x, y, bc, s);
     return;
   }
+  const double* xl = x;  // local pointers (the exchange's combine shifts them itself)
+  double* yl = y;
+  x = shifted(x, g, BT_SPACE_P1, st.level);  // local -> global-cell indexing
+  y = shifted(y, g, BT_SPACE_P1, st.level);
+  BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
+            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, n_tet(n + 1),
+            g.part_begin, g.part_end};
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
-  const bool prism = prism_ok(st, x) && (parts & 16);
+  // partitioned: the rank-spanning groups' partial rows go first, on the side
+  // stream, so the exchange overlaps the interior marches; SMs are reserved
+  // beside the persistent interior grid for it and the boundary kernel
+  const int reserve = part ? 12 : 0;
+  if (part && (parts & 8)) {
+    const XPlan& p = xchg_plan(g, st.level);
+    if (p.buf_size) {
+      BT_CUDA(cudaStreamWaitEvent(ss.s2, ss.fork, 0));
+      if (g.xbuf.n < (size_t)p.buf_size) g.xbuf.alloc((size_t)p.buf_size);
+      BT_CUDA(cudaMemsetAsync(g.xbuf.p, 0, sizeof(double) * (size_t)p.buf_size, ss.s2));
+      const int ne = (int)p.entries.size();
+      if (ne) {
+        k_xpartials<<<(ne + 127) / 128, 128, 0, ss.s2>>>(x, g.xbuf.p, p.d_entries.p, p.d_pts.p, ne, a);
+        count_launch();
+      }
+      allreduce(g, g.xbuf.p, p.buf_size, ss.s2);
+      launch_xchg_combine(g, st.level, bc ? IF_SYNC_DIR : IF_SYNC, yl, xl, g.xbuf.p, ss.s2);
+      BT_CUDA(cudaEventRecord(ss.join2, ss.s2));
+    } else {
+      BT_CUDA(cudaEventRecord(ss.join2, s));  // nothing to exchange
+    }
+  }
+  const bool prism = !part && prism_ok(st, x) && (parts & 16);
   if (prism) {
     if (parts & 1) launch_prism(st, x, y, s);  // every interior point (bt_prism.cu)
     BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
   } else {
-    if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s);  // first, so its persistent blocks are resident first
+    if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s, reserve);  // first: its blocks resident first
     BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-    if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s);  // the 2-layer group, beside the main launch
+    if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s, reserve);  // the 2-layer group, beside the main launch
   }
-  if (!(parts & 8)) {
-    BT_CUDA(cudaEventRecord(ss.join, ss.s));
-    BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
-    return;
+  if (parts & 8) {
+    const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
+    const unsigned blocks = (unsigned)((pts + 127) / 128);
+    if (bc)
+      k_boundary<true><<<blocks, 128, 0, ss.s>>>(x, y, a);
+    else
+      k_boundary<false><<<blocks, 128, 0, ss.s>>>(x, y, a);
+    count_launch();
   }
-  BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
-            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, n_tet(n + 1)};
-  const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
-  const unsigned blocks = (unsigned)((pts + 127) / 128);
-  if (bc)
-    k_boundary<true><<<blocks, 128, 0, ss.s>>>(x, y, a);
-  else
-    k_boundary<false><<<blocks, 128, 0, ss.s>>>(x, y, a);
-  count_launch();
   BT_CUDA(cudaEventRecord(ss.join, ss.s));
   BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
+  if (part && (parts & 8)) BT_CUDA(cudaStreamWaitEvent(s, ss.join2, 0));
   check_launch("k_stencil_fused");
 }
 

@@ -140,6 +140,20 @@ const XPlan& xchg_plan(const bt_grid& g, int level) {
   if (!p.built) {
     build_xplan(g.mesh, g.topo, level, g.part_rank, g.part_nranks, p);
     p.d_entries.upload(p.entries);
+    const int w = (1 << level) + 1;
+    const int64_t cs = n_tet(w);
+    std::vector<int4> pts;
+    pts.reserve(p.entries.size());
+    for (const XEntry& e : p.entries) {
+      int64_t t = e.slot % cs;
+      const int cell = (int)(e.slot / cs);
+      int k = 0;
+      while (t >= n_tri(w - k)) t -= n_tri(w - k), ++k;
+      int j = 0;
+      while (t >= w - k - j) t -= w - k - j, ++j;
+      pts.push_back(make_int4(cell, (int)t, j, k));
+    }
+    p.d_pts.upload(pts);
   }
   return p;
 }
