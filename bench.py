@@ -55,8 +55,9 @@ WORKLOADS = {
        "k = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z), + interface sync",
     4: "4x4x4 cubes x 6 perturbed Kuhn tets (384 cells) L7, N1E1 curl-curl + mass (alpha = beta = 1), "
        "tangential zero Dirichlet (identity rows) + signed interface sync",
-    5: "8x8x8 cubes x 6 perturbed Kuhn tets (3,072 cells) L2->7, V(2,2)-cycle, Chebyshev(2)-Jacobi, "
-       "var-coeff elementwise div(k grad), linear transfers, 50 coarse CG its (one step = one V-cycle)",
+    5: "V(2,2)-cycle, Chebyshev(2)-Jacobi, var-coeff elementwise div(k grad), linear transfers, 50 coarse CG "
+       "its, levels 2->8, 64 perturbed Kuhn cubes (384 macro-tets) per GPU (8 GPUs: the 8x8x8-cube config 5); "
+       "one step = one V-cycle",
 }
 # algorithmic fp64 flops of the elementwise apply (bt_ew.cu): per micro-cell the
 # class-matrix row times x_T for its 4 vertices (16 FMA) and the kbar-weighted
@@ -414,13 +415,18 @@ def setup_config(cfg, bt, torch, ws, rank):
                     "0.77 MB: L2-resident by design of the config (latency bound)"}
     elif cfg == 3:
         lvl = 6
-        g = bt.Grid(bt.cubes_mesh_text(4, 0.1, 0), lvl, lvl)
+        # the config-3 mesh with its cubes numbered in 2x2x2 blocks (same geometry
+        # and perturbation as cubes_mesh_text(4)): rank blocks are compact
+        g = bt.Grid(bt.blocked_mesh_text(4, 4, 4, (2, 2, 2), h=0.25, perturb=0.1, seed=0), lvl, lvl)
+        if ws > 1:
+            g.set_partition(rank, ws)
         form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
         x, y = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
         bt.random_fill(x, lvl, 0)
         slots = x.values[lvl].numel()
         w.owned = bt.owned_dof_count(x, lvl)
-        micro = g.n_cells() * 8 ** lvl
+        _, _, cb, ce = g.partition()
+        micro = (ce - cb) * 8 ** lvl
         w.bytes = 16.0 * slots
         w.flops = float(EW_FLOPS_PER_MICROCELL * micro + EW_FLOPS_PER_ANCHOR * slots)
         w.dofs_per_step = w.owned
@@ -438,7 +444,9 @@ def setup_config(cfg, bt, torch, ws, rank):
                  [q.values[lvl] for q in ys])
         w.check = (y.values[lvl], 1)
         w.keep = (g, x, y, xs, ys, cf)
-        w.config = {"workload": WORKLOADS[3], "level": lvl, "cells": g.n_cells(), "slots": slots,
+        w.scaling = "strong"
+        w.config = {"workload": WORKLOADS[3], "mesh_numbering": "cubes in 2x2x2 blocks (compact rank blocks)",
+                    "level": lvl, "cells": g.n_cells(), "slots_per_gpu": slots,
                     "owned_dofs": w.owned, "micro_cells": micro, "bc": "none",
                     "l2": "inputs larger than L2 (x+y = %.0f MB)" % (16e-6 * slots),
                     "flops_model": f"{EW_FLOPS_PER_MICROCELL} per micro-cell + {EW_FLOPS_PER_ANCHOR} per vertex"}
@@ -469,8 +477,14 @@ def setup_config(cfg, bt, torch, ws, rank):
                     "owned_dofs": w.owned, "bc": "tangential Dirichlet identity rows",
                     "l2": "inputs larger than L2 (x+y = %.1f GB)" % (16e-9 * slots)}
     elif cfg == 5:
-        lo, hi = 2, 7
-        g = bt.Grid(bt.cubes_mesh_text(8, 0.1, 0), lo, hi)
+        # weak scaling, 64 cubes (384 macro-tets) per GPU, cubes of side 1/8 in
+        # 4x4x4 blocks: 4x4x4 -> 4x4x8 -> 4x8x8 -> 8x8x8 cubes at 1/2/4/8 GPUs, the
+        # last being config 5 itself (L2 -> 8, 70 GB per vector over 8 GPUs)
+        lo, hi = 2, 8
+        dims = {1: (4, 4, 4), 2: (4, 4, 8), 4: (4, 8, 8), 8: (8, 8, 8)}.get(ws, (4, 4, 4 * ws))
+        g = bt.Grid(bt.blocked_mesh_text(*dims, (4, 4, 4), h=0.125, perturb=0.1, seed=0), lo, hi)
+        if ws > 1:
+            g.set_partition(rank, ws)
         form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
         h = bt.make_hierarchy(g, form, bt.KernelKind.Elementwise)
         rhs, x = bt.allocate(bt.p1_space(), g, lo, hi), bt.allocate(bt.p1_space(), g, lo, hi)
@@ -485,9 +499,10 @@ def setup_config(cfg, bt, torch, ws, rank):
         # per cycle: 9 elementwise applies per level l > lo (2+2 Chebyshev(2)
         # sweeps of 2 applies, plus the residual) and 50 + 1 on the coarse level
         byts = flps = 0.0
+        _, _, cb, ce = g.partition()
         for l in range(lo, hi + 1):
             sl = g.space_size(0, l)
-            micro = g.n_cells() * 8 ** l
+            micro = (ce - cb) * 8 ** l
             na = 9 if l > lo else 51
             byts += na * 16.0 * sl
             flps += na * float(EW_FLOPS_PER_MICROCELL * micro + EW_FLOPS_PER_ANCHOR * sl)
@@ -508,11 +523,13 @@ def setup_config(cfg, bt, torch, ws, rank):
         w.check = None
         w.keep = (g, h, rhs, x, xs)
         w.hist_fn = (h, rhs, x, hi)
-        w.config = {"workload": WORKLOADS[5], "levels": f"{lo}->{hi}", "cells": g.n_cells(),
+        w.scaling = "weak"
+        w.config = {"workload": WORKLOADS[5], "mesh": f"{dims[0]}x{dims[1]}x{dims[2]} cubes of side 1/8 "
+                    f"({g.n_cells()} macro-tets), cubes numbered in 4x4x4 blocks", "levels": f"{lo}->{hi}",
+                    "cells": g.n_cells(),
                     "fine_slots": g.space_size(0, hi), "fine_owned_dofs": w.owned, "coarse_maxit": 50,
                     "coarse_tol": 0.0, "smoother": "Chebyshev(2)-Jacobi V(2,2)",
-                    "note": "full config 5 is L2->8 (70 GB per vector): multi-GPU only; this is the largest "
-                            "single-GPU instance of the family",
+                    "note": "weak-scaled family of config 5 (64 cubes per GPU); at 8 GPUs it is config 5 itself",
                     "roofline_model": "per cycle 9 applies per level > 2 and 51 on level 2, each max(16 B/slot at "
                                       "HBM, elementwise flops at fp64); vector passes and transfers not counted"}
     w.run = run
@@ -562,8 +579,8 @@ def run_config(cfg, args, bt, torch, ws, rank, hbm, fp64, extra=False):
         assert np.array_equal(hy.numpy(), w.check[0].cpu().numpy()), "e2e result differs from resident run"
     e2e_value = w.dofs_per_step * nsteps / (e2e_ms * 1e-3) / 1e9
     out = {"metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": K, "warmup": W,
-           "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f64", "data": "synthetic (random_fill seed 0, reference mt19937_64 stream)",
+           "ms_per_step": ms_step, "higher_is_better": True, "scaling": getattr(w, "scaling", "weak"),
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_fill seed 0, reference mt19937_64 stream)",
            "config": dict(w.config, config=cfg, parallelism=(
                f"cells partitioned over {ws} ranks, memory-sharded vectors (NCCL interface exchange)"
                if ws > 1 else "1 GPU")),
@@ -614,8 +631,8 @@ def run_ours(args):
     import paper_2308_01792_b200 as bt
 
     cfg = args.config
-    if ws > 1 and cfg != 2:
-        raise SystemExit("bench.py: N > 1 runs config 2 (weak-scaled); other configs are single-GPU here")
+    if ws > 1 and cfg in (1, 4):
+        raise SystemExit("bench.py: configs 1 (one macro-tet) and 4 run on one GPU here")
     hbm, _ = measured_hbm()
     fp64 = measure_fp64(bt, torch)
     line = run_config(cfg, args, bt, torch, ws, rank, hbm, fp64)
@@ -658,7 +675,11 @@ def run_reference(args):
         if cfg in (1, 2):
             lvl = 6 if cfg == 1 else 8
             text = po.ref_tet_text() if cfg == 1 else po.cube_kuhn_text()
-            threads = 1 if cfg == 1 else min(6, nproc)  # the reference parallelises over macro-cells only
+            ncells = 1 if cfg == 1 else 6
+            if cfg == 2 and ws > 1:  # the same workload as the ours arm: an N x 1 x 1 box of unit cubes
+                import paper_2308_01792_b200 as bt  # (mesh text generator only: no CUDA)
+                text, ncells = bt.box_mesh_text(ws, 1, 1), 6 * ws
+            threads = 1 if cfg == 1 else min(ncells, nproc)  # the reference parallelises over macro-cells only
             r = po.Reference(text, lvl, lvl)
             x = r.random_fill(lvl, 0)
             owned = r.owned_count(lvl)
@@ -687,7 +708,10 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": args.gpus,
             "steps": K, "warmup": 1, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_fill seed 0)",
-            "config": {"workload": WORKLOADS[cfg], "config": cfg, "threads": threads, "cpu": cpu_model()},
+            "config": {"workload": WORKLOADS[cfg] if not (cfg == 2 and ws > 1) else
+                       f"{ws}x1x1 unit cubes x 6 Kuhn macro-tets ({6 * ws} cells) L8, P1 const-coeff 15-point stencil "
+                       "apply + interface sync (the ours arm's N-GPU workload)", "config": cfg, "threads": threads,
+                       "cpu": cpu_model()},
             "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": "reference",
                              "cpu": cpu_model(),
                              "sample": f"median of {K} applies (buffers allocated and loaded once), {threads} "

@@ -131,6 +131,12 @@ int64_t bt_cubes_mesh_text(int n, double perturb, uint64_t seed, char* buf, int6
 /* nx x ny x nz unit cubes (side 1) x 6 Kuhn tets, same perturbation rule:
  * the weak-scaling workload of bench.py (6 cells per GPU at N = nx ny nz) */
 int64_t bt_box_mesh_text(int nx, int ny, int nz, double perturb, uint64_t seed, char* buf, int64_t buflen);
+/* nx x ny x nz cubes of side h (6 Kuhn tets each, same perturbation rule),
+ * cubes numbered block-major with blocks of bx x by x bz cubes, so the
+ * contiguous cell ranges of bt_grid_set_partition are compact blocks (SURVEY
+ * §8(e)); returns -1 on bad arguments */
+int64_t bt_blocked_mesh_text(int nx, int ny, int nz, int bx, int by, int bz, double h, double perturb, uint64_t seed,
+                             char* buf, int64_t buflen);
 
 /* ---- vectors (fe_function.hpp:324-497, solvers.hpp:53-72) ---------------- */
 /* random_fill (fe_function.hpp:479): mt19937_64 on the host in canonical

@@ -51,6 +51,8 @@ SIGNATURES = {
     "bt_last_error": (C.c_char_p, []),
     "bt_version": (C.c_char_p, []),
     "bt_launch_count": (C.c_uint64, []),
+    "bt_blocked_mesh_text": (C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                         C.c_uint64, C.c_char_p, C.c_int64]),
     "bt_dfma_probe": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "bt_linearize_checked": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
     "bt_linearize_aos": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]),

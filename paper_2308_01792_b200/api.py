@@ -369,6 +369,19 @@ def box_mesh_text(nx: int, ny: int, nz: int, perturb: float = 0.0, seed: int = 0
     return buf.value.decode()
 
 
+def blocked_mesh_text(nx: int, ny: int, nz: int, block=(2, 2, 2), h: float = 1.0, perturb: float = 0.1,
+                      seed: int = 0) -> str:
+    """nx x ny x nz cubes of side h x 6 Kuhn tets, cubes numbered block-major
+    (bt_blocked_mesh_text): contiguous cell ranges are compact blocks."""
+    bx, by, bz = block
+    need = _L.bt_blocked_mesh_text(nx, ny, nz, bx, by, bz, h, perturb, seed, None, 0)
+    if need < 0:
+        raise InvalidArgument("blocked_mesh_text: dimensions, blocks and h must be positive")
+    buf = C.create_string_buffer(need + 1)
+    _L.bt_blocked_mesh_text(nx, ny, nz, bx, by, bz, h, perturb, seed, buf, need + 1)
+    return buf.value.decode()
+
+
 def ref_tet_text():
     return "# reference tetrahedron\nvertices 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ncells 1\n0 1 2 3\n"
 

@@ -475,7 +475,8 @@ void build_ew_cells(const bt_grid& g, const bt_form& f, int level, std::vector<E
 // nx x ny x nz cubes of side h, each split into 6 Kuhn tets (positive
 // orientation); vertices not on the box boundary perturbed per component by
 // U(-perturb h, perturb h) from mt19937_64(seed) in vertex order.
-static std::string box_text(int nx, int ny, int nz, double h, double perturb, uint64_t seed, const char* header) {
+static std::string box_text(int nx, int ny, int nz, double h, double perturb, uint64_t seed, const char* header,
+                            int bx = 0, int by = 0, int bz = 0) {
   const int vx = nx + 1, vy = ny + 1, vz = nz + 1, nverts = vx * vy * vz;
   const int dims[3] = {nx, ny, nz};
   std::vector<double> xyz(3 * (size_t)nverts);
@@ -506,10 +507,23 @@ static std::string box_text(int nx, int ny, int nz, double h, double perturb, ui
   auto vid = [&](int a, int b, int c, int bits) {
     return (a + (bits & 1)) + vx * ((b + ((bits >> 1) & 1)) + vy * (c + ((bits >> 2) & 1)));
   };
-  for (int c = 0; c < nz; ++c)
-    for (int b = 0; b < ny; ++b)
-      for (int a = 0; a < nx; ++a)
-        for (const auto& pm : perms) {
+  // cubes in cube order (a fastest), or block-major with blocks of bx x by x bz
+  // cubes (blocks in block order, cubes inside a block in cube order), so that
+  // contiguous cell ranges (bt_grid_set_partition) are compact blocks
+  if (bx <= 0) bx = nx;
+  if (by <= 0) by = ny;
+  if (bz <= 0) bz = nz;
+  std::vector<std::array<int, 3>> order;
+  for (int BZ = 0; BZ < nz; BZ += bz)
+    for (int BY = 0; BY < ny; BY += by)
+      for (int BX = 0; BX < nx; BX += bx)
+        for (int c = BZ; c < std::min(nz, BZ + bz); ++c)
+          for (int b = BY; b < std::min(ny, BY + by); ++b)
+            for (int a = BX; a < std::min(nx, BX + bx); ++a) order.push_back({a, b, c});
+  for (const auto& abc : order)
+    for (const auto& pm : perms) {
+      const int a = abc[0], b = abc[1], c = abc[2];
+      {
           int loc[4] = {0, 0, 0, 7};
           loc[1] = 1 << pm[0];
           loc[2] = loc[1] | (1 << pm[1]);
@@ -529,6 +543,7 @@ static std::string box_text(int nx, int ny, int nz, double h, double perturb, ui
                    vid(a, b, c, loc[3]));
           out += tmp;
         }
+    }
   return out;
 }
 
@@ -544,6 +559,18 @@ std::string box_mesh_text(int nx, int ny, int nz, double perturb, uint64_t seed)
   snprintf(header, sizeof header, "# %dx%dx%d unit cubes x 6 Kuhn tets, perturb %.17g, seed %llu\n", nx, ny, nz,
            perturb, (unsigned long long)seed);
   return box_text(nx, ny, nz, 1.0, perturb, seed, header);
+}
+
+// nx x ny x nz cubes of side h, cubes numbered block-major (blocks of
+// bx x by x bz cubes): the multi-GPU workloads, whose contiguous cell ranges
+// are then compact blocks
+std::string blocked_mesh_text(int nx, int ny, int nz, int bx, int by, int bz, double h, double perturb,
+                              uint64_t seed) {
+  char header[256];
+  snprintf(header, sizeof header,
+           "# %dx%dx%d cubes of side %.17g x 6 Kuhn tets, blocks %dx%dx%d, perturb %.17g, seed %llu\n", nx, ny, nz, h,
+           bx, by, bz, perturb, (unsigned long long)seed);
+  return box_text(nx, ny, nz, h, perturb, seed, header, bx, by, bz);
 }
 
 // Elementwise tables are cached on the grid per (form, level): a repeated
@@ -915,6 +942,18 @@ bt_status bt_grid_groups(const bt_grid* g, int level, int space, int64_t* n_grou
 int64_t bt_box_mesh_text(int nx, int ny, int nz, double perturb, uint64_t seed, char* buf, int64_t buflen) {
   if (nx < 1 || ny < 1 || nz < 1) return -1;
   const std::string s = box_mesh_text(nx, ny, nz, perturb, seed);
+  if (buf && buflen > 0) {
+    const int64_t k = std::min<int64_t>((int64_t)s.size(), buflen - 1);
+    std::memcpy(buf, s.data(), (size_t)k);
+    buf[k] = 0;
+  }
+  return (int64_t)s.size();
+}
+
+int64_t bt_blocked_mesh_text(int nx, int ny, int nz, int bx, int by, int bz, double h, double perturb, uint64_t seed,
+                             char* buf, int64_t buflen) {
+  if (nx < 1 || ny < 1 || nz < 1 || bx < 1 || by < 1 || bz < 1 || !(h > 0)) return -1;
+  const std::string s = blocked_mesh_text(nx, ny, nz, bx, by, bz, h, perturb, seed);
   if (buf && buflen > 0) {
     const int64_t k = std::min<int64_t>((int64_t)s.size(), buflen - 1);
     std::memcpy(buf, s.data(), (size_t)k);

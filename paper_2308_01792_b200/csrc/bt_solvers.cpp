@@ -115,6 +115,10 @@ static double lambda_max(bt_hierarchy& h, int l, cudaStream_t s) {
   BT_CUDA(cudaMemcpyAsync(&hs, S, sizeof(LamState), cudaMemcpyDeviceToHost, s));
   BT_CUDA(cudaStreamSynchronize(s));
   L.lambda = 1.1 * hs.rho;
+  // the iterate vectors are dead now (a coarse-level CG reallocates its own)
+  L.p.release();
+  L.ap.release();
+  L.z.release();
   return L.lambda;
 }
 

@@ -45,3 +45,26 @@ def test_linearize_checked_aos_soa():
             bt.linearize_aos(w, 2, p, 2)
         with pytest.raises(bt.OutOfRange):
             bt.linearize_soa(w, 2, p, -1)
+
+
+def test_blocked_mesh_partition_blocks_are_compact():
+    """bt_blocked_mesh_text numbers cubes block-major, so bt_grid_set_partition's
+    contiguous cell ranges are compact blocks of cubes: 4x4x4
+    cubes in 2x2x2 blocks over 8 ranks give each rank one 2x2x2 block; the
+    unblocked numbering gives 4x2x1 slabs."""
+    text = bt.blocked_mesh_text(4, 4, 4, (2, 2, 2), h=0.25, perturb=0.0)
+    m = bt.parse_mesh(text)
+    assert m.n_cells() == 384
+    for r in range(8):
+        b, e = bt.partition_range(384, r, 8)
+        xyz = m.vertex_coords[m.cells[b:e].ravel()]
+        ext = xyz.max(axis=0) - xyz.min(axis=0)
+        assert np.allclose(ext, [0.5, 0.5, 0.5])
+    plain = bt.parse_mesh(bt.cubes_mesh_text(4, 0.0, 0))
+    b, e = bt.partition_range(384, 0, 8)
+    ext = np.ptp(plain.vertex_coords[plain.cells[b:e].ravel()], axis=0)
+    assert np.allclose(sorted(ext), [0.25, 0.5, 1.0])
+    # the same geometry and perturbation as the unblocked generator, cells renumbered
+    a = bt.parse_mesh(bt.blocked_mesh_text(4, 4, 4, (4, 4, 4), h=0.25, perturb=0.1, seed=0))
+    c = bt.parse_mesh(bt.cubes_mesh_text(4, 0.1, 0))
+    assert np.array_equal(a.vertex_coords, c.vertex_coords) and np.array_equal(a.cells, c.cells)
