@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "bt_internal.hpp"
@@ -50,6 +51,15 @@ __constant__ uint32_t kEwPresent[16] = {0xffffff, 0xe8cc8e, 0x962b4d, 0x80080c, 
                                         0x11003,  0x2,      0x1,      0x0};
 __constant__ uint32_t kEwDirMask[16] = {0x7fff, 0x7f71, 0x26ff, 0x2671, 0x5d6f, 0x5d61, 0x46f, 0x461,
                                         0x3b9f, 0x3b11, 0x229f, 0x2211, 0x190f, 0x1901, 0xf,   0x0};
+
+// a 16-byte read-only load the compiler may not hoist out of a loop: the
+// per-cell class rows and kbar coefficients are re-read (L1 broadcast) each
+// layer instead of pinning 144 registers
+__device__ __forceinline__ double2 ldg2_nohoist(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
 
 __host__ __device__ inline int ew_class_width(int s, int n) { return s == 0 ? n : (s == 1 ? n - 2 : n - 1); }
 
@@ -252,6 +262,196 @@ __global__ void __launch_bounds__(kET) k_ew(const double* __restrict__ x, double
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-autonomous variant (k_ew_row, the default): a warp owns one row j of
+// one macro-cell, lanes = columns 31q - 1 + lane (lane 0 only supplies the
+// i - 1 anchors of lane 1), and marches the layers k. Per step each lane
+// evaluates kbar of the 6 classes at its two anchors (c, j - 1, k) and
+// (c, j, k) — the micro-cells anchored in layer k that its vertex column
+// touches — keeps the previous layer's, and takes the column c - 1 ones from
+// lane - 1 by shuffle. No barriers and no shared memory: every anchor row is
+// evaluated by the two warps of the rows it touches (each bitwise alike: same
+// column table, same row/layer recurrence from k = 0), which costs less than
+// the synchronisation of a shared ring. The sin/cos of the row/layer phase
+// beta_d1 (j - o_j) + beta_d2 k advance by rotation, the column phase
+// beta_d0 c is one sincos per lane per row.
+// ---------------------------------------------------------------------------
+template <int CK, bool DIAG>
+__global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, double* __restrict__ y,
+                                                const EwCell* __restrict__ cells, const int4* __restrict__ tasks,
+                                                int ntasks, double c0, int n, int64_t cs,
+                                                const double* __restrict__ phase, int cell0) {
+  // per warp: kbar of the lanes' anchors, [layer parity][o * 6 + class][lane]
+  // (o = 0: anchor row j, o = 1: row j - 1); lane - 1's entries are the
+  // column c - 1 anchors, so no shuffles and nothing held in registers
+  __shared__ double kbs[4][2][12][32];
+  // the warp's cell: class rows G_s and kbar coefficients, read through a
+  // volatile pointer each layer (held in registers they would take 144)
+  __shared__ __align__(16) double egs[4][96 + 48];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int task = blockIdx.x * 4 + wib;
+  if (task >= ntasks) return;
+  const int4 T = tasks[task];
+  const int cell = T.x, j = T.y, c = 31 * T.z - 1 + lane, kmax = T.w;
+  const int w = n + 1;
+  const EwCell* __restrict__ E = cells + cell;
+  double (*kb)[12][32] = kbs[wib];
+  for (int q = lane; q < 96; q += 32) egs[wib][q] = __ldg(&E->G[0][0] + q);
+  for (int q = lane; q < 48; q += 32) egs[wib][96 + q] = __ldg(&E->coefh[0][0] + q);
+  __syncwarp();
+  const volatile double* EG = egs[wib];       // G_s row slot: EG[16 s + 4 slot + jj]
+  const volatile double* EC = egs[wib] + 96;  // coefh: EC[8 s + m]
+  constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
+  constexpr int kTetDir[6][4][4] = {{{0, 1, 2, 3}, {8, 0, 11, 12}, {9, 4, 0, 13}, {10, 5, 6, 0}},
+                                    {{0, 13, 12, 3}, {6, 0, 11, 2}, {5, 4, 0, 1}, {10, 9, 8, 0}},
+                                    {{0, 13, 7, 3}, {6, 0, 1, 2}, {14, 8, 0, 11}, {10, 9, 4, 0}},
+                                    {{0, 11, 2, 3}, {4, 0, 1, 7}, {9, 8, 0, 13}, {10, 14, 6, 0}},
+                                    {{0, 11, 12, 3}, {4, 0, 13, 7}, {5, 6, 0, 1}, {10, 14, 8, 0}},
+                                    {{0, 1, 7, 3}, {8, 0, 13, 12}, {14, 6, 0, 11}, {10, 5, 4, 0}}};
+  const double* __restrict__ xc = x + (int64_t)cell * cs;
+  double* __restrict__ yc = y + (int64_t)cell * cs;
+  // column phase (per lane), one-layer rotation, row/layer phases of anchor
+  // rows j, j - 1: from the per-cell phase tables (ew_phase_tables)
+  double sa[3], ca[3], sr[3], cr[3], sb[2][3], cb[2][3];
+  if (CK == 1) {
+    const int np = n + 2;  // table entries for -1 .. n
+    const double* __restrict__ P = phase + (int64_t)(cell - cell0) * (12 * np + 6);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      sa[d] = __ldg(P + (0 * 3 + d) * np + c + 1);
+      ca[d] = __ldg(P + (1 * 3 + d) * np + c + 1);
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        sb[o][d] = __ldg(P + (2 * 3 + d) * np + j - o + 1);
+        cb[o][d] = __ldg(P + (3 * 3 + d) * np + j - o + 1);
+      }
+      sr[d] = __ldg(P + 12 * np + d);
+      cr[d] = __ldg(P + 12 * np + 3 + d);
+    }
+  }
+  const int cl = lane > 0 ? lane - 1 : 0;  // lane of column c - 1 (lane 0's vertex is never live)
+  int t0 = row_start(w, j, 0);
+#pragma unroll 1
+  for (int k = 0; k <= kmax; ++k) {
+    const int b = k & 1;
+    // ---- kbar of the 6 classes at anchors (c, j - o, k) ----
+    if (CK == 0) {
+#pragma unroll
+      for (int q = 0; q < 12; ++q) kb[b][q][lane] = c0;
+    } else if (CK == 2) {
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const double lp = __ldg(&E->lin[0]) * c + __ldg(&E->lin[1]) * (j - o) + __ldg(&E->lin[2]) * k;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) kb[b][o * 6 + s][lane] = __ldg(&E->lin0[s]) + lp;
+      }
+    } else {
+      double M[2][8];
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        double S[3], C[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          S[d] = fma(sa[d], cb[o][d], ca[d] * sb[o][d]);
+          C[d] = fma(ca[d], cb[o][d], -(sa[d] * sb[o][d]));
+        }
+        const double m2[4] = {S[0] * S[1], C[0] * S[1], S[0] * C[1], C[0] * C[1]};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          M[o][m] = m2[m] * S[2];
+          M[o][m + 4] = m2[m] * C[2];
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        double k0v = c0, k1v = c0;
+#pragma unroll
+        for (int m = 0; m < 8; m += 2) {
+          const double cx = EC[8 * s + m], cy = EC[8 * s + m + 1];
+          k0v = fma(cx, M[0][m], k0v);
+          k0v = fma(cy, M[0][m + 1], k0v);
+          k1v = fma(cx, M[1][m], k1v);
+          k1v = fma(cy, M[1][m + 1], k1v);
+        }
+        kb[b][s][lane] = k0v;
+        kb[b][6 + s][lane] = k1v;
+      }
+    }
+    if (CK == 1) {
+#pragma unroll
+      for (int o = 0; o < 2; ++o)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {  // rotate the row/layer phase by one layer
+          const double sn = fma(sb[o][d], cr[d], cb[o][d] * sr[d]);
+          cb[o][d] = fma(cb[o][d], cr[d], -(sb[o][d] * sr[d]));
+          sb[o][d] = sn;
+        }
+    }
+    __syncwarp();
+    // ---- the vertex (c, j, k) ----
+    const bool live = lane > 0 && c >= 0 && c + j + k <= n;
+    const int z = live ? zero_set(n, c, j, k) : 15;
+    const uint32_t present = kEwPresent[z];
+    double xv[15];
+    if (!DIAG) {
+      int off[15];
+      row_offsets(w, j, k, off);
+      const uint32_t dm = kEwDirMask[z];
+#pragma unroll
+      for (int d = 0; d < 15; ++d) xv[d] = (dm >> d & 1) ? __ldg(xc + t0 + c + off[d]) : 0.0;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+#pragma unroll
+      for (int slot = 0; slot < 4; ++slot) {
+        const int oi = kOff[s][slot][0], oj = kOff[s][slot][1], ok = kOff[s][slot][2];
+        const double kr = kb[(k - ok) & 1][oj * 6 + s][oi ? cl : lane];
+        const double kv = (present >> (4 * s + slot) & 1) ? kr : 0.0;
+        if (DIAG) {
+          acc = fma(kv, EG[16 * s + 5 * slot], acc);
+        } else {
+          const int gb = 16 * s + 4 * slot;
+          double row = EG[gb] * xv[kTetDir[s][slot][0]];
+          row = fma(EG[gb + 1], xv[kTetDir[s][slot][1]], row);
+          row = fma(EG[gb + 2], xv[kTetDir[s][slot][2]], row);
+          row = fma(EG[gb + 3], xv[kTetDir[s][slot][3]], row);
+          acc = fma(kv, row, acc);
+        }
+      }
+    }
+    if (live) yc[t0 + c] = acc;
+    t0 += tri32(w - k) - j;  // row j of layer k + 1
+    __syncwarp();            // every lane has read the ring slot rewritten next step
+  }
+}
+
+// Per-cell sin/cos tables of the sin-product phases for k_ew_row, cells
+// [cell0, cell0 + ncells): [sin, cos] x [d] of beta_d0 i and of beta_d1 j for
+// i, j = -1 .. n, then sin, cos of beta_d2 (one layer step).
+__global__ void __launch_bounds__(256) k_ew_phase(const EwCell* __restrict__ cells, int n, int cell0,
+                                                  double* __restrict__ out) {
+  const int cell = cell0 + blockIdx.y, np = n + 2;
+  const EwCell* E = cells + cell;
+  double* P = out + (int64_t)blockIdx.y * (12 * np + 6);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 3 * np; q += gridDim.x * blockDim.x) {
+    const int d = q / np, t = q % np - 1;
+    double sv, cv;
+    sincos(E->beta[d][0] * t, &sv, &cv);
+    P[(0 * 3 + d) * np + t + 1] = sv;
+    P[(1 * 3 + d) * np + t + 1] = cv;
+    sincos(E->beta[d][1] * t, &sv, &cv);
+    P[(2 * 3 + d) * np + t + 1] = sv;
+    P[(3 * 3 + d) * np + t + 1] = cv;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 3) {
+    double sv, cv;
+    sincos(E->beta[threadIdx.x][2], &sv, &cv);
+    P[12 * np + threadIdx.x] = sv;
+    P[12 * np + 3 + threadIdx.x] = cv;
+  }
+}
+
 // Exact positivity check of k at every quadrature point of every micro-cell
 // (local_matrix's "div_k_grad coefficient must be positive", forms.hpp:114),
 // for coefficients whose sign is not settled on the host. Sets *bad.
@@ -290,6 +490,16 @@ __global__ void __launch_bounds__(256) k_kpos(const double* __restrict__ maps, b
 }
 }  // namespace
 
+void build_ew_phase(const bt_grid& g, int level, const EwCell* d_cells, DevBuf<double>& out) {
+  const int n = 1 << level, nl = g.part_end - g.part_begin;
+  out.alloc((size_t)std::max(nl, 1) * (12 * (n + 2) + 6));
+  if (!nl) return;
+  k_ew_phase<<<dim3((3 * (n + 2) + 255) / 256, nl), 256>>>(d_cells, n, g.part_begin, out.p);
+  count_launch();
+  check_launch("k_ew_phase");
+  BT_CUDA(cudaDeviceSynchronize());
+}
+
 // tiles of this handle's cells: (cell, j0, i0, top layer)
 static const DevBuf<int4>& ew_units(const bt_grid& g, int level, int& count) {
   static thread_local struct {
@@ -320,10 +530,64 @@ static const DevBuf<int4>& ew_units(const bt_grid& g, int level, int& count) {
   return c.d;
 }
 
+// row tasks of this handle's cells for k_ew_row: (cell, j, column chunk q, top layer)
+static const DevBuf<int4>& ew_row_tasks(const bt_grid& g, int level, int& count) {
+  static thread_local struct {
+    const bt_grid* g = nullptr;
+    int level = -1, begin = -1, end = -1, epoch = -1;
+    DevBuf<int4> d;
+    int count = 0;
+  } cache[4];
+  for (auto& c : cache)
+    if (c.g == &g && c.level == level && c.begin == g.part_begin && c.end == g.part_end && c.epoch == g.part_epoch) {
+      count = c.count;
+      return c.d;
+    }
+  auto& c = cache[level & 3];
+  const int n = 1 << level;
+  std::vector<int4> u;
+  // longest marches first (rows near j = 0, chunks near i = 0), cells interleaved
+  for (int j = 0; j <= n; ++j)
+    for (int q = 0; 31 * q + j <= n; ++q)
+      for (int cell = g.part_begin; cell < g.part_end; ++cell) u.push_back(make_int4(cell, j, q, n - j - 31 * q));
+  std::stable_sort(u.begin(), u.end(), [](const int4& a, const int4& b) { return a.w > b.w; });
+  c.d.upload(u);
+  c.g = &g;
+  c.level = level;
+  c.begin = g.part_begin;
+  c.end = g.part_end;
+  c.epoch = g.part_epoch;
+  c.count = (int)u.size();
+  count = c.count;
+  return c.d;
+}
+
 void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells, const double* x,
-                        double* y, bool diag_only, cudaStream_t s) {
+                        double* y, bool diag_only, cudaStream_t s, const double* phase) {
   const int n = 1 << level, w = n + 1;
   if (g.part_end == g.part_begin) return;
+  // BT_EW_KERNEL=1 (profiling): the shared-ring tile kernel k_ew instead of k_ew_row
+  static const int tile = [] {
+    const char* e = std::getenv("BT_EW_KERNEL");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (!tile && (ck != 1 || phase)) {
+    int nt = 0;
+    const DevBuf<int4>& tasks = ew_row_tasks(g, level, nt);
+    const double* xs = shifted(x, g, BT_SPACE_P1, level);
+    double* ys = shifted(y, g, BT_SPACE_P1, level);
+    const unsigned blocks = (unsigned)((nt + 3) / 4);  // 4 warps (rows) per block
+    const double c0r = c[0];
+#define BT_EWR(CK_, D_) \
+  k_ew_row<CK_, D_><<<blocks, 128, 0, s>>>(xs, ys, d_cells, tasks.p, nt, c0r, n, n_tet(w), phase, g.part_begin)
+    if (ck == 0) { if (diag_only) BT_EWR(0, true); else BT_EWR(0, false); }
+    else if (ck == 1) { if (diag_only) BT_EWR(1, true); else BT_EWR(1, false); }
+    else { if (diag_only) BT_EWR(2, true); else BT_EWR(2, false); }
+#undef BT_EWR
+    count_launch();
+    check_launch("k_ew_row");
+    return;
+  }
   int nu = 0;
   const DevBuf<int4>& units = ew_units(g, level, nu);
   x = shifted(x, g, BT_SPACE_P1, level);  // global-cell indexing

@@ -263,7 +263,10 @@ struct EwTables {  // device tables of one (form, level) for the elementwise ker
   bt_form form{};
   int level = 0;
   DevBuf<EwCell> cells;
+  DevBuf<double> phase;  // sin-product phase tables of this handle's cells (build_ew_phase)
 };
+// per-cell sin/cos tables of the sin-product phases (k_ew_row), this handle's cells
+void build_ew_phase(const bt_grid& g, int level, const EwCell* d_cells, DevBuf<double>& out);
 const EwTables& ew_tables(const bt_grid& g, const bt_form& f, int level);
 }  // namespace bt
 
@@ -364,7 +367,7 @@ struct SideStream {
 };
 SideStream& side_stream();
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c, const EwCell* d_cells,
-                        const double* x, double* y, bool diag_only, cudaStream_t s);
+                        const double* x, double* y, bool diag_only, cudaStream_t s, const double* phase = nullptr);
 // local_matrix's positivity check of a div_k_grad coefficient (bt_ew.cu)
 void check_coefficient(const bt_grid& g, const bt_form& f, int level, const double* d_maps, cudaStream_t s);
 // per cell: the affine map (a row-major, b), built on first use (bt_kernels.cu)

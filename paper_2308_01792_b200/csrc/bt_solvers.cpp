@@ -17,6 +17,7 @@ struct LevelData {
   int64_t n = 0;
   std::unique_ptr<bt_stencil> stencil;  // stencil kernel
   DevBuf<EwCell> ew;                    // elementwise kernel tables
+  DevBuf<double> phase;                 // sin-product phase tables (k_ew_row)
   DevBuf<double> diag;
   double lambda = 0.0;
   // work vectors, allocated on first use (need()): the finest level of a
@@ -68,7 +69,8 @@ static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int b
   } else {
     const int ck = h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.coeff_kind : 0;
     static const double one[4] = {1.0, 0.0, 0.0, 0.0};
-    launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, x, y, false, s);
+    launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, x, y, false, s,
+                       L.phase.p);
   }
   sync(*h.grid, l, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
 }
@@ -352,7 +354,8 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
       const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
       static const double one[4] = {1.0, 0.0, 0.0, 0.0};
       const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
-      launch_elementwise(*g, l, ck, c, L->ew.p, nullptr, L->diag.p, true, 0);
+      if (ck == 1) build_ew_phase(*g, l, L->ew.p, L->phase);
+      launch_elementwise(*g, l, ck, c, L->ew.p, nullptr, L->diag.p, true, 0, L->phase.p);
       sync(*g, l, IF_SYNC, L->diag.p, nullptr, 0);
     }
     h->levels.push_back(std::move(L));
