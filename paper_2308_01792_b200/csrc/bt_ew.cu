@@ -52,6 +52,12 @@ __constant__ uint32_t kEwPresent[16] = {0xffffff, 0xe8cc8e, 0x962b4d, 0x80080c, 
 __constant__ uint32_t kEwDirMask[16] = {0x7fff, 0x7f71, 0x26ff, 0x2671, 0x5d6f, 0x5d61, 0x46f, 0x461,
                                         0x3b9f, 0x3b11, 0x229f, 0x2211, 0x190f, 0x1901, 0xf,   0x0};
 
+// a 16-byte shared load the compiler may not hoist out of the layer loop
+__device__ __forceinline__ double2 lds2_v(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
 // a 16-byte read-only load the compiler may not hoist out of a loop: the
 // per-cell class rows and kbar coefficients are re-read (L1 broadcast) each
 // layer instead of pinning 144 registers
@@ -299,8 +305,8 @@ __global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, do
   for (int q = lane; q < 96; q += 32) egs[wib][q] = __ldg(&E->G[0][0] + q);
   for (int q = lane; q < 48; q += 32) egs[wib][96 + q] = __ldg(&E->coefh[0][0] + q);
   __syncwarp();
-  const volatile double* EG = egs[wib];       // G_s row slot: EG[16 s + 4 slot + jj]
-  const volatile double* EC = egs[wib] + 96;  // coefh: EC[8 s + m]
+  const double* EG = egs[wib];       // G_s row slot: EG[16 s + 4 slot + jj] (read with lds2_v)
+  const double* EC = egs[wib] + 96;  // coefh: EC[8 s + m]
   constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
   constexpr int kTetDir[6][4][4] = {{{0, 1, 2, 3}, {8, 0, 11, 12}, {9, 4, 0, 13}, {10, 5, 6, 0}},
                                     {{0, 13, 12, 3}, {6, 0, 11, 2}, {5, 4, 0, 1}, {10, 9, 8, 0}},
@@ -367,7 +373,8 @@ __global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, do
         double k0v = c0, k1v = c0;
 #pragma unroll
         for (int m = 0; m < 8; m += 2) {
-          const double cx = EC[8 * s + m], cy = EC[8 * s + m + 1];
+          const double2 cv = lds2_v(EC + 8 * s + m);
+          const double cx = cv.x, cy = cv.y;
           k0v = fma(cx, M[0][m], k0v);
           k0v = fma(cy, M[0][m + 1], k0v);
           k1v = fma(cx, M[1][m], k1v);
@@ -409,13 +416,14 @@ __global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, do
         const double kr = kb[(k - ok) & 1][oj * 6 + s][oi ? cl : lane];
         const double kv = (present >> (4 * s + slot) & 1) ? kr : 0.0;
         if (DIAG) {
-          acc = fma(kv, EG[16 * s + 5 * slot], acc);
+          const double2 gd = lds2_v(EG + 16 * s + 4 * slot + (slot & ~1));  // holds G_s[slot][slot]
+          acc = fma(kv, (slot & 1) ? gd.y : gd.x, acc);
         } else {
-          const int gb = 16 * s + 4 * slot;
-          double row = EG[gb] * xv[kTetDir[s][slot][0]];
-          row = fma(EG[gb + 1], xv[kTetDir[s][slot][1]], row);
-          row = fma(EG[gb + 2], xv[kTetDir[s][slot][2]], row);
-          row = fma(EG[gb + 3], xv[kTetDir[s][slot][3]], row);
+          const double2 g01 = lds2_v(EG + 16 * s + 4 * slot), g23 = lds2_v(EG + 16 * s + 4 * slot + 2);
+          double row = g01.x * xv[kTetDir[s][slot][0]];
+          row = fma(g01.y, xv[kTetDir[s][slot][1]], row);
+          row = fma(g23.x, xv[kTetDir[s][slot][2]], row);
+          row = fma(g23.y, xv[kTetDir[s][slot][3]], row);
           acc = fma(kv, row, acc);
         }
       }
