@@ -122,7 +122,9 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
                                                   int vgrid, double* ring_all) {
   constexpr int NS = N + 2;  // staged rows per step: C (layer k-1), layers k..k+N-1, Q (layer k+N)
   constexpr int kStageD = NS * kRowD;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp index and task words broadcast by shuffles: provably warp-uniform, so
+  // the march loop's shuffles need no divergence handling (WARPSYNC)
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int G = vgrid * kFW;
   const int t0 = vblock * kFW + warp;
   if (t0 >= ntasks) return;
@@ -201,7 +203,11 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
 
 #pragma unroll 1
   for (int t = t0; t < ntasks; t += G) {
-    const int4 tk = tasks[t];
+    int4 tk = tasks[t];
+    tk.x = __shfl_sync(0xffffffffu, tk.x, 0);
+    tk.y = __shfl_sync(0xffffffffu, tk.y, 0);
+    tk.z = __shfl_sync(0xffffffffu, tk.z, 0);
+    tk.w = __shfl_sync(0xffffffffu, tk.w, 0);
     const int k = tk.x, blk = tk.y & 0xffff, cl = tk.y >> 16, j0 = tk.z, j1 = tk.w;
     double W[8];
 #pragma unroll
