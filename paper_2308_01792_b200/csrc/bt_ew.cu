@@ -510,48 +510,27 @@ void build_ew_phase(const bt_grid& g, int level, const EwCell* d_cells, DevBuf<d
 
 // tiles of this handle's cells: (cell, j0, i0, top layer)
 static const DevBuf<int4>& ew_units(const bt_grid& g, int level, int& count) {
-  static thread_local struct {
-    const bt_grid* g = nullptr;
-    int level = -1, begin = -1, end = -1, epoch = -1;
-    DevBuf<int4> d;
-    int count = 0;
-  } cache[4];
-  for (auto& c : cache)
-    if (c.g == &g && c.level == level && c.begin == g.part_begin && c.end == g.part_end && c.epoch == g.part_epoch) {
-      count = c.count;
-      return c.d;
-    }
-  auto& c = cache[level & 3];
+  if (g.ew_tiles[level].p || g.ew_ntiles[level] == -1) {
+    count = std::max(0, g.ew_ntiles[level]);
+    return g.ew_tiles[level];
+  }
   const int n = 1 << level;
   std::vector<int4> u;
   for (int cell = g.part_begin; cell < g.part_end; ++cell)
     for (int j0 = 0; j0 <= n; j0 += kER)
       for (int i0 = 0; i0 + j0 <= n; i0 += kEC) u.push_back(make_int4(cell, j0, i0, n - j0 - i0));
-  c.d.upload(u);
-  c.g = &g;
-  c.level = level;
-  c.begin = g.part_begin;
-  c.end = g.part_end;
-  c.epoch = g.part_epoch;
-  c.count = (int)u.size();
-  count = c.count;
-  return c.d;
+  g.ew_tiles[level].upload(u);
+  g.ew_ntiles[level] = u.empty() ? -1 : (int)u.size();
+  count = (int)u.size();
+  return g.ew_tiles[level];
 }
 
 // row tasks of this handle's cells for k_ew_row: (cell, j, column chunk q, top layer)
 static const DevBuf<int4>& ew_row_tasks(const bt_grid& g, int level, int& count) {
-  static thread_local struct {
-    const bt_grid* g = nullptr;
-    int level = -1, begin = -1, end = -1, epoch = -1;
-    DevBuf<int4> d;
-    int count = 0;
-  } cache[4];
-  for (auto& c : cache)
-    if (c.g == &g && c.level == level && c.begin == g.part_begin && c.end == g.part_end && c.epoch == g.part_epoch) {
-      count = c.count;
-      return c.d;
-    }
-  auto& c = cache[level & 3];
+  if (g.ew_rows[level].p || g.ew_nrows[level] == -1) {
+    count = std::max(0, g.ew_nrows[level]);
+    return g.ew_rows[level];
+  }
   const int n = 1 << level;
   std::vector<int4> u;
   // longest marches first (rows near j = 0, chunks near i = 0), cells interleaved
@@ -559,15 +538,10 @@ static const DevBuf<int4>& ew_row_tasks(const bt_grid& g, int level, int& count)
     for (int q = 0; 31 * q + j <= n; ++q)
       for (int cell = g.part_begin; cell < g.part_end; ++cell) u.push_back(make_int4(cell, j, q, n - j - 31 * q));
   std::stable_sort(u.begin(), u.end(), [](const int4& a, const int4& b) { return a.w > b.w; });
-  c.d.upload(u);
-  c.g = &g;
-  c.level = level;
-  c.begin = g.part_begin;
-  c.end = g.part_end;
-  c.epoch = g.part_epoch;
-  c.count = (int)u.size();
-  count = c.count;
-  return c.d;
+  g.ew_rows[level].upload(u);
+  g.ew_nrows[level] = u.empty() ? -1 : (int)u.size();
+  count = (int)u.size();
+  return g.ew_rows[level];
 }
 
 void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells, const double* x,

@@ -821,6 +821,10 @@ bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks) {
   for (auto& p : g->xplan_edges) p.reset();
   g->ew_cache.clear();
   g->ew_scratch.release();
+  for (auto& b : g->ew_rows) b.release();
+  for (auto& b : g->ew_tiles) b.release();
+  g->ew_nrows.fill(0);
+  g->ew_ntiles.fill(0);
   g->d_partials.release();
   g->dot_cells.release();
   g->xbuf.release();

@@ -236,6 +236,9 @@ struct bt_grid {
   // elementwise-kernel tables per (form, level), built on first use
   mutable std::vector<std::unique_ptr<bt::EwTables>> ew_cache;
   mutable bt::DevBuf<double> ew_scratch;  // ApplyMode::Add without a caller scratch
+  // elementwise work lists per level (bt_ew.cu: row tasks, tile units), built on first use
+  mutable std::array<bt::DevBuf<int4>, 11> ew_rows, ew_tiles;
+  mutable std::array<int, 11> ew_nrows{}, ew_ntiles{};
   // reduction scratch for dot products
   mutable bt::DevBuf<double> d_partials;
   mutable bt::DevBuf<double> d_maps;  // per cell: the affine map (a row-major, b), built on first use
@@ -286,6 +289,7 @@ struct bt_stencil {
   bool symmetric = false;                    // fast-path preconditions hold (see bt_stencil.cu)
   std::vector<double> fast;                  // per cell: the 8 symmetric interior weights
   bt::DevBuf<double> d_ends;                 // per cell: typed rows of the two row ends (11 + 11)
+  bt::DevBuf<int> bnd_f, bnd_e, bnd_v;       // k_boundary: faces / macro edges / vertices with every member local
   bt::DevBuf<int4> d_prism;                  // k_stencil_prism units (bt_prism.cu), longest first
   int nprism = 0;
   bt::DevBuf<double> d_w8;                   // per cell (global index): the 8 symmetric weights

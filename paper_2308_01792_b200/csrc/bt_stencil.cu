@@ -352,6 +352,11 @@ struct BndArgs {
   int nf, ne, nv, n;
   int64_t cs;
   int cb, ce;  // this handle's cells: groups with a member outside are skipped (exchanged instead)
+  // the groups this handle computes (every member local): indices into
+  // faces / eh / vh; nf, ne, nv count these lists
+  const int* lf;
+  const int* le;
+  const int* lv;
 };
 
 __device__ __forceinline__ void bary_ijk(const int8_t* lv, int nl, const int* wt, int& i, int& j, int& k) {
@@ -462,7 +467,7 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
   const DevFace* F = nullptr;
   const DevPrimMem* mem = nullptr;
   if (q < (int64_t)a.nf * fpts) {  // face-interior point (a, b), weights (n - a - b, a, b)
-    F = a.faces + q / fpts;
+    F = a.faces + __ldg(a.lf + q / fpts);
     int ap, bp;
     decode_tri(n - 2, (int)(q % fpts), ap, bp);
     wt[0] = n - (ap + 1) - (bp + 1);
@@ -475,7 +480,7 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
     q -= (int64_t)a.nf * fpts;
     DevPrimHdr h;
     if (q < (int64_t)a.ne * (n - 1)) {  // macro-edge point a = 1..n-1, weights (n - a, a)
-      h = a.eh[q / (n - 1)];
+      h = a.eh[__ldg(a.le + q / (n - 1))];
       mem = a.em + h.first;
       wt[1] = (int)(q % (n - 1)) + 1;
       wt[0] = n - wt[1];
@@ -483,7 +488,7 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
     } else {  // macro vertex
       q -= (int64_t)a.ne * (n - 1);
       if (q >= a.nv) return;
-      h = a.vh[q];
+      h = a.vh[__ldg(a.lv + q)];
       mem = a.vm + h.first;
       wt[0] = n;
       nl = 1;
@@ -747,6 +752,29 @@ void init_stencil_tasks(bt_stencil& st) {
     }
   }
   st.d_ends.upload(ends);
+  // the interface groups whose members are all this handle's cells (k_boundary)
+  {
+    const Topology& t = st.grid->topo;
+    auto local = [&](int c) { return c >= st.part_begin && c < st.part_end; };
+    std::vector<int> lf, le, lv;
+    for (int f = 0; f < (int)t.faces.size(); ++f) {
+      bool ok = true;
+      for (int m = 0; m < t.faces[f].ncell; ++m) ok = ok && local(t.faces[f].cell[m]);
+      if (ok) lf.push_back(f);
+    }
+    auto prims = [&](const std::vector<DevPrimHdr>& hs, const std::vector<DevPrimMem>& mem, std::vector<int>& out) {
+      for (int e = 0; e < (int)hs.size(); ++e) {
+        bool ok = true;
+        for (int m = 0; m < hs[e].count; ++m) ok = ok && local(mem[hs[e].first + m].cell);
+        if (ok) out.push_back(e);
+      }
+    };
+    prims(t.ehdr, t.emem, le);
+    prims(t.vhdr, t.vmem, lv);
+    st.bnd_f.upload(lf);
+    st.bnd_e.upload(le);
+    st.bnd_v.upload(lv);
+  }
   init_prism_tasks(st);
 }
 
@@ -886,7 +914,8 @@ static void launch_stencil_small(const bt_stencil& st, const double* x, double* 
   const int n = 1 << st.level, w = n + 1;
   const int64_t cs = n_tet(w);
   BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
-            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, cs, 0, g.mesh.n_cells()};
+            (int)st.bnd_f.n, (int)st.bnd_e.n, (int)st.bnd_v.n, n, cs, 0, g.mesh.n_cells(),
+            st.bnd_f.p, st.bnd_e.p, st.bnd_v.p};
   const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
   const int n4 = st.fast4.ntasks, n2 = st.fast2.ntasks;
   const int b4 = (n4 + kFW - 1) / kFW, b2 = (n2 + kFW - 1) / kFW;
@@ -922,8 +951,8 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
   x = shifted(x, g, BT_SPACE_P1, st.level);  // local -> global-cell indexing
   y = shifted(y, g, BT_SPACE_P1, st.level);
   BndArgs a{g.d_faces.p, g.d_ehdr.p, g.d_emem.p, g.d_vhdr.p, g.d_vmem.p, st.d_cells.p,
-            (int)g.topo.faces.size(), (int)g.topo.ehdr.size(), (int)g.topo.vhdr.size(), n, n_tet(n + 1),
-            g.part_begin, g.part_end};
+            (int)st.bnd_f.n, (int)st.bnd_e.n, (int)st.bnd_v.n, n, n_tet(n + 1),
+            g.part_begin, g.part_end, st.bnd_f.p, st.bnd_e.p, st.bnd_v.p};
   SideStream& ss = side_stream();
   BT_CUDA(cudaEventRecord(ss.fork, s));
   // partitioned: the rank-spanning groups' partial rows go first, on the side
@@ -957,7 +986,7 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
     BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
     if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s, reserve);  // the 2-layer group, beside the main launch
   }
-  if (parts & 8) {
+  if ((parts & 8) && (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv > 0) {
     const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
     const unsigned blocks = (unsigned)((pts + 127) / 128);
     if (bc)
