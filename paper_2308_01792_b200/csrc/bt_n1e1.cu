@@ -435,7 +435,9 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
                                                         int64_t cs, const double* __restrict__ cellw,
                                                         int* __restrict__ next_march) {
   extern __shared__ __align__(16) double n1_smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp index and march words broadcast by shuffles: provably warp-uniform,
+  // so the march's shuffles need no divergence handling (WARPSYNC)
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int cl = blockIdx.y;  // this block's cell
   double* sw = n1_smem;       // the cell's weights (kN1CellWP)
   for (int q = threadIdx.x; q < kN1CellWP; q += kN1FT) sw[q] = __ldg(cellw + (size_t)cl * kN1CellWP + q);
@@ -516,7 +518,10 @@ __global__ void __launch_bounds__(kN1FT, 2) k_n1e1_fast(const double* __restrict
   int t = t0;
 #pragma unroll 1
   while (t < nmarch) {
-    const int4 tk = marches[t];
+    int4 tk = marches[t];
+    tk.x = __shfl_sync(0xffffffffu, tk.x, 0);
+    tk.y = __shfl_sync(0xffffffffu, tk.y, 0);
+    tk.z = __shfl_sync(0xffffffffu, tk.z, 0);
     const int k = tk.x & 0xffff, b = tk.x >> 16, j0 = tk.y, j1 = tk.z;
     const int i = kN1Cols * b - 1 + lane;
     const bool out = lane >= 1 && lane <= kN1Cols;
