@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "bt_internal.hpp"
@@ -282,31 +283,16 @@ __global__ void __launch_bounds__(kET) k_ew(const double* __restrict__ x, double
 // beta_d1 (j - o_j) + beta_d2 k advance by rotation, the column phase
 // beta_d0 c is one sincos per lane per row.
 // ---------------------------------------------------------------------------
-template <int CK, bool DIAG>
-__global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, double* __restrict__ y,
-                                                const EwCell* __restrict__ cells, const int4* __restrict__ tasks,
-                                                int ntasks, double c0, int n, int64_t cs,
-                                                const double* __restrict__ phase, int cell0) {
-  // per warp: kbar of the lanes' anchors, [layer parity][o * 6 + class][lane]
-  // (o = 0: anchor row j, o = 1: row j - 1); lane - 1's entries are the
-  // column c - 1 anchors, so no shuffles and nothing held in registers
-  __shared__ double kbs[4][2][12][32];
-  // the warp's cell: class rows G_s and kbar coefficients, read through a
-  // volatile pointer each layer (held in registers they would take 144)
-  __shared__ __align__(16) double egs[4][96 + 48];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int task = blockIdx.x * 4 + wib;
-  if (task >= ntasks) return;
-  const int4 T = tasks[task];
-  const int cell = T.x, j = T.y, c = 31 * T.z - 1 + lane, kmax = T.w;
+// The march of one warp (row j of one cell, lanes = columns c): GA(i) / CA(i)
+// return 2 consecutive class-row / kbar-coefficient values of the cell
+// (shared-memory copies, or kernel parameters that reach the FMAs as uniform
+// registers).
+template <int CK, bool DIAG, class GAcc, class CAcc>
+__device__ __forceinline__ void ew_row_march(const double* __restrict__ x, double* __restrict__ y,
+                                             const EwCell* __restrict__ E, int cell, int j, int c, int kmax,
+                                             double c0, int n, int64_t cs, const double* __restrict__ phase,
+                                             int cell0, double (*kb)[12][32], int lane, GAcc GA, CAcc CA) {
   const int w = n + 1;
-  const EwCell* __restrict__ E = cells + cell;
-  double (*kb)[12][32] = kbs[wib];
-  for (int q = lane; q < 96; q += 32) egs[wib][q] = __ldg(&E->G[0][0] + q);
-  for (int q = lane; q < 48; q += 32) egs[wib][96 + q] = __ldg(&E->coefh[0][0] + q);
-  __syncwarp();
-  const double* EG = egs[wib];       // G_s row slot: EG[16 s + 4 slot + jj] (read with lds2_v)
-  const double* EC = egs[wib] + 96;  // coefh: EC[8 s + m]
   constexpr int kOff[6][4][3] = BT_CELL_OFFSETS;
   constexpr int kTetDir[6][4][4] = {{{0, 1, 2, 3}, {8, 0, 11, 12}, {9, 4, 0, 13}, {10, 5, 6, 0}},
                                     {{0, 13, 12, 3}, {6, 0, 11, 2}, {5, 4, 0, 1}, {10, 9, 8, 0}},
@@ -373,7 +359,7 @@ __global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, do
         double k0v = c0, k1v = c0;
 #pragma unroll
         for (int m = 0; m < 8; m += 2) {
-          const double2 cv = lds2_v(EC + 8 * s + m);
+          const double2 cv = CA(8 * s + m);
           const double cx = cv.x, cy = cv.y;
           k0v = fma(cx, M[0][m], k0v);
           k0v = fma(cy, M[0][m + 1], k0v);
@@ -416,10 +402,10 @@ __global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, do
         const double kr = kb[(k - ok) & 1][oj * 6 + s][oi ? cl : lane];
         const double kv = (present >> (4 * s + slot) & 1) ? kr : 0.0;
         if (DIAG) {
-          const double2 gd = lds2_v(EG + 16 * s + 4 * slot + (slot & ~1));  // holds G_s[slot][slot]
+          const double2 gd = GA(16 * s + 4 * slot + (slot & ~1));  // holds G_s[slot][slot]
           acc = fma(kv, (slot & 1) ? gd.y : gd.x, acc);
         } else {
-          const double2 g01 = lds2_v(EG + 16 * s + 4 * slot), g23 = lds2_v(EG + 16 * s + 4 * slot + 2);
+          const double2 g01 = GA(16 * s + 4 * slot), g23 = GA(16 * s + 4 * slot + 2);
           double row = g01.x * xv[kTetDir[s][slot][0]];
           row = fma(g01.y, xv[kTetDir[s][slot][1]], row);
           row = fma(g23.x, xv[kTetDir[s][slot][2]], row);
@@ -432,6 +418,60 @@ __global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, do
     t0 += tri32(w - k) - j;  // row j of layer k + 1
     __syncwarp();            // every lane has read the ring slot rewritten next step
   }
+}
+
+template <int CK, bool DIAG>
+__global__ void __launch_bounds__(128) k_ew_row(const double* __restrict__ x, double* __restrict__ y,
+                                                const EwCell* __restrict__ cells, const int4* __restrict__ tasks,
+                                                int ntasks, double c0, int n, int64_t cs,
+                                                const double* __restrict__ phase, int cell0) {
+  // per warp: kbar of the lanes' anchors, [layer parity][o * 6 + class][lane]
+  // (o = 0: anchor row j, o = 1: row j - 1); lane - 1's entries are the
+  // column c - 1 anchors, so no shuffles and nothing held in registers
+  __shared__ double kbs[4][2][12][32];
+  // the warp's cell: class rows G_s and kbar coefficients, read with
+  // non-hoisted loads each layer (held in registers they would take 144)
+  __shared__ __align__(16) double egs[4][96 + 48];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int task = blockIdx.x * 4 + wib;
+  if (task >= ntasks) return;
+  const int4 T = tasks[task];
+  const int cell = T.x;
+  const EwCell* __restrict__ E = cells + cell;
+  for (int q = lane; q < 96; q += 32) egs[wib][q] = __ldg(&E->G[0][0] + q);
+  for (int q = lane; q < 48; q += 32) egs[wib][96 + q] = __ldg(&E->coefh[0][0] + q);
+  __syncwarp();
+  const double* EG = egs[wib];
+  const double* EC = egs[wib] + 96;
+  ew_row_march<CK, DIAG>(x, y, E, cell, T.y, 31 * T.z - 1 + lane, T.w, c0, n, cs, phase, cell0, kbs[wib], lane,
+                         [&](int i) { return lds2_v(EG + i); }, [&](int i) { return lds2_v(EC + i); });
+}
+
+// Per-cell weights as kernel parameters: a block is 4 warps of one cell
+// (blockIdx.y), so every weight is read at a block-uniform address and
+// reaches the FMAs through the uniform datapath (LDCU -> DFMA R, R, UR):
+// no shared-memory traffic for the 144 weights of a step.
+constexpr int kEwPC = 27;  // cells per launch (27 x 1152 B of parameters)
+struct EwParams {
+  double G[kEwPC][96];
+  double coefh[kEwPC][48];
+};
+template <int CK, bool DIAG>
+__global__ void __launch_bounds__(128) k_ew_rowp(const double* __restrict__ x, double* __restrict__ y,
+                                                 const EwCell* __restrict__ cells, const int4* __restrict__ rows,
+                                                 int nrows, double c0, int n, int64_t cs,
+                                                 const double* __restrict__ phase, int cell0, int chunk0,
+                                                 const __grid_constant__ EwParams p) {
+  __shared__ double kbs[4][2][12][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int task = blockIdx.y * 4 + wib;
+  if (task >= nrows) return;
+  const int4 T = rows[task];  // (j, q, kmax)
+  const int cell = chunk0 + blockIdx.x;
+  const int pc = blockIdx.x;
+  ew_row_march<CK, DIAG>(x, y, cells + cell, cell, T.x, 31 * T.y - 1 + lane, T.z, c0, n, cs, phase, cell0,
+                         kbs[wib], lane, [&](int i) { return make_double2(p.G[pc][i], p.G[pc][i + 1]); },
+                         [&](int i) { return make_double2(p.coefh[pc][i], p.coefh[pc][i + 1]); });
 }
 
 // Per-cell sin/cos tables of the sin-product phases for k_ew_row, cells
@@ -544,10 +584,67 @@ static const DevBuf<int4>& ew_row_tasks(const bt_grid& g, int level, int& count)
   return g.ew_rows[level];
 }
 
+// the (j, q, top layer) row marches of one cell (the same for every cell of a
+// level), longest first, for k_ew_rowp
+static const DevBuf<int4>& ew_row_table(const bt_grid& g, int level, int& count) {
+  if (!g.ew_rowtab[level].p) {
+    const int n = 1 << level;
+    std::vector<int4> u;
+    for (int j = 0; j <= n; ++j)
+      for (int q = 0; 31 * q + j <= n; ++q) u.push_back(make_int4(j, q, n - j - 31 * q, 0));
+    std::stable_sort(u.begin(), u.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
+    g.ew_rowtab[level].upload(u);
+  }
+  count = (int)g.ew_rowtab[level].n;
+  return g.ew_rowtab[level];
+}
+
 void launch_elementwise(const bt_grid& g, int level, int ck, const double* c, const EwCell* d_cells, const double* x,
-                        double* y, bool diag_only, cudaStream_t s, const double* phase) {
+                        double* y, bool diag_only, cudaStream_t s, const double* phase, const EwCell* h_cells) {
   const int n = 1 << level, w = n + 1;
   if (g.part_end == g.part_begin) return;
+  // levels >= 5 with host copies of the cells: weights as kernel parameters
+  // (k_ew_rowp, one launch per kEwPC cells); coarser levels: k_ew_row
+  static const int noparam = [] {
+    const char* e = std::getenv("BT_EW_NOPARAM");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (h_cells && n >= 32 && !noparam && (ck != 1 || phase)) {
+    int nr = 0;
+    const DevBuf<int4>& rows = ew_row_table(g, level, nr);
+    const double* xs = shifted(x, g, BT_SPACE_P1, level);
+    double* ys = shifted(y, g, BT_SPACE_P1, level);
+    EwParams prm;
+    // chunks round-robin over the main and two side streams, so one launch's
+    // tail overlaps the next launch's blocks
+    SideStream& ss = side_stream();
+    BT_CUDA(cudaEventRecord(ss.fork, s));
+    BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+    BT_CUDA(cudaStreamWaitEvent(ss.s2, ss.fork, 0));
+    int chunk = 0;
+    for (int c0 = g.part_begin; c0 < g.part_end; c0 += kEwPC, ++chunk) {
+      cudaStream_t st = chunk % 3 == 0 ? s : (chunk % 3 == 1 ? ss.s : ss.s2);
+      const int cnt = std::min(kEwPC, g.part_end - c0);
+      for (int q = 0; q < cnt; ++q) {
+        std::memcpy(prm.G[q], &h_cells[c0 + q].G[0][0], sizeof(double) * 96);
+        std::memcpy(prm.coefh[q], &h_cells[c0 + q].coefh[0][0], sizeof(double) * 48);
+      }
+      const dim3 grid((unsigned)cnt, (unsigned)((nr + 3) / 4));  // cells fastest: every cell's longest rows first
+#define BT_EWP(CK_, D_) \
+  k_ew_rowp<CK_, D_><<<grid, 128, 0, st>>>(xs, ys, d_cells, rows.p, nr, c[0], n, n_tet(w), phase, g.part_begin, c0, prm)
+      if (ck == 0) { if (diag_only) BT_EWP(0, true); else BT_EWP(0, false); }
+      else if (ck == 1) { if (diag_only) BT_EWP(1, true); else BT_EWP(1, false); }
+      else { if (diag_only) BT_EWP(2, true); else BT_EWP(2, false); }
+#undef BT_EWP
+      count_launch();
+    }
+    BT_CUDA(cudaEventRecord(ss.join, ss.s));
+    BT_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
+    BT_CUDA(cudaEventRecord(ss.join2, ss.s2));
+    BT_CUDA(cudaStreamWaitEvent(s, ss.join2, 0));
+    check_launch("k_ew_rowp");
+    return;
+  }
   // BT_EW_KERNEL=1 (profiling): the shared-ring tile kernel k_ew instead of k_ew_row
   static const int tile = [] {
     const char* e = std::getenv("BT_EW_KERNEL");

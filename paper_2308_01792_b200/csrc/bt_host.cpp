@@ -593,6 +593,7 @@ const EwTables& ew_tables(const bt_grid& g, const bt_form& f, int level) {
   std::vector<EwCell> cells;
   build_ew_cells(g, f, level, cells);
   t->cells.upload(cells);
+  t->host = cells;
   if (f.kind == BT_FORM_DIV_K_GRAD && f.coeff_kind == 1) build_ew_phase(g, level, t->cells.p, t->phase);
   if (g.ew_cache.size() >= 16) g.ew_cache.erase(g.ew_cache.begin());
   g.ew_cache.push_back(std::move(t));
@@ -823,6 +824,7 @@ bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks) {
   g->ew_scratch.release();
   for (auto& b : g->ew_rows) b.release();
   for (auto& b : g->ew_tiles) b.release();
+  for (auto& b : g->ew_rowtab) b.release();
   g->ew_nrows.fill(0);
   g->ew_ntiles.fill(0);
   g->d_partials.release();

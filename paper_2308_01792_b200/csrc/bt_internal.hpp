@@ -237,7 +237,7 @@ struct bt_grid {
   mutable std::vector<std::unique_ptr<bt::EwTables>> ew_cache;
   mutable bt::DevBuf<double> ew_scratch;  // ApplyMode::Add without a caller scratch
   // elementwise work lists per level (bt_ew.cu: row tasks, tile units), built on first use
-  mutable std::array<bt::DevBuf<int4>, 11> ew_rows, ew_tiles;
+  mutable std::array<bt::DevBuf<int4>, 11> ew_rows, ew_tiles, ew_rowtab;
   mutable std::array<int, 11> ew_nrows{}, ew_ntiles{};
   // reduction scratch for dot products
   mutable bt::DevBuf<double> d_partials;
@@ -266,6 +266,7 @@ struct EwTables {  // device tables of one (form, level) for the elementwise ker
   bt_form form{};
   int level = 0;
   DevBuf<EwCell> cells;
+  std::vector<EwCell> host;  // the same on the host (kernel-parameter weights)
   DevBuf<double> phase;  // sin-product phase tables of this handle's cells (build_ew_phase)
 };
 // per-cell sin/cos tables of the sin-product phases (k_ew_row), this handle's cells
@@ -371,7 +372,8 @@ struct SideStream {
 };
 SideStream& side_stream();
 void launch_elementwise(const bt_grid& g, int level, int coeff_kind, const double* c, const EwCell* d_cells,
-                        const double* x, double* y, bool diag_only, cudaStream_t s, const double* phase = nullptr);
+                        const double* x, double* y, bool diag_only, cudaStream_t s, const double* phase = nullptr,
+                        const EwCell* h_cells = nullptr);
 // local_matrix's positivity check of a div_k_grad coefficient (bt_ew.cu)
 void check_coefficient(const bt_grid& g, const bt_form& f, int level, const double* d_maps, cudaStream_t s);
 // per cell: the affine map (a row-major, b), built on first use (bt_kernels.cu)

@@ -799,7 +799,7 @@ bt_status bt_apply_elementwise(const bt_grid* g, const bt_form* form, int level,
     }
     out = scratch;
   }
-  launch_elementwise(*g, level, ck, c, t.cells.p, x, out, false, s, t.phase.p);
+  launch_elementwise(*g, level, ck, c, t.cells.p, x, out, false, s, t.phase.p, t.host.data());
   sync(*g, level, bc ? IF_SYNC_DIR : IF_SYNC, out, x, s);
   if (mode == BT_MODE_ADD) launch_vec(V_AXPY, y, out, 1.0, bt_space_size(g, BT_SPACE_P1, level), s);
   BT_CATCH
@@ -814,7 +814,7 @@ bt_status bt_extract_diagonal(const bt_grid* g, const bt_form* form, int level, 
   const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
   const double one[4] = {1.0, 0.0, 0.0, 0.0};
   const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
-  launch_elementwise(*g, level, ck, c, t.cells.p, nullptr, diag, true, s, t.phase.p);
+  launch_elementwise(*g, level, ck, c, t.cells.p, nullptr, diag, true, s, t.phase.p, t.host.data());
   sync(*g, level, IF_SYNC, diag, nullptr, s);
   BT_CATCH
 }

@@ -18,6 +18,7 @@ struct LevelData {
   std::unique_ptr<bt_stencil> stencil;  // stencil kernel
   DevBuf<EwCell> ew;                    // elementwise kernel tables
   DevBuf<double> phase;                 // sin-product phase tables (k_ew_row)
+  std::vector<EwCell> ew_host;          // host copy of ew (kernel-parameter weights)
   DevBuf<double> diag;
   double lambda = 0.0;
   // work vectors, allocated on first use (need()): the finest level of a
@@ -70,7 +71,7 @@ static void hier_apply(bt_hierarchy& h, int l, const double* x, double* y, int b
     const int ck = h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.coeff_kind : 0;
     static const double one[4] = {1.0, 0.0, 0.0, 0.0};
     launch_elementwise(*h.grid, l, ck, h.form.kind == BT_FORM_DIV_K_GRAD ? h.form.c : one, L.ew.p, x, y, false, s,
-                       L.phase.p);
+                       L.phase.p, L.ew_host.data());
   }
   sync(*h.grid, l, bc ? IF_SYNC_DIR : IF_SYNC, y, x, s);
 }
@@ -351,11 +352,12 @@ bt_status bt_hierarchy_create(const bt_grid* g, const bt_form* form, int kernel,
       std::vector<EwCell> cells;
       build_ew_cells(*g, *form, l, cells);
       L->ew.upload(cells);
+      L->ew_host = cells;
       const int ck = form->kind == BT_FORM_DIV_K_GRAD ? form->coeff_kind : 0;
       static const double one[4] = {1.0, 0.0, 0.0, 0.0};
       const double* c = form->kind == BT_FORM_DIV_K_GRAD ? form->c : one;
       if (ck == 1) build_ew_phase(*g, l, L->ew.p, L->phase);
-      launch_elementwise(*g, l, ck, c, L->ew.p, nullptr, L->diag.p, true, 0, L->phase.p);
+      launch_elementwise(*g, l, ck, c, L->ew.p, nullptr, L->diag.p, true, 0, L->phase.p, L->ew_host.data());
       sync(*g, l, IF_SYNC, L->diag.p, nullptr, 0);
     }
     h->levels.push_back(std::move(L));
