@@ -184,10 +184,12 @@ def roofline(bytes_, flops, sec, hbm_gbs, fp64_tflops, kernel, kernel_ms, share,
     return r
 
 
-def timed_steps(torch, step, K, W, stream, dist_max=False):
+def timed_steps(torch, step, K, W, stream, dist_max=False, per_step=True):
     """W untimed steps, then K steps between events (barrier + sync both
     sides); per-step events for the kernel share. Returns (total_ms, per-step
-    ms list)."""
+    ms list). per_step=False: the step is the measured kernels alone (configs 1
+    and 2), whose time is then the timed region / K; an event pair around
+    every ~90 us stencil apply costs ~5.5 us of it (measured on B200)."""
     for _ in range(W):
         step(None)
     torch.cuda.synchronize()
@@ -198,7 +200,7 @@ def timed_steps(torch, step, K, W, stream, dist_max=False):
     torch.cuda.synchronize()
     t0.record(stream)
     for q in range(K):
-        step(evs[q])
+        step(evs[q] if per_step else None)
     t1.record(stream)
     torch.cuda.synchronize()
     total = t0.elapsed_time(t1)
@@ -206,6 +208,8 @@ def timed_steps(torch, step, K, W, stream, dist_max=False):
         t = torch.tensor([total], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total = float(t.item())
+    if not per_step:
+        return total, [total / K] * K
     return total, [a.elapsed_time(b) for a, b in evs]
 
 
@@ -556,7 +560,8 @@ def run_config(cfg, args, bt, torch, ws, rank, hbm, fp64, extra=False):
     clocks.start()
     time.sleep(0.3)
     launches0 = L.bt_launch_count()
-    total_ms, kern = timed_steps(torch, step, K, max(W, 1 if cfg == 5 else 3), stream, dist_max=ws > 1)
+    total_ms, kern = timed_steps(torch, step, K, max(W, 1 if cfg == 5 else 3), stream, dist_max=ws > 1,
+                                 per_step=cfg not in (1, 2))
     launches = int(L.bt_launch_count() - launches0)
     if getattr(w, "graph_launches", 0):  # graph replays launch the captured kernels without host calls
         launches = w.graph_launches * K
@@ -565,10 +570,11 @@ def run_config(cfg, args, bt, torch, ws, rank, hbm, fp64, extra=False):
     value = w.dofs_per_step / (ms_step * 1e-3) / 1e9  # owned DoFs of the whole job (all ranks)
     kmean = float(np.mean(kern))
     rl = roofline(w.bytes, w.flops, kmean * 1e-3, hbm, fp64, w.kernel, kmean, kmean / ms_step)
-    if cfg == 2 and ws == 1:
+    if cfg in (2, 3, 4) and ws == 1:  # steady-state ncu DRAM bytes per apply (profiles/r2_traffic.json)
         try:
-            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-                rl["traffic"] = float(json.load(f)["apply_total"])
+            with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
+                rl["traffic"] = float(json.load(f)[f"config{cfg}"]["apply_total"])
+            rl["traffic_source"] = "profiles/r2_traffic.json (ncu --cache-control none, consecutive applies)"
         except Exception:
             pass
     # e2e through the public API with host buffers

@@ -958,7 +958,8 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
   // partitioned: the rank-spanning groups' partial rows go first, on the side
   // stream, so the exchange overlaps the interior marches; SMs are reserved
   // beside the persistent interior grid for it and the boundary kernel
-  const int reserve = part ? 12 : 0;
+  static const int env_reserve = getenv("BT_STENCIL_RESERVE") ? atoi(getenv("BT_STENCIL_RESERVE")) : -1;
+  const int reserve = env_reserve >= 0 ? env_reserve : (part ? 12 : 0);
   if (part && (parts & 8)) {
     const XPlan& p = xchg_plan(g, st.level);
     if (p.buf_size) {
