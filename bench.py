@@ -363,6 +363,7 @@ def setup_config(cfg, bt, torch, ws, rank):
         g = bt.Grid(text, lvl, lvl)
         if ws > 1:
             g.set_partition(rank, ws)
+            w.plane = g.data_plane()
         t = bt.compute_stencil(bt.FormId.diffusion(), g, lvl)
         x, y = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
         bt.random_fill(x, lvl, 0)
@@ -378,7 +379,8 @@ def setup_config(cfg, bt, torch, ws, rank):
         w.flops = 2.0 * 15 * slots * reps
         w.dofs_per_step = w.owned * reps
         w.kernel = "k_stencil_small (one launch)" if cfg == 1 else (
-            "k_stencil_fast || k_boundary" if ws == 1 else "k_stencil (per-cell rows) + exchange")
+            "k_stencil_fast || k_boundary" if ws == 1 else
+            "k_stencil_fast || k_boundary (rank-local groups) || k_xpartials + neighbour exchange")
         if cfg == 1:
             graph = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
@@ -424,6 +426,7 @@ def setup_config(cfg, bt, torch, ws, rank):
         g = bt.Grid(bt.blocked_mesh_text(4, 4, 4, (2, 2, 2), h=0.25, perturb=0.1, seed=0), lvl, lvl)
         if ws > 1:
             g.set_partition(rank, ws)
+            w.plane = g.data_plane()
         form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
         x, y = bt.allocate(bt.p1_space(), g), bt.allocate(bt.p1_space(), g)
         bt.random_fill(x, lvl, 0)
@@ -489,6 +492,7 @@ def setup_config(cfg, bt, torch, ws, rank):
         g = bt.Grid(bt.blocked_mesh_text(*dims, (4, 4, 4), h=0.125, perturb=0.1, seed=0), lo, hi)
         if ws > 1:
             g.set_partition(rank, ws)
+            w.plane = g.data_plane()
         form = bt.FormId.div_k_grad(bt.Coefficient.sin_product(1.0, 0.5, 2 * math.pi))
         h = bt.make_hierarchy(g, form, bt.KernelKind.Elementwise)
         rhs, x = bt.allocate(bt.p1_space(), g, lo, hi), bt.allocate(bt.p1_space(), g, lo, hi)
@@ -588,7 +592,9 @@ def run_config(cfg, args, bt, torch, ws, rank, hbm, fp64, extra=False):
            "ms_per_step": ms_step, "higher_is_better": True, "scaling": getattr(w, "scaling", "weak"),
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_fill seed 0, reference mt19937_64 stream)",
            "config": dict(w.config, config=cfg, parallelism=(
-               f"cells partitioned over {ws} ranks, memory-sharded vectors (NCCL interface exchange)"
+               f"cells partitioned over {ws} ranks, memory-sharded vectors, interface exchange inside libbt: "
+               + ("neighbour-only ncclSend/ncclRecv (bt_comm)" if getattr(w, "plane", "") == "nccl" else
+                  f"data plane {getattr(w, 'plane', '?')}")
                if ws > 1 else "1 GPU")),
            "roofline": rl,
            "e2e": {"value": e2e_value, "unit": "GDoF/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,

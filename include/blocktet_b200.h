@@ -50,6 +50,7 @@ typedef struct bt_grid bt_grid;           /* Grid (fe_function.hpp:92) */
 typedef struct bt_stencil bt_stencil;     /* StencilTable (operators.hpp:174) */
 typedef struct bt_hierarchy bt_hierarchy; /* GridHierarchy (solvers.hpp:308) */
 typedef struct bt_n1e1 bt_n1e1;           /* N1E1 curl-curl + mass operator (no ref) */
+typedef struct bt_comm bt_comm;           /* the ranks' NCCL communicator (multi-GPU data plane) */
 
 /* Bilinear form descriptor — FormId (forms.hpp:29-41). The reference's
  * std::function coefficient cannot cross to the device; div_k_grad takes an
@@ -301,6 +302,36 @@ bt_status bt_fmg(bt_hierarchy* h, int finest, const double* const* rhs_levels, d
  * order. */
 typedef int (*bt_allreduce_fn)(double* buf, int64_t n, void* stream, void* user);
 bt_status bt_grid_set_allreduce(bt_grid* g, bt_allreduce_fn fn, void* user);
+/* Native data plane (no hook, no Python): an NCCL communicator over the
+ * ranks, created by every rank from one unique id (rank 0 draws it with
+ * bt_comm_unique_id and the ranks share its 128 bytes out of band). With a
+ * communicator set (bt_grid_set_comm; it takes precedence over the hook):
+ *   - the interface exchange is neighbour-only: each rank sends to each peer
+ *     only its members of the rank-spanning groups it shares with that peer
+ *     and receives the peer's (grouped ncclSend / ncclRecv on the call's
+ *     stream), instead of an allreduce of the whole exchange buffer;
+ *   - dot partials are summed by ncclAllReduce.
+ * The communicator's (rank, nranks) must be the grid's partition. NCCL is
+ * loaded at bt_comm_create (libnccl.so.2, the one already in the process if
+ * any). The caller owns the communicator and destroys it after the grids
+ * that use it. */
+bt_status bt_comm_unique_id(uint8_t id[128]);
+bt_status bt_comm_create(const uint8_t id[128], int rank, int nranks, int device, bt_comm** out);
+void bt_comm_destroy(bt_comm* c);
+bt_status bt_grid_set_comm(bt_grid* g, bt_comm* c); /* NULL detaches */
+/* host-only neighbour plan of the P1 exchange of `rank`: which = 0 the
+ * (peer, buffer position) pairs it sends, 1 those it receives, in the order
+ * the messages carry them; NULL arrays query the count. -1 on error. */
+int64_t bt_xchg_peers_host(const char* mesh_text, int level, int rank, int nranks, int which, int32_t* peer,
+                           int32_t* pos);
+/* The same neighbour exchange over a caller transport (e.g. MPI, gloo): fn
+ * sends peer i the doubles sendbuf[send_off[i], send_off[i+1]) and receives
+ * recvbuf[recv_off[i], recv_off[i+1]) from it, for the npeers peers (ranks,
+ * ascending), stream-ordered like the allreduce hook; returns 0 on success.
+ * Used when no communicator is set; it takes precedence over the hook. */
+typedef int (*bt_sendrecv_fn)(int npeers, const int* peers, const int64_t* send_off, const int64_t* recv_off,
+                              const double* sendbuf, double* recvbuf, void* stream, void* user);
+bt_status bt_grid_set_sendrecv(bt_grid* g, bt_sendrecv_fn fn, void* user);
 /* pack + hook + finish in one call (mode as bt_xchg_finish) */
 bt_status bt_exchange(const bt_grid* g, int level, int mode, double* x, const double* src, void* stream);
 bt_status bt_grid_set_partition(bt_grid* g, int rank, int nranks);

@@ -125,6 +125,12 @@ SIGNATURES = {
     "bt_grid_set_allreduce": (I, [P, P, P]),
     "bt_exchange": (I, [P, I, I, P, P, P]),
     "bt_xchg_plan_host": (I64, [C.c_char_p, I, I, I, PI64, PI64, PI32, PI32, PI32, PU8]),
+    "bt_comm_unique_id": (I, [PU8]),
+    "bt_comm_create": (I, [PU8, I, I, I, C.POINTER(P)]),
+    "bt_comm_destroy": (None, [P]),
+    "bt_grid_set_comm": (I, [P, P]),
+    "bt_xchg_peers_host": (I64, [C.c_char_p, I, I, I, I, PI32, PI32]),
+    "bt_grid_set_sendrecv": (I, [P, P, P]),
 }
 
 

@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import math
+import os
 import traceback
 import weakref
 from dataclasses import dataclass, field
@@ -32,6 +33,8 @@ from ._lib import bt_field, bt_fmg_row, bt_form, bt_multigrid_config, bt_smoothe
 
 # bt_allreduce_fn: int (*)(double* buf, int64_t n, void* stream, void* user)
 _ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+_SENDRECV_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
 
 
 class _DeviceArray:
@@ -268,7 +271,7 @@ class Grid:
         return _L.bt_space_size(self._h, space, level)
 
     # ---- multi-GPU cell partition ---------------------------
-    def set_partition(self, rank: int, nranks: int, allreduce=None):
+    def set_partition(self, rank: int, nranks: int, allreduce=None, comm="auto"):
         """Restrict this handle's compute to the cell block of `rank` out of
         `nranks` (bt_grid_set_partition). `allreduce(tensor)` sums a device
         tensor over the ranks in place, stream-ordered on the current stream
@@ -277,7 +280,9 @@ class Grid:
         a partitioned grid hold the rank's cells only (space_size is local).
         The library calls `allreduce` itself (bt_grid_set_allreduce) inside
         syncs, dots, applies and solvers, which become collectives: every
-        rank calls them in the same order."""
+        rank calls them in the same order. `comm` ("auto", None or a Comm):
+        the native NCCL data plane, which replaces the hook (see set_comm);
+        "auto" creates it when torch.distributed runs over NCCL."""
         _check(_L.bt_grid_set_partition(self._h, rank, nranks))
         self._allreduce = allreduce
         self._xbufs = {}
@@ -299,6 +304,73 @@ class Grid:
 
         self._hook = _ALLREDUCE_FN(hook)
         _check(_L.bt_grid_set_allreduce(self._h, C.cast(self._hook, C.c_void_p), None))
+        # the native data plane (neighbour-only NCCL send/recv inside the
+        # library) whenever the ranks run torch.distributed over NCCL and no
+        # custom allreduce was given; BT_XCHG=hook keeps the Python hook
+        self._comm = None
+        self._sr_hook = None
+        mode = os.environ.get("BT_XCHG", "auto")  # auto | nccl | sendrecv | allreduce (A/B knob)
+        if comm == "auto":
+            comm = None
+            if allreduce is None and nranks > 1 and mode != "allreduce":
+                import torch.distributed as dist
+                if dist.is_available() and dist.is_initialized():
+                    if dist.get_backend() == "nccl" and mode != "sendrecv":
+                        comm = nccl_comm(rank, nranks, dev)
+                    else:
+                        self._set_sendrecv_torch()
+        if comm is not None:
+            self.set_comm(comm)
+
+    def _set_sendrecv_torch(self):
+        """The library's neighbour exchange over torch.distributed point-to-
+        point messages (bt_grid_set_sendrecv), staged through the host: the
+        transport for process groups without NCCL (gloo, CPU tests)."""
+        dev = self.device
+
+        def sr(npeers, peers, soff, roff, sbuf, rbuf, stream, user):
+            try:
+                import torch.distributed as dist
+                s = torch.cuda.ExternalStream(stream, device=dev) if stream else torch.cuda.default_stream(dev)
+                s.synchronize()
+                ns, nr = soff[npeers], roff[npeers]
+                send = torch.as_tensor(_DeviceArray(sbuf, ns), device=f"cuda:{dev}").cpu() if ns else None
+                recv = torch.empty(nr, dtype=torch.float64)
+                reqs = []
+                for i in range(npeers):
+                    if soff[i + 1] > soff[i]:
+                        reqs.append(dist.isend(send[soff[i]:soff[i + 1]].clone(), peers[i]))
+                    if roff[i + 1] > roff[i]:
+                        reqs.append(dist.irecv(recv[roff[i]:roff[i + 1]], peers[i]))
+                for r in reqs:
+                    r.wait()
+                if nr:
+                    torch.as_tensor(_DeviceArray(rbuf, nr), device=f"cuda:{dev}").copy_(recv)
+                    torch.cuda.synchronize(dev)
+                return 0
+            except Exception:  # reported as BT_RUNTIME_ERROR by the library
+                traceback.print_exc()
+                return 1
+
+        self._sr_hook = _SENDRECV_FN(sr)
+        _check(_L.bt_grid_set_sendrecv(self._h, C.cast(self._sr_hook, C.c_void_p), None))
+
+    def set_comm(self, comm: Optional["Comm"]):
+        """Attach the ranks' NCCL communicator (bt_grid_set_comm): the
+        library then exchanges interface values neighbour-only over NCCL and
+        sums dot partials with ncclAllReduce, with no Python on the path."""
+        _check(_L.bt_grid_set_comm(self._h, comm._h if comm is not None else None))
+        self._comm = comm
+
+    def data_plane(self) -> str:
+        """'nccl' (native neighbour exchange), 'sendrecv' (the neighbour
+        exchange over torch.distributed messages), 'allreduce' (the hook) or
+        'none'."""
+        if getattr(self, "_comm", None) is not None:
+            return "nccl"
+        if getattr(self, "_sr_hook", None) is not None:
+            return "sendrecv"
+        return "allreduce" if getattr(self, "_hook", None) is not None else "none"
 
     def partition(self):
         """(rank, nranks, cell_begin, cell_end)"""
@@ -536,6 +608,65 @@ def xchg_plan_host(mesh_text: str, level: int, rank: int, nranks: int) -> dict:
                          buf.ctypes.data_as(_lib.PI32), base.ctypes.data_as(_lib.PI32),
                          count.ctypes.data_as(_lib.PI32), d.ctypes.data_as(_lib.PU8))
     return {"buf_size": bs.value, "slot": slot, "buf": buf, "base": base, "count": count, "dir": d}
+
+
+def xchg_peers_host(mesh_text: str, level: int, rank: int, nranks: int) -> dict:
+    """The neighbour plan of one rank's P1 exchange, built on the host
+    (bt_xchg_peers_host): {"sends": (peer, pos), "recvs": (peer, pos)} int32
+    arrays in message order. For tests of the data plane on CPU."""
+    out = {}
+    for which, key in ((0, "sends"), (1, "recvs")):
+        n = _L.bt_xchg_peers_host(mesh_text.encode(), level, rank, nranks, which, None, None)
+        if n < 0:
+            raise InvalidArgument(_L.bt_last_error().decode())
+        peer = np.zeros(n, np.int32)
+        pos = np.zeros(n, np.int32)
+        _L.bt_xchg_peers_host(mesh_text.encode(), level, rank, nranks, which, peer.ctypes.data_as(_lib.PI32),
+                              pos.ctypes.data_as(_lib.PI32))
+        out[key] = (peer, pos)
+    return out
+
+
+class Comm:
+    """The ranks' NCCL communicator (bt_comm): the library's native
+    multi-GPU data plane. Every rank constructs it with the same 128-byte
+    unique id (Comm.unique_id() on one rank, shared out of band)."""
+
+    def __init__(self, unique_id: bytes, rank: int, nranks: int, device: int):
+        if len(unique_id) != 128:
+            raise InvalidArgument("Comm: the unique id is 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _check(_L.bt_comm_create(C.cast(buf, _lib.PU8), rank, nranks, device, C.byref(h)))
+        self._h = h
+        self.rank, self.nranks, self.device = rank, nranks, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(_L.bt_comm_unique_id(C.cast(buf, _lib.PU8)))
+        return bytes(buf)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _L.bt_comm_destroy(self._h)
+            self._h = None
+
+
+_COMMS: Dict[tuple, Comm] = {}
+
+
+def nccl_comm(rank: int, nranks: int, device: int) -> Comm:
+    """The process's Comm over the torch.distributed world (rank 0 draws
+    the id, broadcast over the default group), created once per
+    (rank, nranks, device) and kept for the life of the process."""
+    key = (rank, nranks, device)
+    if key not in _COMMS:
+        import torch.distributed as dist
+        obj = [Comm.unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        _COMMS[key] = Comm(obj[0], rank, nranks, device)
+    return _COMMS[key]
 
 
 def partition_range(n_cells: int, rank: int, nranks: int):

@@ -29,7 +29,7 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-fno-fast-math", "-ffp-contract=off"
              f"-I{CUDA_HOME}/include"]
 
 CU_SOURCES = ["bt_kernels.cu", "bt_stencil.cu", "bt_prism.cu", "bt_ew.cu", "bt_interface.cu", "bt_n1e1.cu", "bt_xchg.cu"]
-CXX_SOURCES = ["bt_host.cpp", "bt_solvers.cpp"]
+CXX_SOURCES = ["bt_host.cpp", "bt_solvers.cpp", "bt_comm.cpp"]
 
 
 def _deps(src=None):

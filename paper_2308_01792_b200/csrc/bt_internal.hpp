@@ -163,14 +163,38 @@ struct XPlan {
   // stencil apply, which computes this rank's members' partial rows straight
   // into the exchange buffer (k_xpartials, bt_stencil.cu)
   DevBuf<int4> d_pts;
+  // neighbour-only exchange (bt_comm): (peer, buffer position) of this
+  // rank's members of groups shared with the peer (sends), and of the peer's
+  // members of groups with a member here (recvs), in group order on every
+  // rank, so rank r's sends to p are p's recvs from r, entry for entry
+  std::vector<std::pair<int, int32_t>> sends, recvs;
+  // built on first exchange (exchange_buffer)
+  mutable bool nbr_built = false;
+  mutable std::vector<int> peers;                  // ascending
+  mutable std::vector<int64_t> send_off, recv_off;  // per peer, CSR (peers + 1)
+  mutable DevBuf<int32_t> d_send_pos, d_recv_pos;
+  mutable DevBuf<double> d_sendbuf, d_recvbuf;
   void reset() {
     built = false;
     buf_size = 0;
     entries.clear();
     d_entries.release();
     d_pts.release();
+    sends.clear();
+    recvs.clear();
+    nbr_built = false;
+    peers.clear();
+    send_off.clear();
+    recv_off.clear();
+    d_send_pos.release();
+    d_recv_pos.release();
+    d_sendbuf.release();
+    d_recvbuf.release();
   }
 };
+// record the neighbour traffic of one rank-spanning group: owner[m] is the
+// rank of member m, positions off .. off + count - 1
+void xplan_group_peers(XPlan& p, int rank, const int* owner, int count, int64_t off);
 
 // fast-kernel march schedule of one layer-group size (see bt_stencil.cu)
 struct FastTasks {
@@ -231,6 +255,9 @@ struct bt_grid {
   // the exchange itself inside syncs, dots and solvers
   bt_allreduce_fn allreduce = nullptr;
   void* allreduce_user = nullptr;
+  bt_comm* comm = nullptr;  // native data plane (bt_grid_set_comm), takes precedence over the hook
+  bt_sendrecv_fn sendrecv = nullptr;  // neighbour exchange over a caller transport (bt_grid_set_sendrecv)
+  void* sendrecv_user = nullptr;
   mutable bt::DevBuf<double> xbuf;       // exchange buffer of the library's own syncs
   mutable bt::DevBuf<double> dot_cells;  // per-cell dot partials of every cell (partitioned dots)
   // elementwise-kernel tables per (form, level), built on first use
@@ -331,6 +358,16 @@ void launch_interface(const bt_grid& g, int level, IfaceMode mode, double* v, co
 void sync(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s);
 // the grid's allreduce hook on n doubles (raises if none is set)
 void allreduce(const bt_grid& g, double* buf, int64_t n, cudaStream_t s);
+// the exchange step of a rank-spanning sync: buf holds this rank's members
+// (zeros elsewhere); afterwards every position of every group with a member
+// here holds its member's value. Neighbour-only send/recv over the grid's
+// communicator, else the allreduce hook.
+void exchange_buffer(const bt_grid& g, const XPlan& p, double* buf, cudaStream_t s);
+// NCCL (bt_comm.cpp): grouped send/recv with each peer, stream-ordered
+void comm_check(const bt_comm* c, int rank, int nranks);
+void comm_sendrecv(bt_comm* c, const std::vector<int>& peers, const std::vector<int64_t>& send_off,
+                   const std::vector<int64_t>& recv_off, const double* sendbuf, double* recvbuf, cudaStream_t s);
+void comm_allreduce(bt_comm* c, double* buf, int64_t n, cudaStream_t s);
 // assembled diagonal of a stencil table (collective on a partitioned grid)
 const double* stencil_diag(const bt_stencil& st, cudaStream_t s);
 // exchange for rank-spanning groups (bt_xchg.cu)

@@ -980,19 +980,23 @@ static void build_xplan_edges(const bt_grid& g, int level, XPlan& out) {
     for (int c = b; c < e; ++c) owner[c] = r;
   }
   const Topology& t = g.topo;
-  out.entries.clear();
+  out.reset();
   int64_t off = 0;
+  std::vector<int> own;
   auto add = [&](int count, int dir, auto&& member) {  // member(m, cell&, slot&, sign&)
+    own.resize(count);
     for (int m = 0; m < count; ++m) {
       int cell, sg;
       int64_t slot;
       member(m, cell, slot, sg);
+      own[m] = owner[cell];
       if (owner[cell] == g.part_rank) {
         XEntry e{slot, (int32_t)(off + m), (int32_t)off, count, dir};
         e.sign = sg;
         out.entries.push_back(e);
       }
     }
+    xplan_group_peers(out, g.part_rank, own.data(), count, off);
     off += count;
   };
   for (const DevFace& F : t.faces) {
@@ -1054,7 +1058,7 @@ void sync_edges(const bt_grid& g, int level, IfaceMode mode, double* v, const do
     if (needs_buf && p.buf_size) {
       if (g.xbuf.n < (size_t)p.buf_size) g.xbuf.alloc((size_t)p.buf_size);
       launch_xchg_pack_plan(p, shift, v, g.xbuf.p, s);
-      allreduce(g, g.xbuf.p, p.buf_size, s);
+      exchange_buffer(g, p, g.xbuf.p, s);
       buf = g.xbuf.p;
     }
     launch_edge_interface(g, level, mode, v, src, s);

@@ -971,7 +971,7 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
         k_xpartials<<<(ne + 127) / 128, 128, 0, ss.s2>>>(x, g.xbuf.p, p.d_entries.p, p.d_pts.p, ne, a);
         count_launch();
       }
-      allreduce(g, g.xbuf.p, p.buf_size, ss.s2);
+      exchange_buffer(g, p, g.xbuf.p, ss.s2);
       launch_xchg_combine(g, st.level, bc ? IF_SYNC_DIR : IF_SYNC, yl, xl, g.xbuf.p, ss.s2);
       BT_CUDA(cudaEventRecord(ss.join2, ss.s2));
     } else {

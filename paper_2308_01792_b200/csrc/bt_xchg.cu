@@ -79,12 +79,17 @@ void build_xplan(const Mesh& m, const Topology& t, int level, int rank, int nran
     partition_range(nc, r, nranks, b, e);
     for (int c = b; c < e; ++c) owner[c] = r;
   }
-  out.entries.clear();
+  out.reset();
   int64_t off = 0;
+  std::vector<int> own;
   auto add_group = [&](int count, int dir, auto&& slot_of_member, auto&& cell_of_member) {
-    for (int mm = 0; mm < count; ++mm)
-      if (owner[cell_of_member(mm)] == rank)
+    own.resize(count);
+    for (int mm = 0; mm < count; ++mm) {
+      own[mm] = owner[cell_of_member(mm)];
+      if (own[mm] == rank)
         out.entries.push_back(XEntry{slot_of_member(mm), (int32_t)(off + mm), (int32_t)off, count, dir});
+    }
+    xplan_group_peers(out, rank, own.data(), count, off);
     off += count;
   };
   // shared macro faces: interior points (a, b), weights (n - a - b, a, b)
@@ -133,6 +138,24 @@ void build_xplan(const Mesh& m, const Topology& t, int level, int rank, int nran
   if (off > INT32_MAX) raise(BT_OUT_OF_RANGE, "exchange buffer exceeds 2^31 entries");
   out.buf_size = off;
   out.built = true;
+}
+
+void xplan_group_peers(XPlan& p, int rank, const int* owner, int count, int64_t off) {
+  bool here = false;
+  for (int m = 0; m < count; ++m) here = here || owner[m] == rank;
+  if (!here) return;
+  for (int m = 0; m < count; ++m) {
+    if (owner[m] != rank) {
+      p.recvs.emplace_back(owner[m], (int32_t)(off + m));
+      continue;
+    }
+    // this member goes once to every other rank of the group
+    for (int q = 0; q < count; ++q) {
+      bool first = owner[q] != rank;
+      for (int r = 0; r < q && first; ++r) first = owner[r] != owner[q];
+      if (first) p.sends.emplace_back(owner[q], (int32_t)(off + m));
+    }
+  }
 }
 
 const XPlan& xchg_plan(const bt_grid& g, int level) {
@@ -199,10 +222,82 @@ void launch_xchg_combine_plan(const XPlan& p, int64_t shift, IfaceMode mode, dou
 }
 
 void allreduce(const bt_grid& g, double* buf, int64_t n, cudaStream_t s) {
+  if (g.comm) {
+    comm_check(g.comm, g.part_rank, g.part_nranks);
+    comm_allreduce(g.comm, buf, n, s);
+    return;
+  }
   if (!g.allreduce)
     raise(BT_LOGIC_ERROR, "partitioned grid: this call needs the ranks' allreduce (bt_grid_set_allreduce)");
   // stream-ordered: the hook enqueues the collective on s (or blocks until done)
   if (g.allreduce(buf, n, (void*)s, g.allreduce_user) != 0) raise(BT_RUNTIME_ERROR, "allreduce hook failed");
+}
+
+namespace {
+__global__ void __launch_bounds__(kT) k_xgather(const int32_t* __restrict__ pos, int64_t n,
+                                                const double* __restrict__ buf, double* __restrict__ out) {
+  const int64_t q = (int64_t)blockIdx.x * kT + threadIdx.x;
+  if (q < n) out[q] = buf[pos[q]];
+}
+__global__ void __launch_bounds__(kT) k_xscatter(const int32_t* __restrict__ pos, int64_t n,
+                                                 const double* __restrict__ in, double* __restrict__ buf) {
+  const int64_t q = (int64_t)blockIdx.x * kT + threadIdx.x;
+  if (q < n) buf[pos[q]] = in[q];
+}
+
+// per-peer CSR of the plan's (peer, position) lists; messages keep the
+// build (group) order, which every rank shares
+void build_neighbours(const XPlan& p) {
+  if (p.nbr_built) return;
+  std::vector<int> peers;
+  for (const auto& e : p.sends) peers.push_back(e.first);
+  for (const auto& e : p.recvs) peers.push_back(e.first);
+  std::sort(peers.begin(), peers.end());
+  peers.erase(std::unique(peers.begin(), peers.end()), peers.end());
+  auto csr = [&](const std::vector<std::pair<int, int32_t>>& v, std::vector<int64_t>& off, DevBuf<int32_t>& d) {
+    off.assign(peers.size() + 1, 0);
+    std::vector<int32_t> pos;
+    pos.reserve(v.size());
+    for (size_t i = 0; i < peers.size(); ++i) {
+      for (const auto& e : v)
+        if (e.first == peers[i]) pos.push_back(e.second);
+      off[i + 1] = (int64_t)pos.size();
+    }
+    d.upload(pos);
+  };
+  csr(p.sends, p.send_off, p.d_send_pos);
+  csr(p.recvs, p.recv_off, p.d_recv_pos);
+  p.d_sendbuf.alloc(p.send_off.back());
+  p.d_recvbuf.alloc(p.recv_off.back());
+  p.peers = std::move(peers);
+  p.nbr_built = true;
+}
+}  // namespace
+
+void exchange_buffer(const bt_grid& g, const XPlan& p, double* buf, cudaStream_t s) {
+  if (!g.comm && !g.sendrecv) {
+    allreduce(g, buf, p.buf_size, s);
+    return;
+  }
+  if (g.comm) comm_check(g.comm, g.part_rank, g.part_nranks);
+  build_neighbours(p);
+  if (p.peers.empty()) return;
+  const int64_t ns = p.send_off.back(), nr = p.recv_off.back();
+  if (ns) {
+    k_xgather<<<(unsigned)((ns + kT - 1) / kT), kT, 0, s>>>(p.d_send_pos.p, ns, buf, p.d_sendbuf.p);
+    count_launch();
+  }
+  if (g.comm) {
+    comm_sendrecv(g.comm, p.peers, p.send_off, p.recv_off, p.d_sendbuf.p, p.d_recvbuf.p, s);
+  } else if (g.sendrecv((int)p.peers.size(), p.peers.data(), p.send_off.data(), p.recv_off.data(), p.d_sendbuf.p,
+                        p.d_recvbuf.p, (void*)s, g.sendrecv_user) != 0) {
+    raise(BT_RUNTIME_ERROR, "sendrecv hook failed");
+  }
+  if (nr) {
+    k_xscatter<<<(unsigned)((nr + kT - 1) / kT), kT, 0, s>>>(p.d_recv_pos.p, nr, p.d_recvbuf.p, buf);
+    count_launch();
+  }
+  check_launch("exchange_buffer");
 }
 
 void sync(const bt_grid& g, int level, IfaceMode mode, double* v, const double* src, cudaStream_t s) {
@@ -212,7 +307,7 @@ void sync(const bt_grid& g, int level, IfaceMode mode, double* v, const double* 
     if (needs_buffer(mode) && p.buf_size) {
       if (g.xbuf.n < (size_t)p.buf_size) g.xbuf.alloc((size_t)p.buf_size);
       launch_xchg_pack(g, level, v, g.xbuf.p, s);
-      allreduce(g, g.xbuf.p, p.buf_size, s);
+      exchange_buffer(g, p, g.xbuf.p, s);
       buf = g.xbuf.p;
     }
     launch_interface(g, level, mode, v, src, s);
@@ -280,6 +375,44 @@ bt_status bt_grid_set_allreduce(bt_grid* g, bt_allreduce_fn fn, void* user) {
   g->allreduce = fn;
   g->allreduce_user = user;
   BT_CATCH
+}
+
+bt_status bt_grid_set_comm(bt_grid* g, bt_comm* c) {
+  BT_TRY
+  if (!g) raise(BT_INVALID_ARGUMENT, "bt_grid_set_comm: grid required");
+  if (c) comm_check(c, g->part_rank, g->part_nranks);
+  g->comm = c;
+  BT_CATCH
+}
+
+bt_status bt_grid_set_sendrecv(bt_grid* g, bt_sendrecv_fn fn, void* user) {
+  BT_TRY
+  if (!g) raise(BT_INVALID_ARGUMENT, "bt_grid_set_sendrecv: grid required");
+  g->sendrecv = fn;
+  g->sendrecv_user = user;
+  BT_CATCH
+}
+
+int64_t bt_xchg_peers_host(const char* mesh_text, int level, int rank, int nranks, int which, int32_t* peer,
+                           int32_t* pos) {
+  try {
+    if (!mesh_text || level < 1 || level > 10 || nranks < 1 || rank < 0 || rank >= nranks || which < 0 || which > 1)
+      raise(BT_INVALID_ARGUMENT, "bt_xchg_peers_host: bad arguments");
+    const Mesh m = parse_mesh(mesh_text);
+    Topology t;
+    build_topology(m, t);
+    XPlan p;
+    build_xplan(m, t, level, rank, nranks, p);
+    const auto& v = which ? p.recvs : p.sends;
+    for (size_t q = 0; q < v.size(); ++q) {
+      if (peer) peer[q] = v[q].first;
+      if (pos) pos[q] = v[q].second;
+    }
+    return (int64_t)v.size();
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return -1;
+  }
 }
 
 bt_status bt_exchange(const bt_grid* g, int level, int mode, double* x, const double* src, void* stream) {

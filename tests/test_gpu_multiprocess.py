@@ -1,10 +1,12 @@
 """The library's own exchange across real processes.
 
 Two processes (torch.multiprocessing, gloo process group over 127.0.0.1), each
-with its own bt_grid partitioned by Grid.set_partition(rank, 2) and the
-DEFAULT allreduce hook (torch.distributed.all_reduce on the library's
-exchange buffer, called by the library itself inside every collective
-entry point). Each process also runs the same program on an unpartitioned
+with its own bt_grid partitioned by Grid.set_partition(rank, 2): once with
+the default data plane for a non-NCCL group (the library's neighbour-only
+exchange, torch.distributed send/recv as the transport) and once with the
+allreduce hook (torch.distributed.all_reduce on the library's exchange
+buffer), both called by the library itself inside every collective entry
+point. Each process also runs the same program on an unpartitioned
 grid and checks its slice of every result bitwise: apply_stencil (both BCs),
 the elementwise apply, diagonals and transfers, a V-cycle with Chebyshev
 smoothing and coarse CG (solution, residual norms and CG history), and the
@@ -33,8 +35,9 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, failures):
+def _worker(rank, world, port, failures, xchg):
     try:
+        os.environ["BT_XCHG"] = xchg
         import paper_2308_01792_b200 as bt
         from test_gpu_partition_solvers import n1e1_body, operators_body, vcycle_body
 
@@ -42,7 +45,8 @@ def _worker(rank, world, port, failures):
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
         try:
             def part(g):
-                g.set_partition(rank, world)  # default hook: torch.distributed.all_reduce
+                g.set_partition(rank, world)  # default data plane for a gloo group
+                assert g.data_plane() == ("allreduce" if xchg == "allreduce" else "sendrecv")
 
             text = bt.cubes_mesh_text(2, 0.1, 0)
             L = 4
@@ -75,8 +79,12 @@ def _worker(rank, world, port, failures):
         raise
 
 
-def test_library_exchange_two_processes():
+@pytest.mark.parametrize("xchg", ["auto", "allreduce"])
+def test_library_exchange_two_processes(xchg):
+    """auto: the library's neighbour-only exchange (gather, per-peer
+    messages, scatter) with torch.distributed as the transport; allreduce:
+    the allreduce hook over the whole exchange buffer."""
     ctx = mp.get_context("spawn")
     failures = ctx.Queue()
-    mp.start_processes(_worker, args=(2, _free_port(), failures), nprocs=2, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(2, _free_port(), failures, xchg), nprocs=2, join=True, start_method="spawn")
     assert failures.empty()
