@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbt_b200.so")
+# BT_LIB_PATH: profiling aid (scripts/build_variants.py builds ablated copies of the library)
+LIB_PATH = os.environ.get("BT_LIB_PATH") or os.path.join(_HERE, "libbt_b200.so")
 
 P = C.c_void_p
 D = C.c_double

@@ -9,6 +9,8 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <map>
+#include <memory>
 #include <vector>
 
 #include "../../include/blocktet_b200.h"
@@ -197,10 +199,21 @@ struct XPlan {
 void xplan_group_peers(XPlan& p, int rank, const int* owner, int count, int64_t off);
 
 // fast-kernel march schedule of one layer-group size (see bt_stencil.cu)
+// A balanced per-warp schedule of the fast marches of one chunk of cells for
+// a grid of G persistent warps (bt_stencil.cu: build_sched)
+struct FastSched {
+  DevBuf<int4> d_tasks;  // slot s of warp g at s * G + g; empty slots are null tasks (w < z)
+  int ntasks = 0;        // slots * G
+};
 struct FastTasks {
   DevBuf<int4> d_tasks;
   int ntasks = 0;
   std::vector<int> chunk_first;  // first task of each kMaxCells-cell chunk (+ end)
+  // whole column segments (k, column block, j0, j1) of one cell, unsplit: the
+  // source of the balanced schedules, built per (chunk, G) on first use
+  std::vector<int4> segs;
+  mutable std::map<std::pair<int, int>, std::unique_ptr<FastSched>> sched;
+  mutable DevBuf<int> d_ctr;  // dynamic schedule: task queue head + finished-warp count (self-resetting)
 };
 struct EwCell;
 struct EwTables;

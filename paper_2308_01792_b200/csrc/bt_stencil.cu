@@ -44,6 +44,19 @@
 
 namespace bt {
 
+#ifndef BT_FAST2
+#define BT_FAST2 1  // 0: the round-1 consumer (two window sets, 8-byte stores)
+#endif
+#ifndef BT_ST16
+#define BT_ST16 0  // 1: 16-byte stores of address-aligned pairs
+#endif
+#ifndef BT_STQ
+#define BT_STQ ""  // cache qualifier of the march's stores (profiling: ".cg", ".cs", ".wt")
+#endif
+#ifndef BT_ABL
+#define BT_ABL 0  // profiling ablations of the fast march (scripts/build_variants.py); 0 in the product
+#endif
+
 namespace {
 constexpr int kMarchRows = 32;
 // small problems (all slots of the handle <= kSmallSlots): one launch for the
@@ -72,7 +85,10 @@ struct FastParams {
 constexpr int kMaxCells = 256;  // 256 * 8 * 8 B = 16 KB of kernel parameters
 
 // per-warp staging ring: kStages stages x (N + 2) staged rows of kRowD doubles
-constexpr int kStages = 4;
+#ifndef BT_STAGES
+#define BT_STAGES 3  // measured: 3 beats 4 (more L1 beside the rings) and 2
+#endif
+constexpr int kStages = BT_STAGES;
 constexpr int kRowD = 64;  // staged columns [base - 2, base + 62)
 constexpr int kFT = 128;   // k_stencil_fast block
 constexpr int kFW = kFT / 32;
@@ -115,11 +131,29 @@ struct Win {
 // any march of any cell runs here, whatever the vector's extent.
 // (body shared by k_stencil_fast and the single-launch k_stencil_small: block
 // vblock of a vgrid-block persistent grid)
+// predicated stores of the fast march (one SETP + one predicated STG each, no branches)
+__device__ __forceinline__ void st_if(double* p, double v, int ly, int thr) {  // *p = v if ly > thr
+  asm volatile("{ .reg .pred q; setp.gt.s32 q, %2, %3; @q st.global" BT_STQ ".f64 [%0], %1; }" ::"l"(p), "d"(v), "r"(ly), "r"(thr)
+               : "memory");
+}
+// (p[0], p[1]) = (a, b), p 16-byte aligned: one 16-byte store if ly > ta and ly > tb, else the valid half
+__device__ __forceinline__ void st_pair(double* p, double a, double b, int ly, int ta, int tb) {
+  asm volatile(
+      "{ .reg .pred qa, qb, qab, qa1, qb1;\n"
+      "setp.gt.s32 qa, %3, %4; setp.gt.s32 qb, %3, %5;\n"
+      "and.pred qab, qa, qb; and.pred qa1, qa, !qb; and.pred qb1, qb, !qa;\n"
+      "@qab st.global.v2.f64 [%0], {%1, %2};\n"
+      "@qa1 st.global.f64 [%0], %1;\n"
+      "@qb1 st.global.f64 [%0+8], %2; }" ::"l"(p),
+      "d"(a), "d"(b), "r"(ly), "r"(ta), "r"(tb)
+      : "memory");
+}
+
 template <int N, int kMaxC>
 __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, double* __restrict__ y,
                                                   const int4* __restrict__ tasks, int ntasks, int w,
                                                   int64_t cell_slots, const FastParams<kMaxC>& fp, int vblock,
-                                                  int vgrid, double* ring_all) {
+                                                  int vgrid, double* ring_all, int* __restrict__ ctr = nullptr) {
   constexpr int NS = N + 2;  // staged rows per step: C (layer k-1), layers k..k+N-1, Q (layer k+N)
   constexpr int kStageD = NS * kRowD;
   // warp index and task words broadcast by shuffles: provably warp-uniform, so
@@ -127,8 +161,24 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int G = vgrid * kFW;
   const int t0 = vblock * kFW + warp;
-  if (t0 >= ntasks) return;
+  // ctr != nullptr: dynamic schedule. Warps draw tasks (sorted longest first)
+  // from the queue ctr[0] as they finish, so SMs that run slower (the two
+  // dies' different distances to a cell's memory) take fewer tasks; the
+  // producer, which runs ahead of the consumer, hands each task word over
+  // through a four-deep per-warp ring in shared memory. ctr[1] counts
+  // finished warps; the last one resets both for the next launch.
+  const bool dyn = ctr != nullptr;
+  if (!dyn && t0 >= ntasks) return;
   const double* ring = ring_all + warp * ring_doubles<N>();
+  int4* fifo = reinterpret_cast<int4*>(ring_all + kFW * ring_doubles<N>()) + 4 * warp;
+  const int4 kNull = make_int4(1, 0, 1, -1);  // no steps (w - z + 2 == 0)
+  auto draw = [&]() -> int4 {  // the next task of the queue (dynamic schedule)
+    int i = 0;
+    if (lane == 0) i = atomicAdd(ctr, 1);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    return i < ntasks ? tasks[i] : kNull;
+  };
+  int pn = 0, cn = 0;  // task words pushed / popped
   const uint32_t my_s = smem_u32(ring) + 8u * lane;
 
   // ---- producer (every lane copies its two columns of each staged row) ----
@@ -138,9 +188,13 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
   int pt = t0, pr = 0, pleft = 0, pcol = 0;
   int po[NS];
   const double* pcell = x;
-  int4 pnext = tasks[t0];
+  int4 pnext = dyn ? draw() : tasks[t0];
   auto p_start = [&]() {
     const int4 tk = pnext;
+    if (dyn) {
+      if (lane == 0) fifo[pn & 3] = tk;
+      ++pn;
+    }
     const int k = tk.x, base = kFastCols * (tk.y & 0xffff), cl = tk.y >> 16;
     const int j = tk.z - 2, cb = base - 2 + lane;
     pcol = cb;  // this lane's first staged column (the second is pcol + 32)
@@ -151,7 +205,11 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     po[N + 1] = cb + row_start(w, j, k + N);
     pr = w - k - j - 1;
     pleft = tk.w - tk.z + 2;
-    if (pt + G < ntasks) pnext = tasks[pt + G];
+    if (dyn) {
+      if (pleft > 0) pnext = draw();
+    } else if (pt + G < ntasks) {
+      pnext = tasks[pt + G];
+    }
   };
   p_start();
   int ps = 0;  // producer stage
@@ -162,16 +220,18 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
       for (int s = 0; s < NS; ++s) {
         // length of stream s's current row; columns past it are never used
         const int len = s == 0 ? pr + 1 : (s <= N ? pr - (s - 1) : pr + 1 - N);
-        const double* src = pcell + po[s];
-        if ((unsigned)pcol < (unsigned)len) cp8(d + s * kRowD * 8, src);
-        if (pcol + 32 < len) cp8(d + s * kRowD * 8 + 256, src + 32);
+        const double* src = (BT_ABL & 32) ? x + (int64_t)(t0 % G) * 4096 + s * 512 + lane : pcell + po[s];
+        if (!(BT_ABL & 8) || w < 0) {
+          if ((unsigned)pcol < (unsigned)len) cp8(d + s * kRowD * 8, src);
+          if (pcol + 32 < len) cp8(d + s * kRowD * 8 + 256, src + 32);
+        }
         po[s] += len;  // next row of the stream
       }
       ps = ps == kStages - 1 ? 0 : ps + 1;
       --pr;
       if (--pleft == 0) {
         pt += G;
-        if (pt < ntasks) p_start();
+        if (dyn || pt < ntasks) p_start();
       }
     }
     cp_commit();
@@ -201,14 +261,133 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     produce();
   };
 
+#if BT_FAST2
+  // Window rows rotate through three register sets (phase p: row j-1 in set
+  // p, row j in set p+1, the step's new row j+1 into set p+2, all mod 3), so
+  // the march loop, unrolled over the three phases, moves no registers.
+  Row2 R[3][N], Cc[3], Qq[3];
+  const unsigned ybits = (unsigned)(reinterpret_cast<uintptr_t>(y) >> 3);
 #pragma unroll 1
-  for (int t = t0; t < ntasks; t += G) {
-    int4 tk = tasks[t];
+  for (int t = t0; dyn || t < ntasks; t += G) {
+    int4 tk;
+    if (dyn) {
+      __syncwarp();
+      tk = fifo[cn & 3];
+      ++cn;
+    } else {
+      tk = tasks[t];
+    }
     tk.x = __shfl_sync(0xffffffffu, tk.x, 0);
     tk.y = __shfl_sync(0xffffffffu, tk.y, 0);
     tk.z = __shfl_sync(0xffffffffu, tk.z, 0);
     tk.w = __shfl_sync(0xffffffffu, tk.w, 0);
     const int k = tk.x, blk = tk.y & 0xffff, cl = tk.y >> 16, j0 = tk.z, j1 = tk.w;
+    if (j1 < j0) break;  // null task: the end of this warp's list in a balanced schedule (build_sched)
+    double W[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) W[d] = fp.w[cl][d];
+    const int base = kFastCols * blk;
+    const int c0 = base - 2 + 2 * lane;  // this lane's two columns: c0, c0 + 1
+    const bool out = lane >= 1 && lane <= 30;
+    const int pmin = blk == 0 ? 3 : 0;  // shorter rows of column block 0 are not interior rows
+    // Store thresholds: column c of a row of length LY is an interior output
+    // iff 0 < c < LY - 1 (row ends are the boundary kernel's) and LY >= pmin,
+    // i.e. LY > max(c + 1, pmin - 1). T0 / T1: this lane's c0 / c0 + 1; T2:
+    // the next lane's c0 (= c0 + 2), stored by this lane when the row's
+    // address parity pairs it with this lane's c0 + 1.
+    constexpr int kNever = 1 << 30;
+    const int T0 = out && c0 > 0 ? max(c0 + 1, pmin - 1) : kNever;
+    const int T1 = out ? max(c0 + 2, pmin - 1) : kNever;
+    const int T2 = lane <= 29 && c0 + 2 > 0 ? max(c0 + 3, pmin - 1) : kNever;
+    {
+      Row2 cj, qj;
+      consume(cj, R[0], qj);         // phantom step j0 - 2: rows j0 - 1
+      consume(Cc[0], R[1], Qq[0]);   // phantom step j0 - 1: rows j0, C(j0), Q(j0 - 1)
+    }
+    int LA = w - k - j0;  // length of row j of layer k; layer k+q's is LA - q
+    const int64_t celloff = (int64_t)cl * cell_slots;
+    double* __restrict__ yl = y + celloff + c0;  // + a row's start: this lane's c0 in that row
+    const unsigned ypar = ybits + (unsigned)celloff;  // parity of (yl + oy) is that of ypar + oy (c0 is even)
+    int oy[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) oy[q] = row_start(w, j0, k + q);
+    int j = j0;
+
+    // One layer's output row at columns c0 (s0) and c0 + 1 (s1): see the
+    // formula at the other body. Stored as one 16-byte store per lane: of
+    // (c0, c0 + 1) when that pair is 16-byte aligned in y, else of (c0 + 1,
+    // next lane's c0); pairs broken by a row end fall back to 8-byte stores.
+    auto layer = [&](const Row2& a, const Row2& b, const Row2& c, const Row2& am1, const Row2& A1, const Row2& B0,
+                     const Row2& C1, int LY, int o) {
+      const double upv = fma(W[7], C1.v1, fma(W[5], B0.v1, fma(W[4], A1.v1, W[1] * a.v1)));  // to column c1 + 1
+      const double dnv = fma(W[7], b.v0, fma(W[5], c.v0, fma(W[4], am1.v0, W[1] * a.v0)));   // to column c0 - 1
+      const double lft = __shfl_up_sync(0xffffffffu, upv, 1);    // column c0 - 1's, for c0
+      const double rgt = __shfl_down_sync(0xffffffffu, dnv, 1);  // column c1 + 1's, for c1
+      double s0 = fma(W[6], C1.v0 + b.v0, fma(W[3], B0.v0 + c.v0, fma(W[2], A1.v0 + am1.v0, W[0] * a.v0)));
+      double s1 = fma(W[6], C1.v1 + b.v1, fma(W[3], B0.v1 + c.v1, fma(W[2], A1.v1 + am1.v1, W[0] * a.v1)));
+      s0 += lft;
+      s0 += fma(W[7], b.v1, fma(W[5], c.v1, fma(W[4], am1.v1, W[1] * a.v1)));  // i+1 of c0 = own c1
+      s1 += fma(W[7], C1.v0, fma(W[5], B0.v0, fma(W[4], A1.v0, W[1] * a.v0)));  // i-1 of c1 = own c0
+      s1 += rgt;
+#if BT_ST16
+      double* p = yl + o;
+      if ((ypar + (unsigned)o) & 1u) {  // warp-uniform
+        const double nx = __shfl_down_sync(0xffffffffu, s0, 1);  // the next lane's c0
+        st_pair(p + 1, s1, nx, LY, T1, T2);
+      } else {
+        st_pair(p, s0, s1, LY, T0, T1);
+      }
+#else
+      double* p;
+      asm("mad.wide.s32 %0, %1, 8, %2;" : "=l"(p) : "r"(o), "l"(yl));
+      st_if(p, s0, LY, T0);
+      st_if(p + 1, s1, LY, T1);
+#endif
+    };
+    // phase P: am1 = R[P], a = R[P+1], new rows into R[P+2] (mod 3); c / C1 and qm1 / Q0 likewise in Cc, Qq
+#define BT_STEP(P)                                                                                       \
+  {                                                                                                      \
+    constexpr int im = (P) % 3, ia = ((P) + 1) % 3, in = ((P) + 2) % 3;                                  \
+    consume(Cc[ia], R[in], Qq[ia]);                                                                      \
+    _Pragma("unroll") for (int q = 0; q < N; ++q) {                                                      \
+      const int qu = q < N - 1 ? q + 1 : q, ql = q > 0 ? q - 1 : q; /* in-range indices */               \
+      const Row2& b = q < N - 1 ? R[im][qu] : Qq[im];                                                    \
+      const Row2& B0 = q < N - 1 ? R[ia][qu] : Qq[ia];                                                   \
+      const Row2& c = q > 0 ? R[ia][ql] : Cc[im];                                                        \
+      const Row2& Cn = q > 0 ? R[in][ql] : Cc[ia];                                                       \
+      layer(R[ia][q], b, c, R[im][q], R[in][q], B0, Cn, LA - q, oy[q]);                                  \
+      oy[q] += LA - q;                                                                                   \
+    }                                                                                                    \
+    --LA;                                                                                                \
+    ++j;                                                                                                 \
+  }
+    while (true) {
+      BT_STEP(0)
+      if (j >= j1) break;
+      BT_STEP(1)
+      if (j >= j1) break;
+      BT_STEP(2)
+      if (j >= j1) break;
+    }
+#undef BT_STEP
+  }
+#else
+#pragma unroll 1
+  for (int t = t0; dyn || t < ntasks; t += G) {
+    int4 tk;
+    if (dyn) {
+      __syncwarp();
+      tk = fifo[cn & 3];
+      ++cn;
+    } else {
+      tk = tasks[t];
+    }
+    tk.x = __shfl_sync(0xffffffffu, tk.x, 0);
+    tk.y = __shfl_sync(0xffffffffu, tk.y, 0);
+    tk.z = __shfl_sync(0xffffffffu, tk.z, 0);
+    tk.w = __shfl_sync(0xffffffffu, tk.w, 0);
+    const int k = tk.x, blk = tk.y & 0xffff, cl = tk.y >> 16, j0 = tk.z, j1 = tk.w;
+    if (j1 < j0) break;  // null task: the end of this warp's list in a balanced schedule (build_sched)
     double W[8];
 #pragma unroll
     for (int d = 0; d < 8; ++d) W[d] = fp.w[cl][d];
@@ -229,6 +408,10 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     double* __restrict__ py[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) py[q] = y + (int64_t)cl * cell_slots + row_start(w, j0, k + q);
+#if BT_ABL & 16
+#pragma unroll
+    for (int q = 0; q < N; ++q) py[q] = y + (int64_t)(t0 % G) * 4096 + q * 512 - base;
+#endif
     const int pmin = blk == 0 ? 3 : 0;  // shorter rows of column block 0 are not interior rows
     int j = j0;
 
@@ -247,8 +430,12 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
       // expressions per column, so the two kernels agree bit for bit
       const double upv = fma(W[7], C1.v1, fma(W[5], B0.v1, fma(W[4], A1.v1, W[1] * a.v1)));  // to column c1 + 1
       const double dnv = fma(W[7], b.v0, fma(W[5], c.v0, fma(W[4], am1.v0, W[1] * a.v0)));   // to column c0 - 1
+#if BT_ABL & 2
+      const double lft = upv, rgt = dnv;
+#else
       const double lft = __shfl_up_sync(0xffffffffu, upv, 1);    // column c0 - 1's, for c0
       const double rgt = __shfl_down_sync(0xffffffffu, dnv, 1);  // column c1 + 1's, for c1
+#endif
       double s0 = fma(W[6], C1.v0 + b.v0, fma(W[3], B0.v0 + c.v0, fma(W[2], A1.v0 + am1.v0, W[0] * a.v0)));
       double s1 = fma(W[6], C1.v1 + b.v1, fma(W[3], B0.v1 + c.v1, fma(W[2], A1.v1 + am1.v1, W[0] * a.v1)));
       // every column: (centre + its i-1 partial) + its i+1 partial
@@ -256,6 +443,13 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
       s0 += fma(W[7], b.v1, fma(W[5], c.v1, fma(W[4], am1.v1, W[1] * a.v1)));  // i+1 of c0 = own c1
       s1 += fma(W[7], C1.v0, fma(W[5], B0.v0, fma(W[4], A1.v0, W[1] * a.v0)));  // i-1 of c1 = own c0
       s1 += rgt;
+#if BT_ABL & 4
+      s0 = (a.v0 + A1.v0) + (B0.v0 + C1.v0) + lft;
+      s1 = (a.v1 + A1.v1) + (B0.v1 + C1.v1) + rgt;
+#endif
+#if BT_ABL & 1
+      ok = ok && w < 0;
+#endif
       // row ends (i = 0, i = LY - 1) are the boundary kernel's
       if (ok && out && c0 < LY - 1 && c0 > 0) py_[c0] = s0;
       if (ok && out && c1 < LY - 1) py_[c1] = s1;
@@ -271,7 +465,7 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
       const Row2& c = q > 0 ? cur.a[ql] : cur.c;                                                    \
       const Row2& Cn = q > 0 ? A1[ql] : C1;                                                         \
       layer(cur.a[q], b, c, cur.am1[q], A1[q], B0, Cn, LA - q, py[q], LA - q >= pmin);              \
-      py[q] += LA - q;                                                                              \
+      if (!(BT_ABL & 16)) py[q] += LA - q;                                                          \
     }                                                                                               \
     --LA;                                                                                           \
     ++j;                                                                                            \
@@ -290,15 +484,24 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     }
 #undef BT_STEP
   }
+#endif
   cp_wait<0>();
+  if (dyn && lane == 0) {
+    const int total = G;
+    if (atomicAdd(ctr + 1, 1) == total - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 template <int N, int kMaxC>
 __global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2))
     k_stencil_fast(const double* __restrict__ x, double* __restrict__ y, const int4* __restrict__ tasks, int ntasks,
-                   int w, int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp) {
+                   int w, int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp, int* __restrict__ ctr) {
   extern __shared__ __align__(128) double ring_all[];
-  stencil_fast_body<N, kMaxC>(x, y, tasks, ntasks, w, cell_slots, fp, blockIdx.x, gridDim.x, ring_all);
+  stencil_fast_body<N, kMaxC>(x, y, tasks, ntasks, w, cell_slots, fp, blockIdx.x, gridDim.x, ring_all, ctr);
 }
 
 // Both ends of every fast row (1 <= k <= n-2, j >= 1, length L >= 3): the
@@ -646,9 +849,17 @@ __global__ void __launch_bounds__(kGT, 9) k_stencil_general(const double* __rest
 void init_stencil_tasks(bt_stencil& st) {
   const int w = (1 << st.level) + 1;
   const int n = w - 1;
-  const int march =
-      (int64_t)(st.grid->part_end - st.grid->part_begin) * n_tet(w) <= kSmallSlots ? kSmallMarch : kMarchRows;
+  static const int env_march = std::getenv("BT_STENCIL_MARCH") ? std::atoi(std::getenv("BT_STENCIL_MARCH")) : 0;
+  const int march = (int64_t)(st.grid->part_end - st.grid->part_begin) * n_tet(w) <= kSmallSlots
+                        ? kSmallMarch
+                        : (env_march > 0 ? env_march : kMarchRows);
   std::vector<int4> fast, fast2, gen, all;  // fast: groups of kGroup layers; fast2: the 2-layer group
+  for (FastTasks* ft : {&st.fast4, &st.fast2}) {
+    ft->segs.clear();
+    ft->sched.clear();
+    ft->d_ctr.alloc(2);
+    BT_CUDA(cudaMemset(ft->d_ctr.p, 0, 2 * sizeof(int)));
+  }
   // general rows are unprefetched: one row per task keeps them parallel
   auto push1 = [](std::vector<int4>& v, int k, int b, int a, int e) {
     for (int j = a; j < e; ++j) v.push_back(make_int4(k, b, j, j + 1));
@@ -675,6 +886,7 @@ void init_stencil_tasks(bt_stencil& st) {
     for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (60 wide)
       const int jmax = w - k - kFastCols * b;
       const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;  // layer k's fast rows
+      if (fe > 1) (start4 ? st.fast4 : st.fast2).segs.push_back(make_int4(k, b, 1, fe));
       for (int j0 = 1; j0 < fe; j0 += march)
         (start4 ? fast : fast2).push_back(make_int4(k, b, j0, std::min(j0 + march, fe)));
     }
@@ -813,13 +1025,72 @@ static int stencil_parts() {
 
 // fast kernel launches (interior rows of the N-layer marches in ft) for this
 // handle's cells, on stream s
+
+// Balanced schedule of one chunk's fast marches over G persistent warps. The
+// column segments (cell, layer group, column block; rows j0..j1) are cut so
+// that every warp's list costs the same number of march steps (a piece of r
+// rows costs r + 2: two phantom steps fill the register window): segments are
+// dealt in order, a warp taking rows until its list reaches the target, so
+// consecutive warps work on consecutive pieces of the same segment. (The
+// round-1 schedule of fixed 32-row marches dealt round-robin left 1,776 warps
+// with 58.4 steps on average and 68 at most at level 8.)
+static const FastSched& build_sched(const FastTasks& ft, int chunk, int cnt, int G) {
+  auto& slot = ft.sched[{chunk, G}];
+  if (slot) return *slot;
+  constexpr int kMinPiece = 6;  // rows; shorter pieces only where a segment ends
+  int64_t rows = 0;
+  for (const int4& sg : ft.segs) rows += sg.w - sg.z;
+  rows *= cnt;
+  const int64_t nseg = (int64_t)ft.segs.size() * cnt;
+  std::vector<std::vector<int4>> lists;
+  for (int64_t T = (rows + 2 * (nseg + G) + G - 1) / G;; ++T) {
+    lists.assign(G, {});
+    int g = 0, load = 0;
+    bool fits = true;
+    for (size_t si = 0; si < ft.segs.size() && fits; ++si) {
+      for (int c = 0; c < cnt && fits; ++c) {
+        const int4 sg = ft.segs[si];
+        int j = sg.z;
+        while (j < sg.w) {
+          const int rem = sg.w - j, room = (int)T - load - 2;
+          if (room >= std::min(rem, kMinPiece)) {
+            int take = std::min(rem, room);
+            if (rem - take > 0 && rem - take < kMinPiece && take - (kMinPiece - (rem - take)) >= kMinPiece)
+              take -= kMinPiece - (rem - take);  // leave a remainder worth its two phantom steps
+            lists[g].push_back(make_int4(sg.x, sg.y | (c << 16), j, j + take));
+            load += take + 2;
+            j += take;
+          } else if (++g < G) {
+            load = 0;
+          } else {
+            fits = false;
+            break;
+          }
+        }
+      }
+    }
+    if (fits) break;
+  }
+  size_t slots = 1;
+  for (const auto& l : lists) slots = std::max(slots, l.size());
+  std::vector<int4> flat(slots * (size_t)G, make_int4(1, 0, 1, -1));  // null task: no steps (w - z + 2 == 0)
+  for (int g = 0; g < G; ++g)
+    for (size_t q = 0; q < lists[g].size(); ++q) flat[q * G + g] = lists[g][q];
+  slot = std::make_unique<FastSched>();
+  slot->ntasks = (int)flat.size();
+  slot->d_tasks.upload(flat);
+  return *slot;
+}
+
 template <int N>
 static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double* x, double* y, cudaStream_t s,
                         int reserve_sms = 0) {
   if (!ft.ntasks) return;
   const int w = (1 << st.level) + 1;
   const int64_t cs = n_tet(w);
-  const size_t smem = sizeof(double) * kFW * ring_doubles<N>();
+  // BT_STENCIL_PAD (profiling): extra dynamic shared memory per block, to lower the resident blocks per SM
+  static const size_t pad = std::getenv("BT_STENCIL_PAD") ? (size_t)std::atoi(std::getenv("BT_STENCIL_PAD")) : 0;
+  const size_t smem = sizeof(double) * kFW * ring_doubles<N>() + sizeof(int4) * 4 * kFW + (N == kGroup ? pad : 0);
   auto kern = k_stencil_fast<N, kMaxCells>;
   // persistent grid: SMs x resident blocks, per device (set up once)
   static std::mutex mu;
@@ -841,6 +1112,13 @@ static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double*
     grid = gr;
     per_sm = persm[dev & 63];
   }
+  // BT_STENCIL_SCHED (profiling): 0 = the round-1 schedule (fixed 32-row marches dealt round-robin, longest first)
+  // 1 = balanced static lists (build_sched), 2 = dynamic queue
+  static const int sched = [] {
+    const char* e = std::getenv("BT_STENCIL_SCHED");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool balanced = sched == 1;
   FastParams<kMaxCells> fp;  // copied into the launch's parameter buffer
   for (int ch = 0; ch + 1 < (int)ft.chunk_first.size(); ++ch) {
     const int cc0 = st.part_begin + ch * kMaxCells, cnt = std::min(kMaxCells, st.part_end - cc0);
@@ -852,8 +1130,24 @@ static void launch_fast(const bt_stencil& st, const FastTasks& ft, const double*
     }
     const int64_t e0 = (int64_t)cc0 * cs;
     // reserve_sms: leave SMs free for concurrent kernels (exchange, boundary)
-    const int blocks = std::min(std::max(per_sm, grid - reserve_sms * per_sm), (nt + kFW - 1) / kFW);
-    kern<<<blocks, kFT, smem, s>>>(x + e0, y + e0, ft.d_tasks.p + t0, nt, w, cs, fp);
+    const int avail = std::max(per_sm, grid - reserve_sms * per_sm);
+    // one warp per ~40 march steps at least, else the whole persistent grid;
+    // little work (under half the grid at that rate) keeps the short marches
+    int64_t cost = 0;
+    for (const int4& sg : ft.segs) cost += sg.w - sg.z + 2;
+    cost *= cnt;
+    if (balanced && cost / (40 * kFW) >= avail / 2) {
+      const int blocks = (int)std::min<int64_t>(avail, std::max<int64_t>(1, cost / (40 * kFW)));
+      std::lock_guard<std::mutex> lock(mu);
+      const FastSched& sc = build_sched(ft, ch, cnt, blocks * kFW);
+      kern<<<blocks, kFT, smem, s>>>(x + e0, y + e0, sc.d_tasks.p, sc.ntasks, w, cs, fp, nullptr);
+    } else {
+      const int blocks = std::min(avail, (nt + kFW - 1) / kFW);
+      // enough tasks per warp: dynamic queue (the list is sorted longest first)
+      int* ctr = nullptr;
+      if (sched == 2 && nt > blocks * kFW) ctr = ft.d_ctr.p;
+      kern<<<blocks, kFT, smem, s>>>(x + e0, y + e0, ft.d_tasks.p + t0, nt, w, cs, fp, ctr);
+    }
     count_launch();
   }
 }
