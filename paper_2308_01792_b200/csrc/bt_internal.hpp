@@ -331,6 +331,9 @@ struct bt_stencil {
   std::vector<double> fast;                  // per cell: the 8 symmetric interior weights
   bt::DevBuf<double> d_ends;                 // per cell: typed rows of the two row ends (11 + 11)
   bt::DevBuf<int> bnd_f, bnd_e, bnd_v;       // k_boundary: faces / macro edges / vertices with every member local
+  bt::DevBuf<int4> d_ftasks;                 // k_face_march tasks (strided faces' partial rows)
+  int nftasks = 0;
+  mutable bt::DevBuf<double> d_fpart;        // ... their output, read by k_boundary (allocated on first use)
   bt::DevBuf<int4> d_prism;                  // k_stencil_prism units (bt_prism.cu), longest first
   int nprism = 0;
   bt::DevBuf<double> d_w8;                   // per cell (global index): the 8 symmetric weights

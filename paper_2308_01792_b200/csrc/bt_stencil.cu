@@ -560,7 +560,14 @@ struct BndArgs {
   const int* lf;
   const int* le;
   const int* lv;
+  // per-cell partial rows of the i = 0 and diagonal face-interior points,
+  // precomputed by k_face_march (nullptr: gathered here like the other faces)
+  const double* fpart = nullptr;
 };
+// slot of point (j, k) of local cell c, face f (0: i = 0, 1: diagonal) in fpart
+__device__ __forceinline__ int64_t fpart_slot(int w, int c, int f, int j, int k) {
+  return (int64_t)(2 * c + f) * tri32(w) + (k * w - k * (k - 1) / 2) + j;
+}
 
 __device__ __forceinline__ void bary_ijk(const int8_t* lv, int nl, const int* wt, int& i, int& j, int& k) {
   i = j = k = 0;
@@ -719,16 +726,24 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
   if (F) {  // face point: one or two members, all their loads in flight together
     Gather11 g0, g1;
     int cell, i, j, k;
-    member(0, cell, i, j, k);
-    gather11(x, a, cell, i, j, k, g0);
-    if (count == 2) {
-      member(1, cell, i, j, k);
-      gather11(x, a, cell, i, j, k, g1);
-    }
-    single = face_row(g0);
+    double pre[2] = {0.0, 0.0};
+    bool has[2] = {false, false};
+    auto fetch = [&](int m, Gather11& g) {
+      member(m, cell, i, j, k);
+      const int z = zero_set(n, i, j, k);
+      if (a.fpart && (z == 1 || z == 2)) {  // strided faces: the march kernel's partial row
+        has[m] = true;
+        pre[m] = __ldg(a.fpart + fpart_slot(w, cell - a.cb, z == 2 ? 0 : 1, j, k));
+      } else {
+        gather11(x, a, cell, i, j, k, g);
+      }
+    };
+    fetch(0, g0);
+    if (count == 2) fetch(1, g1);
+    single = has[0] ? pre[0] : face_row(g0);
     sum += single;
     if (count == 2) {
-      single = face_row(g1);
+      single = has[1] ? pre[1] : face_row(g1);
       sum += single;
     }
   } else {
@@ -752,6 +767,106 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
 template <bool kDir>
 __global__ void __launch_bounds__(128) k_boundary(const double* __restrict__ x, double* __restrict__ y, BndArgs a) {
   boundary_body<kDir>(x, y, a, blockIdx.x);
+}
+
+// Per-cell partial rows of the two strided faces of every local cell: the
+// i = 0 face (F = 0) and the diagonal face i + j + k = n (F = 1). Their
+// face-interior points (j, k >= 1, j + k <= n - 1) sit at one end of row
+// (j, k), a row length apart in memory, so a gather per point (k_boundary)
+// costs 11 single-lane L1 wavefronts. Here a warp owns 30 consecutive j and
+// marches k: each lane loads only the two end values of its row (j, k + 1) per
+// step, keeps the pairs of layers k - 1, k, k + 1 in registers, and gets rows
+// j - 1, j + 1 from the neighbour lanes by shuffle: 2 loads per point. The
+// partial row is evaluated in k_boundary's order (direction 0, then the
+// present directions ascending), so the values are bitwise the gathered ones.
+// Task: x = local cell | face << 16, y = j block, z = k0, w = k1.
+constexpr int kFaceCols = 30;
+constexpr int kFaceChunk = 8;  // layers per task (plus two phantom steps)
+template <int F>
+__device__ __forceinline__ double2 face_pair(const double* __restrict__ xc, int w, int j, int k) {
+  // F = 0: (x[0], x[1]) of row (j, k); F = 1: (x[L - 2], x[L - 1]); 0.0 where the row has no such entry
+  const int L = w - j - k;
+  if (j < 0 || k < 0 || L < 1) return make_double2(0.0, 0.0);
+  const double* r = xc + row_start(w, j, k);
+  if (F == 0) return make_double2(__ldg(r), L >= 2 ? __ldg(r + 1) : 0.0);
+  return make_double2(L >= 2 ? __ldg(r + L - 2) : 0.0, __ldg(r + L - 1));
+}
+struct FacePair {  // a row's end pair and its copies from the rows j - 1 (up) and j + 1 (dn)
+  double v0, v1, u0, u1, d0, d1;
+};
+__device__ __forceinline__ FacePair face_spread(double2 p) {
+  FacePair q;
+  q.v0 = p.x;
+  q.v1 = p.y;
+  q.u0 = __shfl_up_sync(0xffffffffu, p.x, 1);
+  q.u1 = __shfl_up_sync(0xffffffffu, p.y, 1);
+  q.d0 = __shfl_down_sync(0xffffffffu, p.x, 1);
+  q.d1 = __shfl_down_sync(0xffffffffu, p.y, 1);
+  return q;
+}
+template <int F>
+__device__ __forceinline__ void face_march_body(const double* __restrict__ x, double* __restrict__ fpart,
+                                                const StencilCell* __restrict__ cells, int4 T, int n, int64_t cs,
+                                                int cb) {
+  const int w = n + 1, lane = threadIdx.x & 31;
+  const int lc = T.x & 0xffff, cell = cb + lc;
+  const int j = kFaceCols * T.y + lane;  // lanes 1..30 hold outputs, 0 and 31 their neighbours
+  const double* __restrict__ xc = x + (int64_t)cell * cs;
+  const double* __restrict__ wz = cells[cell].w[F == 0 ? 2 : 1];
+  constexpr int dirs0[11] = {0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 13};
+  constexpr int dirs1[11] = {0, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14};
+  double W[11];
+#pragma unroll
+  for (int q = 0; q < 11; ++q) W[q] = __ldg(wz + (F == 0 ? dirs0[q] : dirs1[q]));
+  const int k0 = T.z, k1 = T.w;
+  FacePair C = face_spread(face_pair<F>(xc, w, j, k0 - 1));  // layer k - 1
+  FacePair A = face_spread(face_pair<F>(xc, w, j, k0));      // layer k
+  double2 nx = face_pair<F>(xc, w, j, k0 + 1);
+  for (int k = k0; k < k1; ++k) {
+    const FacePair B = face_spread(nx);  // layer k + 1
+    nx = face_pair<F>(xc, w, j, k + 2);  // in flight during this step
+    double acc;
+    if (F == 0) {
+      acc = W[0] * A.v0;
+      acc = fma(W[1], A.v1, acc);   // (1, 0, 0)
+      acc = fma(W[2], A.d0, acc);   // (0, 1, 0)
+      acc = fma(W[3], B.v0, acc);   // (0, 0, 1)
+      acc = fma(W[4], A.u1, acc);   // (1, -1, 0)
+      acc = fma(W[5], C.v1, acc);   // (1, 0, -1)
+      acc = fma(W[6], C.d0, acc);   // (0, 1, -1)
+      acc = fma(W[7], B.u1, acc);   // (1, -1, 1)
+      acc = fma(W[8], A.u0, acc);   // (0, -1, 0)
+      acc = fma(W[9], C.v0, acc);   // (0, 0, -1)
+      acc = fma(W[10], B.u0, acc);  // (0, -1, 1)
+    } else {
+      acc = W[0] * A.v1;
+      acc = fma(W[1], A.u1, acc);   // (1, -1, 0): row j - 1's last
+      acc = fma(W[2], C.v1, acc);   // (1, 0, -1): layer k - 1's last
+      acc = fma(W[3], C.d1, acc);   // (0, 1, -1)
+      acc = fma(W[4], A.v0, acc);   // (-1, 0, 0)
+      acc = fma(W[5], A.u0, acc);   // (0, -1, 0)
+      acc = fma(W[6], C.v0, acc);   // (0, 0, -1)
+      acc = fma(W[7], A.d1, acc);   // (-1, 1, 0): row j + 1's last
+      acc = fma(W[8], B.v1, acc);   // (-1, 0, 1)
+      acc = fma(W[9], B.u1, acc);   // (0, -1, 1)
+      acc = fma(W[10], C.d0, acc);  // (-1, 1, -1)
+    }
+    if (lane >= 1 && lane <= kFaceCols && j + k <= n - 1) fpart[fpart_slot(w, lc, F, j, k)] = acc;
+    C = A;
+    A = B;
+  }
+}
+__global__ void __launch_bounds__(128) k_face_march(const double* __restrict__ x, double* __restrict__ fpart,
+                                                    const StencilCell* __restrict__ cells,
+                                                    const int4* __restrict__ tasks, int ntasks, int n, int64_t cs,
+                                                    int cb) {
+  const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (t >= ntasks) return;
+  const int4 T = tasks[t];
+  if (T.x >> 16)
+    face_march_body<1>(x, fpart, cells, T, n, cs, cb);
+  else
+    face_march_body<0>(x, fpart, cells, T, n, cs, cb);
 }
 
 // Rank-spanning interface groups of a partitioned fused apply: this rank's
@@ -854,6 +969,19 @@ void init_stencil_tasks(bt_stencil& st) {
                         ? kSmallMarch
                         : (env_march > 0 ? env_march : kMarchRows);
   std::vector<int4> fast, fast2, gen, all;  // fast: groups of kGroup layers; fast2: the 2-layer group
+  {  // k_face_march tasks: (local cell, face) x j block x k chunk, longest first
+    std::vector<int4> ft;
+    const int ncl = st.grid->part_end - st.grid->part_begin;
+    for (int kc = 1; kc <= n - 2; kc += kFaceChunk)
+      for (int b = 0; kFaceCols * b + 1 <= n - 1 - kc; ++b)
+        for (int f = 0; f < 2; ++f)
+          for (int c = 0; c < ncl; ++c)
+            ft.push_back(make_int4(c | (f << 16), b, kc, std::min(kc + kFaceChunk, n - 1 - (kFaceCols * b + 1) + 1)));
+    st.nftasks = (int)ft.size();
+    st.d_ftasks.upload(ft);
+    if (std::getenv("BT_STENCIL_FACEMARCH") && std::atoi(std::getenv("BT_STENCIL_FACEMARCH")))
+      st.d_fpart.alloc((size_t)2 * std::max(1, ncl) * tri32(w));
+  }
   for (FastTasks* ft : {&st.fast4, &st.fast2}) {
     ft->segs.clear();
     ft->sched.clear();
@@ -1280,6 +1408,17 @@ void launch_stencil_fused(const bt_stencil& st, const double* x, double* y, int 
     if (parts & 1) launch_fast<kGroup>(st, st.fast4, x, y, s, reserve);  // first: its blocks resident first
     BT_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
     if (parts & 1) launch_fast<2>(st, st.fast2, x, y, ss.s, reserve);  // the 2-layer group, beside the main launch
+  }
+  // BT_STENCIL_FACEMARCH=1 (opt-in): the strided faces' partial rows by warp marches (k_face_march) instead of
+  // k_boundary's gathers. Bitwise the same values; measured slower in the whole apply (92.5 vs 85.1 us at config 2:
+  // k_boundary stays instruction-bound, 8.3 M instead of 9.6 M warp instructions, and the march adds a 13 us
+  // latency-bound pass), profiles/r2_notes.md section 7.
+  static const bool facemarch = std::getenv("BT_STENCIL_FACEMARCH") && std::atoi(std::getenv("BT_STENCIL_FACEMARCH"));
+  if ((parts & 8) && facemarch && st.nftasks && a.nf && st.d_fpart.n) {
+    k_face_march<<<(st.nftasks + 3) / 4, 128, 0, ss.s>>>(x, st.d_fpart.p, st.d_cells.p, st.d_ftasks.p, st.nftasks, n,
+                                                        n_tet(n + 1), g.part_begin);
+    count_launch();
+    a.fpart = st.d_fpart.p;
   }
   if ((parts & 8) && (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv > 0) {
     const int64_t pts = (int64_t)a.nf * tri32(n - 2) + (int64_t)a.ne * (n - 1) + a.nv;
