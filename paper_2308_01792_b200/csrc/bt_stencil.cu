@@ -569,6 +569,18 @@ __device__ __forceinline__ int64_t fpart_slot(int w, int c, int f, int j, int k)
   return (int64_t)(2 * c + f) * tri32(w) + (k * w - k * (k - 1) / 2) + j;
 }
 
+// decode_tri (bt_index.cuh) with a single-precision first guess: the two
+// correction loops make the result exact whatever the guess's rounding
+__device__ __forceinline__ void decode_tri_f(int m, int q, int& a, int& b) {
+  const float c = 2.0f * m + 1.0f;
+  int bb = (int)((c - sqrtf(fmaxf(c * c - 8.0f * (float)q, 0.0f))) * 0.5f);
+  bb = max(0, min(bb, m - 1));
+  while (bb > 0 && bb * m - bb * (bb - 1) / 2 > q) --bb;
+  while ((bb + 1) * m - (bb + 1) * bb / 2 <= q) ++bb;
+  b = bb;
+  a = q - (bb * m - bb * (bb - 1) / 2);
+}
+
 __device__ __forceinline__ void bary_ijk(const int8_t* lv, int nl, const int* wt, int& i, int& j, int& k) {
   i = j = k = 0;
   for (int q = 0; q < nl; ++q) {
@@ -677,9 +689,18 @@ __device__ __forceinline__ void boundary_body(const double* __restrict__ x, doub
   const DevFace* F = nullptr;
   const DevPrimMem* mem = nullptr;
   if (q < (int64_t)a.nf * fpts) {  // face-interior point (a, b), weights (n - a - b, a, b)
-    F = a.faces + __ldg(a.lf + q / fpts);
+    // 32-bit index arithmetic where the point count allows (a 64-bit division is a subroutine)
+    int fi, fr;
+    if ((int64_t)a.nf * fpts < (int64_t(1) << 31)) {
+      fi = (int)((uint32_t)q / (uint32_t)fpts);
+      fr = (int)((uint32_t)q - (uint32_t)fi * (uint32_t)fpts);
+    } else {
+      fi = (int)(q / fpts);
+      fr = (int)(q % fpts);
+    }
+    F = a.faces + __ldg(a.lf + fi);
     int ap, bp;
-    decode_tri(n - 2, (int)(q % fpts), ap, bp);
+    decode_tri_f(n - 2, fr, ap, bp);
     wt[0] = n - (ap + 1) - (bp + 1);
     wt[1] = ap + 1;
     wt[2] = bp + 1;
