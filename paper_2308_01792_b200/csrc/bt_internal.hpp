@@ -448,9 +448,11 @@ void launch_smooth_update(int kind, double* x, double* d, const double* ax, cons
 // device-resident estimate_lambda_max scalars
 struct LamState {
   double num, den, nn2, rho, inv;
-  int done, empty;
+  int done, empty, zero_diag;
 };
 void launch_lam_step(LamState* st, bool first, cudaStream_t s);
+// zero_diag = 1 if any entry of diag[0, n) is 0.0 (estimate_lambda_max's precondition, solvers.hpp:143-147)
+void launch_lam_check_diag(LamState* st, const double* diag, int64_t n, cudaStream_t s);
 void launch_cg_alpha(CgState* st, cudaStream_t s);
 void launch_cg_update(CgState* st, double tol, double* hist, cudaStream_t s);
 void launch_vec_dev(int op, double* y, const double* x, const double* a, const int* done, int64_t n, cudaStream_t s);

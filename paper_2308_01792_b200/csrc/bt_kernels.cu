@@ -294,6 +294,20 @@ __global__ void k_lam_norm(LamState* st) {  // the start vector's normalisation
   st->done = 0;
   st->rho = 0.0;
 }
+__global__ void k_lam_check_diag(LamState* st, const double* __restrict__ diag, int64_t n) {
+  bool zero = false;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    zero = zero || diag[t] == 0.0;
+  if (__syncthreads_or(zero) && threadIdx.x == 0) st->zero_diag = 1;
+}
+void launch_lam_check_diag(LamState* st, const double* diag, int64_t n, cudaStream_t s) {
+  BT_CUDA(cudaMemsetAsync(&st->zero_diag, 0, sizeof(int), s));
+  if (n > 0) {
+    const int blocks = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 8);
+    k_lam_check_diag<<<blocks, kThreads, 0, s>>>(st, diag, n);
+    count_launch();
+  }
+}
 void launch_lam_step(LamState* st, bool first, cudaStream_t s) {
   if (first) k_lam_norm<<<1, 1, 0, s>>>(st);
   else k_lam_step<<<1, 1, 0, s>>>(st);

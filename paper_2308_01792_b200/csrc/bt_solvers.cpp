@@ -93,6 +93,7 @@ static double lambda_max(bt_hierarchy& h, int l, cudaStream_t s) {
   if (!L.lam.p) L.lam.alloc(1);
   LamState* S = L.lam.p;
   BT_CUDA(cudaStreamSynchronize(s));
+  launch_lam_check_diag(S, L.diag.p, n, s);  // read back with the start vector's norm below
   if (bt_random_fill(h.grid, BT_SPACE_P1, l, 0x51cbu, v, s) != BT_OK) raise(BT_CUDA_ERROR, bt_last_error());
   if (h.grid->part_nranks > 1) sync(*h.grid, l, IF_BCAST, v, nullptr, s);  // rank-spanning groups
   sync(*h.grid, l, IF_ZERO_DIR, v, nullptr, s);
@@ -101,6 +102,7 @@ static double lambda_max(bt_hierarchy& h, int l, cudaStream_t s) {
   LamState hs{};
   BT_CUDA(cudaMemcpyAsync(&hs, S, sizeof(LamState), cudaMemcpyDeviceToHost, s));
   BT_CUDA(cudaStreamSynchronize(s));
+  if (hs.zero_diag) raise(BT_INVALID_ARGUMENT, "estimate_lambda_max: zero diagonal entry");
   if (hs.empty) raise(BT_RUNTIME_ERROR, "estimate_lambda_max: empty free space");
   launch_vec_dev(V_SCALE, v, nullptr, &S->inv, &S->done, n, s);
   for (int k = 0; k < 25; ++k) {
