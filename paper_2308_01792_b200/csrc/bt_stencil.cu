@@ -2,11 +2,11 @@
 // operators.hpp:247-271), per-cell phase. The interface phase (replica sums
 // and Dirichlet rows) is bt_interface.cu.
 //
-// Data path (k_stencil_fast). A warp owns 60 consecutive output columns i of
-// one layer k of one macro-cell (lane l: the pair c0 = base - 2 + 2l, c0 + 1)
+// Data path (k_stencil_fast). A warp owns 62 consecutive output columns i of
+// one layer k of one macro-cell (lane l: the pair c0 = base - 1 + 2l, c0 + 1)
 // and marches up to kMarchRows rows j. Each step needs three new rows — A(j+1)
 // of layer k, B(j) of layer k+1 and C(j+1) of layer k-1 — over the warp's 64
-// staged columns [base - 2, base + 62). Every lane stages its two columns of
+// staged columns [base - 1, base + 63). Every lane stages its two columns of
 // each row with 8-byte cp.async into a per-warp kStages-deep shared ring (so a
 // row lands at a fixed place whatever its alignment), then reads its pair
 // with one 16-byte shared load and the i-1 / i+1 neighbours by shuffle.
@@ -44,17 +44,11 @@
 
 namespace bt {
 
-#ifndef BT_FAST2
-#define BT_FAST2 1  // 0: the round-1 consumer (two window sets, 8-byte stores)
-#endif
 #ifndef BT_ST16
 #define BT_ST16 0  // 1: 16-byte stores of address-aligned pairs
 #endif
 #ifndef BT_STQ
 #define BT_STQ ""  // cache qualifier of the march's stores (profiling: ".cg", ".cs", ".wt")
-#endif
-#ifndef BT_ABL
-#define BT_ABL 0  // profiling ablations of the fast march (scripts/build_variants.py); 0 in the product
 #endif
 
 namespace {
@@ -65,7 +59,7 @@ constexpr int kMarchRows = 32;
 constexpr int64_t kSmallSlots = int64_t(1) << 21;
 constexpr int kSmallMarch = 4;
 constexpr int kGroup = 4;  // layers per fast march (plus one 2-layer group); 6 measured slower (2 blocks/SM)
-constexpr int kFastCols = 60;  // output columns per warp in k_stencil_fast
+constexpr int kFastCols = 62;  // output columns per warp in k_stencil_fast (of 64 staged: one halo column each side)
 constexpr int kGenCols = 30;   // output columns per warp in k_stencil_general
 // k_stencil_general / k_stencil_ends blocks are small and register-light so
 // that one fits on an SM beside three k_stencil_fast blocks: they run on a
@@ -89,7 +83,7 @@ constexpr int kMaxCells = 256;  // 256 * 8 * 8 B = 16 KB of kernel parameters
 #define BT_STAGES 3  // measured: 3 beats 4 (more L1 beside the rings) and 2
 #endif
 constexpr int kStages = BT_STAGES;
-constexpr int kRowD = 64;  // staged columns [base - 2, base + 62)
+constexpr int kRowD = 64;  // staged columns [base - 1, base + 63)
 constexpr int kFT = 128;   // k_stencil_fast block
 constexpr int kFW = kFT / 32;
 template <int N>
@@ -112,7 +106,7 @@ struct Win {
 // Task word: x = k (first layer of the march's N layers), y = column block |
 // (cell - cell0) << 16, z = j0, w = j1.
 //
-// A warp owns 60 output columns of N adjacent layers k .. k+N-1 of one cell
+// A warp owns 62 output columns of N adjacent layers k .. k+N-1 of one cell
 // and marches rows j0..j1-1 of all of them (each layer's rows end one row
 // before the one below; rows that are not interior rows are masked). Per
 // step it stages N + 2 rows — row j+1 of layers k-1 .. k+N-1 and row j of
@@ -122,12 +116,12 @@ struct Win {
 // tasks by length, longest first). Each march is preceded by two phantom
 // steps (j0 - 2, j0 - 1) whose staged rows fill the register window, so the
 // staging stream runs through the ring across task boundaries without
-// draining. Lane l stages columns base - 2 + l and base + 30 + l of each row
+// draining. Lane l stages columns base - 1 + l and base + 31 + l of each row
 // (two 8-byte cp.async, each warp-contiguous; none past the row's end), so
 // every row lands at the same place whatever its alignment and lane l reads
-// its pair (c0, c1) with one 16-byte shared load. Columns -2, -1 (lanes 0, 1
-// of column block 0) are not staged: they feed only lane 0's outputs and
-// column 0's, which are never stored. So every copy stays inside its row:
+// its pair (c0, c1) with one 16-byte shared load. Column -1 (lane 0 of
+// column block 0) is not staged: it feeds only column 0's output, which is
+// never stored. So every copy stays inside its row:
 // any march of any cell runs here, whatever the vector's extent.
 // (body shared by k_stencil_fast and the single-launch k_stencil_small: block
 // vblock of a vgrid-block persistent grid)
@@ -182,7 +176,7 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
   const uint32_t my_s = smem_u32(ring) + 8u * lane;
 
   // ---- producer (every lane copies its two columns of each staged row) ----
-  // po[s]: element offset (within the cell) of column base - 2 + lane in the
+  // po[s]: element offset (within the cell) of column base - 1 + lane in the
   // producer's next step j of stream s: 0 = C(j+1) (layer k-1), 1 + q = row
   // j+1 of layer k+q, N+1 = Q(j) (layer k+N); pr = len(row j+1 of layer k)
   int pt = t0, pr = 0, pleft = 0, pcol = 0;
@@ -196,7 +190,7 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
       ++pn;
     }
     const int k = tk.x, base = kFastCols * (tk.y & 0xffff), cl = tk.y >> 16;
-    const int j = tk.z - 2, cb = base - 2 + lane;
+    const int j = tk.z - 2, cb = base - 1 + lane;
     pcol = cb;  // this lane's first staged column (the second is pcol + 32)
     pcell = x + (int64_t)cl * cell_slots;
     po[0] = cb + row_start(w, j + 1, k - 1);
@@ -220,11 +214,9 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
       for (int s = 0; s < NS; ++s) {
         // length of stream s's current row; columns past it are never used
         const int len = s == 0 ? pr + 1 : (s <= N ? pr - (s - 1) : pr + 1 - N);
-        const double* src = (BT_ABL & 32) ? x + (int64_t)(t0 % G) * 4096 + s * 512 + lane : pcell + po[s];
-        if (!(BT_ABL & 8) || w < 0) {
-          if ((unsigned)pcol < (unsigned)len) cp8(d + s * kRowD * 8, src);
-          if (pcol + 32 < len) cp8(d + s * kRowD * 8 + 256, src + 32);
-        }
+        const double* src = pcell + po[s];
+        if ((unsigned)pcol < (unsigned)len) cp8(d + s * kRowD * 8, src);
+        if (pcol + 32 < len) cp8(d + s * kRowD * 8 + 256, src + 32);
         po[s] += len;  // next row of the stream
       }
       ps = ps == kStages - 1 ? 0 : ps + 1;
@@ -261,7 +253,6 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     produce();
   };
 
-#if BT_FAST2
   // Window rows rotate through three register sets (phase p: row j-1 in set
   // p, row j in set p+1, the step's new row j+1 into set p+2, all mod 3), so
   // the march loop, unrolled over the three phases, moves no registers.
@@ -287,8 +278,9 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
 #pragma unroll
     for (int d = 0; d < 8; ++d) W[d] = fp.w[cl][d];
     const int base = kFastCols * blk;
-    const int c0 = base - 2 + 2 * lane;  // this lane's two columns: c0, c0 + 1
-    const bool out = lane >= 1 && lane <= 30;
+    // this lane's two columns: c0, c0 + 1. Lane 0's c0 (base - 1) and lane 31's c0 + 1 (base + 62) are halo
+    // columns: they only feed their neighbours' +-i partial sums.
+    const int c0 = base - 1 + 2 * lane;
     const int pmin = blk == 0 ? 3 : 0;  // shorter rows of column block 0 are not interior rows
     // Store thresholds: column c of a row of length LY is an interior output
     // iff 0 < c < LY - 1 (row ends are the boundary kernel's) and LY >= pmin,
@@ -296,9 +288,9 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     // the next lane's c0 (= c0 + 2), stored by this lane when the row's
     // address parity pairs it with this lane's c0 + 1.
     constexpr int kNever = 1 << 30;
-    const int T0 = out && c0 > 0 ? max(c0 + 1, pmin - 1) : kNever;
-    const int T1 = out ? max(c0 + 2, pmin - 1) : kNever;
-    const int T2 = lane <= 29 && c0 + 2 > 0 ? max(c0 + 3, pmin - 1) : kNever;
+    const int T0 = lane >= 1 && c0 > 0 ? max(c0 + 1, pmin - 1) : kNever;
+    const int T1 = lane <= 30 && c0 + 1 > 0 ? max(c0 + 2, pmin - 1) : kNever;
+    const int T2 = lane <= 30 && c0 + 2 > 0 ? max(c0 + 3, pmin - 1) : kNever;
     {
       Row2 cj, qj;
       consume(cj, R[0], qj);         // phantom step j0 - 2: rows j0 - 1
@@ -307,7 +299,7 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     int LA = w - k - j0;  // length of row j of layer k; layer k+q's is LA - q
     const int64_t celloff = (int64_t)cl * cell_slots;
     double* __restrict__ yl = y + celloff + c0;  // + a row's start: this lane's c0 in that row
-    const unsigned ypar = ybits + (unsigned)celloff;  // parity of (yl + oy) is that of ypar + oy (c0 is even)
+    const unsigned ypar = ybits + (unsigned)celloff + (unsigned)(c0 & 1);  // parity of (yl + oy): that of ypar + oy
     int oy[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) oy[q] = row_start(w, j0, k + q);
@@ -371,120 +363,6 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
     }
 #undef BT_STEP
   }
-#else
-#pragma unroll 1
-  for (int t = t0; dyn || t < ntasks; t += G) {
-    int4 tk;
-    if (dyn) {
-      __syncwarp();
-      tk = fifo[cn & 3];
-      ++cn;
-    } else {
-      tk = tasks[t];
-    }
-    tk.x = __shfl_sync(0xffffffffu, tk.x, 0);
-    tk.y = __shfl_sync(0xffffffffu, tk.y, 0);
-    tk.z = __shfl_sync(0xffffffffu, tk.z, 0);
-    tk.w = __shfl_sync(0xffffffffu, tk.w, 0);
-    const int k = tk.x, blk = tk.y & 0xffff, cl = tk.y >> 16, j0 = tk.z, j1 = tk.w;
-    if (j1 < j0) break;  // null task: the end of this warp's list in a balanced schedule (build_sched)
-    double W[8];
-#pragma unroll
-    for (int d = 0; d < 8; ++d) W[d] = fp.w[cl][d];
-    const int base = kFastCols * blk;
-    const int c0 = base - 2 + 2 * lane, c1 = c0 + 1;  // this lane's two columns
-    const bool out = lane >= 1 && lane <= 30;
-    Win<N> X, Y;
-    {
-      Row2 cj, qj, a1[N];
-      consume(cj, a1, qj);  // phantom step j0 - 2: rows j0 - 1
-#pragma unroll
-      for (int q = 0; q < N; ++q) X.am1[q] = a1[q];
-      consume(X.c, a1, X.qm1);  // phantom step j0 - 1: rows j0, C(j0), Q(j0 - 1)
-#pragma unroll
-      for (int q = 0; q < N; ++q) X.a[q] = a1[q];
-    }
-    int LA = w - k - j0;  // length of row j of layer k; layer k+q's is LA - q
-    double* __restrict__ py[N];
-#pragma unroll
-    for (int q = 0; q < N; ++q) py[q] = y + (int64_t)cl * cell_slots + row_start(w, j0, k + q);
-#if BT_ABL & 16
-#pragma unroll
-    for (int q = 0; q < N; ++q) py[q] = y + (int64_t)(t0 % G) * 4096 + q * 512 - base;
-#endif
-    const int pmin = blk == 0 ? 3 : 0;  // shorter rows of column block 0 are not interior rows
-    int j = j0;
-
-    // One layer's output row at columns c0 (s0) and c1 (s1) from its window:
-    // a = row j, b = upper layer row j-1, c = lower layer row j, am1 = row
-    // j-1, A1 = row j+1, B0 = upper row j, C1 = lower row j+1. The merged row
-    // is bitwise symmetric (W[d] == W[d+7]):
-    //   y_i = W0 a_i + W2 (A1_i + am1_i) + W3 (B0_i + c_i) + W6 (C1_i + b_i)
-    //       + [W1 a + W4 am1 + W5 c + W7 b]_{i+1} + [W1 a + W4 A1 + W5 B0 + W7 C1]_{i-1}
-    // The bracketed sums are formed by the lane that owns column i+1 / i-1 and
-    // shuffled (one double each way per layer), so neighbour values never
-    // cross lanes. Within the 1e-12 parity tolerance of the reference order.
-    auto layer = [&](const Row2& a, const Row2& b, const Row2& c, const Row2& am1, const Row2& A1, const Row2& B0,
-                     const Row2& C1, int LY, double* py_, bool ok) {
-      // explicit fma chains: k_stencil_prism (bt_prism.cu) evaluates the same
-      // expressions per column, so the two kernels agree bit for bit
-      const double upv = fma(W[7], C1.v1, fma(W[5], B0.v1, fma(W[4], A1.v1, W[1] * a.v1)));  // to column c1 + 1
-      const double dnv = fma(W[7], b.v0, fma(W[5], c.v0, fma(W[4], am1.v0, W[1] * a.v0)));   // to column c0 - 1
-#if BT_ABL & 2
-      const double lft = upv, rgt = dnv;
-#else
-      const double lft = __shfl_up_sync(0xffffffffu, upv, 1);    // column c0 - 1's, for c0
-      const double rgt = __shfl_down_sync(0xffffffffu, dnv, 1);  // column c1 + 1's, for c1
-#endif
-      double s0 = fma(W[6], C1.v0 + b.v0, fma(W[3], B0.v0 + c.v0, fma(W[2], A1.v0 + am1.v0, W[0] * a.v0)));
-      double s1 = fma(W[6], C1.v1 + b.v1, fma(W[3], B0.v1 + c.v1, fma(W[2], A1.v1 + am1.v1, W[0] * a.v1)));
-      // every column: (centre + its i-1 partial) + its i+1 partial
-      s0 += lft;
-      s0 += fma(W[7], b.v1, fma(W[5], c.v1, fma(W[4], am1.v1, W[1] * a.v1)));  // i+1 of c0 = own c1
-      s1 += fma(W[7], C1.v0, fma(W[5], B0.v0, fma(W[4], A1.v0, W[1] * a.v0)));  // i-1 of c1 = own c0
-      s1 += rgt;
-#if BT_ABL & 4
-      s0 = (a.v0 + A1.v0) + (B0.v0 + C1.v0) + lft;
-      s1 = (a.v1 + A1.v1) + (B0.v1 + C1.v1) + rgt;
-#endif
-#if BT_ABL & 1
-      ok = ok && w < 0;
-#endif
-      // row ends (i = 0, i = LY - 1) are the boundary kernel's
-      if (ok && out && c0 < LY - 1 && c0 > 0) py_[c0] = s0;
-      if (ok && out && c1 < LY - 1) py_[c1] = s1;
-    };
-#define BT_STEP(cur, nxt)                                                                           \
-  {                                                                                                 \
-    Row2 C1, Q0, A1[N];                                                                             \
-    consume(C1, A1, Q0);                                                                            \
-    _Pragma("unroll") for (int q = 0; q < N; ++q) {                                                 \
-      const int qu = q < N - 1 ? q + 1 : q, ql = q > 0 ? q - 1 : q; /* in-range indices */          \
-      const Row2& b = q < N - 1 ? cur.am1[qu] : cur.qm1;                                            \
-      const Row2& B0 = q < N - 1 ? cur.a[qu] : Q0;                                                  \
-      const Row2& c = q > 0 ? cur.a[ql] : cur.c;                                                    \
-      const Row2& Cn = q > 0 ? A1[ql] : C1;                                                         \
-      layer(cur.a[q], b, c, cur.am1[q], A1[q], B0, Cn, LA - q, py[q], LA - q >= pmin);              \
-      if (!(BT_ABL & 16)) py[q] += LA - q;                                                          \
-    }                                                                                               \
-    --LA;                                                                                           \
-    ++j;                                                                                            \
-    _Pragma("unroll") for (int q = 0; q < N; ++q) {                                                 \
-      nxt.am1[q] = cur.a[q];                                                                        \
-      nxt.a[q] = A1[q];                                                                             \
-    }                                                                                               \
-    nxt.c = C1;                                                                                     \
-    nxt.qm1 = Q0;                                                                                   \
-  }
-    while (true) {
-      BT_STEP(X, Y)
-      if (j >= j1) break;
-      BT_STEP(Y, X)
-      if (j >= j1) break;
-    }
-#undef BT_STEP
-  }
-#endif
   cp_wait<0>();
   if (dyn && lane == 0) {
     const int total = G;
@@ -1032,7 +910,7 @@ void init_stencil_tasks(bt_stencil& st) {
     const bool start4 = fast_layer && (k - 1) % kGroup == 0 && (k - 1) / kGroup < ng;
     const bool start2 = fast_layer && k == 1 + ng * kGroup && k + 1 <= n - 2;
     if (!start4 && !start2) continue;
-    for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (60 wide)
+    for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (62 wide)
       const int jmax = w - k - kFastCols * b;
       const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;  // layer k's fast rows
       if (fe > 1) (start4 ? st.fast4 : st.fast2).segs.push_back(make_int4(k, b, 1, fe));
