@@ -17,6 +17,7 @@ in the same run, each with its own roofline (the slower of HBM bytes at the
 measured copy peak and fp64 flops at the fp64 peak measured here by a DFMA
 microbenchmark), e2e and CPU baseline (bounded samples, stated):
   1  ref-tet L6 stencil, Dirichlet rows, 1 + 10 applies per step (CUDA graph)
+  2  (headline) cube-kuhn L8 stencil + interface sync; at N = 1 each step replays a CUDA graph of one apply
   3  384 perturbed Kuhn tets L6, div(k grad) elementwise (k = 1 + .5 sin sin sin)
   4  384 perturbed Kuhn tets L7, N1E1 curl-curl + mass, tangential Dirichlet
   5  V(2,2) Chebyshev(2) multigrid, var-coeff elementwise, 50 coarse CG its:
@@ -381,17 +382,18 @@ def setup_config(cfg, bt, torch, ws, rank):
         w.kernel = "k_stencil_small (one launch)" if cfg == 1 else (
             "k_stencil_fast || k_boundary" if ws == 1 else
             "k_stencil_fast || k_boundary (rank-local groups) || k_xpartials + neighbour exchange")
-        if cfg == 1:
+        if cfg == 1 or (cfg == 2 and ws == 1):  # the step's applies replayed from a CUDA graph (no host launch gaps)
             graph = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
-                bt.apply_stencil(t, x, y, lvl, bt.BC.DirichletIdentity)
+                gbc = bt.BC.DirichletIdentity if bc else bt.BC.None_
+                bt.apply_stencil(t, x, y, lvl, gbc)
                 torch.cuda.synchronize()
                 n0 = L.bt_launch_count()
                 with torch.cuda.graph(graph, stream=s):
                     for _ in range(reps):
-                        bt.apply_stencil(t, x, y, lvl, bt.BC.DirichletIdentity)
+                        bt.apply_stencil(t, x, y, lvl, gbc)
             torch.cuda.synchronize()
             w.graph = graph
             w.graph_launches = int(L.bt_launch_count() - n0)  # the library kernels each replay runs
@@ -417,6 +419,8 @@ def setup_config(cfg, bt, torch, ws, rank):
                     "15-point stencil apply + interface sync (cells partitioned over ranks)",
                     "level": lvl, "cells": g.n_cells(), "slots_per_gpu": slots, "owned_dofs": w.owned,
                     "bc": "dirichlet identity rows" if bc else "none",
+                    "launch": "each step replays a CUDA graph of the step's applies (bt_apply_stencil captured once)"
+                    if (cfg == 1 or ws == 1) else "bt_apply_stencil called per step (NCCL exchange inside)",
                     "l2": ("inputs larger than L2 (x+y = %.0f MB per GPU)" % (16e-6 * slots)) if cfg == 2 else
                     "0.77 MB: L2-resident by design of the config (latency bound)"}
     elif cfg == 3:

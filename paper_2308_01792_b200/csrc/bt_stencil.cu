@@ -84,7 +84,11 @@ constexpr int kMaxCells = 256;  // 256 * 8 * 8 B = 16 KB of kernel parameters
 #endif
 constexpr int kStages = BT_STAGES;
 constexpr int kRowD = 64;  // staged columns [base - 1, base + 63)
-constexpr int kFT = 128;   // k_stencil_fast block
+#ifndef BT_FT
+#define BT_FT 128
+#endif
+constexpr int kFT = BT_FT;  // k_stencil_fast block (warps of a block are independent: the size only sets how early a
+                            // finished block's registers return to the SM)
 constexpr int kFW = kFT / 32;
 template <int N>
 __host__ __device__ constexpr int ring_doubles() {  // per warp
@@ -375,7 +379,7 @@ __device__ __forceinline__ void stencil_fast_body(const double* __restrict__ x, 
 }
 
 template <int N, int kMaxC>
-__global__ void __launch_bounds__(kFT, N <= 2 ? 4 : (N <= 4 ? 3 : 2))
+__global__ void __launch_bounds__(kFT, (N <= 2 ? 16 : (N <= 4 ? 12 : 8)) / kFW)
     k_stencil_fast(const double* __restrict__ x, double* __restrict__ y, const int4* __restrict__ tasks, int ntasks,
                    int w, int64_t cell_slots, const __grid_constant__ FastParams<kMaxC> fp, int* __restrict__ ctr) {
   extern __shared__ __align__(128) double ring_all[];
@@ -797,7 +801,7 @@ __global__ void __launch_bounds__(128) k_xpartials(const double* __restrict__ x,
 // the 2-layer group, the rest the boundary points. The three sets of points
 // are disjoint, so the roles need no ordering.
 template <bool kDir>
-__global__ void __launch_bounds__(kFT, 3)
+__global__ void __launch_bounds__(kFT, 12 / kFW)
     k_stencil_small(const double* __restrict__ x, double* __restrict__ y, const int4* __restrict__ t4, int n4,
                     const int4* __restrict__ t2, int n2, int w, int64_t cell_slots, int b4, int b2, BndArgs a,
                     const __grid_constant__ FastParams<kMaxCells> fp) {
