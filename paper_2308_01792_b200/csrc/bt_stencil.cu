@@ -52,7 +52,7 @@ namespace bt {
 #endif
 
 namespace {
-constexpr int kMarchRows = 32;
+constexpr int kMarchRows = 64;  // measured at config 2 (r2_notes section 7): 32 -> 84.1, 64 -> 81.5, 72 -> 81.1, 128 -> 91.7 us per apply
 // small problems (all slots of the handle <= kSmallSlots): one launch for the
 // whole apply (k_stencil_small) and short marches, whose serial step chains
 // set the latency there
@@ -868,9 +868,6 @@ void init_stencil_tasks(bt_stencil& st) {
   const int w = (1 << st.level) + 1;
   const int n = w - 1;
   static const int env_march = std::getenv("BT_STENCIL_MARCH") ? std::atoi(std::getenv("BT_STENCIL_MARCH")) : 0;
-  const int march = (int64_t)(st.grid->part_end - st.grid->part_begin) * n_tet(w) <= kSmallSlots
-                        ? kSmallMarch
-                        : (env_march > 0 ? env_march : kMarchRows);
   std::vector<int4> fast, fast2, gen, all;  // fast: groups of kGroup layers; fast2: the 2-layer group
   {  // k_face_march tasks: (local cell, face) x j block x k chunk, longest first
     std::vector<int4> ft;
@@ -918,10 +915,28 @@ void init_stencil_tasks(bt_stencil& st) {
       const int jmax = w - k - kFastCols * b;
       const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;  // layer k's fast rows
       if (fe > 1) (start4 ? st.fast4 : st.fast2).segs.push_back(make_int4(k, b, 1, fe));
-      for (int j0 = 1; j0 < fe; j0 += march)
-        (start4 ? fast : fast2).push_back(make_int4(k, b, j0, std::min(j0 + march, fe)));
     }
   }
+  // March length. Every march costs two phantom steps, so long marches mean
+  // less work, and the idle tail their coarser balance leaves is where the
+  // boundary kernel runs (config 2: 32 rows 84.1, 64 rows 81.5, 128 rows 91.7
+  // us per apply). With little work per warp (level 7 on one GPU: 64 rows
+  // 27.9 us against 18.9) the marches stay short, and the single-launch
+  // path's are shorter still.
+  int march = kSmallMarch;
+  if ((int64_t)(st.grid->part_end - st.grid->part_begin) * n_tet(w) > kSmallSlots) {
+    int64_t rows = 0;
+    for (const int4& sg : st.fast4.segs) rows += sg.w - sg.z;
+    rows *= st.grid->part_end - st.grid->part_begin;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.grid->device);
+    march = rows / (12 * (int64_t)sms) >= 40 ? kMarchRows : kMarchRows / 2;
+    if (env_march > 0) march = env_march;
+  }
+  for (int pass = 0; pass < 2; ++pass)
+    for (const int4& sg : (pass == 0 ? st.fast4 : st.fast2).segs)
+      for (int j0 = sg.z; j0 < sg.w; j0 += march)
+        (pass == 0 ? fast : fast2).push_back(make_int4(sg.x, sg.y, j0, std::min(j0 + march, sg.w)));
   if ((n - 2) % kGroup != 0 && (n - 2) % kGroup != 2)
     raise(BT_LOGIC_ERROR, "stencil: fast layer count must be 0 or 2 mod the group size");
   // Fast tasks of every cell of this handle, in chunks of kMaxCells cells
