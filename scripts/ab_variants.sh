@@ -1,5 +1,6 @@
 #!/bin/bash
-# Time the interior marches (BT_STENCIL_PARTS=1) and the whole apply (15) of config 2 for library variants built by
+# Time the interior marches (BT_STENCIL_PARTS=1) and the whole apply (15) of config 2 for library variants (compile-time
+# knobs of bt_stencil.cu: BT_STAGES, BT_FT, BT_ST16, BT_STQ) built by
 # scripts/build_variants.py. Usage: gpurun -- 'bash scripts/ab_variants.sh name1 name2 ...'
 cd "${GRAFT_REPO_ROOT:-.}" || exit 1
 mkdir -p gpurun_out

@@ -1,5 +1,5 @@
 """Build profiling variants of libbt_b200.so: bt_stencil.cu recompiled with extra -D flags, linked against the
-product's other objects. Usage: python scripts/build_variants.py name1=-DBT_ABL=1 name2="-DBT_ABL=2 -DX=3" ...
+product's other objects. Usage: python scripts/build_variants.py s4=-DBT_STAGES=4 ft64="-DBT_FT=64 -DBT_ST16=1" ...
 Outputs paper_2308_01792_b200/variants/libbt_<name>.so (git-ignored; they travel to the GPU box). Run with
 BT_LIB_PATH=<that file>."""
 import concurrent.futures as cf
