@@ -913,7 +913,9 @@ void init_stencil_tasks(bt_stencil& st) {
     if (!start4 && !start2) continue;
     for (int b = 0; kFastCols * b < w - k; ++b) {  // fast blocks (62 wide)
       const int jmax = w - k - kFastCols * b;
-      const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax;  // layer k's fast rows
+      // layer k's fast rows: in block b >= 1 the row whose only column here is its diagonal end (L = 62 b + 1)
+      // has no interior output
+      const int fe = b == 0 ? std::min(jmax, w - k - 2) : jmax - 1;
       if (fe > 1) (start4 ? st.fast4 : st.fast2).segs.push_back(make_int4(k, b, 1, fe));
     }
   }
