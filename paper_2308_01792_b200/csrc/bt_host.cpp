@@ -13,7 +13,20 @@
 
 #include "bt_internal.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace bt {
+
+bool nvtx_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("BT_NVTX");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+void nvtx_push(const char* name) { nvtxRangePushA(name); }
+void nvtx_pop() { nvtxRangePop(); }
+
 
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }

@@ -36,7 +36,25 @@ void set_error(const std::string& m);
   } while (0)
 
 // C-ABI entry point bodies: exceptions inside, statuses at the boundary.
-#define BT_TRY try {
+bool nvtx_enabled();  // BT_NVTX=1 (bt_host.cpp)
+void nvtx_push(const char* name);
+void nvtx_pop();
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) : on(nvtx_enabled()) {
+    if (on) nvtx_push(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtx_pop();
+  }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+// Every C-ABI entry point opens an NVTX range named after itself when BT_NVTX=1 (nsys / ncu --nvtx timelines of
+// the applies, cycles and transfers; off by default: one predictable branch per call).
+#define BT_TRY                            \
+  ::bt::NvtxRange bt_nvtx_range_(__func__); \
+  try {
 #define BT_CATCH                                     \
   }                                                  \
   catch (const ::bt::Error& e) {                     \
